@@ -1,0 +1,164 @@
+"""CPU oracle for the DTSDF raycast hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2301_12796_b200``) never imports it, and it never imports the product path.
+
+``liboracle.so`` is plain C in fp64 (``oracle.c``); this module only marshals arguments.
+Every function cites the passage it follows in ``oracle.c``; DESIGN.md §4 lists the readings.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+CFLAGS = ["-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-shared", "-fPIC",
+          "-pthread"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no -ffast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-lm", "-o", tmp])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB_PATH)
+        P, D, I64, I32 = C.c_void_p, C.c_double, C.c_int64, C.c_int
+        L.oracle_volume_create.argtypes = [D, D, D, D, I64, P, P, P, P, C.POINTER(P)]
+        L.oracle_volume_create.restype = I32
+        L.oracle_volume_destroy.argtypes = [P]
+        L.oracle_enable_counting.argtypes = [P]
+        L.oracle_counts.argtypes = [P, P]
+        L.oracle_trilinear.argtypes = [P, I32, P, P, P]
+        L.oracle_gradient.argtypes = [P, I32, P, P]
+        L.oracle_w_dir.argtypes = [D, D]
+        L.oracle_w_dir.restype = D
+        L.oracle_eval.argtypes = [P, P, P, P]
+        L.oracle_render.argtypes = [P, P, P, I64, P, I32, I32, P, P, P, P, P]
+        L.oracle_render.restype = None
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def w_dir(cosang: float, theta: float) -> float:
+    """eq:direction_weight with reading R1."""
+    return lib().oracle_w_dir(float(cosang), float(theta))
+
+
+class OracleVolume:
+    """Dense per-direction block grid over a BlockVolume (keeps references to its arrays)."""
+
+    def __init__(self, vol, counting: bool = False):
+        self.vol = vol
+        self._keys = np.ascontiguousarray(vol.keys, np.int32)
+        self._sdf = np.ascontiguousarray(vol.sdf, np.float32)
+        self._w = np.ascontiguousarray(vol.weight, np.float32)
+        self._rgb = np.ascontiguousarray(vol.rgb, np.uint8)
+        h = C.c_void_p()
+        rc = lib().oracle_volume_create(vol.voxel_size, vol.truncation, vol.theta, vol.step, vol.n_blocks,
+                                        _ptr(self._keys), _ptr(self._sdf), _ptr(self._w), _ptr(self._rgb),
+                                        C.byref(h))
+        if rc != 0:
+            raise ValueError(f"oracle_volume_create failed: {rc}")
+        self.h = h
+        if counting and lib().oracle_enable_counting(self.h) != 0:
+            raise MemoryError("oracle counting buffers")
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.oracle_volume_destroy(h)
+            self.h = None
+
+    def counts(self):
+        out = np.zeros(3, np.int64)
+        lib().oracle_counts(self.h, _ptr(out))
+        return {"voxel_records": int(out[0]), "rgb_records": int(out[1]), "locations": int(out[2])}
+
+    def trilinear(self, D, x):
+        x = np.asarray(x, np.float64)
+        phi, om = C.c_double(), C.c_double()
+        ok = lib().oracle_trilinear(self.h, D, _ptr(x), C.byref(phi), C.byref(om))
+        return (phi.value, om.value) if ok else None
+
+    def gradient(self, D, x):
+        x = np.asarray(x, np.float64)
+        g = np.zeros(3)
+        ok = lib().oracle_gradient(self.h, D, _ptr(x), _ptr(g))
+        return g if ok else None
+
+    def eval(self, x, r):
+        """O3 F(x, r): dict(valid, f, S, regime, W[6], nt[6,3], phi[6], omega[6], present[6], has_grad[6])."""
+        x = np.asarray(x, np.float64)
+        r = np.asarray(r, np.float64)
+        out = np.zeros(52)
+        lib().oracle_eval(self.h, _ptr(x), _ptr(r), _ptr(out))
+        return dict(valid=bool(out[0]), f=out[1], S=out[2], regime=int(out[3]), W=out[4:10].copy(),
+                    nt=out[10:28].reshape(6, 3).copy(), phi=out[28:34].copy(), omega=out[34:40].copy(),
+                    present=out[40:46].astype(bool), has_grad=out[46:52].astype(bool))
+
+    def render(self, pose, K, pixels=None, row0=0, row1=None, threads=None, nsamples=False):
+        """Render one view.  pixels: int [P, 2] (u, v) list, or None for rows [row0, row1).
+
+        Inputs are the float32 values the GPU path receives (pose and intrinsics are rounded
+        to float32 first).  Returns dict(depth [P] or [h,W], normal, color, mask[, nsamples])."""
+        pose32 = np.asarray(pose, np.float32).astype(np.float64).reshape(16)
+        intr = np.array([np.float32(K.fx), np.float32(K.fy), np.float32(K.cx), np.float32(K.cy), K.width, K.height,
+                         np.float32(K.z_min), np.float32(K.z_max)], np.float64)
+        if pixels is None:
+            row1 = K.height if row1 is None else row1
+            npix = (row1 - row0) * K.width
+            uv = None
+            shape = (row1 - row0, K.width)
+        else:
+            uv = np.ascontiguousarray(pixels, np.int32).reshape(-1, 2)
+            npix = uv.shape[0]
+            shape = (npix,)
+        depth = np.zeros(npix)
+        normal = np.zeros((npix, 3))
+        color = np.zeros((npix, 3), np.uint8)
+        mask = np.zeros(npix, np.uint8)
+        ns = np.zeros(npix, np.int32) if nsamples else None
+        threads = threads or os.cpu_count() or 1
+        lib().oracle_render(self.h, _ptr(pose32), _ptr(intr), npix, _ptr(uv), row0, threads, _ptr(depth),
+                            _ptr(normal), _ptr(color), _ptr(mask), _ptr(ns))
+        out = dict(depth=depth.reshape(shape), normal=normal.reshape(shape + (3,)),
+                   color=color.reshape(shape + (3,)), mask=mask.reshape(shape))
+        if nsamples:
+            out["nsamples"] = ns.reshape(shape)
+        return out
+
+
+def ray_dirs(pose, K, pixels=None):
+    """O1 in numpy for test-side closed forms: camera-centre o and unit world rays r per pixel
+    plus L = |d~| (depth = t / L).  pose/intrinsics rounded to float32 like the render inputs."""
+    pose = np.asarray(pose, np.float32).astype(np.float64)
+    if pixels is None:
+        v, u = np.mgrid[0:K.height, 0:K.width]
+        u, v = u.ravel(), v.ravel()
+    else:
+        u, v = np.asarray(pixels)[:, 0], np.asarray(pixels)[:, 1]
+    fx, fy, cx, cy = (float(np.float32(a)) for a in (K.fx, K.fy, K.cx, K.cy))
+    dt = np.stack([(u - cx) / fx, (v - cy) / fy, np.ones_like(u, dtype=np.float64)], -1)
+    L = np.linalg.norm(dt, axis=-1)
+    r = (dt / L[:, None]) @ pose[:3, :3].T
+    return pose[:3, 3], r, L

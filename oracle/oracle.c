@@ -1,0 +1,434 @@
+/*
+ * oracle.c -- plain, slow, fp64 CPU reference of the DTSDF raycast hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code, header,
+ * table or constant with the CUDA path in paper_2301_12796_b200/ and never calls it.
+ *
+ * What it computes (readings R1-R31 in DESIGN.md §4):
+ *   O1 ray          d~ = ((u-cx)/fx, (v-cy)/fy, 1), L = |d~|, r = R d~/L, o = t
+ *                   (pinhole reprojection eq:reprojection)
+ *   O2 lattice      t_k = k*Delta, k = ceil(zmin L/Delta) .. floor(zmax L/Delta)
+ *                   ("probing the TSDF along the ray at regular intervals")
+ *   O3 sample       per direction D: trilinear phi_D, omega_D over the 8 cell
+ *                   corners; central-difference gradient n_D;
+ *                   membership w_dir (eq:direction_weight, reading R1);
+ *                   combination weight w_comb = w_dir(n_D) <n_D,-r> w_D
+ *                   (eq:combine_weight) or, when no direction holding
+ *                   data has a gradient, w_noGrad = w_D <v^D,-r> (eq:combine_tsdf_weight,
+ *                   PAPER.md:265-270); f = sum W phi / sum W
+ *   O4 crossing     first valid + -> valid - lattice pair
+ *   O5 refinement   60 bisection steps in the bracket (reading R5/R21)
+ *   O6-O8           depth = camera z, normal, colour, direction mask; zeros on a miss
+ *
+ * Brute force: every lattice point from zmin to zmax is evaluated; there is no range pass,
+ * no block skipping and no hash -- the volume is a dense per-direction block-index grid.
+ *
+ * Pins: tests/test_oracle_*.py (closed forms, invariants, library reductions).
+ * parity pinned: every exported function has at least one closed-form or reduction pin.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_BLOCK 8
+#define OR_VPB 512
+
+typedef struct {
+  double s, tau, theta, delta;
+  int64_t n;
+  const int32_t *keys;  /* [n][4] (bx,by,bz,D) */
+  const float *sdf;     /* [n][512] */
+  const float *weight;  /* [n][512] */
+  const uint8_t *rgb;   /* [n][512][3] or NULL */
+  int64_t lo[3], dim[3];
+  int32_t *grid;        /* [6][dim2][dim1][dim0] -> block id, -1 = unallocated */
+  /* optional instrumentation: distinct records touched (algorithmic bytes) */
+  uint8_t *touch_vox;   /* [n*512] sdf+weight record read by a sample evaluation */
+  uint8_t *touch_rgb;   /* [n*512] colour record read by shading */
+  uint8_t *touch_loc;   /* [dim2*dim1*dim0] block location whose presence was resolved */
+} ovol;
+
+/* v^D: X+, X-, Y+, Y-, Z+, Z- */
+static const double VDIR[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+
+static int64_t floordiv8(int64_t i) { return (i >= 0) ? i / 8 : -((-i + 7) / 8); }
+
+/* ---------------------------------------------------------------------------------------
+ * volume: dense per-direction block grid.  Returns 0, -1 bad key, -2 duplicate key.
+ * ------------------------------------------------------------------------------------- */
+int oracle_volume_create(double s, double tau, double theta, double delta, int64_t n, const int32_t *keys,
+                         const float *sdf, const float *weight, const uint8_t *rgb, void **out) {
+  *out = NULL;
+  ovol *v = (ovol *)calloc(1, sizeof(ovol));
+  if (!v) return -4;
+  v->s = s; v->tau = tau; v->theta = theta; v->delta = delta > 0 ? delta : s;
+  v->n = n; v->keys = keys; v->sdf = sdf; v->weight = weight; v->rgb = rgb;
+  int64_t lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  for (int64_t b = 0; b < n; ++b) {
+    if (keys[4 * b + 3] < 0 || keys[4 * b + 3] > 5) { free(v); return -1; }
+    for (int a = 0; a < 3; ++a) {
+      int64_t c = keys[4 * b + a];
+      if (b == 0 || c < lo[a]) lo[a] = c;
+      if (b == 0 || c > hi[a]) hi[a] = c;
+    }
+  }
+  int64_t cells = 1;
+  for (int a = 0; a < 3; ++a) {
+    v->lo[a] = lo[a];
+    v->dim[a] = n ? hi[a] - lo[a] + 1 : 0;
+    cells *= v->dim[a];
+  }
+  v->grid = (int32_t *)malloc(sizeof(int32_t) * (size_t)(6 * (cells ? cells : 1)));
+  if (!v->grid) { free(v); return -4; }
+  for (int64_t i = 0; i < 6 * cells; ++i) v->grid[i] = -1;
+  for (int64_t b = 0; b < n; ++b) {
+    int64_t D = keys[4 * b + 3];
+    int64_t gi = ((D * v->dim[2] + (keys[4 * b + 2] - lo[2])) * v->dim[1] + (keys[4 * b + 1] - lo[1])) * v->dim[0] +
+                 (keys[4 * b + 0] - lo[0]);
+    if (v->grid[gi] >= 0) { free(v->grid); free(v); return -2; }
+    v->grid[gi] = (int32_t)b;
+  }
+  *out = v;
+  return 0;
+}
+
+void oracle_volume_destroy(void *p) {
+  ovol *v = (ovol *)p;
+  if (!v) return;
+  free(v->grid);
+  free(v->touch_vox);
+  free(v->touch_rgb);
+  free(v->touch_loc);
+  free(v);
+}
+
+/* enable instrumentation; returns 0 or -4 */
+int oracle_enable_counting(void *p) {
+  ovol *v = (ovol *)p;
+  size_t cells = (size_t)(v->dim[0] * v->dim[1] * v->dim[2]);
+  v->touch_vox = (uint8_t *)calloc((size_t)v->n * OR_VPB + 1, 1);
+  v->touch_rgb = (uint8_t *)calloc((size_t)v->n * OR_VPB + 1, 1);
+  v->touch_loc = (uint8_t *)calloc(cells + 1, 1);
+  return (v->touch_vox && v->touch_rgb && v->touch_loc) ? 0 : -4;
+}
+
+/* counts[0] = distinct voxel records, [1] = distinct colour records, [2] = distinct locations */
+void oracle_counts(void *p, int64_t *counts) {
+  ovol *v = (ovol *)p;
+  counts[0] = counts[1] = counts[2] = 0;
+  if (!v->touch_vox) return;
+  for (int64_t i = 0; i < v->n * OR_VPB; ++i) { counts[0] += v->touch_vox[i]; counts[1] += v->touch_rgb[i]; }
+  for (int64_t i = 0; i < v->dim[0] * v->dim[1] * v->dim[2]; ++i) counts[2] += v->touch_loc[i];
+}
+
+/* block id holding voxel (i,j,k) of direction D, or -1 (unallocated / outside the grid) */
+static int64_t block_of(const ovol *v, int D, int64_t i, int64_t j, int64_t k) {
+  int64_t b[3] = {floordiv8(i) - v->lo[0], floordiv8(j) - v->lo[1], floordiv8(k) - v->lo[2]};
+  for (int a = 0; a < 3; ++a)
+    if (b[a] < 0 || b[a] >= v->dim[a]) return -1;
+  int64_t cell = (b[2] * v->dim[1] + b[1]) * v->dim[0] + b[0];
+  int32_t id = v->grid[(int64_t)D * v->dim[0] * v->dim[1] * v->dim[2] + cell];
+  if (id >= 0 && v->touch_loc) __atomic_store_n(&v->touch_loc[cell], 1, __ATOMIC_RELAXED);
+  return id;
+}
+
+/* record index of voxel (i,j,k) in direction D, or -1 */
+static int64_t record_of(const ovol *v, int D, int64_t i, int64_t j, int64_t k) {
+  int64_t b = block_of(v, D, i, j, k);
+  if (b < 0) return -1;
+  int64_t l = (i - 8 * floordiv8(i)) + 8 * (j - 8 * floordiv8(j)) + 64 * (k - 8 * floordiv8(k));
+  return b * OR_VPB + l;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * O3(a): trilinear interpolation of cell (ci,cj,ck) with fractions fr.
+ * Plain trilinear over the 8 corners including weight-0 voxels (reading R11); the direction
+ * is absent (returns 0) unless all 8 corners lie in allocated blocks of D.
+ * ------------------------------------------------------------------------------------- */
+static int cell_interp(const ovol *v, int D, const int64_t c[3], const double fr[3], double *phi, double *omega,
+                       int want_w, int64_t rec_out[8]) {
+  double p = 0.0, w = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+    int64_t r = record_of(v, D, c[0] + dx, c[1] + dy, c[2] + dz);
+    if (r < 0) return 0;
+    double wt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
+    p += wt * (double)v->sdf[r];
+    if (want_w) w += wt * (double)v->weight[r];
+    if (v->touch_vox) __atomic_store_n(&v->touch_vox[r], 1, __ATOMIC_RELAXED);
+    if (rec_out) rec_out[q] = r;
+  }
+  *phi = p;
+  if (want_w) *omega = w;
+  return 1;
+}
+
+/* base cell and fractions of a world point (voxel (i,j,k) at (i,j,k)*s, reading R17) */
+static void locate(const ovol *v, const double x[3], int64_t c[3], double fr[3]) {
+  for (int a = 0; a < 3; ++a) {
+    double g = x[a] / v->s;
+    double fl = floor(g);
+    c[a] = (int64_t)fl;
+    fr[a] = g - fl;
+  }
+}
+
+int oracle_trilinear(void *p, int D, const double x[3], double *phi, double *omega) {
+  const ovol *v = (const ovol *)p;
+  int64_t c[3];
+  double fr[3];
+  locate(v, x, c, fr);
+  return cell_interp(v, D, c, fr, phi, omega, 1, NULL);
+}
+
+/* O3(c): g_a = (phi(cell + e_a) - phi(cell - e_a)) / (2s), the shifted cells taken with the
+ * same fractions (central differences of trilinear phi at x +- s e_a, reading R7).
+ * Returns 1 iff all six shifted cells are fully allocated in D. */
+static int cell_gradient(const ovol *v, int D, const int64_t c[3], const double fr[3], double g[3]) {
+  for (int a = 0; a < 3; ++a) {
+    int64_t cp[3] = {c[0], c[1], c[2]}, cm[3] = {c[0], c[1], c[2]};
+    cp[a] += 1;
+    cm[a] -= 1;
+    double pp, pm, dummy;
+    if (!cell_interp(v, D, cp, fr, &pp, &dummy, 0, NULL)) return 0;
+    if (!cell_interp(v, D, cm, fr, &pm, &dummy, 0, NULL)) return 0;
+    g[a] = (pp - pm) / (2.0 * v->s);
+  }
+  return 1;
+}
+
+int oracle_gradient(void *p, int D, const double x[3], double g[3]) {
+  const ovol *v = (const ovol *)p;
+  int64_t c[3];
+  double fr[3];
+  locate(v, x, c, fr);
+  return cell_gradient(v, D, c, fr, g);
+}
+
+/* eq:direction_weight with reading R1: clamp((theta - acos<n,v>) / (2 theta - pi/2), 0, 1) */
+double oracle_w_dir(double cosang, double theta) {
+  double c = cosang < -1.0 ? -1.0 : (cosang > 1.0 ? 1.0 : cosang);
+  double w = (theta - acos(c)) / (2.0 * theta - M_PI / 2.0);
+  return w < 0.0 ? 0.0 : (w > 1.0 ? 1.0 : w);
+}
+
+#define OR_EPS_GRAD 1e-3 /* reading R8: |g| <= 1e-3 m^-1 means "no gradient" */
+
+typedef struct {
+  int valid;
+  double f, S;
+  double W[6], nt[6][3], phi[6], omega[6];
+  int present[6], data[6], has_grad[6];
+  int regime; /* 1 = eq:combine_weight, 2 = eq:combine_tsdf_weight fallback */
+  int64_t c[3];
+  double fr[3];
+} osample;
+
+/* O3: F(x, r) */
+static void eval_sample(const ovol *v, const double x[3], const double r[3], osample *o) {
+  memset(o, 0, sizeof(*o));
+  locate(v, x, o->c, o->fr);
+  double sum_omega = 0.0;
+  for (int D = 0; D < 6; ++D) {
+    o->present[D] = cell_interp(v, D, o->c, o->fr, &o->phi[D], &o->omega[D], 1, NULL);
+    if (o->present[D]) sum_omega += o->omega[D];
+  }
+  /* O3(b): W_D is proportional to omega_D in both regimes */
+  if (!(sum_omega > 0.0)) return;
+  double n[6][3];
+  int any_grad = 0;
+  for (int D = 0; D < 6; ++D) {
+    o->data[D] = o->present[D] && o->omega[D] > 0.0; /* reading R8: "directions" = those holding data at x */
+    if (!o->data[D]) continue;
+    double g[3];
+    if (cell_gradient(v, D, o->c, o->fr, g)) {
+      double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+      if (gn > OR_EPS_GRAD) {
+        o->has_grad[D] = 1;
+        any_grad = 1;
+        for (int a = 0; a < 3; ++a) n[D][a] = g[a] / gn;
+      }
+    }
+  }
+  double S = 0.0, F = 0.0;
+  o->regime = any_grad ? 1 : 2;
+  for (int D = 0; D < 6; ++D) {
+    double W = 0.0;
+    if (any_grad) {
+      if (o->has_grad[D]) {
+        double nv = n[D][0] * VDIR[D][0] + n[D][1] * VDIR[D][1] + n[D][2] * VDIR[D][2];
+        double nr = -(n[D][0] * r[0] + n[D][1] * r[1] + n[D][2] * r[2]);
+        W = oracle_w_dir(nv, v->theta) * (nr > 0.0 ? nr : 0.0) * o->omega[D]; /* eq:combine_weight */
+        for (int a = 0; a < 3; ++a) o->nt[D][a] = n[D][a];
+      }
+    } else if (o->data[D]) {
+      double vr = -(VDIR[D][0] * r[0] + VDIR[D][1] * r[1] + VDIR[D][2] * r[2]);
+      W = o->omega[D] * (vr > 0.0 ? vr : 0.0); /* eq:combine_tsdf_weight */
+      for (int a = 0; a < 3; ++a) o->nt[D][a] = VDIR[D][a];
+    }
+    o->W[D] = W;
+    S += W;
+    F += W * o->phi[D];
+  }
+  o->S = S;
+  if (!(S > 0.0)) return; /* O3(e) */
+  o->valid = 1;
+  o->f = F / S;
+}
+
+/* exported single-sample evaluation for unit tests.
+ * out[0]=valid out[1]=f out[2]=S out[3]=regime out[4..9]=W out[10..27]=nt out[28..33]=phi
+ * out[34..39]=omega out[40..45]=present out[46..51]=has_grad */
+int oracle_eval(void *p, const double x[3], const double r[3], double *out) {
+  osample o;
+  eval_sample((const ovol *)p, x, r, &o);
+  out[0] = o.valid; out[1] = o.f; out[2] = o.S; out[3] = o.regime;
+  for (int D = 0; D < 6; ++D) {
+    out[4 + D] = o.W[D];
+    for (int a = 0; a < 3; ++a) out[10 + 3 * D + a] = o.nt[D][a];
+    out[28 + D] = o.phi[D];
+    out[34 + D] = o.omega[D];
+    out[40 + D] = o.present[D];
+    out[46 + D] = o.has_grad[D];
+  }
+  return o.valid;
+}
+
+/* ---------------------------------------------------------------------------------------
+ * O4-O8: one pixel
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  const ovol *v;
+  double R[9], t[3];
+  double fx, fy, cx, cy, zmin, zmax;
+  int W, H;
+  int64_t npix;
+  const int32_t *uv; /* [npix][2] or NULL = all pixels row-major from row0 */
+  int row0;
+  double *depth, *normal;
+  uint8_t *color, *mask;
+  int32_t *nsamples; /* optional per-pixel lattice evaluations with a present direction */
+  int64_t next;      /* work counter */
+} ojob;
+
+static void shade(const ovol *v, const osample *o, double *nrm, uint8_t *col, uint8_t *msk) {
+  double N[3] = {0, 0, 0}, c[3] = {0, 0, 0};
+  int m = 0;
+  for (int D = 0; D < 6; ++D) {
+    if (!(o->W[D] > 0.0)) continue;
+    m |= 1 << D;
+    for (int a = 0; a < 3; ++a) N[a] += o->W[D] * o->nt[D][a];
+    if (v->rgb) {
+      int64_t rec[8];
+      double ph, om;
+      cell_interp(v, D, o->c, o->fr, &ph, &om, 0, rec); /* corners are present (W_D > 0) */
+      for (int q = 0; q < 8; ++q) {
+        int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+        double wt = (dx ? o->fr[0] : 1.0 - o->fr[0]) * (dy ? o->fr[1] : 1.0 - o->fr[1]) *
+                    (dz ? o->fr[2] : 1.0 - o->fr[2]);
+        for (int a = 0; a < 3; ++a) c[a] += o->W[D] * wt * (double)v->rgb[3 * rec[q] + a];
+        if (v->touch_rgb) __atomic_store_n(&v->touch_rgb[rec[q]], 1, __ATOMIC_RELAXED);
+      }
+    }
+  }
+  double nn = sqrt(N[0] * N[0] + N[1] * N[1] + N[2] * N[2]);
+  for (int a = 0; a < 3; ++a) nrm[a] = nn > 0.0 ? N[a] / nn : 0.0;
+  for (int a = 0; a < 3; ++a) {
+    double q = floor(c[a] / o->S + 0.5); /* reading R13: round half up, clamp at 255 */
+    col[a] = (uint8_t)(q > 255.0 ? 255.0 : (q < 0.0 ? 0.0 : q));
+  }
+  *msk = (uint8_t)m;
+}
+
+static void render_pixel(ojob *J, int u, int vrow, int64_t out) {
+  const ovol *v = J->v;
+  double dt[3] = {(u - J->cx) / J->fx, (vrow - J->cy) / J->fy, 1.0};
+  double L = sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]);
+  double r[3], o[3] = {J->t[0], J->t[1], J->t[2]};
+  for (int a = 0; a < 3; ++a) r[a] = (J->R[3 * a] * dt[0] + J->R[3 * a + 1] * dt[1] + J->R[3 * a + 2] * dt[2]) / L;
+  int64_t k0 = (int64_t)ceil(J->zmin * L / v->delta), k1 = (int64_t)floor(J->zmax * L / v->delta);
+  int prev_valid = 0;
+  double prev_f = 0.0;
+  int32_t ns = 0;
+  J->depth[out] = 0.0;
+  for (int a = 0; a < 3; ++a) { J->normal[3 * out + a] = 0.0; J->color[3 * out + a] = 0; }
+  J->mask[out] = 0;
+  for (int64_t k = k0; k <= k1; ++k) {
+    double t = (double)k * v->delta;
+    double x[3] = {o[0] + t * r[0], o[1] + t * r[1], o[2] + t * r[2]};
+    osample s;
+    eval_sample(v, x, r, &s);
+    for (int D = 0; D < 6; ++D) if (s.present[D]) { ns++; break; }
+    if (s.valid && prev_valid && prev_f > 0.0 && s.f <= 0.0) {
+      /* O5: bisection in [t_{k-1}, t_k]; invalid midpoints count as positive (R21) */
+      double a = t - v->delta, b = t;
+      for (int it = 0; it < 60 && b - a >= 1e-9; ++it) {
+        double m = 0.5 * (a + b);
+        double xm[3] = {o[0] + m * r[0], o[1] + m * r[1], o[2] + m * r[2]};
+        osample sm;
+        eval_sample(v, xm, r, &sm);
+        if (!sm.valid || sm.f > 0.0) a = m; else b = m;
+      }
+      double ts = 0.5 * (a + b);
+      J->depth[out] = ts / L; /* O6 */
+      double xs[3] = {o[0] + ts * r[0], o[1] + ts * r[1], o[2] + ts * r[2]};
+      osample ss;
+      eval_sample(v, xs, r, &ss);
+      if (!ss.valid) { /* O7: fall back to the b end of the bracket */
+        double xb[3] = {o[0] + b * r[0], o[1] + b * r[1], o[2] + b * r[2]};
+        eval_sample(v, xb, r, &ss);
+      }
+      shade(v, &ss, &J->normal[3 * out], &J->color[3 * out], &J->mask[out]);
+      break;
+    }
+    prev_valid = s.valid;
+    prev_f = s.f;
+  }
+  if (J->nsamples) J->nsamples[out] = ns;
+}
+
+static void *worker(void *arg) {
+  ojob *J = (ojob *)arg;
+  const int64_t chunk = 64;
+  for (;;) {
+    int64_t i0 = __atomic_fetch_add(&J->next, chunk, __ATOMIC_RELAXED);
+    if (i0 >= J->npix) break;
+    int64_t i1 = i0 + chunk < J->npix ? i0 + chunk : J->npix;
+    for (int64_t i = i0; i < i1; ++i) {
+      int u, vr;
+      if (J->uv) { u = J->uv[2 * i]; vr = J->uv[2 * i + 1]; }
+      else { u = (int)(i % J->W); vr = J->row0 + (int)(i / J->W); }
+      render_pixel(J, u, vr, i);
+    }
+  }
+  return NULL;
+}
+
+/*
+ * Render npix pixels of one view.  pose: world-from-camera 4x4 row-major; intr: fx fy cx cy
+ * W H zmin zmax.  uv: [npix][2] pixel (column,row) list, or NULL for rows [row0, row0 + npix/W).
+ * Outputs are indexed like the pixel list: depth [npix], normal [npix][3] (world, unit),
+ * color [npix][3], mask [npix]; nsamples may be NULL.  nthreads <= 0 -> 1.
+ */
+void oracle_render(void *p, const double pose[16], const double intr[8], int64_t npix, const int32_t *uv, int row0,
+                   int nthreads, double *depth, double *normal, uint8_t *color, uint8_t *mask, int32_t *nsamples) {
+  ojob J;
+  memset(&J, 0, sizeof(J));
+  J.v = (const ovol *)p;
+  for (int a = 0; a < 3; ++a) {
+    for (int b = 0; b < 3; ++b) J.R[3 * a + b] = pose[4 * a + b];
+    J.t[a] = pose[4 * a + 3];
+  }
+  J.fx = intr[0]; J.fy = intr[1]; J.cx = intr[2]; J.cy = intr[3];
+  J.W = (int)intr[4]; J.H = (int)intr[5]; J.zmin = intr[6]; J.zmax = intr[7];
+  J.npix = npix; J.uv = uv; J.row0 = row0;
+  J.depth = depth; J.normal = normal; J.color = color; J.mask = mask; J.nsamples = nsamples;
+  if (nthreads <= 1) { worker(&J); return; }
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, worker, &J);
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+  free(th);
+}
