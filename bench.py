@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the DTSDF raycast hot path (BASELINE.json metric on configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dtsdf|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+One step = every rank renders one 640x480 depth+normal+colour+dirmask view of the configs[1]
+room volume (seeded synthetic) through dtsdf_render_batch; per-GPU work is fixed
+(weak scaling).  The volume is generated on rank 0, replicated by one NCCL broadcast per buffer
+into the library-owned buffers and committed on every rank before timing.  L2 is flushed
+(256 MiB write) between timed steps; each step is timed with CUDA events on the render stream,
+and the job time is the max over ranks.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "Mrays/s"
+FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["dtsdf", "reference"], default="dtsdf")
+    ap.add_argument("--config", choices=["C0", "C1", "C2", "C3"], default="C1",
+                    help="C1 is the bench workload; others are for profiling only")
+    ap.add_argument("--views", type=int, default=1, help="views per rank per step (1 = the configs[1] workload)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
+    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--no-flush", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name):
+    import scenes
+    if name == "C0":
+        return scenes.c0_sphere()
+    if name == "C2":
+        return scenes.c2_thin()
+    if name == "C3":
+        return scenes.c3_batch()
+    return scenes.c1_room()
+
+
+def describe(w, views):
+    K = w.intrinsics
+    return {"workload": f"{w.name}: " + {
+        "C1": "room scale, 20 seeded boxes on a 4x4 m floor, 1 cm voxels, tau 4 cm, one 640x480 view at the "
+              "seeded pose (fx=fy=525, cx=319.5, cy=239.5)",
+        "C0": "dense sphere r=0.2 m, 64^3 voxels at 1 cm, 80x60 view",
+        "C2": "200 thin plates, 5 mm voxels, 640x480 views",
+        "C3": "configs[1] volume, orbit views"}[w.name],
+        "width": K.width, "height": K.height, "views_per_step_per_gpu": views,
+        "n_blocks": int(w.volume.n_blocks), "theta_deg": 65.0, "outputs": "depth+normal+color+dirmask",
+        "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ------------------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"unavailable": "nvidia-smi not runnable"}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [[c.strip() for c in ln.split(",")] for ln in self.lines if ln.count(",") >= 6]
+        if not rows:
+            return {"unavailable": "no samples"}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle (TEST INFRASTRUCTURE, the one other place bench may run it)
+# ------------------------------------------------------------------------------------------
+def oracle_sample_rate(w, n_pix, seed=0, threads=None):
+    import oracle
+    K = w.intrinsics
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(K.width * K.height, size=min(n_pix, K.width * K.height), replace=False)
+    px = np.stack([idx % K.width, idx // K.width], 1).astype(np.int32)
+    ov = oracle.OracleVolume(w.volume)
+    t0 = time.perf_counter()
+    out = ov.render(w.poses[0], K, pixels=px, threads=threads)
+    dt = time.perf_counter() - t0
+    return len(px), dt, px, out
+
+
+def cpu_baseline(w, seconds):
+    threads = os.cpu_count() or 1
+    n0, dt0, _, _ = oracle_sample_rate(w, 2048, seed=1, threads=threads)
+    n = int(min(w.intrinsics.width * w.intrinsics.height, max(2048, n0 * seconds / max(dt0, 1e-3))))
+    n, dt, px, out = oracle_sample_rate(w, n, seed=2, threads=threads)
+    return {"value": n / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{n} of {w.intrinsics.width * w.intrinsics.height} pixel rays of the {w.name} view "
+                      f"(seeded uniform subset), fp64 brute-force march, {dt:.1f} s"}, px, out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = workload(args.config)
+    threads = os.cpu_count() or 1
+    n0, dt0, _, _ = oracle_sample_rate(w, 1024, seed=1, threads=threads)
+    rate = n0 / max(dt0, 1e-3)
+    per_step = min(2.0, 150.0 / max(args.steps + args.warmup, 1))
+    n = int(min(w.intrinsics.width * w.intrinsics.height, max(256, rate * per_step)))
+    for i in range(args.warmup):
+        oracle_sample_rate(w, n, seed=100 + i, threads=threads)
+    tot = 0.0
+    for i in range(args.steps):
+        _, dt, _, _ = oracle_sample_rate(w, n, seed=1000 + i, threads=threads)
+        tot += dt
+    value = n * args.steps / tot / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": describe(w, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"each step: {n} of {w.intrinsics.width * w.intrinsics.height} pixel rays "
+                                       f"of the {w.name} view (seeded uniform subset)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# the product arm
+# ------------------------------------------------------------------------------------------
+def load_json(path):
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
+
+
+def run_dtsdf(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2301_12796_b200 import Renderer
+    from paper_2301_12796_b200 import dist as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = workload(args.config) if rank == 0 else None
+    R = Renderer(local)
+    stream = torch.cuda.current_stream()
+
+    # ---- replicate the volume: rank 0 fills its buffers, NCCL broadcast into the others' ----
+    t_up = time.perf_counter()
+    if world > 1:
+        meta = None
+        if rank == 0:
+            v = w.volume
+            meta = {"n_blocks": v.n_blocks, "voxel_size": v.voxel_size, "truncation": v.truncation,
+                    "theta": v.theta, "step": v.step}
+        meta = pdist.broadcast_volume_meta(dist, meta, dev)
+        bufs = R.alloc(meta["voxel_size"], meta["truncation"], meta["theta"], meta["n_blocks"], meta["step"])
+        if rank == 0:
+            for k, t in pdist.volume_arrays_to_tensors(w.volume).items():
+                bufs[k].copy_(t)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tb = time.perf_counter()
+        pdist.broadcast_buffers(dist, bufs)
+        torch.cuda.synchronize()
+        bcast_ms = 1e3 * (time.perf_counter() - tb)
+        cs = pdist.checksum(bufs)
+        sums = [None] * world
+        dist.all_gather_object(sums, cs)
+        if len(set(sums)) != 1:
+            raise SystemExit(f"volume replicas differ after broadcast: {sums}")
+        R.commit(stream)
+        # everything rank 0 knows about the workload (poses, intrinsics) travels as an object
+        objs = [w if rank == 0 else None]
+        dist.broadcast_object_list(objs, 0)
+        if rank != 0:
+            w = objs[0]
+    else:
+        bcast_ms = 0.0
+        R.upload_volume(w.volume)
+    upload_ms = 1e3 * (time.perf_counter() - t_up)
+    K = w.intrinsics
+    poses = np.repeat(np.asarray(w.poses[:1], np.float32), args.views, axis=0)
+    rays_per_step = K.width * K.height * args.views
+    out = R.render(poses, K)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(args.warmup):
+        if not args.no_flush:
+            flush.fill_(1.0)
+        R.render_into(poses, K, out["depth"], out["normal"], out["color"], out["mask"], stream=stream)
+    torch.cuda.synchronize()
+    R.reset_kernel_times()
+    R.set_profiling(True)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n_launch0 = R.launch_count()
+    for i in range(args.steps):
+        if not args.no_flush:
+            flush.fill_(1.0)
+        starts[i].record(stream)
+        R.render_into(poses, K, out["depth"], out["normal"], out["color"], out["mask"], stream=stream)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = R.launch_count() - n_launch0
+    clk = clocks.stop()
+    R.set_profiling(False)
+    kt = R.kernel_times()
+    total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    max_ms = pdist.max_over_ranks(dist, total_ms, dev) if world > 1 else total_ms
+    value = world * rays_per_step * args.steps / (max_ms / 1e3) / 1e6
+
+    # ---- roofline of the dominant kernel (raycast) ----
+    ray_ms = kt["raycast_ms"] / max(kt["raycast_launches"], 1)
+    balg = load_json(os.path.join(ROOT, "profiles", "b_alg.json")) or {}
+    b_ray = balg.get(w.name, {}).get("bytes_per_ray")
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
+    traffic = ncu.get(w.name, {}).get("raycast_dram_bytes_per_launch")
+    achieved = (b_ray * rays_per_step / (ray_ms / 1e3) / 1e9) if b_ray else None
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "k_raycast", "kernel_ms": ray_ms, "bytes_per_ray_alg": b_ray,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
+            "range_pass_ms": kt["range_ms"] / max(kt["range_launches"], 1)}
+
+    # ---- end to end through the C ABI with pinned HOST outputs (copies inside the timing) ----
+    H, W = K.height, K.width
+    V = args.views
+    hd = torch.empty((V, H, W), dtype=torch.float32).pin_memory()
+    hn = torch.empty((V, H, W, 3), dtype=torch.float32).pin_memory()
+    hc = torch.empty((V, H, W, 3), dtype=torch.uint8).pin_memory()
+    hm = torch.empty((V, H, W), dtype=torch.uint8).pin_memory()
+    pose_host = torch.from_numpy(np.ascontiguousarray(poses)).pin_memory()
+    e2e_steps = min(args.e2e_steps, args.steps)
+    for _ in range(3):
+        R.render_into(pose_host.numpy(), K, hd, hn, hc, hm, stream=stream)
+    e2e_tot = 0.0
+    if world > 1:
+        dist.barrier()
+    for _ in range(e2e_steps):
+        if not args.no_flush:
+            flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        R.render_into(pose_host.numpy(), K, hd, hn, hc, hm, stream=stream)  # synchronizes (host outputs)
+        e2e_tot += time.perf_counter() - t0
+    e2e_max = pdist.max_over_ranks(dist, e2e_tot, dev) if world > 1 else e2e_tot
+    e2e = {"value": world * rays_per_step * e2e_steps / e2e_max / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": int(pose_host.numel() * 4 + 32),
+           "d2h_bytes_per_step": int(hd.numel() * 4 + hn.numel() * 4 + hc.numel() + hm.numel()),
+           "timing": "host wall clock per dtsdf_render_batch call with host outputs (D2H inside)"}
+
+    if rank != 0:
+        dist.barrier() if world > 1 else None
+        dist.destroy_process_group() if world > 1 else None
+        return 0
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) + a sampled parity check of this run ----
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu, px, ora = cpu_baseline(w, args.cpu_seconds)
+        g = {k: v[0].cpu().numpy()[px[:, 1], px[:, 0]] for k, v in out.items()}
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from parity import compare
+        parity = compare(g, ora)
+    st = R.stats()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scene, DESIGN.md §3)",
+        "config": describe(w, args.views),
+        "frames_per_s": world * args.views * args.steps / (max_ms / 1e3),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk,
+        "extra": {"upload_and_index_ms": upload_ms, "broadcast_ms": bcast_ms, "n_locations": st["n_locations"],
+                  "device_bytes": st["bytes"], "parity_sample_vs_oracle": parity,
+                  "device": torch.cuda.get_device_name(dev)},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_dtsdf(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

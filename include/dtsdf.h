@@ -1,0 +1,165 @@
+/*
+ * dtsdf.h -- C ABI of libdtsdf.so, the B200 (sm_100a) DTSDF raycast renderer.
+ *
+ * The library renders depth, normal, colour and direction-mask images from a six-direction
+ * Directional TSDF ("one for each direction {X+, X-, Y+, Y-, Z+, Z-}") stored as
+ * 8x8x8 voxel blocks keyed by (x, y, z, D).  Each ray probes the field at
+ * regular intervals until the first positive -> negative transition and refines the root
+ * (PAPER.md:178); every probe combines the directions on the fly with the
+ * combination weight eq:combine_weight or, when no direction has a
+ * gradient, eq:combine_tsdf_weight.  DESIGN.md §2 states the exact
+ * definition the results follow and §4 the readings of the paper it rests on.
+ *
+ * Conventions (DESIGN.md §4 readings R14-R17):
+ *   - voxel (i,j,k) sits at world (i,j,k) * voxel_size; block = floor(i/8) per axis;
+ *     local voxel index l = lx + 8*ly + 64*lz;
+ *   - direction D in 0..5 = X+, X-, Y+, Y-, Z+, Z-;
+ *   - sdf is normalised (units of truncation), positive in front of the surface;
+ *   - camera frame x right, y down, z forward; pixel (u, v) at integer coordinates;
+ *     ray direction ((u-cx)/fx, (v-cy)/fy, 1) (eq:reprojection);
+ *   - output depth is camera-frame z (0 = miss), normals are unit world-frame vectors facing
+ *     the camera (0 = miss), colour is u8 RGB, dirmask bit D set iff direction D contributed.
+ *
+ * Memory: "device" pointers are CUDA device memory of the context's device (e.g. a torch
+ * tensor's data_ptr()); the library auto-detects host vs device where stated.  Small structs
+ * (pose, intrinsics, params) are always host memory.
+ *
+ * Errors: every call returns DTSDF_OK (0) or a negative code; arguments are checked before
+ * any launch; no C++ exception crosses the ABI; dtsdf_last_error() returns a thread-local
+ * message for the last failing call on this thread.  DTSDF_ERR_CUDA is sticky: destroy the
+ * context.  A ray that finds no surface is not an error (it yields a zero pixel).
+ *
+ * Threading: one host thread per context at a time; one context per GPU.  The volume is
+ * immutable between commits; do not commit while a render is in flight on another stream.
+ */
+#ifndef DTSDF_H_
+#define DTSDF_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DTSDF_API __attribute__((visibility("default")))
+#else
+#define DTSDF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DTSDF_OK 0
+#define DTSDF_ERR_INVALID_ARGUMENT (-1) /* null pointer, bad size/intrinsics/params, D not in 0..5, coords out of range */
+#define DTSDF_ERR_DUPLICATE_KEY (-2)    /* two blocks with the same (bx,by,bz,D) */
+#define DTSDF_ERR_NO_VOLUME (-3)        /* render before a successful commit */
+#define DTSDF_ERR_OUT_OF_MEMORY (-4)    /* device allocation failed */
+#define DTSDF_ERR_CUDA (-5)             /* CUDA runtime error (sticky) */
+
+/* block coordinates must lie in [-2^20, 2^20) (21-bit packed index key) */
+#define DTSDF_MAX_BLOCK_COORD (1 << 20)
+/* views rendered per kernel launch; larger batches are split into several launches */
+#define DTSDF_VIEWS_PER_LAUNCH 256
+
+typedef struct dtsdf_ctx dtsdf_ctx; /* opaque, one per device */
+
+/* Pinhole intrinsics and the march depth range.  fx, fy > 0; width, height > 0;
+ * 0 < z_min < z_max (camera-frame z, metres; reading R24). */
+typedef struct {
+  float fx, fy, cx, cy;
+  int32_t width, height;
+  float z_min, z_max;
+} dtsdf_intrinsics;
+
+/* Volume parameters.
+ *   voxel_size  > 0 (metres)
+ *   truncation  >= 2 * voxel_size (metres) -- metadata: stored sdf is normalised
+ *   theta       angular threshold in (pi/4, pi/2]; used by eq:direction_weight
+ *   step        lattice step Delta (metres); 0 -> voxel_size (reading R4)
+ *   n_blocks    N >= 0 */
+typedef struct {
+  float voxel_size, truncation, theta, step;
+  int64_t n_blocks;
+} dtsdf_volume_params;
+
+/* Library-owned device buffers of the current volume (filled by dtsdf_alloc_volume).
+ *   keys    int32 [N][4] = (bx, by, bz, D)
+ *   sdf     f32   [N][512] normalised signed distance, positive in front (NaN is reserved)
+ *   weight  f32   [N][512] distance weight w_d >= 0
+ *   rgb     u8    [N][512][3] */
+typedef struct {
+  int32_t *keys;
+  float *sdf;
+  float *weight;
+  uint8_t *rgb;
+} dtsdf_volume_buffers;
+
+/* Create a context on CUDA device `cuda_device`.  *out receives the handle. */
+DTSDF_API int dtsdf_create(int cuda_device, dtsdf_ctx **out);
+/* Destroy the context and free all device memory it owns.  NULL is a no-op. */
+DTSDF_API int dtsdf_destroy(dtsdf_ctx *ctx);
+
+/* Allocate library-owned device buffers for N blocks (dropping any previous volume) and return
+ * their pointers in *out; the caller fills them (cudaMemcpy, NCCL broadcast, a kernel) and then
+ * calls dtsdf_commit_volume.  Validates params (see dtsdf_volume_params). */
+DTSDF_API int dtsdf_alloc_volume(dtsdf_ctx *ctx, const dtsdf_volume_params *params, dtsdf_volume_buffers *out);
+
+/* Validate the filled buffers and build the device index on `cuda_stream` (a cudaStream_t, or
+ * NULL for the legacy default stream): the (x,y,z) -> six direction slots hash table, the
+ * block-occupancy bitmap, the location list and the apron bricks the raycast kernel reads
+ * (DESIGN.md §5).  Synchronous: returns after the index is built.  Errors: INVALID_ARGUMENT
+ * (D not in 0..5 or a coordinate out of range), DUPLICATE_KEY, OUT_OF_MEMORY, CUDA. */
+DTSDF_API int dtsdf_commit_volume(dtsdf_ctx *ctx, void *cuda_stream);
+
+/* Convenience: alloc + copy + commit.  keys/sdf/weight/rgb may be host or device pointers (auto
+ * detected per pointer); rgb may be NULL (all zero).  Synchronous; the caller may free its
+ * inputs on return. */
+DTSDF_API int dtsdf_upload_volume(dtsdf_ctx *ctx, const dtsdf_volume_params *params, const int32_t *keys, const float *sdf,
+                        const float *weight, const uint8_t *rgb);
+
+/* Render one view.  pose_w_c: world-from-camera 4x4 row-major (host; the bottom row is ignored).
+ * Outputs (all [H][W] row-major, caller-owned):
+ *   out_depth   f32 [H][W]      camera z of the surface, 0 = miss
+ *   out_normal  f32 [H][W][3]   unit world normal, 0 = miss        (may be NULL)
+ *   out_color   u8  [H][W][3]   RGB, 0 = miss                      (may be NULL)
+ *   out_dirmask u8  [H][W]      bit D set iff W_D > 0 at the hit    (may be NULL)
+ * If all non-NULL outputs are device pointers the call is asynchronous on cuda_stream; if they
+ * are host pointers the library renders into its own scratch, copies back and synchronizes. */
+DTSDF_API int dtsdf_render(dtsdf_ctx *ctx, const float pose_w_c[16], const dtsdf_intrinsics *intr, float *out_depth,
+                 float *out_normal, uint8_t *out_color, uint8_t *out_dirmask, void *cuda_stream);
+
+/* Render n_views views with shared intrinsics.  poses_w_c: host [n_views][16].  Only image rows
+ * [row0, row1) are rendered (0 <= row0 < row1 <= height), so one large view can be sharded by
+ * rows across GPUs; outputs are contiguous [n_views][row1-row0][W][...] with the layouts of
+ * dtsdf_render.  Host/device output handling as in dtsdf_render. */
+DTSDF_API int dtsdf_render_batch(dtsdf_ctx *ctx, int32_t n_views, const float *poses_w_c, const dtsdf_intrinsics *intr,
+                       int32_t row0, int32_t row1, float *out_depth, float *out_normal, uint8_t *out_color,
+                       uint8_t *out_dirmask, void *cuda_stream);
+
+/* Current volume: N blocks, U distinct block locations, device bytes held by the context. */
+DTSDF_API int dtsdf_volume_stats(dtsdf_ctx *ctx, int64_t *n_blocks, int64_t *n_locations, int64_t *bytes);
+
+/* Kernel timing (tracing).  While enabled, every range-pass and raycast launch is
+ * bracketed by CUDA events on its stream.  dtsdf_kernel_times synchronizes those events and
+ * returns the summed milliseconds and launch counts since the last reset: times_ms[0] range
+ * pass, [1] raycast, [2] other (index build, memsets); counts[0..2] likewise. */
+DTSDF_API int dtsdf_set_profiling(dtsdf_ctx *ctx, int enable);
+DTSDF_API int dtsdf_kernel_times(dtsdf_ctx *ctx, double times_ms[3], int64_t counts[3]);
+DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
+
+/* Exact accelerations that can be switched off to check they are result-invisible:
+ *   DTSDF_OPT_RANGE_PASS  1 (default) narrow each ray to its tile's [z_near, z_far] from the
+ *                         block-bounds range pass; 0 march every lattice point from z_min to z_max
+ *   DTSDF_OPT_BLOCK_SKIP  1 (default) jump over unallocated block locations; 0 step every point */
+#define DTSDF_OPT_RANGE_PASS 1
+#define DTSDF_OPT_BLOCK_SKIP 2
+DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
+
+/* Kernel launches issued by this context since creation (all kinds). */
+DTSDF_API int64_t dtsdf_launch_count(dtsdf_ctx *ctx);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+DTSDF_API const char *dtsdf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTSDF_H_ */

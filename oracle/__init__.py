@@ -74,7 +74,10 @@ class OracleVolume:
         self._w = np.ascontiguousarray(vol.weight, np.float32)
         self._rgb = np.ascontiguousarray(vol.rgb, np.uint8)
         h = C.c_void_p()
-        rc = lib().oracle_volume_create(vol.voxel_size, vol.truncation, vol.theta, vol.step, vol.n_blocks,
+        # the scalar parameters as the float32 values the C ABI receives (dtsdf_volume_params)
+        f32 = lambda a: float(np.float32(a))  # noqa: E731
+        rc = lib().oracle_volume_create(f32(vol.voxel_size), f32(vol.truncation), f32(vol.theta), f32(vol.step),
+                                        vol.n_blocks,
                                         _ptr(self._keys), _ptr(self._sdf), _ptr(self._w), _ptr(self._rgb),
                                         C.byref(h))
         if rc != 0:

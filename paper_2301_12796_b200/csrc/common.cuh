@@ -1,0 +1,112 @@
+// common.cuh -- device-side data layout shared by the index build (volume.cu) and the
+// raycast (render.cu).  DESIGN.md §5 describes the layout in HBM.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dtsdf {
+
+constexpr int kBlock = 8;          // 8^3 voxel blocks
+constexpr int kVoxPerBlock = 512;
+constexpr int kApron = 11;         // apron brick: voxels -1..9 of the block per axis
+constexpr int kApronVox = kApron * kApron * kApron;  // 1331
+constexpr int kApronStride = 1344;                   // float2 records per brick (10752 B, 128-B aligned)
+constexpr int kRgbApron = 9;                         // colour apron: voxels 0..8 per axis (trilinear corners)
+constexpr int kRgbApronVox = kRgbApron * kRgbApron * kRgbApron;  // 729
+constexpr int kRgbApronStride = 736;                 // uchar4 records per brick (2944 B)
+constexpr int kRangeTile = 8;                        // range-pass tile (pixels)
+constexpr int kViewsPerLaunch = 256;
+constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
+
+// Hash-table entry: one per block location (x,y,z); the six direction slots are block ids
+// (rows of the pool / apron) or -1.  32 B = one sector: one probe returns all directions.
+struct __align__(16) HashEntry {
+  unsigned long long key;
+  int slot[6];
+};
+
+__host__ __device__ __forceinline__ unsigned long long pack_key(int bx, int by, int bz) {
+  const unsigned long long m = (1ull << 21) - 1;
+  return ((unsigned long long)(bx + (1 << 20)) & m) | (((unsigned long long)(by + (1 << 20)) & m) << 21) |
+         (((unsigned long long)(bz + (1 << 20)) & m) << 42);
+}
+
+__host__ __device__ __forceinline__ unsigned int hash_key(unsigned long long k) {
+  // splitmix64 finaliser
+  k ^= k >> 30;
+  k *= 0xbf58476d1ce4e5b9ull;
+  k ^= k >> 27;
+  k *= 0x94d049bb133111ebull;
+  k ^= k >> 31;
+  return (unsigned int)k;
+}
+
+// Device view of a committed volume (read-only during rendering).
+struct VolumeView {
+  const HashEntry *table;
+  unsigned int table_mask;
+  const unsigned int *bitmap;  // occupancy bit per block location over the location AABB
+  int lo_x, lo_y, lo_z;        // AABB origin (block coords)
+  int dim_x, dim_y, dim_z;     // AABB extent (blocks)
+  const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}
+  const uchar4 *rgb_apron;     // [N][kRgbApronStride]
+  float voxel_size, inv_voxel;
+  float theta, inv_blend;      // 1 / (2 theta - pi/2)
+  float delta, inv_delta;
+};
+
+// Per-view camera: world-from-camera rotation (row-major) and camera centre.
+struct ViewPose {
+  float r[9];
+  float t[3];
+};
+
+struct RenderLaunch {
+  VolumeView vol;
+  float fx, fy, cx, cy, z_min, z_max;
+  int width, height, row0, row1;
+  int n_views;
+  int tiles_x, tiles_y;            // range tiles per view
+  int use_range, use_skip;         // exact accelerations (DTSDF_OPT_*)
+  const unsigned int *z_near;      // [n_views][tiles_y][tiles_x] float bits
+  const unsigned int *z_far;
+  float *out_depth;                // [n_views][rows][W]
+  float *out_normal;               // [n_views][rows][W][3] or null
+  unsigned char *out_color;        // [n_views][rows][W][3] or null
+  unsigned char *out_mask;         // [n_views][rows][W] or null
+  ViewPose pose[kViewsPerLaunch];
+};
+
+struct RangeLaunch {
+  VolumeView vol;
+  const int4 *locations;  // [U] (bx,by,bz,-)
+  long long n_locations;
+  float fx, fy, cx, cy, z_min, z_max;
+  int width, height, row0, row1;
+  int n_views;
+  int tiles_x, tiles_y;
+  unsigned int *z_near;
+  unsigned int *z_far;
+  ViewPose pose[kViewsPerLaunch];
+};
+
+// host launchers (render.cu)
+cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
+cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s);
+
+// host launchers (volume.cu); all run on stream s and return the first launch error
+struct CommitScratch {
+  int *flags;          // [0] bad key, [1] duplicate, [2] table full
+  int *aabb;           // [6] min xyz, max xyz
+  unsigned long long *n_loc;
+};
+cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s);
+cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsigned int mask, int4 *locations,
+                          CommitScratch sc, cudaStream_t s);
+cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
+                          int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
+                         const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
+                         cudaStream_t s);
+
+}  // namespace dtsdf

@@ -1,0 +1,506 @@
+// dtsdf_abi.cu -- host side of the C ABI declared in include/dtsdf.h.
+//
+// Argument checking, device memory ownership, index build orchestration (volume.cu) and
+// per-batch launch packing (render.cu).  No C++ exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dtsdf.h"
+#include "common.cuh"
+
+using namespace dtsdf;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+struct TimedLaunch {
+  cudaEvent_t start, stop;
+  int kind;  // 0 range, 1 raycast, 2 other
+};
+
+}  // namespace
+
+struct dtsdf_ctx {
+  int device = 0;
+  bool sticky = false;
+  // current volume
+  dtsdf_volume_params params{};
+  bool allocated = false, committed = false;
+  int32_t *keys = nullptr;
+  float *sdf = nullptr, *weight = nullptr;
+  uint8_t *rgb = nullptr;
+  int64_t n = 0;
+  // index
+  HashEntry *table = nullptr;
+  unsigned int table_cap = 0;
+  unsigned int *bitmap = nullptr;
+  int lo[3] = {0, 0, 0}, dim[3] = {0, 0, 0};
+  int4 *locations = nullptr;
+  int64_t n_loc = 0;
+  float2 *apron = nullptr;
+  uchar4 *rgb_apron = nullptr;
+  size_t index_bytes = 0;
+  // commit scratch
+  int *scratch = nullptr;  // flags[4] + aabb[6] + n_loc(u64)
+  // render scratch
+  unsigned int *z_near = nullptr, *z_far = nullptr;
+  size_t range_cap = 0;  // tiles
+  void *host_stage = nullptr;  // device scratch for host-output renders
+  size_t host_stage_cap = 0;
+  int use_range = 1, use_skip = 1;
+  // tracing
+  bool profiling = false;
+  std::vector<TimedLaunch> timed;
+  double times_ms[3] = {0, 0, 0};
+  int64_t counts[3] = {0, 0, 0};
+  int64_t launches = 0;
+};
+
+namespace {
+
+int cuda_fail(dtsdf_ctx *ctx, cudaError_t e, const char *what) {
+  if (ctx) ctx->sticky = true;
+  return fail(DTSDF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, expr, what)                                \
+  do {                                                     \
+    cudaError_t _e = (expr);                               \
+    if (_e != cudaSuccess) return cuda_fail(ctx, _e, what); \
+  } while (0)
+
+template <typename T>
+void dfree(T *&p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+void free_volume(dtsdf_ctx *c) {
+  dfree(c->keys);
+  dfree(c->sdf);
+  dfree(c->weight);
+  dfree(c->rgb);
+  dfree(c->table);
+  dfree(c->bitmap);
+  dfree(c->locations);
+  dfree(c->apron);
+  dfree(c->rgb_apron);
+  c->allocated = c->committed = false;
+  c->n = c->n_loc = 0;
+  c->index_bytes = 0;
+}
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int check_params(const dtsdf_volume_params *p) {
+  if (!p) return fail(DTSDF_ERR_INVALID_ARGUMENT, "params is NULL");
+  if (!(p->voxel_size > 0.f) || !std::isfinite(p->voxel_size))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "voxel_size must be > 0");
+  if (!(p->truncation >= 2.f * p->voxel_size)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "truncation must be >= 2*voxel_size");
+  const double pi = 3.14159265358979323846;
+  if (!(p->theta > pi / 4) || !(p->theta <= pi / 2 + 1e-6))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "theta must lie in (pi/4, pi/2]");
+  if (!(p->step >= 0.f) || !std::isfinite(p->step)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "step must be >= 0");
+  if (p->n_blocks < 0 || p->n_blocks > (int64_t)INT32_MAX) return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad n_blocks");
+  return DTSDF_OK;
+}
+
+int check_intr(const dtsdf_intrinsics *K) {
+  if (!K) return fail(DTSDF_ERR_INVALID_ARGUMENT, "intrinsics is NULL");
+  if (!(K->fx > 0.f) || !(K->fy > 0.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "fx, fy must be > 0");
+  if (K->width <= 0 || K->height <= 0) return fail(DTSDF_ERR_INVALID_ARGUMENT, "width, height must be > 0");
+  if (!(K->z_min > 0.f) || !(K->z_min < K->z_max) || !std::isfinite(K->z_max))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "need 0 < z_min < z_max");
+  if (!std::isfinite(K->cx) || !std::isfinite(K->cy)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "cx, cy not finite");
+  return DTSDF_OK;
+}
+
+template <typename T>
+cudaError_t dalloc(T *&p, size_t bytes) {
+  return cudaMalloc((void **)&p, std::max<size_t>(bytes, 16));
+}
+
+// kernels: number of this library's kernels the bracketed region launches (memsets: 0)
+void begin_timed(dtsdf_ctx *c, int kind, cudaStream_t s, TimedLaunch *tl, int kernels = 1) {
+  c->launches += kernels;
+  if (!c->profiling) return;
+  tl->kind = kind;
+  cudaEventCreate(&tl->start);
+  cudaEventCreate(&tl->stop);
+  cudaEventRecord(tl->start, s);
+}
+
+void end_timed(dtsdf_ctx *c, cudaStream_t s, TimedLaunch *tl) {
+  if (!c->profiling) return;
+  cudaEventRecord(tl->stop, s);
+  c->timed.push_back(*tl);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dtsdf_last_error(void) { return g_err.c_str(); }
+
+int dtsdf_create(int cuda_device, dtsdf_ctx **out) {
+  if (!out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return fail(DTSDF_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  if (cuda_device < 0 || cuda_device >= n) return fail(DTSDF_ERR_INVALID_ARGUMENT, "no such CUDA device");
+  if ((e = cudaSetDevice(cuda_device)) != cudaSuccess)
+    return fail(DTSDF_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  dtsdf_ctx *c = new (std::nothrow) dtsdf_ctx();
+  if (!c) return fail(DTSDF_ERR_OUT_OF_MEMORY, "host allocation");
+  c->device = cuda_device;
+  if (dalloc(c->scratch, 64) != cudaSuccess) {
+    delete c;
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "scratch allocation");
+  }
+  *out = c;
+  return DTSDF_OK;
+}
+
+int dtsdf_destroy(dtsdf_ctx *c) {
+  if (!c) return DTSDF_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_volume(c);
+  dfree(c->scratch);
+  dfree(c->z_near);
+  dfree(c->z_far);
+  if (c->host_stage) cudaFree(c->host_stage);
+  for (auto &t : c->timed) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  delete c;
+  return DTSDF_OK;
+}
+
+int dtsdf_alloc_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, dtsdf_volume_buffers *out) {
+  if (!c || !out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_params(p);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  free_volume(c);
+  const size_t n = (size_t)p->n_blocks;
+  if (dalloc(c->keys, n * 16) != cudaSuccess || dalloc(c->sdf, n * 512 * 4) != cudaSuccess ||
+      dalloc(c->weight, n * 512 * 4) != cudaSuccess || dalloc(c->rgb, n * 512 * 3) != cudaSuccess) {
+    cudaGetLastError();
+    free_volume(c);
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "volume buffers");
+  }
+  c->params = *p;
+  c->n = (int64_t)n;
+  c->allocated = true;
+  out->keys = c->keys;
+  out->sdf = c->sdf;
+  out->weight = c->weight;
+  out->rgb = c->rgb;
+  return DTSDF_OK;
+}
+
+int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  if (!c->allocated) return fail(DTSDF_ERR_NO_VOLUME, "no allocated volume");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  c->committed = false;
+  dfree(c->table);
+  dfree(c->bitmap);
+  dfree(c->locations);
+  dfree(c->apron);
+  dfree(c->rgb_apron);
+  const long long n = c->n;
+  // scratch: flags[4] | aabb[6] | pad[2] | n_loc (8 B aligned at int offset 12)
+  CommitScratch sc;
+  sc.flags = c->scratch;
+  sc.aabb = c->scratch + 4;
+  sc.n_loc = reinterpret_cast<unsigned long long *>(c->scratch + 12);
+  int init[14] = {0, 0, 0, 0, INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN, 0, 0, 0, 0};
+  CK(c, cudaMemcpyAsync(c->scratch, init, sizeof(init), cudaMemcpyHostToDevice, s), "commit init");
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_validate_aabb(reinterpret_cast<const int4 *>(c->keys), n, sc, s), "validate");
+  end_timed(c, s, &tl);
+  int host[14];
+  CK(c, cudaMemcpyAsync(host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, s), "commit readback");
+  CK(c, cudaStreamSynchronize(s), "commit sync");
+  if (host[0]) return fail(DTSDF_ERR_INVALID_ARGUMENT, "block key with D outside 0..5 or coordinate out of range");
+  // hash table: capacity = next power of two >= 2N (load factor <= 1/2 over locations)
+  unsigned int cap = 64;
+  while ((long long)cap < 2 * n) cap <<= 1;
+  c->table_cap = cap;
+  int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
+  if (n > 0)
+    for (int a = 0; a < 3; ++a) { lo[a] = host[4 + a]; hi[a] = host[7 + a]; }
+  for (int a = 0; a < 3; ++a) { c->lo[a] = lo[a]; c->dim[a] = hi[a] - lo[a] + 1; }
+  const size_t cells = (size_t)c->dim[0] * c->dim[1] * c->dim[2];
+  const size_t bm_words = (cells + 31) / 32;
+  if (dalloc(c->table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
+      dalloc(c->locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
+      dalloc(c->bitmap, bm_words * 4) != cudaSuccess ||
+      dalloc(c->apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
+      dalloc(c->rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
+  }
+  c->index_bytes = (size_t)cap * sizeof(HashEntry) + (size_t)n * sizeof(int4) + bm_words * 4 +
+                   (size_t)n * kApronStride * sizeof(float2) + (size_t)n * kRgbApronStride * sizeof(uchar4);
+  CK(c, cudaMemsetAsync(c->table, 0xFF, (size_t)cap * sizeof(HashEntry), s), "table init");
+  CK(c, cudaMemsetAsync(c->bitmap, 0, bm_words * 4 + 4, s), "bitmap init");
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_insert(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->locations, sc, s), "insert");
+  end_timed(c, s, &tl);
+  CK(c, cudaMemcpyAsync(host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, s), "commit readback");
+  CK(c, cudaStreamSynchronize(s), "commit sync");
+  if (host[1]) return fail(DTSDF_ERR_DUPLICATE_KEY, "duplicate (bx,by,bz,D) block key");
+  if (host[2]) return fail(DTSDF_ERR_OUT_OF_MEMORY, "hash table full");
+  unsigned long long nl;
+  std::memcpy(&nl, &host[12], sizeof(nl));
+  c->n_loc = (int64_t)nl;
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_bitmap(c->locations, c->n_loc, c->bitmap, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s), "bitmap");
+  end_timed(c, s, &tl);
+  begin_timed(c, 2, s, &tl, 2);  // launch_apron issues two kernels
+  CK(c, launch_apron(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
+                     c->apron, c->rgb_apron, s),
+     "apron");
+  end_timed(c, s, &tl);
+  CK(c, cudaStreamSynchronize(s), "commit sync");
+  c->committed = true;
+  return DTSDF_OK;
+}
+
+int dtsdf_upload_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, const int32_t *keys, const float *sdf,
+                        const float *weight, const uint8_t *rgb) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  int rc = check_params(p);
+  if (rc) return rc;
+  if (p->n_blocks > 0 && (!keys || !sdf || !weight))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "keys/sdf/weight must not be NULL");
+  dtsdf_volume_buffers b;
+  if ((rc = dtsdf_alloc_volume(c, p, &b))) return rc;
+  const size_t n = (size_t)p->n_blocks;
+  auto kind = [](const void *ptr) { return is_device_ptr(ptr) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice; };
+  if (n > 0) {
+    CK(c, cudaMemcpy(b.keys, keys, n * 16, kind(keys)), "upload keys");
+    CK(c, cudaMemcpy(b.sdf, sdf, n * 512 * 4, kind(sdf)), "upload sdf");
+    CK(c, cudaMemcpy(b.weight, weight, n * 512 * 4, kind(weight)), "upload weight");
+    if (rgb) CK(c, cudaMemcpy(b.rgb, rgb, n * 512 * 3, kind(rgb)), "upload rgb");
+    else CK(c, cudaMemset(b.rgb, 0, n * 512 * 3), "zero rgb");
+  }
+  return dtsdf_commit_volume(c, nullptr);
+}
+
+static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
+                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, cudaStream_t s) {
+  const int W = K->width;
+  const int rows = row1 - row0;
+  const int tiles_x = (W + kRangeTile - 1) / kRangeTile, tiles_y = (rows + kRangeTile - 1) / kRangeTile;
+  const size_t tiles = (size_t)tiles_x * tiles_y * std::min(n_views, kViewsPerLaunch);
+  if (tiles > c->range_cap) {
+    dfree(c->z_near);
+    dfree(c->z_far);
+    c->range_cap = 0;
+    if (dalloc(c->z_near, tiles * 4) != cudaSuccess || dalloc(c->z_far, tiles * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "range buffers");
+    }
+    c->range_cap = tiles;
+  }
+  VolumeView V;
+  V.table = c->table;
+  V.table_mask = c->table_cap - 1;
+  V.bitmap = c->bitmap;
+  V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
+  V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];
+  V.apron = c->apron;
+  V.rgb_apron = c->rgb_apron;
+  V.voxel_size = c->params.voxel_size;
+  V.inv_voxel = 1.0f / c->params.voxel_size;
+  V.theta = c->params.theta;
+  V.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
+  V.delta = c->params.step > 0.f ? c->params.step : c->params.voxel_size;
+  V.inv_delta = 1.0f / V.delta;
+  static thread_local RangeLaunch rl;
+  static thread_local RenderLaunch pl;
+  for (int v0 = 0; v0 < n_views; v0 += kViewsPerLaunch) {
+    const int nv = std::min(kViewsPerLaunch, n_views - v0);
+    rl.vol = V;
+    rl.locations = c->locations;
+    rl.n_locations = c->n_loc;
+    rl.fx = K->fx; rl.fy = K->fy; rl.cx = K->cx; rl.cy = K->cy; rl.z_min = K->z_min; rl.z_max = K->z_max;
+    rl.width = W; rl.height = K->height; rl.row0 = row0; rl.row1 = row1;
+    rl.n_views = nv; rl.tiles_x = tiles_x; rl.tiles_y = tiles_y;
+    rl.z_near = c->z_near; rl.z_far = c->z_far;
+    for (int i = 0; i < nv; ++i) {
+      const float *T = poses + 16 * (size_t)(v0 + i);
+      for (int a = 0; a < 3; ++a) {
+        for (int b = 0; b < 3; ++b) rl.pose[i].r[3 * a + b] = T[4 * a + b];
+        rl.pose[i].t[a] = T[4 * a + 3];
+      }
+    }
+    const size_t vt = (size_t)tiles_x * tiles_y * nv;
+    TimedLaunch tl{};
+    begin_timed(c, 2, s, &tl, 0);
+    CK(c, cudaMemsetAsync(c->z_near, 0x7F, vt * 4, s), "range init");  // 0x7F7F7F7F = 3.4e38
+    CK(c, cudaMemsetAsync(c->z_far, 0x00, vt * 4, s), "range init");
+    end_timed(c, s, &tl);
+    begin_timed(c, 0, s, &tl, c->n_loc > 0 ? 1 : 0);
+    CK(c, launch_range(rl, s), "range pass");
+    end_timed(c, s, &tl);
+    pl.vol = V;
+    pl.fx = K->fx; pl.fy = K->fy; pl.cx = K->cx; pl.cy = K->cy; pl.z_min = K->z_min; pl.z_max = K->z_max;
+    pl.width = W; pl.height = K->height; pl.row0 = row0; pl.row1 = row1;
+    pl.n_views = nv; pl.tiles_x = tiles_x; pl.tiles_y = tiles_y;
+    pl.use_range = c->use_range; pl.use_skip = c->use_skip;
+    pl.z_near = c->z_near; pl.z_far = c->z_far;
+    const size_t px = (size_t)v0 * rows * W;
+    pl.out_depth = depth + px;
+    pl.out_normal = normal ? normal + 3 * px : nullptr;
+    pl.out_color = color ? color + 3 * px : nullptr;
+    pl.out_mask = mask ? mask + px : nullptr;
+    std::memcpy(pl.pose, rl.pose, sizeof(ViewPose) * nv);
+    begin_timed(c, 1, s, &tl);
+    CK(c, launch_raycast(pl, s), "raycast");
+    end_timed(c, s, &tl);
+  }
+  return DTSDF_OK;
+}
+
+int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
+                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, void *stream) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  if (n_views < 1) return fail(DTSDF_ERR_INVALID_ARGUMENT, "n_views must be >= 1");
+  if (!poses || !depth) return fail(DTSDF_ERR_INVALID_ARGUMENT, "poses/out_depth is NULL");
+  if (row0 < 0 || row1 > K->height || row0 >= row1) return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad row range");
+  for (int64_t i = 0; i < 16 * (int64_t)n_views; ++i)
+    if (!std::isfinite(poses[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
+  if (!c->committed) return fail(DTSDF_ERR_NO_VOLUME, "no committed volume");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool dev = is_device_ptr(depth);
+  if ((normal && is_device_ptr(normal) != dev) || (color && is_device_ptr(color) != dev) ||
+      (mask && is_device_ptr(mask) != dev))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "outputs must be all device or all host pointers");
+  if (dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s);
+  // host outputs: render into device scratch, copy back, synchronize
+  const size_t px = (size_t)n_views * (row1 - row0) * K->width;
+  const size_t need = px * (4 + 12 + 3 + 1) + 64;
+  if (need > c->host_stage_cap) {
+    if (c->host_stage) cudaFree(c->host_stage);
+    c->host_stage = nullptr;
+    c->host_stage_cap = 0;
+    if (cudaMalloc(&c->host_stage, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "host-output staging");
+    }
+    c->host_stage_cap = need;
+  }
+  char *base = (char *)c->host_stage;
+  float *dd = (float *)base;
+  float *dn = normal ? (float *)(base + px * 4) : nullptr;
+  uint8_t *dc = color ? (uint8_t *)(base + px * 16) : nullptr;
+  uint8_t *dm = mask ? (uint8_t *)(base + px * 19) : nullptr;
+  rc = render_impl(c, n_views, poses, K, row0, row1, dd, dn, dc, dm, s);
+  if (rc) return rc;
+  CK(c, cudaMemcpyAsync(depth, dd, px * 4, cudaMemcpyDeviceToHost, s), "d2h depth");
+  if (normal) CK(c, cudaMemcpyAsync(normal, dn, px * 12, cudaMemcpyDeviceToHost, s), "d2h normal");
+  if (color) CK(c, cudaMemcpyAsync(color, dc, px * 3, cudaMemcpyDeviceToHost, s), "d2h color");
+  if (mask) CK(c, cudaMemcpyAsync(mask, dm, px, cudaMemcpyDeviceToHost, s), "d2h mask");
+  CK(c, cudaStreamSynchronize(s), "render sync");
+  return DTSDF_OK;
+}
+
+int dtsdf_render(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float *depth, float *normal,
+                 uint8_t *color, uint8_t *mask, void *stream) {
+  if (!K) return fail(DTSDF_ERR_INVALID_ARGUMENT, "intrinsics is NULL");
+  return dtsdf_render_batch(c, 1, pose, K, 0, K->height, depth, normal, color, mask, stream);
+}
+
+int dtsdf_volume_stats(dtsdf_ctx *c, int64_t *n_blocks, int64_t *n_locations, int64_t *bytes) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (n_blocks) *n_blocks = c->n;
+  if (n_locations) *n_locations = c->n_loc;
+  if (bytes) *bytes = (int64_t)(c->n * (16 + 512 * 11) + c->index_bytes);
+  return DTSDF_OK;
+}
+
+int dtsdf_set_profiling(dtsdf_ctx *c, int enable) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  c->profiling = enable != 0;
+  return DTSDF_OK;
+}
+
+int dtsdf_kernel_times(dtsdf_ctx *c, double times_ms[3], int64_t counts[3]) {
+  if (!c || !times_ms || !counts) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  for (auto &t : c->timed) {
+    cudaError_t e = cudaEventSynchronize(t.stop);
+    if (e != cudaSuccess) return cuda_fail(c, e, "event sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.start, t.stop);
+    c->times_ms[t.kind] += ms;
+    c->counts[t.kind] += 1;
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  c->timed.clear();
+  for (int i = 0; i < 3; ++i) {
+    times_ms[i] = c->times_ms[i];
+    counts[i] = c->counts[i];
+  }
+  return DTSDF_OK;
+}
+
+int dtsdf_reset_kernel_times(dtsdf_ctx *c) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  double t[3];
+  int64_t n[3];
+  int rc = dtsdf_kernel_times(c, t, n);
+  for (int i = 0; i < 3; ++i) {
+    c->times_ms[i] = 0;
+    c->counts[i] = 0;
+  }
+  return rc;
+}
+
+int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (option == DTSDF_OPT_RANGE_PASS) c->use_range = value ? 1 : 0;
+  else if (option == DTSDF_OPT_BLOCK_SKIP) c->use_skip = value ? 1 : 0;
+  else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
+  return DTSDF_OK;
+}
+
+int64_t dtsdf_launch_count(dtsdf_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"

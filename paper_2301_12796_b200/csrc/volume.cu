@@ -1,0 +1,170 @@
+// volume.cu -- index build for a committed volume.
+//
+//   validate + AABB     one thread per block: D in 0..5, coordinates in range, AABB min/max
+//   insert              one thread per block: open-addressing insert of the location key
+//                       (64-bit CAS, linear probing), then CAS of the direction slot; a slot
+//                       already taken means a duplicate (x,y,z,D) key
+//   bitmap              one thread per location: occupancy bit over the location AABB
+//   apron               one thread per apron voxel: each (location, D) brick gets the voxels
+//                       -1..9 of its block per axis gathered from up to 27 neighbouring blocks
+//                       of the same direction, NaN sdf where that neighbour is unallocated --
+//                       so one brick serves a whole sample (8 trilinear corners + 24 gradient
+//                       stencil voxels) with a single index lookup
+//
+// Slot placement in the table depends on insertion order; lookups do not.
+#include "common.cuh"
+
+namespace dtsdf {
+
+__global__ void k_validate_aabb(const int4 *__restrict__ keys, long long n, int *flags, int *aabb) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 k = keys[i];
+  const int lim = 1 << 20;
+  if (k.w < 0 || k.w > 5 || k.x < -lim || k.x >= lim || k.y < -lim || k.y >= lim || k.z < -lim || k.z >= lim) {
+    atomicExch(&flags[0], 1);
+    return;
+  }
+  atomicMin(&aabb[0], k.x);
+  atomicMin(&aabb[1], k.y);
+  atomicMin(&aabb[2], k.z);
+  atomicMax(&aabb[3], k.x);
+  atomicMax(&aabb[4], k.y);
+  atomicMax(&aabb[5], k.z);
+}
+
+__device__ __forceinline__ int find_entry(const HashEntry *__restrict__ table, unsigned int mask,
+                                          unsigned long long key) {
+  unsigned int h = hash_key(key) & mask;
+  for (unsigned int probe = 0; probe <= mask; ++probe) {
+    unsigned long long k = table[h].key;
+    if (k == key) return (int)h;
+    if (k == kEmptyKey) return -1;
+    h = (h + 1) & mask;
+  }
+  return -1;
+}
+
+__global__ void k_insert(const int4 *__restrict__ keys, long long n, HashEntry *table, unsigned int mask,
+                         int4 *locations, int *flags, unsigned long long *n_loc) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 k = keys[i];
+  unsigned long long key = pack_key(k.x, k.y, k.z);
+  unsigned int h = hash_key(key) & mask;
+  for (unsigned int probe = 0; probe <= mask; ++probe) {
+    unsigned long long prev = atomicCAS(&table[h].key, kEmptyKey, key);
+    if (prev == kEmptyKey) {  // claimed a new location
+      unsigned long long u = atomicAdd(n_loc, 1ull);
+      locations[u] = make_int4(k.x, k.y, k.z, (int)h);
+    }
+    if (prev == kEmptyKey || prev == key) {
+      int old = atomicCAS(&table[h].slot[k.w], -1, (int)i);
+      if (old != -1) atomicExch(&flags[1], 1);
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+  atomicExch(&flags[2], 1);
+}
+
+__global__ void k_bitmap(const int4 *__restrict__ loc, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y,
+                         int lo_z, int dim_x, int dim_y) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_loc) return;
+  int4 b = loc[i];
+  long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
+  atomicOr(&bitmap[cell >> 5], 1u << (cell & 31));
+}
+
+// One thread per (brick, apron voxel).  Apron voxel a in [0,11)^3 is block-local voxel a-1.
+__global__ void k_apron(const int4 *__restrict__ keys, long long n, const HashEntry *__restrict__ table,
+                        unsigned int mask, const float *__restrict__ sdf, const float *__restrict__ weight,
+                        float2 *__restrict__ apron) {
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long b = gid / kApronStride;
+  int a = (int)(gid - b * kApronStride);
+  if (b >= n) return;
+  float2 out = make_float2(__int_as_float(0x7fc00000), 0.0f);  // NaN sdf = unallocated
+  if (a < kApronVox) {
+    int4 k = keys[b];
+    int ax = a % kApron, ay = (a / kApron) % kApron, az = a / (kApron * kApron);
+    int lx = ax - 1, ly = ay - 1, lz = az - 1;  // -1..9
+    int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
+    int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
+    int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
+    int src = (int)b;
+    if (ox | oy | oz) {
+      int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
+      src = (e >= 0) ? table[e].slot[k.w] : -1;
+    }
+    if (src >= 0) {
+      int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+      long long r = (long long)src * kVoxPerBlock + l;
+      out = make_float2(sdf[r], weight[r]);
+    }
+  } else {
+    out = make_float2(__int_as_float(0x7fc00000), 0.0f);
+  }
+  apron[gid] = out;
+}
+
+__global__ void k_rgb_apron(const int4 *__restrict__ keys, long long n, const HashEntry *__restrict__ table,
+                            unsigned int mask, const unsigned char *__restrict__ rgb, uchar4 *__restrict__ rgb_apron) {
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long b = gid / kRgbApronStride;
+  int a = (int)(gid - b * kRgbApronStride);
+  if (b >= n) return;
+  uchar4 out = make_uchar4(0, 0, 0, 0);
+  if (a < kRgbApronVox && rgb != nullptr) {
+    int4 k = keys[b];
+    int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
+    int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
+    int src = (int)b;
+    if (ox | oy | oz) {
+      int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
+      src = (e >= 0) ? table[e].slot[k.w] : -1;
+    }
+    if (src >= 0) {
+      int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+      const unsigned char *c = rgb + 3 * ((long long)src * kVoxPerBlock + l);
+      out = make_uchar4(c[0], c[1], c[2], 0);
+    }
+  }
+  rgb_apron[gid] = out;
+}
+
+static inline unsigned int grid_for(long long n, int threads) { return (unsigned int)((n + threads - 1) / threads); }
+
+cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_validate_aabb<<<grid_for(n, 256), 256, 0, s>>>(keys, n, sc.flags, sc.aabb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsigned int mask, int4 *locations,
+                          CommitScratch sc, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_insert<<<grid_for(n, 256), 256, 0, s>>>(keys, n, table, mask, locations, sc.flags, sc.n_loc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
+                          int dim_x, int dim_y, cudaStream_t s) {
+  if (n_loc == 0) return cudaSuccess;
+  k_bitmap<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, bitmap, lo_x, lo_y, lo_z, dim_x, dim_y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
+                         const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
+                         cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_apron<<<grid_for(n * kApronStride, 256), 256, 0, s>>>(keys, n, table, mask, sdf, weight, apron);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_rgb_apron<<<grid_for(n * kRgbApronStride, 256), 256, 0, s>>>(keys, n, table, mask, rgb, rgb_apron);
+  return cudaGetLastError();
+}
+
+}  // namespace dtsdf

@@ -1,0 +1,225 @@
+"""Thin ctypes binding of libdtsdf.so (include/dtsdf.h) -- argument marshalling only.
+
+Every step of the render runs in the CUDA kernels of ``csrc/``; this module passes torch
+tensors' device pointers, host structs and the current CUDA stream.  There is no CPU
+fallback: if ``libdtsdf.so`` is missing or no CUDA device is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdtsdf.so")
+
+OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR = 0, -1, -2, -3, -4, -5
+VIEWS_PER_LAUNCH = 256
+
+EXPORTS = [
+    "dtsdf_create", "dtsdf_destroy", "dtsdf_alloc_volume", "dtsdf_commit_volume", "dtsdf_upload_volume",
+    "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
+    "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
+]
+OPT_RANGE_PASS, OPT_BLOCK_SKIP = 1, 2
+
+
+class DtsdfError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dtsdf error {code}: {msg}")
+        self.code = code
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32),
+                ("height", C.c_int32), ("z_min", C.c_float), ("z_max", C.c_float)]
+
+
+class VolumeParams(C.Structure):
+    _fields_ = [("voxel_size", C.c_float), ("truncation", C.c_float), ("theta", C.c_float), ("step", C.c_float),
+                ("n_blocks", C.c_int64)]
+
+
+class VolumeBuffers(C.Structure):
+    _fields_ = [("keys", C.c_void_p), ("sdf", C.c_void_p), ("weight", C.c_void_p), ("rgb", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdtsdf.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2301_12796_b200.build` "
+                              "or __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
+        L.dtsdf_create.argtypes = [C.c_int, C.POINTER(P)]
+        L.dtsdf_destroy.argtypes = [P]
+        L.dtsdf_alloc_volume.argtypes = [P, C.POINTER(VolumeParams), C.POINTER(VolumeBuffers)]
+        L.dtsdf_commit_volume.argtypes = [P, P]
+        L.dtsdf_upload_volume.argtypes = [P, C.POINTER(VolumeParams), P, P, P, P]
+        L.dtsdf_render.argtypes = [P, P, C.POINTER(Intrinsics), P, P, P, P, P]
+        L.dtsdf_render_batch.argtypes = [P, I32, P, C.POINTER(Intrinsics), I32, I32, P, P, P, P, P]
+        L.dtsdf_volume_stats.argtypes = [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]
+        L.dtsdf_set_profiling.argtypes = [P, C.c_int]
+        L.dtsdf_kernel_times.argtypes = [P, P, P]
+        L.dtsdf_reset_kernel_times.argtypes = [P]
+        L.dtsdf_set_option.argtypes = [P, C.c_int, C.c_int]
+        L.dtsdf_launch_count.argtypes = [P]
+        L.dtsdf_launch_count.restype = I64
+        L.dtsdf_last_error.argtypes = []
+        L.dtsdf_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != OK:
+        raise DtsdfError(rc, lib().dtsdf_last_error().decode())
+
+
+def _ptr(x) -> Optional[int]:
+    """Device/host address of a torch tensor or numpy array (None passes NULL)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return x.data_ptr()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return x.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def make_intrinsics(K) -> Intrinsics:
+    """From any object with fx fy cx cy width height z_min z_max."""
+    return Intrinsics(K.fx, K.fy, K.cx, K.cy, int(K.width), int(K.height), K.z_min, K.z_max)
+
+
+class Renderer:
+    """One libdtsdf context on one CUDA device."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().dtsdf_create(int(device), C.byref(self._h)))
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().dtsdf_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- volume -------------------------------------------------------------------------
+    def upload(self, voxel_size, truncation, theta, keys, sdf, weight, rgb=None, step=0.0):
+        """dtsdf_upload_volume: arrays may be numpy (host) or torch tensors (host or device)."""
+        n = int(keys.shape[0])
+        p = VolumeParams(voxel_size, truncation, theta, step, n)
+        _check(lib().dtsdf_upload_volume(self._h, C.byref(p), _ptr(keys), _ptr(sdf), _ptr(weight), _ptr(rgb)))
+
+    def upload_volume(self, vol):
+        """Upload a scenes.BlockVolume (host arrays)."""
+        self.upload(vol.voxel_size, vol.truncation, vol.theta, vol.keys, vol.sdf, vol.weight, vol.rgb, vol.step)
+
+    def alloc(self, voxel_size, truncation, theta, n_blocks, step=0.0):
+        """dtsdf_alloc_volume: returns torch tensors aliasing the library-owned device buffers."""
+        import torch
+        p = VolumeParams(voxel_size, truncation, theta, step, int(n_blocks))
+        b = VolumeBuffers()
+        _check(lib().dtsdf_alloc_volume(self._h, C.byref(p), C.byref(b)))
+        return {"keys": _wrap_device(b.keys, (n_blocks, 4), torch.int32, self.device),
+                "sdf": _wrap_device(b.sdf, (n_blocks, 512), torch.float32, self.device),
+                "weight": _wrap_device(b.weight, (n_blocks, 512), torch.float32, self.device),
+                "rgb": _wrap_device(b.rgb, (n_blocks, 512, 3), torch.uint8, self.device)}
+
+    def commit(self, stream=None):
+        _check(lib().dtsdf_commit_volume(self._h, _stream_ptr(stream)))
+
+    def stats(self):
+        n, u, b = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().dtsdf_volume_stats(self._h, C.byref(n), C.byref(u), C.byref(b)))
+        return {"n_blocks": n.value, "n_locations": u.value, "bytes": b.value}
+
+    # -- render -------------------------------------------------------------------------
+    def render_into(self, poses, K, depth, normal=None, color=None, mask=None, row0=0, row1=None, stream=None):
+        """dtsdf_render_batch into caller-owned outputs (all device tensors -> async on the stream;
+        all host arrays/tensors -> synchronous)."""
+        poses = np.ascontiguousarray(np.asarray(poses, np.float32).reshape(-1, 16))
+        row1 = K.height if row1 is None else row1
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_render_batch(self._h, poses.shape[0], poses.ctypes.data, C.byref(k), int(row0), int(row1),
+                                        _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask), _stream_ptr(stream)))
+
+    def render(self, poses, K, row0=0, row1=None, stream=None, outputs=("normal", "color", "mask")):
+        """Allocate device outputs and render; returns dict of torch tensors [V, rows, W, ...]."""
+        import torch
+        poses = np.asarray(poses, np.float32).reshape(-1, 4, 4)
+        row1 = K.height if row1 is None else row1
+        V, rows, W = poses.shape[0], row1 - row0, K.width
+        dev = torch.device("cuda", self.device)
+        out = {"depth": torch.empty((V, rows, W), dtype=torch.float32, device=dev)}
+        if "normal" in outputs:
+            out["normal"] = torch.empty((V, rows, W, 3), dtype=torch.float32, device=dev)
+        if "color" in outputs:
+            out["color"] = torch.empty((V, rows, W, 3), dtype=torch.uint8, device=dev)
+        if "mask" in outputs:
+            out["mask"] = torch.empty((V, rows, W), dtype=torch.uint8, device=dev)
+        self.render_into(poses, K, out["depth"], out.get("normal"), out.get("color"), out.get("mask"), row0, row1,
+                         stream)
+        return out
+
+    # -- tracing ------------------------------------------------------------------------
+    def set_profiling(self, enable: bool):
+        _check(lib().dtsdf_set_profiling(self._h, int(bool(enable))))
+
+    def kernel_times(self):
+        t = np.zeros(3, np.float64)
+        n = np.zeros(3, np.int64)
+        _check(lib().dtsdf_kernel_times(self._h, t.ctypes.data, n.ctypes.data))
+        return {"range_ms": t[0], "raycast_ms": t[1], "other_ms": t[2], "range_launches": int(n[0]),
+                "raycast_launches": int(n[1]), "other_launches": int(n[2])}
+
+    def reset_kernel_times(self):
+        _check(lib().dtsdf_reset_kernel_times(self._h))
+
+    def set_option(self, option: int, value: int):
+        _check(lib().dtsdf_set_option(self._h, int(option), int(value)))
+
+    def launch_count(self) -> int:
+        return int(lib().dtsdf_launch_count(self._h))
+
+
+def _wrap_device(ptr, shape, dtype, device):
+    """A torch tensor view of library-owned device memory (no copy, no ownership)."""
+    import torch
+    nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+    if nbytes == 0:
+        return torch.empty(shape, dtype=dtype, device=f"cuda:{device}")
+    # __cuda_array_interface__ lets torch alias external device memory without taking ownership
+    typestr = {torch.int32: "<i4", torch.float32: "<f4", torch.uint8: "|u1"}[dtype]
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                    "version": 3, "strides": None}
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(), device=f"cuda:{device}")
