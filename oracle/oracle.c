@@ -18,8 +18,10 @@
  *                   data has a gradient, w_noGrad = w_D <v^D,-r> (eq:combine_tsdf_weight,
  *                   PAPER.md:265-270); f = sum W phi / sum W
  *   O4 crossing     first valid + -> valid - lattice pair
- *   O5 refinement   60 bisection steps in the bracket (reading R5/R21)
- *   O6-O8           depth = camera z, normal, colour, direction mask; zeros on a miss
+ *   O5 refinement   60 bisection steps in the bracket, or until it reaches the fp64
+ *                   resolution of t (reading R5/R21)
+ *   O6-O8           depth = camera z of the root; normal, colour, direction mask from the sample
+ *                   at the final bracket end b (reading R32); zeros on a miss
  *
  * Brute force: every lattice point from zmin to zmax is evaluated; there is no range pass,
  * no block skipping and no hash -- the volume is a dense per-direction block-index grid.
@@ -365,8 +367,9 @@ static void render_pixel(ojob *J, int u, int vrow, int64_t out) {
     if (s.valid && prev_valid && prev_f > 0.0 && s.f <= 0.0) {
       /* O5: bisection in [t_{k-1}, t_k]; invalid midpoints count as positive (R21) */
       double a = t - v->delta, b = t;
-      for (int it = 0; it < 60 && b - a >= 1e-9; ++it) {
+      for (int it = 0; it < 60; ++it) {
         double m = 0.5 * (a + b);
+        if (!(m > a && m < b)) break; /* bracket at the fp64 resolution of t */
         double xm[3] = {o[0] + m * r[0], o[1] + m * r[1], o[2] + m * r[2]};
         osample sm;
         eval_sample(v, xm, r, &sm);
@@ -374,13 +377,11 @@ static void render_pixel(ojob *J, int u, int vrow, int64_t out) {
       }
       double ts = 0.5 * (a + b);
       J->depth[out] = ts / L; /* O6 */
-      double xs[3] = {o[0] + ts * r[0], o[1] + ts * r[1], o[2] + ts * r[2]};
+      /* O7 (reading R32): shade at the final bracket end b -- a valid sample with f <= 0 at the
+       * root to fp64 resolution, always on the surface side of a jump of F at the root */
+      double xb[3] = {o[0] + b * r[0], o[1] + b * r[1], o[2] + b * r[2]};
       osample ss;
-      eval_sample(v, xs, r, &ss);
-      if (!ss.valid) { /* O7: fall back to the b end of the bracket */
-        double xb[3] = {o[0] + b * r[0], o[1] + b * r[1], o[2] + b * r[2]};
-        eval_sample(v, xb, r, &ss);
-      }
+      eval_sample(v, xb, r, &ss);
       shade(v, &ss, &J->normal[3 * out], &J->color[3 * out], &J->mask[out]);
       break;
     }

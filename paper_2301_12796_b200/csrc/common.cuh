@@ -68,6 +68,7 @@ struct RenderLaunch {
   int n_views;
   int tiles_x, tiles_y;            // range tiles per view
   int use_range, use_skip;         // exact accelerations (DTSDF_OPT_*)
+  int n_bisect;                    // bisection steps: bracket Delta -> <= 5e-5 m
   const unsigned int *z_near;      // [n_views][tiles_y][tiles_x] float bits
   const unsigned int *z_far;
   float *out_depth;                // [n_views][rows][W]

@@ -264,7 +264,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   const size_t bm_words = (cells + 31) / 32;
   if (dalloc(c->table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
       dalloc(c->locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
-      dalloc(c->bitmap, bm_words * 4) != cudaSuccess ||
+      dalloc(c->bitmap, (bm_words + 1) * 4) != cudaSuccess ||
       dalloc(c->apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
       dalloc(c->rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
     cudaGetLastError();
@@ -273,7 +273,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   c->index_bytes = (size_t)cap * sizeof(HashEntry) + (size_t)n * sizeof(int4) + bm_words * 4 +
                    (size_t)n * kApronStride * sizeof(float2) + (size_t)n * kRgbApronStride * sizeof(uchar4);
   CK(c, cudaMemsetAsync(c->table, 0xFF, (size_t)cap * sizeof(HashEntry), s), "table init");
-  CK(c, cudaMemsetAsync(c->bitmap, 0, bm_words * 4 + 4, s), "bitmap init");
+  CK(c, cudaMemsetAsync(c->bitmap, 0, (bm_words + 1) * 4, s), "bitmap init");
   begin_timed(c, 2, s, &tl);
   CK(c, launch_insert(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->locations, sc, s), "insert");
   end_timed(c, s, &tl);
@@ -380,6 +380,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.width = W; pl.height = K->height; pl.row0 = row0; pl.row1 = row1;
     pl.n_views = nv; pl.tiles_x = tiles_x; pl.tiles_y = tiles_y;
     pl.use_range = c->use_range; pl.use_skip = c->use_skip;
+    pl.n_bisect = 0;
+    while (V.delta / (float)(1 << pl.n_bisect) > 5e-5f && pl.n_bisect < 20) ++pl.n_bisect;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
     const size_t px = (size_t)v0 * rows * W;
     pl.out_depth = depth + px;

@@ -289,6 +289,34 @@ __device__ __forceinline__ SampleResult eval_at(const VolumeView &V, Cursor &cur
   return eval_sample<SHADE>(V, cur.slots, ix & 7, iy & 7, iz & 7, gx - flx, gy - fly, gz - flz, r[0], r[1], r[2], sh);
 }
 
+// Same as eval_at, but the sample position x = o + t r and its cell/fractions are computed in
+// fp64 (refinement and shading only): near a root the combination weights can vary on a
+// sub-micrometre scale (ill-conditioned mixtures of directions, e.g. configs[2]), so the shading
+// point must be located to ~1e-9 m, finer than an fp32 coordinate can resolve.
+template <bool SHADE>
+__device__ __forceinline__ SampleResult eval_at_d(const VolumeView &V, Cursor &cur, double t, const double o[3],
+                                                  const double r[3], const float rf[3], ShadeResult *sh) {
+  const double inv_s = 1.0 / (double)V.voxel_size;
+  const double gx = fma(t, r[0], o[0]) * inv_s, gy = fma(t, r[1], o[1]) * inv_s, gz = fma(t, r[2], o[2]) * inv_s;
+  const double flx = floor(gx), fly = floor(gy), flz = floor(gz);
+  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
+  const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
+  if (bx != cur.bx || by != cur.by || bz != cur.bz) {
+    cur.bx = bx; cur.by = by; cur.bz = bz;
+    cur.occ = occupied(V, bx, by, bz);
+    if (cur.occ) lookup_slots(V, bx, by, bz, cur.slots);
+  }
+  if (!cur.occ) {
+    SampleResult s;
+    s.valid = false;
+    s.f = 0.f;
+    if (SHADE) { sh->S = 0.f; sh->mask = 0; }
+    return s;
+  }
+  return eval_sample<SHADE>(V, cur.slots, ix & 7, iy & 7, iz & 7, (float)(gx - flx), (float)(gy - fly),
+                            (float)(gz - flz), rf[0], rf[1], rf[2], sh);
+}
+
 __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RenderLaunch p) {
   const int view = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -356,36 +384,58 @@ __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RenderL
       continue;
     }
     if (s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f) {
-      // a6: refine the root in [t_{k-1}, t_k] (Illinois regula falsi; invalid -> positive, R21)
-      float a = t - V.delta, b = t, fa = prev_f, fb = s.f;
-      int side = 0;
-      bool bisect = false;
-      float tstar = 0.5f * (a + b);
-      for (int it = 0; it < 8; ++it) {
-        float m = bisect ? 0.5f * (a + b) : b - fb * (b - a) / (fb - fa);
-        if (!(m > a && m < b)) m = 0.5f * (a + b);
-        bool occm;
-        const SampleResult sm = eval_at<false>(V, cur, m, o, r, nullptr, &occm);
-        tstar = m;
-        if (!sm.valid) {
+      // a6: refine the root in [t_{k-1}, t_k] with fp64 ray positions.  Phase 1: bisection
+      // with the oracle's decisions (an invalid midpoint counts as positive, R21) until the
+      // bracket is <= 5e-5 m, so it keeps the oracle's root when F has several sign changes
+      // (reading R20).  Phase 2: Illinois regula falsi inside it until b sits on the root.
+      double od[3], rd[3];
+      {
+        const double ddx = ((double)u - (double)p.cx) / (double)p.fx, ddy = ((double)v - (double)p.cy) / (double)p.fy;
+        const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0);
+        for (int q = 0; q < 3; ++q) {
+          rd[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
+          od[q] = (double)P.t[q];
+        }
+      }
+      const double dd = (double)V.delta;
+      double a = (double)(k - 1) * dd, b = (double)k * dd;
+      float fa = prev_f, fb = s.f;
+      bool fa_valid = true;
+      for (int it = 0; it < p.n_bisect; ++it) {
+        const double m = 0.5 * (a + b);
+        const SampleResult sm = eval_at_d<false>(V, cur, m, od, rd, r, nullptr);
+        if (!sm.valid || sm.f > 0.0f) {
           a = m;
-          bisect = true;
-        } else if (sm.f > 0.0f) {
-          a = m; fa = sm.f; bisect = false;
+          fa = sm.f;
+          fa_valid = sm.valid;
+        } else {
+          b = m;
+          fb = sm.f;
+        }
+      }
+      int side = 0;
+      for (int it = 0; it < 12 && b - a > 1e-12; ++it) {
+        double m = (fa_valid && fa > fb) ? a + (double)(fa / (fa - fb)) * (b - a) : 0.5 * (a + b);
+        if (!(m > a && m < b)) m = 0.5 * (a + b);
+        const SampleResult sm = eval_at_d<false>(V, cur, m, od, rd, r, nullptr);
+        if (!sm.valid || sm.f > 0.0f) {
+          a = m;
+          fa = sm.f;
+          fa_valid = sm.valid;
           if (side == 1) fb *= 0.5f;
           side = 1;
         } else {
-          b = m; fb = sm.f;
+          b = m;
+          fb = sm.f;
           if (side == -1) fa *= 0.5f;
           side = -1;
+          if (sm.f > -1e-7f) break;  // b sits on the root
         }
-        if (sm.valid && fabsf(sm.f) < 1e-6f) break;
-        if (b - a < 2e-6f) { tstar = 0.5f * (a + b); break; }
       }
-      // a7: shading at the root (or at the b end if the root sample is invalid, O7)
+      const float tstar = (float)b;
+      // a7: shading at the bracket end b, a valid sample on the surface side (reading R32)
       ShadeResult sh;
-      SampleResult ss = eval_at<true>(V, cur, tstar, o, r, &sh, &occ);
-      if (!ss.valid) ss = eval_at<true>(V, cur, b, o, r, &sh, &occ);
+      eval_at_d<true>(V, cur, b, od, rd, r, &sh);
       hit = true;
       depth = tstar * iL;
       const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
