@@ -46,12 +46,16 @@ struct VolumeView {
   const HashEntry *table;
   unsigned int table_mask;
   const unsigned int *bitmap;  // occupancy bit per block location over the location AABB
+  const unsigned int *surface; // same layout: 1 iff some direction has a corner voxel with sdf <= 0
+  const unsigned int *cell_pos;  // [table_cap][16]: bit l of location entry h = base cell l is
+                                 // "certainly positive": every present direction's 8 corners > 0
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
   int dim_x, dim_y, dim_z;     // AABB extent (blocks)
   const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}
   const uchar4 *rgb_apron;     // [N][kRgbApronStride]
   float voxel_size, inv_voxel;
   float theta, inv_blend;      // 1 / (2 theta - pi/2)
+  float cos_theta, sin_theta;  // membership band edges: w_dir = 0 below cos(theta), 1 above sin(theta)
   float delta, inv_delta;
 };
 
@@ -106,6 +110,10 @@ cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsig
                           CommitScratch sc, cudaStream_t s);
 cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
                           int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
+                            unsigned int *cell_pos, cudaStream_t s);
+cudaError_t launch_surface(const int4 *keys, long long n, const float2 *apron, unsigned int *surface, int lo_x,
+                           int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                          const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
                          cudaStream_t s);

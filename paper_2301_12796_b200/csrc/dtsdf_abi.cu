@@ -45,7 +45,7 @@ struct dtsdf_ctx {
   // index
   HashEntry *table = nullptr;
   unsigned int table_cap = 0;
-  unsigned int *bitmap = nullptr;
+  unsigned int *bitmap = nullptr, *surface = nullptr, *cell_pos = nullptr;
   int lo[3] = {0, 0, 0}, dim[3] = {0, 0, 0};
   int4 *locations = nullptr;
   int64_t n_loc = 0;
@@ -94,6 +94,8 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->rgb);
   dfree(c->table);
   dfree(c->bitmap);
+  dfree(c->surface);
+  dfree(c->cell_pos);
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
@@ -233,6 +235,8 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   c->committed = false;
   dfree(c->table);
   dfree(c->bitmap);
+  dfree(c->surface);
+  dfree(c->cell_pos);
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
@@ -264,16 +268,18 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   const size_t bm_words = (cells + 31) / 32;
   if (dalloc(c->table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
       dalloc(c->locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
-      dalloc(c->bitmap, (bm_words + 1) * 4) != cudaSuccess ||
+      dalloc(c->bitmap, (bm_words + 1) * 4) != cudaSuccess || dalloc(c->surface, (bm_words + 1) * 4) != cudaSuccess ||
+      dalloc(c->cell_pos, (size_t)cap * 64) != cudaSuccess ||
       dalloc(c->apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
       dalloc(c->rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
   }
-  c->index_bytes = (size_t)cap * sizeof(HashEntry) + (size_t)n * sizeof(int4) + bm_words * 4 +
+  c->index_bytes = (size_t)cap * (sizeof(HashEntry) + 64) + (size_t)n * sizeof(int4) + 2 * bm_words * 4 +
                    (size_t)n * kApronStride * sizeof(float2) + (size_t)n * kRgbApronStride * sizeof(uchar4);
   CK(c, cudaMemsetAsync(c->table, 0xFF, (size_t)cap * sizeof(HashEntry), s), "table init");
   CK(c, cudaMemsetAsync(c->bitmap, 0, (bm_words + 1) * 4, s), "bitmap init");
+  CK(c, cudaMemsetAsync(c->surface, 0, (bm_words + 1) * 4, s), "surface init");
   begin_timed(c, 2, s, &tl);
   CK(c, launch_insert(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->locations, sc, s), "insert");
   end_timed(c, s, &tl);
@@ -291,6 +297,14 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   CK(c, launch_apron(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
                      c->apron, c->rgb_apron, s),
      "apron");
+  end_timed(c, s, &tl);
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_surface(reinterpret_cast<const int4 *>(c->keys), n, c->apron, c->surface, lo[0], lo[1], lo[2],
+                       c->dim[0], c->dim[1], s),
+     "surface");
+  end_timed(c, s, &tl);
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->apron, c->cell_pos, s), "cell_pos");
   end_timed(c, s, &tl);
   CK(c, cudaStreamSynchronize(s), "commit sync");
   c->committed = true;
@@ -338,6 +352,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.table = c->table;
   V.table_mask = c->table_cap - 1;
   V.bitmap = c->bitmap;
+  V.surface = c->surface;
+  V.cell_pos = c->cell_pos;
   V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
   V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];
   V.apron = c->apron;
@@ -345,6 +361,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.voxel_size = c->params.voxel_size;
   V.inv_voxel = 1.0f / c->params.voxel_size;
   V.theta = c->params.theta;
+  V.cos_theta = cosf(c->params.theta);
+  V.sin_theta = sinf(c->params.theta);
   V.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
   V.delta = c->params.step > 0.f ? c->params.step : c->params.voxel_size;
   V.inv_delta = 1.0f / V.delta;

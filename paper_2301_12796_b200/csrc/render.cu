@@ -16,6 +16,10 @@
 
 #include "common.cuh"
 
+#ifndef DTSDF_RAYCAST_MINB
+#define DTSDF_RAYCAST_MINB 2
+#endif
+
 namespace dtsdf {
 
 // ------------------------------------------------------------------------------------------
@@ -94,14 +98,16 @@ __global__ void __launch_bounds__(256) k_range(const __grid_constant__ RangeLaun
 // ------------------------------------------------------------------------------------------
 // a2: index lookup
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ bool occupied(const VolumeView &V, int bx, int by, int bz) {
+__device__ __forceinline__ bool occupied(const VolumeView &V, int bx, int by, int bz, bool *surf) {
   const unsigned x = (unsigned)(bx - V.lo_x), y = (unsigned)(by - V.lo_y), z = (unsigned)(bz - V.lo_z);
+  *surf = false;
   if (x >= (unsigned)V.dim_x || y >= (unsigned)V.dim_y || z >= (unsigned)V.dim_z) return false;
   const unsigned long long cell = ((unsigned long long)z * V.dim_y + y) * V.dim_x + x;
+  *surf = (__ldg(&V.surface[cell >> 5]) >> (cell & 31)) & 1u;
   return (__ldg(&V.bitmap[cell >> 5]) >> (cell & 31)) & 1u;
 }
 
-__device__ __forceinline__ void lookup_slots(const VolumeView &V, int bx, int by, int bz, int slots[6]) {
+__device__ __forceinline__ int lookup_slots(const VolumeView &V, int bx, int by, int bz, int slots[6]) {
   const unsigned long long key = pack_key(bx, by, bz);
   unsigned int h = hash_key(key) & V.table_mask;
   for (unsigned int probe = 0; probe <= V.table_mask; ++probe) {
@@ -111,13 +117,14 @@ __device__ __forceinline__ void lookup_slots(const VolumeView &V, int bx, int by
     if (k == key) {
       const int4 c = __ldg(e + 1);
       slots[0] = a.z; slots[1] = a.w; slots[2] = c.x; slots[3] = c.y; slots[4] = c.z; slots[5] = c.w;
-      return;
+      return (int)h;
     }
     if (k == kEmptyKey) break;
     h = (h + 1) & V.table_mask;
   }
 #pragma unroll
   for (int d = 0; d < 6; ++d) slots[d] = -1;
+  return -1;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -141,25 +148,58 @@ __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(
 #define RGB_IDX(dx, dy, dz) ((dx) + kRgbApron * (dy) + kRgbApron * kRgbApron * (dz))
 
 // eq:direction_weight with reading R1: clamp((theta - acos c) / (2 theta - pi/2), 0, 1)
+// (outside the blend band the clamp decides: c <= cos(theta) -> 0, c >= sin(theta) -> 1)
 __device__ __forceinline__ float w_dir(float c, const VolumeView &V) {
-  const float a = acosf(fminf(fmaxf(c, -1.0f), 1.0f));
+  if (c <= V.cos_theta) return 0.0f;
+  if (c >= V.sin_theta) return 1.0f;
+  const float a = acosf(fminf(c, 1.0f));
   return fminf(fmaxf((V.theta - a) * V.inv_blend, 0.0f), 1.0f);
 }
 
-template <bool SHADE>
-__device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const int slots[6], int lx, int ly, int lz,
-                                                    float fx, float fy, float fz, float rx, float ry, float rz,
-                                                    ShadeResult *sh) {
+struct Cursor {
+  int bx, by, bz;
+  bool occ;      // location allocated in some direction (occupancy bitmap)
+  bool surf;     // some corner-range voxel has sdf <= 0 (surface bitmap)
+  int present;   // bit D: direction D has a brick at this location
+  int entry;     // hash entry index (row of cell_pos), -1 if unallocated
+  int slots[6];
+};
+
+// cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (k_cell_pos)
+__device__ __forceinline__ bool cell_positive(const VolumeView &V, const Cursor &cur, int l) {
+  return (__ldg(&V.cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;
+}
+
+__device__ __forceinline__ int pick6(const int s[6], int d) {
+  // register-resident select (a dynamic index would spill the array to local memory)
+  int v = s[0];
+  v = d == 1 ? s[1] : v;
+  v = d == 2 ? s[2] : v;
+  v = d == 3 ? s[3] : v;
+  v = d == 4 ? s[4] : v;
+  v = d == 5 ? s[5] : v;
+  return v;
+}
+
+// F(x, r) of DESIGN.md §2 O3 for the sample at base voxel (block-local l, fractions f) of the
+// current cursor location; with shade = true also the shading sums of O7.  One instance of this
+// body is compiled (runtime direction loop) to keep the kernel inside the instruction cache.
+__device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const Cursor &cur, int lx, int ly, int lz,
+                                                 float fx, float fy, float fz, float rx, float ry, float rz,
+                                                 bool shade, ShadeResult *sh) {
   float S1 = 0.f, F1 = 0.f, S2 = 0.f, F2 = 0.f;
   bool any_grad = false;
-  float N1[3] = {0.f, 0.f, 0.f}, N2[3] = {0.f, 0.f, 0.f}, C1[3] = {0.f, 0.f, 0.f}, C2[3] = {0.f, 0.f, 0.f};
+  float N1x = 0.f, N1y = 0.f, N1z = 0.f, N2x = 0.f, N2y = 0.f, N2z = 0.f;
+  float C1r = 0.f, C1g = 0.f, C1b = 0.f, C2r = 0.f, C2g = 0.f, C2b = 0.f;
   int m1 = 0, m2 = 0;
   const float half_inv_s = 0.5f * V.inv_voxel;
   const int off = lx + kApron * ly + kApron * kApron * lz;
-#pragma unroll
-  for (int D = 0; D < 6; ++D) {
-    const int slot = slots[D];
-    if (slot < 0) continue;
+  int present = cur.present;
+#pragma unroll 1
+  while (present) {
+    const int D = __ffs(present) - 1;
+    present &= present - 1;
+    const int slot = pick6(cur.slots, D);
     const float2 *br = V.apron + (size_t)slot * kApronStride + off;
     // O3(a) trilinear phi_D, omega_D over the 8 cell corners
     const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
@@ -169,32 +209,34 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const i
     const float w00 = lerpf(c000.y, c100.y, fx), w10 = lerpf(c010.y, c110.y, fx);
     const float w01 = lerpf(c001.y, c101.y, fx), w11 = lerpf(c011.y, c111.y, fx);
     const float omega = lerpf(lerpf(w00, w10, fy), lerpf(w01, w11, fy), fz);
-    // x-columns of the cell corners: P(dx) = bilinear over (y, z)
-    const float P0 = lerpf(lerpf(c000.x, c010.x, fy), lerpf(c001.x, c011.x, fy), fz);
-    const float P1 = lerpf(lerpf(c100.x, c110.x, fy), lerpf(c101.x, c111.x, fy), fz);
-    const float phi = lerpf(P0, P1, fx);
+    // x-lerps of the four corner rows e_yz; R(dz) = bilinear over (x, y) of slab dz
+    const float e00 = lerpf(c000.x, c100.x, fx), e10 = lerpf(c010.x, c110.x, fx);
+    const float e01 = lerpf(c001.x, c101.x, fx), e11 = lerpf(c011.x, c111.x, fx);
+    const float R0 = lerpf(e00, e10, fy), R1 = lerpf(e01, e11, fy);
+    const float phi = lerpf(R0, R1, fz);
     if (isnan(phi)) continue;       // D absent: a corner lies in an unallocated block
     if (!(omega > 0.0f)) continue;  // D holds no data at x (reading R8)
-    // O3(c) central differences of trilinear phi at x +- s e_a (24 further stencil voxels)
+    // O3(c) central differences of trilinear phi at x +- s e_a (24 further stencil voxels):
+    // phi(x + s e_a) - phi(x - s e_a) = (1 - f_a)(A1 - A-1) + f_a (A2 - A0) with A(d) the
+    // bilinear interpolant of the stencil layer d along axis a
+    const float P0 = lerpf(lerpf(c000.x, c010.x, fy), lerpf(c001.x, c011.x, fy), fz);
+    const float P1 = lerpf(lerpf(c100.x, c110.x, fy), lerpf(c101.x, c111.x, fy), fz);
+    const float Q0 = lerpf(e00, e01, fz), Q1 = lerpf(e10, e11, fz);
     const float Pm = lerpf(lerpf(__ldg(&br[APRON_IDX(-1, 0, 0)].x), __ldg(&br[APRON_IDX(-1, 1, 0)].x), fy),
                            lerpf(__ldg(&br[APRON_IDX(-1, 0, 1)].x), __ldg(&br[APRON_IDX(-1, 1, 1)].x), fy), fz);
     const float Pp = lerpf(lerpf(__ldg(&br[APRON_IDX(2, 0, 0)].x), __ldg(&br[APRON_IDX(2, 1, 0)].x), fy),
                            lerpf(__ldg(&br[APRON_IDX(2, 0, 1)].x), __ldg(&br[APRON_IDX(2, 1, 1)].x), fy), fz);
-    const float Q0 = lerpf(lerpf(c000.x, c100.x, fx), lerpf(c001.x, c101.x, fx), fz);
-    const float Q1 = lerpf(lerpf(c010.x, c110.x, fx), lerpf(c011.x, c111.x, fx), fz);
     const float Qm = lerpf(lerpf(__ldg(&br[APRON_IDX(0, -1, 0)].x), __ldg(&br[APRON_IDX(1, -1, 0)].x), fx),
                            lerpf(__ldg(&br[APRON_IDX(0, -1, 1)].x), __ldg(&br[APRON_IDX(1, -1, 1)].x), fx), fz);
     const float Qp = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 2, 0)].x), __ldg(&br[APRON_IDX(1, 2, 0)].x), fx),
                            lerpf(__ldg(&br[APRON_IDX(0, 2, 1)].x), __ldg(&br[APRON_IDX(1, 2, 1)].x), fx), fz);
-    const float R0 = lerpf(lerpf(c000.x, c100.x, fx), lerpf(c010.x, c110.x, fx), fy);
-    const float R1 = lerpf(lerpf(c001.x, c101.x, fx), lerpf(c011.x, c111.x, fx), fy);
     const float Rm = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 0, -1)].x), __ldg(&br[APRON_IDX(1, 0, -1)].x), fx),
                            lerpf(__ldg(&br[APRON_IDX(0, 1, -1)].x), __ldg(&br[APRON_IDX(1, 1, -1)].x), fx), fy);
     const float Rp = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 0, 2)].x), __ldg(&br[APRON_IDX(1, 0, 2)].x), fx),
                            lerpf(__ldg(&br[APRON_IDX(0, 1, 2)].x), __ldg(&br[APRON_IDX(1, 1, 2)].x), fx), fy);
-    const float gx = (lerpf(P1, Pp, fx) - lerpf(Pm, P0, fx)) * half_inv_s;
-    const float gy = (lerpf(Q1, Qp, fy) - lerpf(Qm, Q0, fy)) * half_inv_s;
-    const float gz = (lerpf(R1, Rp, fz) - lerpf(Rm, R0, fz)) * half_inv_s;
+    const float gx = lerpf(P1 - Pm, Pp - P0, fx) * half_inv_s;
+    const float gy = lerpf(Q1 - Qm, Qp - Q0, fy) * half_inv_s;
+    const float gz = lerpf(R1 - Rm, Rp - R0, fz) * half_inv_s;
     const float gn = sqrtf(gx * gx + gy * gy + gz * gz);
     // v^D = sign * e_axis
     const int axis = D >> 1;
@@ -216,7 +258,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const i
       S1 += W1;
       F1 = fmaf(W1, phi, F1);
     }
-    if (SHADE) {
+    if (shade) {
       const uchar4 *cb = V.rgb_apron + (size_t)slot * kRgbApronStride + (lx + kRgbApron * ly + kRgbApron * kRgbApron * lz);
       const uchar4 q000 = cb[RGB_IDX(0, 0, 0)], q100 = cb[RGB_IDX(1, 0, 0)], q010 = cb[RGB_IDX(0, 1, 0)],
                    q110 = cb[RGB_IDX(1, 1, 0)], q001 = cb[RGB_IDX(0, 0, 1)], q101 = cb[RGB_IDX(1, 0, 1)],
@@ -227,15 +269,14 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const i
       const float cr = TRI_CH(x), cg = TRI_CH(y), cbl = TRI_CH(z);
 #undef TRI_CH
       if (W1 > 0.0f) {
-        N1[0] = fmaf(W1, nx, N1[0]); N1[1] = fmaf(W1, ny, N1[1]); N1[2] = fmaf(W1, nz, N1[2]);
-        C1[0] = fmaf(W1, cr, C1[0]); C1[1] = fmaf(W1, cg, C1[1]); C1[2] = fmaf(W1, cbl, C1[2]);
+        N1x = fmaf(W1, nx, N1x); N1y = fmaf(W1, ny, N1y); N1z = fmaf(W1, nz, N1z);
+        C1r = fmaf(W1, cr, C1r); C1g = fmaf(W1, cg, C1g); C1b = fmaf(W1, cbl, C1b);
         m1 |= 1 << D;
       }
       if (W2 > 0.0f) {
-        if (axis == 0) N2[0] = fmaf(W2, sign, N2[0]);
-        else if (axis == 1) N2[1] = fmaf(W2, sign, N2[1]);
-        else N2[2] = fmaf(W2, sign, N2[2]);
-        C2[0] = fmaf(W2, cr, C2[0]); C2[1] = fmaf(W2, cg, C2[1]); C2[2] = fmaf(W2, cbl, C2[2]);
+        const float ws = W2 * sign;
+        N2x += axis == 0 ? ws : 0.f; N2y += axis == 1 ? ws : 0.f; N2z += axis == 2 ? ws : 0.f;
+        C2r = fmaf(W2, cr, C2r); C2g = fmaf(W2, cg, C2g); C2b = fmaf(W2, cbl, C2b);
         m2 |= 1 << D;
       }
     }
@@ -246,78 +287,22 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const i
   SampleResult res;
   res.valid = S > 0.0f;
   res.f = res.valid ? F / S : 0.0f;
-  if (SHADE) {
-    const float *N = any_grad ? N1 : N2;
-    const float *Cc = any_grad ? C1 : C2;
+  if (shade) {
     sh->S = S;
     sh->mask = any_grad ? m1 : m2;
-    for (int a = 0; a < 3; ++a) { sh->n[a] = N[a]; sh->c[a] = Cc[a]; }
+    sh->n[0] = any_grad ? N1x : N2x; sh->n[1] = any_grad ? N1y : N2y; sh->n[2] = any_grad ? N1z : N2z;
+    sh->c[0] = any_grad ? C1r : C2r; sh->c[1] = any_grad ? C1g : C2g; sh->c[2] = any_grad ? C1b : C2b;
   }
   return res;
 }
 
 // ------------------------------------------------------------------------------------------
-// a4-a7: the raycast kernel
+// a4-a7: the raycast kernel, one state machine per ray so that a warp's rays -- marching,
+// bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
-struct Cursor {
-  int bx, by, bz;
-  bool occ;
-  int slots[6];
-};
+enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
 
-template <bool SHADE>
-__device__ __forceinline__ SampleResult eval_at(const VolumeView &V, Cursor &cur, float t, const float o[3],
-                                                const float r[3], ShadeResult *sh, bool *in_occupied) {
-  const float x = fmaf(t, r[0], o[0]), y = fmaf(t, r[1], o[1]), z = fmaf(t, r[2], o[2]);
-  const float gx = x * V.inv_voxel, gy = y * V.inv_voxel, gz = z * V.inv_voxel;
-  const float flx = floorf(gx), fly = floorf(gy), flz = floorf(gz);
-  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
-  const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
-  if (bx != cur.bx || by != cur.by || bz != cur.bz) {
-    cur.bx = bx; cur.by = by; cur.bz = bz;
-    cur.occ = occupied(V, bx, by, bz);
-    if (cur.occ) lookup_slots(V, bx, by, bz, cur.slots);
-  }
-  *in_occupied = cur.occ;
-  if (!cur.occ) {
-    SampleResult s;
-    s.valid = false;
-    s.f = 0.f;
-    if (SHADE) { sh->S = 0.f; sh->mask = 0; }
-    return s;
-  }
-  return eval_sample<SHADE>(V, cur.slots, ix & 7, iy & 7, iz & 7, gx - flx, gy - fly, gz - flz, r[0], r[1], r[2], sh);
-}
-
-// Same as eval_at, but the sample position x = o + t r and its cell/fractions are computed in
-// fp64 (refinement and shading only): near a root the combination weights can vary on a
-// sub-micrometre scale (ill-conditioned mixtures of directions, e.g. configs[2]), so the shading
-// point must be located to ~1e-9 m, finer than an fp32 coordinate can resolve.
-template <bool SHADE>
-__device__ __forceinline__ SampleResult eval_at_d(const VolumeView &V, Cursor &cur, double t, const double o[3],
-                                                  const double r[3], const float rf[3], ShadeResult *sh) {
-  const double inv_s = 1.0 / (double)V.voxel_size;
-  const double gx = fma(t, r[0], o[0]) * inv_s, gy = fma(t, r[1], o[1]) * inv_s, gz = fma(t, r[2], o[2]) * inv_s;
-  const double flx = floor(gx), fly = floor(gy), flz = floor(gz);
-  const int ix = (int)flx, iy = (int)fly, iz = (int)flz;
-  const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
-  if (bx != cur.bx || by != cur.by || bz != cur.bz) {
-    cur.bx = bx; cur.by = by; cur.bz = bz;
-    cur.occ = occupied(V, bx, by, bz);
-    if (cur.occ) lookup_slots(V, bx, by, bz, cur.slots);
-  }
-  if (!cur.occ) {
-    SampleResult s;
-    s.valid = false;
-    s.f = 0.f;
-    if (SHADE) { sh->S = 0.f; sh->mask = 0; }
-    return s;
-  }
-  return eval_sample<SHADE>(V, cur.slots, ix & 7, iy & 7, iz & 7, (float)(gx - flx), (float)(gy - fly),
-                            (float)(gz - flz), rf[0], rf[1], rf[2], sh);
-}
-
-__global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RenderLaunch p) {
+__global__ void __launch_bounds__(256, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
   const int view = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
@@ -326,133 +311,226 @@ __global__ void __launch_bounds__(256) k_raycast(const __grid_constant__ RenderL
   if (u >= p.width || v >= p.row1) return;
   const VolumeView &V = p.vol;
   const ViewPose &P = p.pose[view];
-  // O1 ray (eq:reprojection)
-  const float dx = (u - p.cx) / p.fx, dy = (v - p.cy) / p.fy;
-  const float L = sqrtf(dx * dx + dy * dy + 1.0f);
-  const float iL = 1.0f / L;
-  float r[3], o[3];
-  for (int a = 0; a < 3; ++a) {
-    r[a] = (P.r[3 * a] * dx + P.r[3 * a + 1] * dy + P.r[3 * a + 2]) * iL;
-    o[a] = P.t[a];
+  // O1 ray (eq:reprojection) in fp64: sample positions are formed in fp64 so that
+  // refinement can locate the shading point to ~1e-9 m (reading R32); the combination itself
+  // runs in fp32 on cell-local fractions
+  double od[3], rd[3];
+  float r[3];
+  double L;
+  {
+    const double ddx = ((double)u - (double)p.cx) / (double)p.fx, ddy = ((double)v - (double)p.cy) / (double)p.fy;
+    L = sqrt(ddx * ddx + ddy * ddy + 1.0);
+    const double iLd = 1.0 / L;
+    for (int q = 0; q < 3; ++q) {
+      rd[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
+      od[q] = (double)P.t[q];
+      r[q] = (float)rd[q];
+    }
   }
   const int rows = p.row1 - p.row0;
   const size_t pix = ((size_t)view * rows + vrel) * p.width + u;
   // O2 lattice bounds, narrowed to the tile's block range (a3)
+  const float Lf = (float)L;
   const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
   const float zn = __uint_as_float(__ldg(&p.z_near[tile])), zf = __uint_as_float(__ldg(&p.z_far[tile]));
-  const int kmin = (int)ceilf(p.z_min * L * V.inv_delta), kmax = (int)floorf(p.z_max * L * V.inv_delta);
+  const int kmin = (int)ceilf(p.z_min * Lf * V.inv_delta), kmax = (int)floorf(p.z_max * Lf * V.inv_delta);
   int k = kmin, k1 = kmax;
-  if (!p.use_range) {
-    // march every lattice point from z_min to z_max
-  } else if (zn <= zf) {
-    k = max(kmin, (int)floorf(zn * (1.0f - 1e-4f) * L * V.inv_delta));
-    k1 = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * L * V.inv_delta) + 1);
-  } else {
-    k1 = k - 1;  // no allocated block projects onto this tile
+  if (p.use_range) {
+    if (zn <= zf) {
+      k = max(kmin, (int)floorf(zn * (1.0f - 1e-4f) * Lf * V.inv_delta));
+      k1 = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * Lf * V.inv_delta) + 1);
+    } else {
+      k1 = k - 1;  // no allocated block projects onto this tile
+    }
   }
-  float inv_r[3];
-  for (int a = 0; a < 3; ++a) inv_r[a] = 1.0f / r[a];
+  const double dd = (double)V.delta, idd = 1.0 / dd, inv_s = 1.0 / (double)V.voxel_size;
+  double ird[3];
+  for (int q = 0; q < 3; ++q) ird[q] = 1.0 / rd[q];
+  const double bsz = (double)kBlock * (double)V.voxel_size;
   Cursor cur;
-  cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false;
+  cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
+#pragma unroll
+  for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
+  int mode = kMarch;
   bool prev_valid = false;
   float prev_f = 0.0f;
+  // refinement state: bracket [a, b] with f(a) > 0 (or invalid), f(b) <= 0
+  double a = 0.0, b = 0.0, t = (double)k * dd;
+  float fa = 0.f, fb = 0.f;
+  bool fa_valid = true;
+  int it = 0, side = 0;
   bool hit = false;
-  float depth = 0.f, nrm[3] = {0.f, 0.f, 0.f};
-  int col[3] = {0, 0, 0}, mask = 0;
-  const float bsz = kBlock * V.voxel_size;
-  while (k <= k1) {
-    const float t = (float)k * V.delta;
-    bool occ;
-    const SampleResult s = eval_at<false>(V, cur, t, o, r, nullptr, &occ);
-    if (!occ && !p.use_skip) {
-      prev_valid = false;
-      ++k;
-      continue;
+  ShadeResult sh;
+#ifdef DTSDF_STATS
+  int st_march = 0, st_refine = 0, st_skip = 0;
+#endif
+  // cell of the current sample and the cursor over its block location
+  double gx = 0, gy = 0, gz = 0, flx = 0, fly = 0, flz = 0;
+  int ix = 0, iy = 0, iz = 0;
+  auto locate = [&](double tt) {
+    gx = fma(tt, rd[0], od[0]) * inv_s;
+    gy = fma(tt, rd[1], od[1]) * inv_s;
+    gz = fma(tt, rd[2], od[2]) * inv_s;
+    flx = floor(gx); fly = floor(gy); flz = floor(gz);
+    ix = (int)flx; iy = (int)fly; iz = (int)flz;
+    const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
+    if (bx != cur.bx || by != cur.by || bz != cur.bz) {
+      cur.bx = bx; cur.by = by; cur.bz = bz;
+      cur.occ = occupied(V, bx, by, bz, &cur.surf);
+      cur.present = 0;
+      cur.entry = -1;
+      if (cur.occ) {
+        cur.entry = lookup_slots(V, bx, by, bz, cur.slots);
+#pragma unroll
+        for (int d = 0; d < 6; ++d) cur.present |= (cur.slots[d] >= 0) << d;
+      }
     }
-    if (!occ) {
-      // a4: skip the rest of this unallocated block location (exact: every lattice point
-      // there is invalid); land on the first lattice point at or before the block exit
-      float texit = CUDART_INF_F;
-      const int bb[3] = {cur.bx, cur.by, cur.bz};
-      for (int a = 0; a < 3; ++a) {
-        if (r[a] > 0.f) texit = fminf(texit, ((bb[a] + 1) * bsz - o[a]) * inv_r[a]);
-        else if (r[a] < 0.f) texit = fminf(texit, (bb[a] * bsz - o[a]) * inv_r[a]);
-      }
-      const float kn = floorf(texit * V.inv_delta);
-      k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);
-      prev_valid = false;
-      continue;
+  };
+  auto block_exit = [&]() {
+    double texit = 1e300;
+    const int bb[3] = {cur.bx, cur.by, cur.bz};
+    for (int q = 0; q < 3; ++q) {
+      if (rd[q] > 0.0) texit = fmin(texit, ((bb[q] + 1) * bsz - od[q]) * ird[q]);
+      else if (rd[q] < 0.0) texit = fmin(texit, (bb[q] * bsz - od[q]) * ird[q]);
     }
-    if (s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f) {
-      // a6: refine the root in [t_{k-1}, t_k] with fp64 ray positions.  Phase 1: bisection
-      // with the oracle's decisions (an invalid midpoint counts as positive, R21) until the
-      // bracket is <= 5e-5 m, so it keeps the oracle's root when F has several sign changes
-      // (reading R20).  Phase 2: Illinois regula falsi inside it until b sits on the root.
-      double od[3], rd[3];
-      {
-        const double ddx = ((double)u - (double)p.cx) / (double)p.fx, ddy = ((double)v - (double)p.cy) / (double)p.fy;
-        const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0);
-        for (int q = 0; q < 3; ++q) {
-          rd[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
-          od[q] = (double)P.t[q];
+    return texit;
+  };
+  for (;;) {
+    if (mode == kMarch) {
+      // a4: advance to the next lattice point that needs an evaluation.  Every step skipped here
+      // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
+      // location without an sdf <= 0 corner, and in a certainly-positive cell followed by
+      // another, no crossing can end or start.  Lanes of a warp run this cheap loop, then all
+      // evaluate together below.
+      bool found = false;
+      while (k <= k1) {
+        t = (double)k * dd;
+        locate(t);
+        if (!cur.occ) {
+          prev_valid = false;
+#ifdef DTSDF_STATS
+          ++st_skip;
+#endif
+          if (p.use_skip) {  // land on the first lattice point at or before the block exit
+            const double kn = floor(block_exit() * idd);
+            k = (kn > (double)k1) ? k1 + 1 : max(k + 1, (int)kn);
+          } else {
+            ++k;
+          }
+          continue;
         }
-      }
-      const double dd = (double)V.delta;
-      double a = (double)(k - 1) * dd, b = (double)k * dd;
-      float fa = prev_f, fb = s.f;
-      bool fa_valid = true;
-      for (int it = 0; it < p.n_bisect; ++it) {
-        const double m = 0.5 * (a + b);
-        const SampleResult sm = eval_at_d<false>(V, cur, m, od, rd, r, nullptr);
-        if (!sm.valid || sm.f > 0.0f) {
-          a = m;
-          fa = sm.f;
-          fa_valid = sm.valid;
-        } else {
-          b = m;
-          fb = sm.f;
+        if (p.use_skip && !cur.surf) {
+          // jump to (at most) the location's second-to-last lattice point: the point evaluated
+          // there becomes prev for the first point of the next location
+          const double kj = ceil(block_exit() * idd) - 2.0;
+          if (kj > (double)k) {
+#ifdef DTSDF_STATS
+            ++st_skip;
+#endif
+            k = (kj > (double)k1) ? k1 + 1 : (int)kj;
+            prev_valid = false;
+            continue;
+          }
         }
-      }
-      int side = 0;
-      for (int it = 0; it < 12 && b - a > 1e-12; ++it) {
-        double m = (fa_valid && fa > fb) ? a + (double)(fa / (fa - fb)) * (b - a) : 0.5 * (a + b);
-        if (!(m > a && m < b)) m = 0.5 * (a + b);
-        const SampleResult sm = eval_at_d<false>(V, cur, m, od, rd, r, nullptr);
-        if (!sm.valid || sm.f > 0.0f) {
-          a = m;
-          fa = sm.f;
-          fa_valid = sm.valid;
-          if (side == 1) fb *= 0.5f;
-          side = 1;
-        } else {
-          b = m;
-          fb = sm.f;
-          if (side == -1) fa *= 0.5f;
-          side = -1;
-          if (sm.f > -1e-7f) break;  // b sits on the root
+        if (p.use_skip && cell_positive(V, cur, (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7))) {
+          const double t2 = t + dd;
+          const int jx = (int)floor(fma(t2, rd[0], od[0]) * inv_s), jy = (int)floor(fma(t2, rd[1], od[1]) * inv_s),
+                    jz = (int)floor(fma(t2, rd[2], od[2]) * inv_s);
+          if ((jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz &&
+              cell_positive(V, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7))) {
+#ifdef DTSDF_STATS
+            ++st_skip;
+#endif
+            prev_valid = false;
+            ++k;
+            continue;
+          }
         }
+        found = true;
+        break;
       }
-      const float tstar = (float)b;
-      // a7: shading at the bracket end b, a valid sample on the surface side (reading R32)
-      ShadeResult sh;
-      eval_at_d<true>(V, cur, b, od, rd, r, &sh);
+      if (!found) break;  // no crossing: a miss
+    } else {
+      locate(t);
+    }
+#ifdef DTSDF_STATS
+    if (mode == kMarch) ++st_march;
+    else ++st_refine;
+#endif
+    SampleResult s;
+    if (cur.occ) {
+      s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, (float)(gx - flx), (float)(gy - fly), (float)(gz - flz), r[0],
+                      r[1], r[2], mode == kShade, &sh);
+    } else {
+      s.valid = false;
+      s.f = 0.f;
+    }
+    if (mode == kMarch) {
+      if (s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f) {
+        // a6: bracket [t_{k-1}, t_k].  Phase 1: bisection with the oracle's decisions (an
+        // invalid midpoint counts as positive, R21) until the bracket is <= 5e-5 m, so it
+        // keeps the oracle's root when F has several sign changes (reading R20).
+        a = (double)(k - 1) * dd;
+        b = t;
+        fa = prev_f;
+        fb = s.f;
+        fa_valid = true;
+        it = 0;
+        side = 0;
+        mode = p.n_bisect > 0 ? kBisect : kIllinois;
+      } else {
+        prev_valid = s.valid;
+        prev_f = s.f;
+        ++k;
+        t = (double)k * dd;
+        continue;
+      }
+    } else if (mode == kBisect) {
+      if (!s.valid || s.f > 0.0f) { a = t; fa = s.f; fa_valid = s.valid; }
+      else { b = t; fb = s.f; }
+      if (++it >= p.n_bisect) { mode = kIllinois; it = 0; }
+    } else if (mode == kIllinois) {
+      // Phase 2: Illinois regula falsi inside the narrowed bracket until b sits on the root
+      if (!s.valid || s.f > 0.0f) {
+        a = t; fa = s.f; fa_valid = s.valid;
+        if (side == 1) fb *= 0.5f;
+        side = 1;
+      } else {
+        b = t; fb = s.f;
+        if (side == -1) fa *= 0.5f;
+        side = -1;
+        if (s.f > -1e-7f) mode = kShade;  // b sits on the root
+      }
+      if (++it >= 12 || b - a <= 1e-12) mode = kShade;
+    } else {  // kShade: a7 done at b, a valid sample on the surface side (reading R32)
       hit = true;
-      depth = tstar * iL;
-      const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
-      const float inn = nn > 0.f ? 1.0f / nn : 0.f;
-      for (int q = 0; q < 3; ++q) {
-        nrm[q] = sh.n[q] * inn;
-        const float c = sh.S > 0.f ? floorf(sh.c[q] / sh.S + 0.5f) : 0.f;  // reading R13
-        col[q] = (int)fminf(fmaxf(c, 0.f), 255.f);
-      }
-      mask = sh.mask;
       break;
     }
-    prev_valid = s.valid;
-    prev_f = s.f;
-    ++k;
+    // next position
+    if (mode == kBisect) t = 0.5 * (a + b);
+    else if (mode == kIllinois) {
+      double m = (fa_valid && fa > fb) ? a + (double)(fa / (fa - fb)) * (b - a) : 0.5 * (a + b);
+      if (!(m > a && m < b)) m = 0.5 * (a + b);
+      t = m;
+    } else t = b;  // kShade
   }
-  p.out_depth[pix] = hit ? depth : 0.0f;
+  float depth = 0.f, nrm[3] = {0.f, 0.f, 0.f};
+  int col[3] = {0, 0, 0}, mask = 0;
+  if (hit) {
+    depth = (float)(b / L);
+    const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
+    const float inn = nn > 0.f ? 1.0f / nn : 0.f;
+    for (int q = 0; q < 3; ++q) {
+      nrm[q] = sh.n[q] * inn;
+      const float c = sh.S > 0.f ? floorf(sh.c[q] / sh.S + 0.5f) : 0.f;  // reading R13
+      col[q] = (int)fminf(fmaxf(c, 0.f), 255.f);
+    }
+    mask = sh.mask;
+  }
+#ifdef DTSDF_STATS
+  nrm[0] = (float)st_march; nrm[1] = (float)st_refine; nrm[2] = (float)st_skip;
+#endif
+  p.out_depth[pix] = depth;
   if (p.out_normal) {
     p.out_normal[3 * pix + 0] = nrm[0];
     p.out_normal[3 * pix + 1] = nrm[1];

@@ -134,6 +134,58 @@ __global__ void k_rgb_apron(const int4 *__restrict__ keys, long long n, const Ha
   rgb_apron[gid] = out;
 }
 
+// Surface bit of a block location: set iff some direction's voxel in the trilinear-corner range
+// of the location (block-local 0..8 per axis) has sdf <= 0.  Where it is clear, every sample whose
+// base voxel lies in the location has F > 0 or is invalid (f is a convex combination of
+// trilinear interpolants of positive values), so the march may skip to the location's last
+// lattice point (render.cu, exact).
+__global__ void k_surface(const int4 *__restrict__ keys, long long n, const float2 *__restrict__ apron,
+                          unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long b = gid / kRgbApronVox;
+  int a = (int)(gid - b * kRgbApronVox);
+  if (b >= n) return;
+  int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
+  float v = apron[b * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1)].x;
+  if (v <= 0.0f) {  // NaN (unallocated) compares false
+    int4 k = keys[b];
+    long long cell = ((long long)(k.z - lo_z) * dim_y + (k.y - lo_y)) * dim_x + (k.x - lo_x);
+    atomicOr(&surface[cell >> 5], 1u << (cell & 31));
+  }
+}
+
+// Certainly-positive base cells: bit l of location h is set iff, for every direction present
+// at the cell (all 8 corners allocated), all 8 corner sdf values are > 0.  A sample in such a cell
+// has F > 0 or is invalid (convex combination, O3(e)), so it can neither end a crossing nor --
+// when the next lattice point is such a sample too -- start one (render.cu, exact).
+// One warp per 32 consecutive cells of a location; the ballot writes one mask word.
+__global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const HashEntry *__restrict__ table,
+                           const float2 *__restrict__ apron, unsigned int *cell_pos) {
+  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long u = gid >> 9;
+  int l = (int)(gid & 511);
+  bool pos = false;
+  if (u < n_loc) {
+    const int h = loc[u].w;
+    const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+    pos = true;
+    for (int D = 0; D < 6; ++D) {
+      const int slot = table[h].slot[D];
+      if (slot < 0) continue;
+      const float2 *br = apron + (size_t)slot * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1);
+      bool absent = false, allpos = true;
+      for (int q = 0; q < 8; ++q) {
+        const float v = br[(q & 1) + kApron * ((q >> 1) & 1) + kApron * kApron * (q >> 2)].x;
+        absent |= isnan(v);
+        allpos &= v > 0.0f;
+      }
+      if (!absent && !allpos) pos = false;
+    }
+  }
+  const unsigned int word = __ballot_sync(0xffffffffu, pos);
+  if (u < n_loc && (l & 31) == 0) cell_pos[(size_t)loc[u].w * 16 + (l >> 5)] = word;
+}
+
 static inline unsigned int grid_for(long long n, int threads) { return (unsigned int)((n + threads - 1) / threads); }
 
 cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s) {
@@ -153,6 +205,20 @@ cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *
                           int dim_x, int dim_y, cudaStream_t s) {
   if (n_loc == 0) return cudaSuccess;
   k_bitmap<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, bitmap, lo_x, lo_y, lo_z, dim_x, dim_y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
+                            unsigned int *cell_pos, cudaStream_t s) {
+  if (n_loc == 0) return cudaSuccess;
+  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, apron, cell_pos);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_surface(const int4 *keys, long long n, const float2 *apron, unsigned int *surface, int lo_x,
+                           int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_surface<<<grid_for(n * kRgbApronVox, 256), 256, 0, s>>>(keys, n, apron, surface, lo_x, lo_y, lo_z, dim_x, dim_y);
   return cudaGetLastError();
 }
 

@@ -13,7 +13,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdtsdf.so")
+LIB_PATH = os.environ.get("DTSDF_LIB") or os.path.join(_HERE, "libdtsdf.so")
 
 OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR = 0, -1, -2, -3, -4, -5
 VIEWS_PER_LAUNCH = 256
