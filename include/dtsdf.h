@@ -151,6 +151,18 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *   DTSDF_OPT_BLOCK_SKIP  1 (default) jump over unallocated block locations; 0 step every point */
 #define DTSDF_OPT_RANGE_PASS 1
 #define DTSDF_OPT_BLOCK_SKIP 2
+/* Tuning (results unchanged):
+ *   DTSDF_OPT_SCHEDULE    0 (default) one CTA per 16x16-pixel tile; 1 persistent warps pulling
+ *                         8x4-pixel tiles from an atomic counter
+ *   DTSDF_OPT_LOCATION_GRID 1 (default) resolve block locations through the dense location grid
+ *                         (built when the location AABB has <= 2^28 cells); 0 through the
+ *                         occupancy bitmaps and the hash table
+ * Testing only (changes which root a multi-root lattice interval yields):
+ *   DTSDF_OPT_BISECT_STEPS  -1 (default) enough bisection steps to narrow the bracket to
+ *                           <= 5e-5 m before regula falsi; n >= 0 forces n steps */
+#define DTSDF_OPT_SCHEDULE 3
+#define DTSDF_OPT_BISECT_STEPS 4
+#define DTSDF_OPT_LOCATION_GRID 5
 DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
 
 /* Kernel launches issued by this context since creation (all kinds). */

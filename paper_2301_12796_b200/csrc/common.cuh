@@ -46,7 +46,10 @@ struct VolumeView {
   const HashEntry *table;
   unsigned int table_mask;
   const unsigned int *bitmap;  // occupancy bit per block location over the location AABB
-  const unsigned int *surface; // same layout: 1 iff some direction has a corner voxel with sdf <= 0
+  const unsigned int *surface; // same layout: 1 unless every base cell of the location is certainly positive
+  const int *loc_grid;         // dense location grid over the AABB (null if too large): for an
+                               // allocated location its hash entry index | (surface bit << 30),
+                               // else -d with d >= 1 its empty-space distance in blocks
   const unsigned int *cell_pos;  // [table_cap][16]: bit l of location entry h = base cell l is
                                  // "certainly positive": every present direction's 8 corners > 0
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
@@ -73,12 +76,15 @@ struct RenderLaunch {
   int tiles_x, tiles_y;            // range tiles per view
   int use_range, use_skip;         // exact accelerations (DTSDF_OPT_*)
   int n_bisect;                    // bisection steps: bracket Delta -> <= 5e-5 m
+  int schedule;                    // 0 grid of 16x16 CTAs, 1 persistent warps + tile counter
+  int *tile_counter;               // persistent schedule work counter (reset per launch)
   const unsigned int *z_near;      // [n_views][tiles_y][tiles_x] float bits
   const unsigned int *z_far;
   float *out_depth;                // [n_views][rows][W]
   float *out_normal;               // [n_views][rows][W][3] or null
   unsigned char *out_color;        // [n_views][rows][W][3] or null
   unsigned char *out_mask;         // [n_views][rows][W] or null
+  unsigned long long *dbg_timeline;  // DTSDF_STATS builds only: per-pixel start/end/smid
   ViewPose pose[kViewsPerLaunch];
 };
 
@@ -110,10 +116,14 @@ cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsig
                           CommitScratch sc, cudaStream_t s);
 cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
                           int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, int *grid,
+                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
+                                  cudaStream_t s);
 cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
                             unsigned int *cell_pos, cudaStream_t s);
-cudaError_t launch_surface(const int4 *keys, long long n, const float2 *apron, unsigned int *surface, int lo_x,
-                           int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
+                           int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                          const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
                          cudaStream_t s);

@@ -32,6 +32,10 @@ struct TimedLaunch {
 
 }  // namespace
 
+#ifdef DTSDF_STATS
+extern "C" __attribute__((visibility("default"))) unsigned long long *dtsdf_debug_timeline = nullptr;
+#endif
+
 struct dtsdf_ctx {
   int device = 0;
   bool sticky = false;
@@ -46,6 +50,7 @@ struct dtsdf_ctx {
   HashEntry *table = nullptr;
   unsigned int table_cap = 0;
   unsigned int *bitmap = nullptr, *surface = nullptr, *cell_pos = nullptr;
+  int *loc_grid = nullptr;
   int lo[3] = {0, 0, 0}, dim[3] = {0, 0, 0};
   int4 *locations = nullptr;
   int64_t n_loc = 0;
@@ -59,7 +64,8 @@ struct dtsdf_ctx {
   size_t range_cap = 0;  // tiles
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
-  int use_range = 1, use_skip = 1;
+  int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1;
+  int *tile_counter = nullptr;
   // tracing
   bool profiling = false;
   std::vector<TimedLaunch> timed;
@@ -96,6 +102,7 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->bitmap);
   dfree(c->surface);
   dfree(c->cell_pos);
+  dfree(c->loc_grid);
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
@@ -176,7 +183,7 @@ int dtsdf_create(int cuda_device, dtsdf_ctx **out) {
   dtsdf_ctx *c = new (std::nothrow) dtsdf_ctx();
   if (!c) return fail(DTSDF_ERR_OUT_OF_MEMORY, "host allocation");
   c->device = cuda_device;
-  if (dalloc(c->scratch, 64) != cudaSuccess) {
+  if (dalloc(c->scratch, 64) != cudaSuccess || dalloc(c->tile_counter, 16) != cudaSuccess) {
     delete c;
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "scratch allocation");
   }
@@ -190,6 +197,7 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   cudaDeviceSynchronize();
   free_volume(c);
   dfree(c->scratch);
+  dfree(c->tile_counter);
   dfree(c->z_near);
   dfree(c->z_far);
   if (c->host_stage) cudaFree(c->host_stage);
@@ -237,6 +245,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   dfree(c->bitmap);
   dfree(c->surface);
   dfree(c->cell_pos);
+  dfree(c->loc_grid);
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
@@ -299,13 +308,38 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
      "apron");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
-  CK(c, launch_surface(reinterpret_cast<const int4 *>(c->keys), n, c->apron, c->surface, lo[0], lo[1], lo[2],
-                       c->dim[0], c->dim[1], s),
-     "surface");
-  end_timed(c, s, &tl);
-  begin_timed(c, 2, s, &tl);
   CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->apron, c->cell_pos, s), "cell_pos");
   end_timed(c, s, &tl);
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_surface(c->locations, c->n_loc, c->cell_pos, c->surface, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s),
+     "surface");
+  end_timed(c, s, &tl);
+  // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
+  // raycast resolves locations through the bitmaps and the hash table
+  if (cells > 0 && cells <= (size_t(1) << 28)) {
+    if (dalloc(c->loc_grid, cells * 4) != cudaSuccess) {
+      cudaGetLastError();
+      c->loc_grid = nullptr;
+    } else {
+      c->index_bytes += cells * 4;
+      CK(c, cudaMemsetAsync(c->loc_grid, 0xFF, cells * 4, s), "grid init");
+      begin_timed(c, 2, s, &tl);
+      CK(c, launch_loc_grid(c->locations, c->n_loc, c->surface, c->loc_grid, lo[0], lo[1], lo[2], c->dim[0],
+                            c->dim[1], s),
+         "loc_grid");
+      end_timed(c, s, &tl);
+      unsigned char *tmp = nullptr;
+      if (dalloc(tmp, 2 * cells) == cudaSuccess) {
+        begin_timed(c, 2, s, &tl, 4);
+        CK(c, launch_empty_distance(c->loc_grid, tmp, tmp + cells, c->dim[0], c->dim[1], c->dim[2], s), "distance");
+        end_timed(c, s, &tl);
+        CK(c, cudaStreamSynchronize(s), "distance sync");
+        cudaFree(tmp);
+      } else {
+        cudaGetLastError();
+      }
+    }
+  }
   CK(c, cudaStreamSynchronize(s), "commit sync");
   c->committed = true;
   return DTSDF_OK;
@@ -354,6 +388,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.bitmap = c->bitmap;
   V.surface = c->surface;
   V.cell_pos = c->cell_pos;
+  V.loc_grid = c->use_grid ? c->loc_grid : nullptr;
   V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
   V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];
   V.apron = c->apron;
@@ -400,12 +435,31 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.use_range = c->use_range; pl.use_skip = c->use_skip;
     pl.n_bisect = 0;
     while (V.delta / (float)(1 << pl.n_bisect) > 5e-5f && pl.n_bisect < 20) ++pl.n_bisect;
+    if (c->bisect_steps >= 0) pl.n_bisect = c->bisect_steps;
+    pl.schedule = c->schedule;
+    pl.tile_counter = c->tile_counter;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
     const size_t px = (size_t)v0 * rows * W;
     pl.out_depth = depth + px;
     pl.out_normal = normal ? normal + 3 * px : nullptr;
     pl.out_color = color ? color + 3 * px : nullptr;
     pl.out_mask = mask ? mask + px : nullptr;
+    pl.dbg_timeline = nullptr;
+#ifdef DTSDF_STATS
+    {
+      static unsigned long long *tl_buf = nullptr;
+      static size_t tl_cap = 0;
+      const size_t need = (size_t)nv * rows * W * 3;
+      if (need > tl_cap) {
+        if (tl_buf) cudaFree(tl_buf);
+        cudaMalloc(&tl_buf, need * 8);
+        tl_cap = need;
+      }
+      pl.dbg_timeline = tl_buf;
+      dtsdf_debug_timeline = tl_buf;
+    }
+#endif
+
     std::memcpy(pl.pose, rl.pose, sizeof(ViewPose) * nv);
     begin_timed(c, 1, s, &tl);
     CK(c, launch_raycast(pl, s), "raycast");
@@ -517,6 +571,9 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (option == DTSDF_OPT_RANGE_PASS) c->use_range = value ? 1 : 0;
   else if (option == DTSDF_OPT_BLOCK_SKIP) c->use_skip = value ? 1 : 0;
+  else if (option == DTSDF_OPT_SCHEDULE && (value == 0 || value == 1)) c->schedule = value;
+  else if (option == DTSDF_OPT_LOCATION_GRID) c->use_grid = value ? 1 : 0;
+  else if (option == DTSDF_OPT_BISECT_STEPS && value >= -1 && value <= 30) c->bisect_steps = value;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

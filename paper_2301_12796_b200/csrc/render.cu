@@ -143,6 +143,10 @@ struct ShadeResult {
 };
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
+// a + t (b - a) on a pair: two packed FFMA2 (a - t a, then + t b)
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
+  return __ffma2_rn(t, b, __ffma2_rn(make_float2(-t.x, -t.y), a, a));
+}
 
 #define APRON_IDX(dx, dy, dz) (((dx) + 1) + kApron * ((dy) + 1) + kApron * kApron * ((dz) + 1))
 #define RGB_IDX(dx, dy, dz) ((dx) + kRgbApron * (dy) + kRgbApron * kRgbApron * (dz))
@@ -162,6 +166,7 @@ struct Cursor {
   bool surf;     // some corner-range voxel has sdf <= 0 (surface bitmap)
   int present;   // bit D: direction D has a brick at this location
   int entry;     // hash entry index (row of cell_pos), -1 if unallocated
+  int dist;      // unallocated: empty-space distance in blocks (>= 1); 0 = outside the AABB
   int slots[6];
 };
 
@@ -193,6 +198,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   float C1r = 0.f, C1g = 0.f, C1b = 0.f, C2r = 0.f, C2g = 0.f, C2b = 0.f;
   int m1 = 0, m2 = 0;
   const float half_inv_s = 0.5f * V.inv_voxel;
+  const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
   const int off = lx + kApron * ly + kApron * kApron * lz;
   int present = cur.present;
 #pragma unroll 1
@@ -201,42 +207,53 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     present &= present - 1;
     const int slot = pick6(cur.slots, D);
     const float2 *br = V.apron + (size_t)slot * kApronStride + off;
-    // O3(a) trilinear phi_D, omega_D over the 8 cell corners
+    // all 32 stencil voxels are issued before any test (one load round per direction; the
+    // apron brick always holds them, NaN marking unallocated neighbours)
     const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
     const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
     const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
     const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
-    const float w00 = lerpf(c000.y, c100.y, fx), w10 = lerpf(c010.y, c110.y, fx);
-    const float w01 = lerpf(c001.y, c101.y, fx), w11 = lerpf(c011.y, c111.y, fx);
-    const float omega = lerpf(lerpf(w00, w10, fy), lerpf(w01, w11, fy), fz);
-    // x-lerps of the four corner rows e_yz; R(dz) = bilinear over (x, y) of slab dz
-    const float e00 = lerpf(c000.x, c100.x, fx), e10 = lerpf(c010.x, c110.x, fx);
-    const float e01 = lerpf(c001.x, c101.x, fx), e11 = lerpf(c011.x, c111.x, fx);
-    const float R0 = lerpf(e00, e10, fy), R1 = lerpf(e01, e11, fy);
-    const float phi = lerpf(R0, R1, fz);
+    const float xm00 = __ldg(&br[APRON_IDX(-1, 0, 0)].x), xm10 = __ldg(&br[APRON_IDX(-1, 1, 0)].x);
+    const float xm01 = __ldg(&br[APRON_IDX(-1, 0, 1)].x), xm11 = __ldg(&br[APRON_IDX(-1, 1, 1)].x);
+    const float xp00 = __ldg(&br[APRON_IDX(2, 0, 0)].x), xp10 = __ldg(&br[APRON_IDX(2, 1, 0)].x);
+    const float xp01 = __ldg(&br[APRON_IDX(2, 0, 1)].x), xp11 = __ldg(&br[APRON_IDX(2, 1, 1)].x);
+    const float ym00 = __ldg(&br[APRON_IDX(0, -1, 0)].x), ym10 = __ldg(&br[APRON_IDX(1, -1, 0)].x);
+    const float ym01 = __ldg(&br[APRON_IDX(0, -1, 1)].x), ym11 = __ldg(&br[APRON_IDX(1, -1, 1)].x);
+    const float yp00 = __ldg(&br[APRON_IDX(0, 2, 0)].x), yp10 = __ldg(&br[APRON_IDX(1, 2, 0)].x);
+    const float yp01 = __ldg(&br[APRON_IDX(0, 2, 1)].x), yp11 = __ldg(&br[APRON_IDX(1, 2, 1)].x);
+    const float zm00 = __ldg(&br[APRON_IDX(0, 0, -1)].x), zm10 = __ldg(&br[APRON_IDX(1, 0, -1)].x);
+    const float zm01 = __ldg(&br[APRON_IDX(0, 1, -1)].x), zm11 = __ldg(&br[APRON_IDX(1, 1, -1)].x);
+    const float zp00 = __ldg(&br[APRON_IDX(0, 0, 2)].x), zp10 = __ldg(&br[APRON_IDX(1, 0, 2)].x);
+    const float zp01 = __ldg(&br[APRON_IDX(0, 1, 2)].x), zp11 = __ldg(&br[APRON_IDX(1, 1, 2)].x);
+    // The lerps run pairwise on Blackwell's packed fp32x2 FMA (FFMA2): {sdf, weight} of the
+    // corners, and pairs of independent stencil layers.
+    // O3(a) trilinear phi_D, omega_D over the 8 cell corners (x: rows e_yz, y: slabs R(dz), z)
+    const float2 e00 = lerp2(c000, c100, fx2), e10 = lerp2(c010, c110, fx2);
+    const float2 e01 = lerp2(c001, c101, fx2), e11 = lerp2(c011, c111, fx2);
+    const float2 R0w = lerp2(e00, e10, fy2), R1w = lerp2(e01, e11, fy2);
+    const float2 pw = lerp2(R0w, R1w, fz2);
+    const float phi = pw.x, omega = pw.y;
     if (isnan(phi)) continue;       // D absent: a corner lies in an unallocated block
     if (!(omega > 0.0f)) continue;  // D holds no data at x (reading R8)
     // O3(c) central differences of trilinear phi at x +- s e_a (24 further stencil voxels):
     // phi(x + s e_a) - phi(x - s e_a) = (1 - f_a)(A1 - A-1) + f_a (A2 - A0) with A(d) the
     // bilinear interpolant of the stencil layer d along axis a
-    const float P0 = lerpf(lerpf(c000.x, c010.x, fy), lerpf(c001.x, c011.x, fy), fz);
-    const float P1 = lerpf(lerpf(c100.x, c110.x, fy), lerpf(c101.x, c111.x, fy), fz);
-    const float Q0 = lerpf(e00, e01, fz), Q1 = lerpf(e10, e11, fz);
-    const float Pm = lerpf(lerpf(__ldg(&br[APRON_IDX(-1, 0, 0)].x), __ldg(&br[APRON_IDX(-1, 1, 0)].x), fy),
-                           lerpf(__ldg(&br[APRON_IDX(-1, 0, 1)].x), __ldg(&br[APRON_IDX(-1, 1, 1)].x), fy), fz);
-    const float Pp = lerpf(lerpf(__ldg(&br[APRON_IDX(2, 0, 0)].x), __ldg(&br[APRON_IDX(2, 1, 0)].x), fy),
-                           lerpf(__ldg(&br[APRON_IDX(2, 0, 1)].x), __ldg(&br[APRON_IDX(2, 1, 1)].x), fy), fz);
-    const float Qm = lerpf(lerpf(__ldg(&br[APRON_IDX(0, -1, 0)].x), __ldg(&br[APRON_IDX(1, -1, 0)].x), fx),
-                           lerpf(__ldg(&br[APRON_IDX(0, -1, 1)].x), __ldg(&br[APRON_IDX(1, -1, 1)].x), fx), fz);
-    const float Qp = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 2, 0)].x), __ldg(&br[APRON_IDX(1, 2, 0)].x), fx),
-                           lerpf(__ldg(&br[APRON_IDX(0, 2, 1)].x), __ldg(&br[APRON_IDX(1, 2, 1)].x), fx), fz);
-    const float Rm = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 0, -1)].x), __ldg(&br[APRON_IDX(1, 0, -1)].x), fx),
-                           lerpf(__ldg(&br[APRON_IDX(0, 1, -1)].x), __ldg(&br[APRON_IDX(1, 1, -1)].x), fx), fy);
-    const float Rp = lerpf(lerpf(__ldg(&br[APRON_IDX(0, 0, 2)].x), __ldg(&br[APRON_IDX(1, 0, 2)].x), fx),
-                           lerpf(__ldg(&br[APRON_IDX(0, 1, 2)].x), __ldg(&br[APRON_IDX(1, 1, 2)].x), fx), fy);
-    const float gx = lerpf(P1 - Pm, Pp - P0, fx) * half_inv_s;
-    const float gy = lerpf(Q1 - Qm, Qp - Q0, fy) * half_inv_s;
-    const float gz = lerpf(R1 - Rm, Rp - R0, fz) * half_inv_s;
+    const float R0 = R0w.x, R1 = R1w.x;
+    // (P0, P1): bilinear over (y, z) of the corner columns x = 0, 1
+    const float2 P01 = lerp2(lerp2(make_float2(c000.x, c100.x), make_float2(c010.x, c110.x), fy2),
+                             lerp2(make_float2(c001.x, c101.x), make_float2(c011.x, c111.x), fy2), fz2);
+    // (Q0, Q1) from the x-lerped rows
+    const float2 Q01 = lerp2(make_float2(e00.x, e10.x), make_float2(e01.x, e11.x), fz2);
+    // (Pm, Pp), (Qm, Qp), (Rm, Rp): the outer stencil layers
+    const float2 Pmp = lerp2(lerp2(make_float2(xm00, xp00), make_float2(xm10, xp10), fy2),
+                             lerp2(make_float2(xm01, xp01), make_float2(xm11, xp11), fy2), fz2);
+    const float2 Qmp = lerp2(lerp2(make_float2(ym00, yp00), make_float2(ym10, yp10), fx2),
+                             lerp2(make_float2(ym01, yp01), make_float2(ym11, yp11), fx2), fz2);
+    const float2 Rmp = lerp2(lerp2(make_float2(zm00, zp00), make_float2(zm10, zp10), fx2),
+                             lerp2(make_float2(zm01, zp01), make_float2(zm11, zp11), fx2), fy2);
+    const float gx = lerpf(P01.y - Pmp.x, Pmp.y - P01.x, fx) * half_inv_s;
+    const float gy = lerpf(Q01.y - Qmp.x, Qmp.y - Q01.x, fy) * half_inv_s;
+    const float gz = lerpf(R1 - Rmp.x, Rmp.y - R0, fz) * half_inv_s;
     const float gn = sqrtf(gx * gx + gy * gy + gz * gz);
     // v^D = sign * e_axis
     const int axis = D >> 1;
@@ -301,119 +318,188 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
 enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
+constexpr int kLookahead = 8;  // lattice points tested per certainly-positive scan
 
-__global__ void __launch_bounds__(256, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
-  const int view = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-  const int vrel = blockIdx.y * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const int v = p.row0 + vrel;
-  if (u >= p.width || v >= p.row1) return;
-  const VolumeView &V = p.vol;
-  const ViewPose &P = p.pose[view];
-  // O1 ray (eq:reprojection) in fp64: sample positions are formed in fp64 so that
-  // refinement can locate the shading point to ~1e-9 m (reading R32); the combination itself
-  // runs in fp32 on cell-local fractions
-  double od[3], rd[3];
-  float r[3];
-  double L;
-  {
-    const double ddx = ((double)u - (double)p.cx) / (double)p.fx, ddy = ((double)v - (double)p.cy) / (double)p.fy;
-    L = sqrt(ddx * ddx + ddy * ddy + 1.0);
-    const double iLd = 1.0 / L;
-    for (int q = 0; q < 3; ++q) {
-      rd[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
-      od[q] = (double)P.t[q];
-      r[q] = (float)rd[q];
-    }
-  }
-  const int rows = p.row1 - p.row0;
-  const size_t pix = ((size_t)view * rows + vrel) * p.width + u;
-  // O2 lattice bounds, narrowed to the tile's block range (a3)
-  const float Lf = (float)L;
-  const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
-  const float zn = __uint_as_float(__ldg(&p.z_near[tile])), zf = __uint_as_float(__ldg(&p.z_far[tile]));
-  const int kmin = (int)ceilf(p.z_min * Lf * V.inv_delta), kmax = (int)floorf(p.z_max * Lf * V.inv_delta);
-  int k = kmin, k1 = kmax;
-  if (p.use_range) {
-    if (zn <= zf) {
-      k = max(kmin, (int)floorf(zn * (1.0f - 1e-4f) * Lf * V.inv_delta));
-      k1 = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * Lf * V.inv_delta) + 1);
-    } else {
-      k1 = k - 1;  // no allocated block projects onto this tile
-    }
-  }
-  const double dd = (double)V.delta, idd = 1.0 / dd, inv_s = 1.0 / (double)V.voxel_size;
-  double ird[3];
-  for (int q = 0; q < 3; ++q) ird[q] = 1.0 / rd[q];
-  const double bsz = (double)kBlock * (double)V.voxel_size;
+// One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
+// step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
+// a warp -- whatever phase each is in -- run the evaluation code together.
+struct Ray {
+  int view, u, vrel;
+  float r[3], o[3], ir[3], iLf;
+  int k, k1;
+  // sample positions in voxel units g = g0 + t * rs relative to the integer cell ib of a frame:
+  // the world origin during the march; re-anchored once per bracket in fp64 at x(t_{k-1}), so g
+  // stays within two voxels of it and fp32 resolves the shading point to ~1e-9 m (reading R32) --
+  // near a root the weights of an ill-conditioned mixture of directions change on a
+  // sub-micrometre scale
+  int ibx, iby, ibz;
+  float g0x, g0y, g0z, rsx, rsy, rsz;
   Cursor cur;
-  cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
-#pragma unroll
-  for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
-  int mode = kMarch;
-  bool prev_valid = false;
-  float prev_f = 0.0f;
-  // refinement state: bracket [a, b] with f(a) > 0 (or invalid), f(b) <= 0
-  double a = 0.0, b = 0.0, t = (double)k * dd;
-  float fa = 0.f, fb = 0.f;
-  bool fa_valid = true;
-  int it = 0, side = 0;
-  bool hit = false;
+  int mode, it, side;
+  bool prev_valid, fa_valid, hit;
+  float prev_f, a, b, t, fa, fb;
   ShadeResult sh;
+  int ix, iy, iz;
+  float frx, fry, frz;
 #ifdef DTSDF_STATS
-  int st_march = 0, st_refine = 0, st_skip = 0;
+  int st_march, st_refine, st_skip, st_empty, st_jump, st_cpi;
+  long long cy_adv, cy_march, cy_refine;
+  unsigned long long g_start, g_end;
+  unsigned smid;
 #endif
-  // cell of the current sample and the cursor over its block location
-  double gx = 0, gy = 0, gz = 0, flx = 0, fly = 0, flz = 0;
-  int ix = 0, iy = 0, iz = 0;
-  auto locate = [&](double tt) {
-    gx = fma(tt, rd[0], od[0]) * inv_s;
-    gy = fma(tt, rd[1], od[1]) * inv_s;
-    gz = fma(tt, rd[2], od[2]) * inv_s;
-    flx = floor(gx); fly = floor(gy); flz = floor(gz);
-    ix = (int)flx; iy = (int)fly; iz = (int)flz;
+
+  __device__ __forceinline__ void init(const RenderLaunch &p, int view_, int u_, int vrel_) {
+    view = view_; u = u_; vrel = vrel_;
+    const VolumeView &V = p.vol;
+    const ViewPose &P = p.pose[view];
+    const int v = p.row0 + vrel;
+    // O1 ray (eq:reprojection)
+    const float dxf = (u - p.cx) / p.fx, dyf = (v - p.cy) / p.fy;
+    const float Lf = sqrtf(dxf * dxf + dyf * dyf + 1.0f);
+    iLf = 1.0f / Lf;
+    for (int q = 0; q < 3; ++q) {
+      r[q] = (P.r[3 * q] * dxf + P.r[3 * q + 1] * dyf + P.r[3 * q + 2]) * iLf;
+      o[q] = P.t[q];
+      ir[q] = 1.0f / r[q];
+    }
+    // O2 lattice bounds, narrowed to the tile's block range (a3)
+    const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
+    const float zn = __uint_as_float(__ldg(&p.z_near[tile])), zf = __uint_as_float(__ldg(&p.z_far[tile]));
+    const int kmin = (int)ceilf(p.z_min * Lf * V.inv_delta), kmax = (int)floorf(p.z_max * Lf * V.inv_delta);
+    k = kmin;
+    k1 = kmax;
+    if (p.use_range) {
+      if (zn <= zf) {
+        k = max(kmin, (int)floorf(zn * (1.0f - 1e-4f) * Lf * V.inv_delta));
+        k1 = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * Lf * V.inv_delta) + 1);
+      } else {
+        k1 = k - 1;  // no allocated block projects onto this tile
+      }
+    }
+    ibx = iby = ibz = 0;
+    g0x = o[0] * V.inv_voxel; g0y = o[1] * V.inv_voxel; g0z = o[2] * V.inv_voxel;
+    rsx = r[0] * V.inv_voxel; rsy = r[1] * V.inv_voxel; rsz = r[2] * V.inv_voxel;
+    cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
+    cur.dist = 1;
+#pragma unroll
+    for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
+    mode = kMarch;
+    prev_valid = false;
+    prev_f = 0.f;
+    a = b = 0.f;
+    t = (float)k * V.delta;
+    fa = fb = 0.f;
+    fa_valid = true;
+    it = side = 0;
+    hit = false;
+#ifdef DTSDF_STATS
+    st_march = st_refine = st_skip = st_empty = st_jump = st_cpi = 0;
+    cy_adv = cy_march = cy_refine = 0;
+#endif
+  }
+
+  __device__ __forceinline__ void locate(const VolumeView &V, float tt) {
+    const float gx = fmaf(tt, rsx, g0x), gy = fmaf(tt, rsy, g0y), gz = fmaf(tt, rsz, g0z);
+    const float flx = floorf(gx), fly = floorf(gy), flz = floorf(gz);
+    frx = gx - flx; fry = gy - fly; frz = gz - flz;
+    ix = ibx + (int)flx; iy = iby + (int)fly; iz = ibz + (int)flz;
     const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
     if (bx != cur.bx || by != cur.by || bz != cur.bz) {
       cur.bx = bx; cur.by = by; cur.bz = bz;
-      cur.occ = occupied(V, bx, by, bz, &cur.surf);
       cur.present = 0;
       cur.entry = -1;
+      if (V.loc_grid) {  // a2 via the dense location grid: one load, then the entry's slots
+        const unsigned x = (unsigned)(bx - V.lo_x), y = (unsigned)(by - V.lo_y), z = (unsigned)(bz - V.lo_z);
+        int gv = 0;  // outside the AABB: distance 0
+        if (x < (unsigned)V.dim_x && y < (unsigned)V.dim_y && z < (unsigned)V.dim_z)
+          gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + y) * V.dim_x + x]);
+        else
+          gv = -0x7fffffff;
+        cur.occ = gv >= 0;
+        cur.dist = gv == -0x7fffffff ? 0 : (gv < 0 ? -gv : 0);
+        cur.surf = (gv >> 30) & 1;
+        if (cur.occ) {
+          cur.entry = gv & 0x3fffffff;
+          const int4 *e = reinterpret_cast<const int4 *>(&V.table[cur.entry]);
+          const int4 ea = __ldg(e), eb = __ldg(e + 1);
+          cur.slots[0] = ea.z; cur.slots[1] = ea.w; cur.slots[2] = eb.x;
+          cur.slots[3] = eb.y; cur.slots[4] = eb.z; cur.slots[5] = eb.w;
+        }
+      } else {  // a2 via occupancy bitmaps + hash probe
+        cur.dist = 1;
+        cur.occ = occupied(V, bx, by, bz, &cur.surf);
+        if (cur.occ) cur.entry = lookup_slots(V, bx, by, bz, cur.slots);
+      }
       if (cur.occ) {
-        cur.entry = lookup_slots(V, bx, by, bz, cur.slots);
 #pragma unroll
         for (int d = 0; d < 6; ++d) cur.present |= (cur.slots[d] >= 0) << d;
       }
     }
-  };
-  auto block_exit = [&]() {
-    double texit = 1e300;
+  }
+
+  // ray parameter where it leaves the cube of blocks within `rad` of the cursor's block (march frame)
+  __device__ __forceinline__ float box_exit(const VolumeView &V, int rad) const {
+    const float bsz = kBlock * V.voxel_size;
+    float texit = 3.0e38f;
     const int bb[3] = {cur.bx, cur.by, cur.bz};
     for (int q = 0; q < 3; ++q) {
-      if (rd[q] > 0.0) texit = fmin(texit, ((bb[q] + 1) * bsz - od[q]) * ird[q]);
-      else if (rd[q] < 0.0) texit = fmin(texit, (bb[q] * bsz - od[q]) * ird[q]);
+      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + rad) * bsz - o[q]) * ir[q]);
+      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - rad) * bsz - o[q]) * ir[q]);
     }
     return texit;
-  };
-  for (;;) {
+  }
+  __device__ __forceinline__ float block_exit(const VolumeView &V) const { return box_exit(V, 0); }
+
+  // Advance (march only), evaluate one sample, update the state.  Returns true when the ray is
+  // finished (hit shaded, or no crossing in range).
+  __device__ __forceinline__ bool step(const RenderLaunch &p) {
+    const VolumeView &V = p.vol;
+#ifdef DTSDF_STATS
+    const long long c0 = clock64();
+#endif
     if (mode == kMarch) {
       // a4: advance to the next lattice point that needs an evaluation.  Every step skipped here
       // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
       // location without an sdf <= 0 corner, and in a certainly-positive cell followed by
-      // another, no crossing can end or start.  Lanes of a warp run this cheap loop, then all
-      // evaluate together below.
-      bool found = false;
-      while (k <= k1) {
-        t = (double)k * dd;
-        locate(t);
+      // another, no crossing can end or start.
+      for (;;) {
+        if (k > k1) return true;  // no crossing: a miss
+        t = (float)k * V.delta;
+        locate(V, t);
+#ifdef DTSDF_STATS
+        ++st_skip;
+#endif
         if (!cur.occ) {
           prev_valid = false;
 #ifdef DTSDF_STATS
-          ++st_skip;
+          ++st_empty;
 #endif
-          if (p.use_skip) {  // land on the first lattice point at or before the block exit
-            const double kn = floor(block_exit() * idd);
-            k = (kn > (double)k1) ? k1 + 1 : max(k + 1, (int)kn);
+          if (p.use_skip) {
+            // land on the first lattice point at or before the exit of the empty region: the
+            // block itself, the cube of blocks within its empty-space distance, or -- outside the
+            // volume's AABB -- straight to the AABB entry (or a miss when the ray leaves it)
+            float texit;
+            if (cur.dist == 0) {
+              const float bsz = kBlock * V.voxel_size;
+              float t0 = -3.0e38f, t1 = 3.0e38f;
+              const int lo3[3] = {V.lo_x, V.lo_y, V.lo_z}, dm3[3] = {V.dim_x, V.dim_y, V.dim_z};
+              for (int q = 0; q < 3; ++q) {
+                const float lo = lo3[q] * bsz - o[q], hi = (lo3[q] + dm3[q]) * bsz - o[q];
+                if (r[q] != 0.f) {
+                  const float ta = lo * ir[q], tb = hi * ir[q];
+                  t0 = fmaxf(t0, fminf(ta, tb));
+                  t1 = fminf(t1, fmaxf(ta, tb));
+                } else if (lo > 0.f || hi < 0.f) {
+                  t0 = 3.0e38f;
+                }
+              }
+              texit = (t0 <= t1 && t1 > t) ? fmaxf(t0, t) : 3.0e38f;
+              if (texit >= 3.0e38f) { k = k1 + 1; continue; }
+            } else {
+              texit = box_exit(V, cur.dist - 1);
+            }
+            const float kn = floorf(texit * V.inv_delta);
+            k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);
           } else {
             ++k;
           }
@@ -422,75 +508,104 @@ __global__ void __launch_bounds__(256, DTSDF_RAYCAST_MINB) k_raycast(const __gri
         if (p.use_skip && !cur.surf) {
           // jump to (at most) the location's second-to-last lattice point: the point evaluated
           // there becomes prev for the first point of the next location
-          const double kj = ceil(block_exit() * idd) - 2.0;
-          if (kj > (double)k) {
+          const float kj = ceilf(block_exit(V) * V.inv_delta) - 2.0f;
+          if (kj > (float)k) {
 #ifdef DTSDF_STATS
-            ++st_skip;
+            ++st_jump;
 #endif
-            k = (kj > (double)k1) ? k1 + 1 : (int)kj;
+            k = (kj > (float)k1) ? k1 + 1 : (int)kj;
             prev_valid = false;
             continue;
           }
         }
         if (p.use_skip && cell_positive(V, cur, (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7))) {
-          const double t2 = t + dd;
-          const int jx = (int)floor(fma(t2, rd[0], od[0]) * inv_s), jy = (int)floor(fma(t2, rd[1], od[1]) * inv_s),
-                    jz = (int)floor(fma(t2, rd[2], od[2]) * inv_s);
-          if ((jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz &&
-              cell_positive(V, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7))) {
+          // look ahead over the next lattice points of this location at once (independent
+          // loads): in a run of certainly-positive points only the last one needs evaluating
+          unsigned run = 1u;
+#pragma unroll
+          for (int j = 1; j < kLookahead; ++j) {
+            const float tj = (float)(k + j) * V.delta;
+            const int jx = ibx + (int)floorf(fmaf(tj, rsx, g0x)), jy = iby + (int)floorf(fmaf(tj, rsy, g0y)),
+                      jz = ibz + (int)floorf(fmaf(tj, rsz, g0z));
+            const bool ok = (jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz &&
+                            cell_positive(V, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7));
+            run |= (unsigned)ok << j;
+          }
+          const int n = __ffs(~run) - 1;  // leading certainly-positive points (>= 1)
+          if (n >= 2) {
 #ifdef DTSDF_STATS
-            ++st_skip;
+            st_cpi += n - 1;
 #endif
             prev_valid = false;
-            ++k;
-            continue;
+            k += n - 1;
+            if (n == kLookahead) continue;  // the run may go on: scan again from its last point
+            t = (float)k * V.delta;
+            locate(V, t);  // the run's last point: evaluate it (prev for the next point)
           }
         }
-        found = true;
         break;
       }
-      if (!found) break;  // no crossing: a miss
     } else {
-      locate(t);
+      locate(V, t);
     }
-#ifdef DTSDF_STATS
-    if (mode == kMarch) ++st_march;
-    else ++st_refine;
-#endif
     SampleResult s;
+#ifdef DTSDF_STATS
+    if (mode == kMarch) { ++st_march; --st_skip; } else ++st_refine;
+    const long long c1 = clock64();
+    cy_adv += c1 - c0;
+#endif
     if (cur.occ) {
-      s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, (float)(gx - flx), (float)(gy - fly), (float)(gz - flz), r[0],
-                      r[1], r[2], mode == kShade, &sh);
+      s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh);
     } else {
       s.valid = false;
       s.f = 0.f;
     }
+#ifdef DTSDF_STATS
+    {
+      const long long c2 = clock64();
+      if (mode == kMarch) cy_march += c2 - c1; else cy_refine += c2 - c1;
+    }
+#endif
     if (mode == kMarch) {
-      if (s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f) {
-        // a6: bracket [t_{k-1}, t_k].  Phase 1: bisection with the oracle's decisions (an
-        // invalid midpoint counts as positive, R21) until the bracket is <= 5e-5 m, so it
-        // keeps the oracle's root when F has several sign changes (reading R20).
-        a = (double)(k - 1) * dd;
-        b = t;
-        fa = prev_f;
-        fb = s.f;
-        fa_valid = true;
-        it = 0;
-        side = 0;
-        mode = p.n_bisect > 0 ? kBisect : kIllinois;
-      } else {
+      if (!(s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f)) {
         prev_valid = s.valid;
         prev_f = s.f;
         ++k;
-        t = (double)k * dd;
-        continue;
+        return false;
       }
+      // a6: bracket [t_{k-1}, t_k]: re-anchor the position frame at x(t_{k-1}) in fp64
+      {
+        const ViewPose &P = p.pose[view];
+        const double ddx = ((double)u - (double)p.cx) / (double)p.fx;
+        const double ddy = ((double)(p.row0 + vrel) - (double)p.cy) / (double)p.fy;
+        const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0), inv_s = 1.0 / (double)V.voxel_size;
+        const double t0 = (double)(k - 1) * (double)V.delta;
+        double rq[3], gq[3];
+        for (int q = 0; q < 3; ++q) {
+          rq[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
+          gq[q] = fma(t0, rq[q], (double)P.t[q]) * inv_s;
+        }
+        const double fx0 = floor(gq[0]), fy0 = floor(gq[1]), fz0 = floor(gq[2]);
+        ibx = (int)fx0; iby = (int)fy0; ibz = (int)fz0;
+        g0x = (float)(gq[0] - fx0); g0y = (float)(gq[1] - fy0); g0z = (float)(gq[2] - fz0);
+        rsx = (float)(rq[0] * inv_s); rsy = (float)(rq[1] * inv_s); rsz = (float)(rq[2] * inv_s);
+      }
+      // Phase 1: bisection with the oracle's decisions (an invalid midpoint counts as positive,
+      // R21) until the bracket is <= 5e-5 m, so it keeps the oracle's root when F has several
+      // sign changes (reading R20).  Phase 2: Illinois regula falsi inside it.
+      a = 0.f;
+      b = V.delta;
+      fa = prev_f;
+      fb = s.f;
+      fa_valid = true;
+      it = 0;
+      side = 0;
+      mode = p.n_bisect > 0 ? kBisect : kIllinois;
     } else if (mode == kBisect) {
       if (!s.valid || s.f > 0.0f) { a = t; fa = s.f; fa_valid = s.valid; }
       else { b = t; fb = s.f; }
       if (++it >= p.n_bisect) { mode = kIllinois; it = 0; }
     } else if (mode == kIllinois) {
-      // Phase 2: Illinois regula falsi inside the narrowed bracket until b sits on the root
       if (!s.valid || s.f > 0.0f) {
         a = t; fa = s.f; fa_valid = s.valid;
         if (side == 1) fb *= 0.5f;
@@ -501,48 +616,67 @@ __global__ void __launch_bounds__(256, DTSDF_RAYCAST_MINB) k_raycast(const __gri
         side = -1;
         if (s.f > -1e-7f) mode = kShade;  // b sits on the root
       }
-      if (++it >= 12 || b - a <= 1e-12) mode = kShade;
-    } else {  // kShade: a7 done at b, a valid sample on the surface side (reading R32)
+      if (++it >= 12) mode = kShade;
+    } else {  // kShade: a7 evaluated at b, a valid sample on the surface side (reading R32)
       hit = true;
-      break;
+      return true;
     }
-    // next position
-    if (mode == kBisect) t = 0.5 * (a + b);
-    else if (mode == kIllinois) {
-      double m = (fa_valid && fa > fb) ? a + (double)(fa / (fa - fb)) * (b - a) : 0.5 * (a + b);
-      if (!(m > a && m < b)) m = 0.5 * (a + b);
-      t = m;
-    } else t = b;  // kShade
-  }
-  float depth = 0.f, nrm[3] = {0.f, 0.f, 0.f};
-  int col[3] = {0, 0, 0}, mask = 0;
-  if (hit) {
-    depth = (float)(b / L);
-    const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
-    const float inn = nn > 0.f ? 1.0f / nn : 0.f;
-    for (int q = 0; q < 3; ++q) {
-      nrm[q] = sh.n[q] * inn;
-      const float c = sh.S > 0.f ? floorf(sh.c[q] / sh.S + 0.5f) : 0.f;  // reading R13
-      col[q] = (int)fminf(fmaxf(c, 0.f), 255.f);
+    // next position (offset from t_{k-1})
+    if (mode == kBisect) {
+      t = 0.5f * (a + b);
+    } else if (mode == kIllinois) {
+      float m = (fa_valid && fa > fb) ? fmaf(fa / (fa - fb), b - a, a) : 0.5f * (a + b);
+      if (!(m > a && m < b)) m = 0.5f * (a + b);
+      if (!(m > a && m < b)) mode = kShade;  // bracket at the fp32 resolution of the offset
+      t = (mode == kShade) ? b : m;
+    } else {
+      t = b;  // kShade
     }
-    mask = sh.mask;
+    return false;
   }
+
+  __device__ __forceinline__ void store(const RenderLaunch &p) const {
+    float depth = 0.f, nrm[3] = {0.f, 0.f, 0.f};
+    int col[3] = {0, 0, 0}, mask = 0;
+    if (hit) {
+      depth = ((float)(k - 1) * p.vol.delta + b) * iLf;
+      const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
+      const float inn = nn > 0.f ? 1.0f / nn : 0.f;
+      for (int q = 0; q < 3; ++q) {
+        nrm[q] = sh.n[q] * inn;
+        const float c = sh.S > 0.f ? floorf(sh.c[q] / sh.S + 0.5f) : 0.f;  // reading R13
+        col[q] = (int)fminf(fmaxf(c, 0.f), 255.f);
+      }
+      mask = sh.mask;
+    }
 #ifdef DTSDF_STATS
-  nrm[0] = (float)st_march; nrm[1] = (float)st_refine; nrm[2] = (float)st_skip;
+    if (p.dbg_timeline) {
+      const size_t pid = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
+      p.dbg_timeline[3 * pid + 0] = g_start;
+      p.dbg_timeline[3 * pid + 1] = g_end;
+      p.dbg_timeline[3 * pid + 2] = smid;
+    }
+    // debug build: normal <- cycles (outside evaluations, march evaluations, refinement
+    // evaluations), colour <- counts (march evaluations, refinement evaluations, advance steps)
+    nrm[0] = (float)cy_adv; nrm[1] = (float)cy_march; nrm[2] = (float)cy_refine;
+    col[0] = min(st_march, 255); col[1] = min(st_refine, 255); col[2] = min(st_empty, 255);
+    mask = min(st_cpi, 255) | 0;  // jumps: st_jump (not stored)
 #endif
-  p.out_depth[pix] = depth;
-  if (p.out_normal) {
-    p.out_normal[3 * pix + 0] = nrm[0];
-    p.out_normal[3 * pix + 1] = nrm[1];
-    p.out_normal[3 * pix + 2] = nrm[2];
+    const size_t pix = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
+    p.out_depth[pix] = depth;
+    if (p.out_normal) {
+      p.out_normal[3 * pix + 0] = nrm[0];
+      p.out_normal[3 * pix + 1] = nrm[1];
+      p.out_normal[3 * pix + 2] = nrm[2];
+    }
+    if (p.out_color) {
+      p.out_color[3 * pix + 0] = (unsigned char)col[0];
+      p.out_color[3 * pix + 1] = (unsigned char)col[1];
+      p.out_color[3 * pix + 2] = (unsigned char)col[2];
+    }
+    if (p.out_mask) p.out_mask[pix] = (unsigned char)mask;
   }
-  if (p.out_color) {
-    p.out_color[3 * pix + 0] = (unsigned char)col[0];
-    p.out_color[3 * pix + 1] = (unsigned char)col[1];
-    p.out_color[3 * pix + 2] = (unsigned char)col[2];
-  }
-  if (p.out_mask) p.out_mask[pix] = (unsigned char)mask;
-}
+};
 
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
   if (p.n_locations == 0 || p.n_views == 0) return cudaSuccess;
@@ -551,10 +685,86 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// grid schedule: one CTA per 16 x (2 * DTSDF_CTA / 64)-pixel tile of 8x4-pixel warps, one ray per thread
+#ifndef DTSDF_CTA
+#define DTSDF_CTA 256
+#endif
+__global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
+  const int vrel = blockIdx.y * (DTSDF_CTA / 16) + (warp >> 1) * 4 + (lane >> 3);
+  if (u >= p.width || p.row0 + vrel >= p.row1) return;
+  Ray ray;
+#ifdef DTSDF_STATS
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+#endif
+  ray.init(p, blockIdx.z, u, vrel);
+#ifdef DTSDF_STATS
+  const long long c0 = clock64();
+#endif
+  while (!ray.step(p)) {
+  }
+#ifdef DTSDF_STATS
+  ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations
+  unsigned long long g_end;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+  ray.g_start = g_start;
+  ray.g_end = g_end;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  ray.smid = smid;
+#endif
+  ray.store(p);
+}
+
+// persistent schedule: resident warps pull 8x4-pixel warp tiles (view-major, row-major) from an
+// atomic counter until the batch is done -- no CTA-granularity tail, uneven tiles balance out
+__global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_constant__ RenderLaunch p) {
+  const int lane = threadIdx.x & 31;
+  const int wx = (p.width + 7) >> 3, wy = (p.row1 - p.row0 + 3) >> 2;
+  const int per_view = wx * wy, total = per_view * p.n_views;
+  for (;;) {
+    int tile = 0;
+    if (lane == 0) tile = atomicAdd(p.tile_counter, 1);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    if (tile >= total) return;
+    const int view = tile / per_view, rr = tile - view * per_view;
+    const int ty = rr / wx, tx = rr - ty * wx;
+    const int u = tx * 8 + (lane & 7), vrel = ty * 4 + (lane >> 3);
+    if (u < p.width && p.row0 + vrel < p.row1) {
+      Ray ray;
+      ray.init(p, view, u, vrel);
+      while (!ray.step(p)) {
+      }
+      ray.store(p);
+    }
+  }
+}
+
 cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s) {
   if (p.n_views == 0) return cudaSuccess;
-  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.row1 - p.row0 + 15) / 16), (unsigned)p.n_views);
-  k_raycast<<<grid, 256, 0, s>>>(p);
+  if (p.schedule == 1) {
+    static int blocks_per_sm = 0, sms = 0;
+    if (!blocks_per_sm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raycast_persistent, 256, 0);
+      if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    cudaError_t e = cudaMemsetAsync(p.tile_counter, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    const long long tiles = (long long)((p.width + 7) >> 3) * ((p.row1 - p.row0 + 3) >> 2) * p.n_views;
+    long long grid = (long long)blocks_per_sm * sms;
+    grid = grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8;
+    k_raycast_persistent<<<(unsigned)grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+  }
+  const int rows_per_cta = DTSDF_CTA / 16;
+  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.row1 - p.row0 + rows_per_cta - 1) / rows_per_cta),
+            (unsigned)p.n_views);
+  k_raycast<<<grid, DTSDF_CTA, 0, s>>>(p);
   return cudaGetLastError();
 }
 

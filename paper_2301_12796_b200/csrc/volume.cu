@@ -134,26 +134,6 @@ __global__ void k_rgb_apron(const int4 *__restrict__ keys, long long n, const Ha
   rgb_apron[gid] = out;
 }
 
-// Surface bit of a block location: set iff some direction's voxel in the trilinear-corner range
-// of the location (block-local 0..8 per axis) has sdf <= 0.  Where it is clear, every sample whose
-// base voxel lies in the location has F > 0 or is invalid (f is a convex combination of
-// trilinear interpolants of positive values), so the march may skip to the location's last
-// lattice point (render.cu, exact).
-__global__ void k_surface(const int4 *__restrict__ keys, long long n, const float2 *__restrict__ apron,
-                          unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long b = gid / kRgbApronVox;
-  int a = (int)(gid - b * kRgbApronVox);
-  if (b >= n) return;
-  int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
-  float v = apron[b * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1)].x;
-  if (v <= 0.0f) {  // NaN (unallocated) compares false
-    int4 k = keys[b];
-    long long cell = ((long long)(k.z - lo_z) * dim_y + (k.y - lo_y)) * dim_x + (k.x - lo_x);
-    atomicOr(&surface[cell >> 5], 1u << (cell & 31));
-  }
-}
-
 // Certainly-positive base cells: bit l of location h is set iff, for every direction present
 // at the cell (all 8 corners allocated), all 8 corner sdf values are > 0.  A sample in such a cell
 // has F > 0 or is invalid (convex combination, O3(e)), so it can neither end a crossing nor --
@@ -186,6 +166,68 @@ __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const 
   if (u < n_loc && (l & 31) == 0) cell_pos[(size_t)loc[u].w * 16 + (l >> 5)] = word;
 }
 
+// Dense location grid: for each allocated location, its hash entry index and surface bit, so
+// the raycast resolves a location with one 4-B load instead of bitmap + surface + hash probe.
+__global__ void k_loc_grid(const int4 *__restrict__ loc, long long n_loc, const unsigned int *__restrict__ surface,
+                           int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_loc) return;
+  const int4 b = loc[i];
+  const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
+  const int surf = (surface[cell >> 5] >> (cell & 31)) & 1;
+  grid[cell] = b.w | (surf << 30);
+}
+
+// Empty-space distance on the location grid (L-infinity, in blocks, capped): separable passes
+// d_x(c) = min{|dx| : c + dx e_x occupied}, then d_xy(c) = min_dy max(|dy|, d_x(c + dy e_y)), then
+// the same along z.  An empty location with distance d has no allocated location within d - 1
+// blocks, so a ray may skip the whole (2d - 1)^3-block cube around it (render.cu, exact).
+constexpr int kDistCap = 31;
+__global__ void k_dist_pass(const int *__restrict__ grid, const unsigned char *__restrict__ in,
+                            unsigned char *__restrict__ out, int axis, int dim_x, int dim_y, int dim_z) {
+  const long long cells = (long long)dim_x * dim_y * dim_z;
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const int x = (int)(c % dim_x), y = (int)((c / dim_x) % dim_y), z = (int)(c / ((long long)dim_x * dim_y));
+  const int pos = axis == 0 ? x : (axis == 1 ? y : z);
+  const int n = axis == 0 ? dim_x : (axis == 1 ? dim_y : dim_z);
+  const long long stride = axis == 0 ? 1 : (axis == 1 ? dim_x : (long long)dim_x * dim_y);
+  int best = kDistCap;
+  for (int d = -kDistCap; d <= kDistCap; ++d) {
+    const int q = pos + d;
+    if (q < 0 || q >= n) continue;
+    const int ad = d < 0 ? -d : d;
+    if (ad >= best) continue;
+    const long long cq = c + d * stride;
+    const int v = (axis == 0) ? (grid[cq] >= 0 ? 0 : kDistCap) : in[cq];
+    const int m = ad > v ? ad : v;
+    if (m < best) best = m;
+  }
+  out[c] = (unsigned char)best;
+}
+
+__global__ void k_dist_store(int *grid, const unsigned char *__restrict__ dist, long long cells) {
+  long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  if (grid[c] < 0) grid[c] = -(dist[c] > 1 ? (int)dist[c] : 1);
+}
+
+// Surface bit of a block location: set unless every base cell of the location is certainly
+// positive (k_cell_pos).  Where it is clear, every sample whose base voxel lies in the location
+// has F > 0 or is invalid, so the march may jump to the location's last lattice points (exact).
+__global__ void k_surface(const int4 *__restrict__ loc, long long n_loc, const unsigned int *__restrict__ cell_pos,
+                          unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_loc) return;
+  const int4 b = loc[i];
+  bool all_pos = true;
+  for (int w = 0; w < 16; ++w) all_pos &= cell_pos[(size_t)b.w * 16 + w] == 0xffffffffu;
+  if (!all_pos) {
+    const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
+    atomicOr(&surface[cell >> 5], 1u << (cell & 31));
+  }
+}
+
 static inline unsigned int grid_for(long long n, int threads) { return (unsigned int)((n + threads - 1) / threads); }
 
 cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s) {
@@ -208,6 +250,24 @@ cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *
   return cudaGetLastError();
 }
 
+cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, int *grid,
+                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
+  if (n_loc == 0) return cudaSuccess;
+  k_loc_grid<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, surface, grid, lo_x, lo_y, lo_z, dim_x, dim_y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
+                                  cudaStream_t s) {
+  const long long cells = (long long)dim_x * dim_y * dim_z;
+  if (cells == 0) return cudaSuccess;
+  k_dist_pass<<<grid_for(cells, 256), 256, 0, s>>>(grid, nullptr, tmp0, 0, dim_x, dim_y, dim_z);
+  k_dist_pass<<<grid_for(cells, 256), 256, 0, s>>>(grid, tmp0, tmp1, 1, dim_x, dim_y, dim_z);
+  k_dist_pass<<<grid_for(cells, 256), 256, 0, s>>>(grid, tmp1, tmp0, 2, dim_x, dim_y, dim_z);
+  k_dist_store<<<grid_for(cells, 256), 256, 0, s>>>(grid, tmp0, cells);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
                             unsigned int *cell_pos, cudaStream_t s) {
   if (n_loc == 0) return cudaSuccess;
@@ -215,10 +275,10 @@ cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEn
   return cudaGetLastError();
 }
 
-cudaError_t launch_surface(const int4 *keys, long long n, const float2 *apron, unsigned int *surface, int lo_x,
-                           int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  k_surface<<<grid_for(n * kRgbApronVox, 256), 256, 0, s>>>(keys, n, apron, surface, lo_x, lo_y, lo_z, dim_x, dim_y);
+cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
+                           int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
+  if (n_loc == 0) return cudaSuccess;
+  k_surface<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, cell_pos, surface, lo_x, lo_y, lo_z, dim_x, dim_y);
   return cudaGetLastError();
 }
 

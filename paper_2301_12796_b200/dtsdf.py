@@ -23,7 +23,7 @@ EXPORTS = [
     "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
     "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
 ]
-OPT_RANGE_PASS, OPT_BLOCK_SKIP = 1, 2
+OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID = 1, 2, 3, 4, 5
 
 
 class DtsdfError(RuntimeError):

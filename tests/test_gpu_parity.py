@@ -146,6 +146,34 @@ def test_accelerations_are_result_invisible(R, c1):
     R.set_option(OPT_BLOCK_SKIP, 1)
 
 
+def test_location_grid_and_hash_paths_agree(R, c1):
+    """The dense location grid and the bitmap + hash-probe path resolve the same slots."""
+    from paper_2301_12796_b200.dtsdf import OPT_LOCATION_GRID
+    R.upload_volume(c1.volume)
+    K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=320, height=240)
+    ref = R.render(c1.poses, K)
+    R.set_option(OPT_LOCATION_GRID, 0)
+    g = R.render(c1.poses, K)
+    R.set_option(OPT_LOCATION_GRID, 1)
+    for k in ref:
+        assert torch.equal(ref[k], g[k]), k
+
+
+def test_schedules_give_identical_bits(R, c1):
+    """Grid and persistent (lane-level work fetching) schedules run the same per-ray code."""
+    from paper_2301_12796_b200.dtsdf import OPT_SCHEDULE
+    w = scenes.c3_batch(n_views=3, room=c1)
+    R.upload_volume(w.volume)
+    K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=321, height=243)
+    R.set_option(OPT_SCHEDULE, 0)
+    ref = R.render(w.poses, K, row0=5, row1=240)
+    R.set_option(OPT_SCHEDULE, 1)
+    g = R.render(w.poses, K, row0=5, row1=240)
+    R.set_option(OPT_SCHEDULE, 0)
+    for k in ref:
+        assert torch.equal(ref[k], g[k]), k
+
+
 def test_host_outputs_equal_device_outputs(R, c1):
     R.upload_volume(c1.volume)
     K = c1.intrinsics
