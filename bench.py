@@ -14,6 +14,7 @@ and the job time is the max over ranks.  Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -37,9 +38,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["dtsdf", "reference"], default="dtsdf")
-    ap.add_argument("--config", choices=["C0", "C1", "C2", "C3"], default="C1",
-                    help="C1 is the bench workload; others are for profiling only")
-    ap.add_argument("--views", type=int, default=1, help="views per rank per step (1 = the configs[1] workload)")
+    ap.add_argument("--config", choices=["C0", "C1", "C2", "C3", "C4"], default="C1",
+                    help="C1 is the bench workload (BASELINE.json metric); the others are for profiling")
+    ap.add_argument("--views", type=int, default=1,
+                    help="views per rank per step, taken round-robin from the config's poses "
+                         "(1 = the configs[1] workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=100)
@@ -55,6 +58,8 @@ def workload(name):
         return scenes.c2_thin()
     if name == "C3":
         return scenes.c3_batch()
+    if name == "C4":
+        return scenes.c4_large()
     return scenes.c1_room()
 
 
@@ -65,9 +70,10 @@ def describe(w, views):
               "seeded pose (fx=fy=525, cx=319.5, cy=239.5)",
         "C0": "dense sphere r=0.2 m, 64^3 voxels at 1 cm, 80x60 view",
         "C2": "200 thin plates, 5 mm voxels, 640x480 views",
-        "C3": "configs[1] volume, orbit views"}[w.name],
+        "C3": "configs[1] volume, orbit views",
+        "C4": "8x8x3 m room of seeded boxes, cylinders and thin plates, 5 mm voxels, tau 2 cm, orbit views"}[w.name],
         "width": K.width, "height": K.height, "views_per_step_per_gpu": views,
-        "n_blocks": int(w.volume.n_blocks), "theta_deg": 65.0, "outputs": "depth+normal+color+dirmask",
+        "n_blocks": int(w.volume.n_blocks if w.volume is not None else w.extra["n_blocks"]), "theta_deg": 65.0, "outputs": "depth+normal+color+dirmask",
         "l2": "flushed between timed steps (256 MiB write)"}
 
 
@@ -227,8 +233,9 @@ def run_dtsdf(args):
         if len(set(sums)) != 1:
             raise SystemExit(f"volume replicas differ after broadcast: {sums}")
         R.commit(stream)
-        # everything rank 0 knows about the workload (poses, intrinsics) travels as an object
-        objs = [w if rank == 0 else None]
+        # the rest of the workload (name, poses, intrinsics) travels as a small object
+        objs = [dataclasses.replace(w, volume=None, patches=None,
+                                    extra=dict(w.extra or {}, n_blocks=w.volume.n_blocks)) if rank == 0 else None]
         dist.broadcast_object_list(objs, 0)
         if rank != 0:
             w = objs[0]
@@ -237,7 +244,9 @@ def run_dtsdf(args):
         R.upload_volume(w.volume)
     upload_ms = 1e3 * (time.perf_counter() - t_up)
     K = w.intrinsics
-    poses = np.repeat(np.asarray(w.poses[:1], np.float32), args.views, axis=0)
+    # this rank's views: round-robin over the config's poses (configs[1] has one)
+    idx = [(rank * args.views + i) % len(w.poses) for i in range(args.views)]
+    poses = np.ascontiguousarray(np.asarray(w.poses, np.float32)[idx])
     rays_per_step = K.width * K.height * args.views
     out = R.render(poses, K)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)

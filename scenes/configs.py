@@ -10,7 +10,7 @@ from typing import Optional
 
 import numpy as np
 
-from .fill import Patches, box_patches, patch_fill, sphere_volume
+from .fill import Patches, box_patches, cylinder_patches, patch_fill, patch_fill_c, sphere_volume
 from .volume import BlockVolume, Intrinsics, look_at
 
 THETA = float(np.deg2rad(65.0))  # reading R2
@@ -140,4 +140,84 @@ def c3_batch(n_views=256, room: Optional[Workload] = None) -> Workload:
     return Workload("C3", room.volume, room.intrinsics, orbit_poses(rng, n_views), room.patches)
 
 
-CONFIGS = {"C0": c0_sphere, "C1": c1_room, "C2": c2_thin, "C3": c3_batch}
+LARGE_K = dict(fx=1050.0, fy=1050.0, cx=639.5, cy=479.5, width=1280, height=960)  # reading R31
+
+
+def large_patches(rng, n_boxes, n_cylinders, n_plates, keep_out=(0.83, 2.03)) -> Patches:
+    """configs[4] geometry in an 8 x 8 x 3 m room: floor, four walls and a ceiling (inward
+    normals), then n_boxes boxes (sides U(0.1,1) m; first half resting on the floor, second
+    half floating with a bottom face; every other one yawed U(0, pi/2)), n_cylinders upright
+    cylinders (r U(0.05,0.3) m, h U(0.2,2) m, side + top cap) and n_plates thin plates
+    (2-6 mm, sides U(0.1,0.5) m, uniform normal, front/back colours >= 96 apart in L1).
+    Objects whose horizontal extent reaches into the annulus keep_out (m from the room's
+    vertical axis) are redrawn so the camera orbit stays in free space.
+
+    Draw order: room colours (6); boxes; cylinders; plates, each as written below."""
+    pat = Patches.empty()
+    room = [([0, 0, 0.0], [0, 0, 1.0], [1.0, 0, 0], [0, 1.0, 0], 4.0, 4.0),      # floor
+            ([0, 0, 3.0], [0, 0, -1.0], [1.0, 0, 0], [0, 1.0, 0], 4.0, 4.0),     # ceiling
+            ([-4.0, 0, 1.5], [1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0], 4.0, 1.5),   # walls
+            ([4.0, 0, 1.5], [-1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0], 4.0, 1.5),
+            ([0, -4.0, 1.5], [0, 1.0, 0], [1.0, 0, 0], [0, 0, 1.0], 4.0, 1.5),
+            ([0, 4.0, 1.5], [0, -1.0, 0], [1.0, 0, 0], [0, 0, 1.0], 4.0, 1.5)]
+    for q, n, u, v, hu, hv in room:
+        pat.extend(q, n, u, v, hu, hv, _rand_color(rng))
+
+    def free(xy, ext):
+        r = float(np.hypot(*xy))
+        return r + ext < keep_out[0] or r - ext > keep_out[1]
+
+    for i in range(n_boxes):
+        while True:
+            size = rng.uniform(0.1, 1.0, size=3)
+            cxy = rng.uniform(-3.5, 3.5, size=2)
+            if free(cxy, 0.5 * float(np.hypot(size[0], size[1]))):
+                break
+        floating = i >= n_boxes // 2
+        cz = rng.uniform(size[2] / 2 + 0.3, 3.0 - size[2] / 2) if floating else size[2] / 2
+        yaw = rng.uniform(0.0, np.pi / 2) if i % 2 else 0.0
+        colors = [_rand_color(rng) for _ in range(6)]
+        box_patches(pat, [cxy[0], cxy[1], cz], size, yaw, colors, with_bottom=floating)
+    for _ in range(n_cylinders):
+        while True:
+            r, h = rng.uniform(0.05, 0.3), rng.uniform(0.2, 2.0)
+            cxy = rng.uniform(-3.5, 3.5, size=2)
+            if free(cxy, r):
+                break
+        cylinder_patches(pat, [cxy[0], cxy[1], 0.0], r, h, [_rand_color(rng), _rand_color(rng)])
+    for _ in range(n_plates):
+        while True:
+            center = rng.uniform([-3.5, -3.5, 0.2], [3.5, 3.5, 2.8])
+            hu, hv = 0.5 * rng.uniform(0.1, 0.5, size=2)
+            if free(center[:2], float(np.hypot(hu, hv))):
+                break
+        n = _unit_sphere(rng)
+        thick = rng.uniform(0.002, 0.006)
+        while True:
+            cf, cb = rng.integers(0, 256, 3), rng.integers(0, 256, 3)
+            if np.abs(cf.astype(int) - cb.astype(int)).sum() >= 96:
+                break
+        u, v = _orthonormal(n, rng)
+        pat.extend(center + 0.5 * thick * n, n, u, v, hu, hv, cf)
+        pat.extend(center - 0.5 * thick * n, -n, u, v, hu, hv, cb)
+    return pat
+
+
+C4_COUNTS = dict(n_boxes=520, n_cylinders=220, n_plates=450)
+
+
+def c4_large(n_views=64, counts=None) -> Workload:
+    """configs[4]: 8 x 8 x 3 m at 5 mm voxels (tau 2 cm) of seeded boxes, cylinders and thin
+    plates, counts tuned towards ~2.5 M blocks (the bench reports the actual N); n_views
+    640x480 views on an orbit of 0.05 m / 2 degree steps at 1.5 m height inside the room
+    looking at its centre, plus one 1280x960 view (reading R31) from the first pose
+    (``extra['large_pose']``, ``extra['large_intrinsics']``)."""
+    rng = np.random.default_rng([4, 0])
+    pat = large_patches(rng, **(counts or C4_COUNTS))
+    poses = orbit_poses(rng, n_views, height=1.5, target=(0.0, 0.0, 0.8))
+    vol = patch_fill_c(pat, voxel_size=0.005, truncation=0.02, theta=THETA)
+    return Workload("C4", vol, Intrinsics(**ROOM_K), poses, pat,
+                    {"large_pose": poses[0], "large_intrinsics": Intrinsics(**LARGE_K)})
+
+
+CONFIGS = {"C0": c0_sphere, "C1": c1_room, "C2": c2_thin, "C3": c3_batch, "C4": c4_large}

@@ -20,7 +20,10 @@ the CUDA path.
 """
 from __future__ import annotations
 
+import ctypes
 import dataclasses
+import os
+import subprocess
 
 import numpy as np
 
@@ -68,10 +71,18 @@ def sphere_volume(radius=0.2, voxel_size=0.01, truncation=0.04, theta=np.deg2rad
 # ----------------------------------------------------------------------------------------
 # G1: ideal-fusion patch fill
 # ----------------------------------------------------------------------------------------
+RECT, DISK, CYL = 0, 1, 2
+
+
 @dataclasses.dataclass
 class Patches:
-    """Rectangles: centre q, unit normal n (outward, towards free space), in-plane unit axes
-    u, v with half extents hu, hv, and an RGB colour."""
+    """Surface patches with outward normals (towards free space) and an RGB colour.
+
+    kind RECT (0): centre q, unit normal n, in-plane unit axes u, v, half extents hu, hv.
+    kind DISK (1): centre q, normal n, in-plane axes u, v, radius hu.
+    kind CYL  (2): lateral surface of a cylinder, axis through q along n, radius hu,
+                   half height hv (u, v: any orthonormal pair perpendicular to n).
+    ``patch_fill`` (numpy) handles RECT only; ``patch_fill_c`` (gen.c) handles all three."""
 
     q: np.ndarray
     n: np.ndarray
@@ -80,16 +91,22 @@ class Patches:
     hu: np.ndarray
     hv: np.ndarray
     color: np.ndarray
+    kind: np.ndarray = None
+
+    def __post_init__(self):
+        if self.kind is None:
+            self.kind = np.zeros(len(self.hu), np.int32)
 
     @staticmethod
     def empty():
         z3 = np.zeros((0, 3))
-        return Patches(z3, z3, z3, z3, np.zeros(0), np.zeros(0), np.zeros((0, 3), np.uint8))
+        return Patches(z3, z3, z3, z3, np.zeros(0), np.zeros(0), np.zeros((0, 3), np.uint8), np.zeros(0, np.int32))
 
     def __len__(self):
         return len(self.hu)
 
-    def extend(self, q, n, u, v, hu, hv, color):
+    def extend(self, q, n, u, v, hu, hv, color, kind=RECT):
+        self.kind = np.concatenate([self.kind, np.atleast_1d(np.int32(kind))])
         self.q = np.vstack([self.q, np.atleast_2d(q)])
         self.n = np.vstack([self.n, np.atleast_2d(n)])
         self.u = np.vstack([self.u, np.atleast_2d(u)])
@@ -101,7 +118,9 @@ class Patches:
     def ray_hit(self, o, d):
         """Closed-form first intersection of rays o + t d (t > 0) with the patches seen from
         their front side.  Returns (t, patch_id) with t = inf / id = -1 on a miss.
-        Test helper for closed-form pins (analytic geometry, not the method)."""
+        Test helper for closed-form pins (analytic geometry, not the method); RECT patches only."""
+        if (self.kind != RECT).any():
+            raise NotImplementedError("ray_hit: RECT patches only")
         o = np.asarray(o, np.float64).reshape(-1, 3)
         d = np.asarray(d, np.float64).reshape(-1, 3)
         best = np.full(len(d), np.inf)
@@ -145,6 +164,8 @@ def patch_fill(pat: Patches, voxel_size: float, truncation: float, theta: float,
     rgb = colour_p; other voxels get phi = 1, omega = 0, rgb = 0.  A block (b, D) is
     allocated iff any voxel was written.
     """
+    if (pat.kind != RECT).any():
+        raise NotImplementedError("patch_fill (numpy): RECT patches only; use patch_fill_c")
     s = voxel_size
     band = truncation + 2.0 * s
     cos_t = np.cos(theta)
@@ -216,3 +237,73 @@ def patch_fill(pat: Patches, voxel_size: float, truncation: float, theta: float,
         rgb_out.append(col[keep].astype(np.uint8))
     return BlockVolume(s, truncation, theta, np.concatenate(keys_out).astype(np.int32),
                        np.concatenate(sdf_out), np.concatenate(w_out), np.concatenate(rgb_out))
+
+
+def cylinder_patches(pat: Patches, base, radius, height, colors):
+    """Upright cylinder standing on z = base[2]: lateral surface plus the top cap (the bottom
+    rests on the floor and is omitted, like a box's bottom face)."""
+    base = np.asarray(base, np.float64)
+    ez = np.array([0.0, 0.0, 1.0])
+    pat.extend(base + 0.5 * height * ez, ez, [1.0, 0, 0], [0, 1.0, 0], radius, 0.5 * height, colors[0], kind=CYL)
+    pat.extend(base + height * ez, ez, [1.0, 0, 0], [0, 1.0, 0], radius, radius, colors[1], kind=DISK)
+
+
+# ----------------------------------------------------------------------------------------
+# G1 in C (gen.c): same rule, multithreaded, all patch kinds -- for the large configs
+# ----------------------------------------------------------------------------------------
+_GEN_SRC = os.path.join(os.path.dirname(os.path.abspath(__file__)), "gen.c")
+_GEN_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libscenegen.so")
+_gen = None
+
+
+def build_gen(force: bool = False) -> str:
+    if force or not os.path.exists(_GEN_LIB) or os.path.getmtime(_GEN_LIB) < os.path.getmtime(_GEN_SRC):
+        tmp = _GEN_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-math",
+                               "-Wall", "-shared", "-fPIC", "-pthread", _GEN_SRC, "-lm", "-o", tmp])
+        os.replace(tmp, _GEN_LIB)
+    return _GEN_LIB
+
+
+def _genlib():
+    global _gen
+    if _gen is None:
+        build_gen()
+        L = ctypes.CDLL(_GEN_LIB)
+        P, D, I = ctypes.c_void_p, ctypes.c_double, ctypes.c_int
+        L.scenegen_plan.argtypes = [I, P, P, P, P, P, P, P, P, D, D, D, I, ctypes.POINTER(P),
+                                    ctypes.POINTER(ctypes.c_int64)]
+        L.scenegen_plan.restype = I
+        L.scenegen_fill.argtypes = [P, I, P, P, P, P]
+        L.scenegen_fill.restype = None
+        L.scenegen_free.argtypes = [P]
+        L.scenegen_free.restype = None
+        _gen = L
+    return _gen
+
+
+def patch_fill_c(pat: Patches, voxel_size: float, truncation: float, theta: float, threads: int = 0) -> BlockVolume:
+    """G1 fill by gen.c: the rule of ``patch_fill`` extended to DISK and CYL patches.
+    On RECT-only scenes it writes the same bytes as ``patch_fill`` (tests/test_scenes.py)."""
+    L = _genlib()
+    arr = {k: np.ascontiguousarray(getattr(pat, k), np.float64) for k in ("q", "n", "u", "v", "hu", "hv")}
+    kind = np.ascontiguousarray(pat.kind, np.int32)
+    color = np.ascontiguousarray(pat.color, np.uint8)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    threads = threads or os.cpu_count() or 1
+    h, n = ctypes.c_void_p(), ctypes.c_int64()
+    rc = L.scenegen_plan(len(pat), ptr(kind), ptr(arr["q"]), ptr(arr["n"]), ptr(arr["u"]), ptr(arr["v"]),
+                         ptr(arr["hu"]), ptr(arr["hv"]), ptr(color), float(voxel_size), float(truncation),
+                         float(theta), threads, ctypes.byref(h), ctypes.byref(n))
+    if rc != 0:
+        raise MemoryError("scenegen_plan")
+    try:
+        N = n.value
+        keys = np.empty((N, 4), np.int32)
+        sdf = np.empty((N, VOXELS_PER_BLOCK), np.float32)
+        w = np.empty((N, VOXELS_PER_BLOCK), np.float32)
+        rgb = np.empty((N, VOXELS_PER_BLOCK, 3), np.uint8)
+        L.scenegen_fill(h, threads, ptr(keys), ptr(sdf), ptr(w), ptr(rgb))
+    finally:
+        L.scenegen_free(h)
+    return BlockVolume(voxel_size, truncation, theta, keys, sdf, w, rgb)
