@@ -51,6 +51,12 @@ def lib():
         L.oracle_eval.argtypes = [P, P, P, P]
         L.oracle_render.argtypes = [P, P, P, I64, P, I32, I32, P, P, P, P, P]
         L.oracle_render.restype = None
+        L.oracle_combined_voxels.argtypes = [P, P, P, D, I64, P, P, P, P, P, P]
+        L.oracle_combined_voxels.restype = None
+        L.oracle_render_combined.argtypes = [P, P, P, D, P, P, I64, P, I32, I32, P, P, P, P]
+        L.oracle_render_combined.restype = None
+        L.oracle_should_recombine.argtypes = [I64, I64, P, P, I64, I64, D, D]
+        L.oracle_should_recombine.restype = I32
         _lib = L
     return _lib
 
@@ -149,6 +155,64 @@ class OracleVolume:
         if nsamples:
             out["nsamples"] = ns.reshape(shape)
         return out
+
+
+MARGIN = 1.0 / 8.0  # PAPER.md:262 "slightly beyond the camera frustum (±1/8 image size)"
+
+
+def _pose32(pose):
+    return np.ascontiguousarray(np.asarray(pose, np.float32).astype(np.float64).reshape(16))
+
+
+def _intr32(K):
+    return np.array([np.float32(K.fx), np.float32(K.fy), np.float32(K.cx), np.float32(K.cy), K.width, K.height,
+                     np.float32(K.z_min), np.float32(K.z_max)], np.float64)
+
+
+def combined_voxels(ov: "OracleVolume", pose, K, ijk, margin: float = MARGIN):
+    """Combined TSDF voxels (oracle.c combine_voxel, readings R33-R35) at integer positions
+    ijk [n, 3] for the source camera (pose, K).  Returns dict(valid, sdf, weight, rgb, mask)."""
+    ijk = np.ascontiguousarray(ijk, np.int64).reshape(-1, 3)
+    n = len(ijk)
+    valid = np.zeros(n, np.int32)
+    sdf, S = np.zeros(n), np.zeros(n)
+    rgb = np.zeros((n, 3), np.uint8)
+    mask = np.zeros(n, np.uint8)
+    lib().oracle_combined_voxels(ov.h, _ptr(_pose32(pose)), _ptr(_intr32(K)), float(margin), n, _ptr(ijk),
+                                 _ptr(valid), _ptr(sdf), _ptr(S), _ptr(rgb), _ptr(mask))
+    return dict(valid=valid.astype(bool), sdf=sdf, weight=S, rgb=rgb, mask=mask)
+
+
+def render_combined(ov: "OracleVolume", src_pose, src_K, pose, K, pixels=None, row0=0, row1=None, threads=None,
+                    margin: float = MARGIN):
+    """Raycast (pose, K) through the combined TSDF of the source camera (src_pose, src_K)
+    (oracle.c render_pixel_combined, readings R36-R37).  Output layout as OracleVolume.render."""
+    if pixels is None:
+        row1 = K.height if row1 is None else row1
+        npix = (row1 - row0) * K.width
+        uv = None
+        shape = (row1 - row0, K.width)
+    else:
+        uv = np.ascontiguousarray(pixels, np.int32).reshape(-1, 2)
+        npix = uv.shape[0]
+        shape = (npix,)
+    depth = np.zeros(npix)
+    normal = np.zeros((npix, 3))
+    color = np.zeros((npix, 3), np.uint8)
+    mask = np.zeros(npix, np.uint8)
+    threads = threads or os.cpu_count() or 1
+    lib().oracle_render_combined(ov.h, _ptr(_pose32(src_pose)), _ptr(_intr32(src_K)), float(margin),
+                                 _ptr(_pose32(pose)), _ptr(_intr32(K)), npix, _ptr(uv), row0, threads, _ptr(depth),
+                                 _ptr(normal), _ptr(color), _ptr(mask))
+    return dict(depth=depth.reshape(shape), normal=normal.reshape(shape + (3,)), color=color.reshape(shape + (3,)),
+                mask=mask.reshape(shape))
+
+
+def should_recombine(frame: int, last: int, pose, last_pose, boot: int = 5, stale: int = 50, trans: float = 0.05,
+                     rot: float = 0.05 * np.pi / 2) -> bool:
+    """Conditional combination, eqs. condition_1-4, reading R38."""
+    return bool(lib().oracle_should_recombine(int(frame), int(last), _ptr(_pose32(pose)), _ptr(_pose32(last_pose)),
+                                              int(boot), int(stale), float(trans), float(rot)))
 
 
 def ray_dirs(pose, K, pixels=None):

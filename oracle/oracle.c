@@ -433,3 +433,337 @@ void oracle_render(void *p, const double pose[16], const double intr[8], int64_t
   for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
   free(th);
 }
+
+/* =======================================================================================
+ * NEXT-1: the view-dependent combined TSDF (Lemma 1, PAPER.md:182-186;
+ * PAPER.md:251-263; implementation note PAPER.md:610) and its raycast.  Readings R33-R40 of
+ * DESIGN.md §4.  Everything is a pure function of (volume, source camera): a combined voxel is
+ * evaluated on demand from the directional voxels, nothing is cached.
+ * ===================================================================================== */
+typedef struct {
+  double R[9], t[3];
+  double fx, fy, cx, cy, zmin, zmax;
+  int W, H;
+  double margin; /* fraction of the image size added on every side (1/8) */
+} ocam;
+
+static void cam_from(ocam *c, const double pose[16], const double intr[8], double margin) {
+  for (int a = 0; a < 3; ++a) {
+    for (int b = 0; b < 3; ++b) c->R[3 * a + b] = pose[4 * a + b];
+    c->t[a] = pose[4 * a + 3];
+  }
+  c->fx = intr[0]; c->fy = intr[1]; c->cx = intr[2]; c->cy = intr[3];
+  c->W = (int)intr[4]; c->H = (int)intr[5]; c->zmin = intr[6]; c->zmax = intr[7];
+  c->margin = margin;
+}
+
+/* R33: voxel (i,j,k) lies in the source view frustum widened by margin*W / margin*H pixels on
+ * every side ("selecting voxels slightly beyond the camera frustum (±1/8 image size)",
+ * PAPER.md:262) and inside [zmin, zmax] in camera z.  Evaluated left to right, one rounding per
+ * operation (the CUDA path evaluates the same expression with the same roundings). */
+static int in_frustum(const ocam *c, double s, int64_t i, int64_t j, int64_t k) {
+  double x[3] = {(double)i * s, (double)j * s, (double)k * s};
+  double d[3] = {x[0] - c->t[0], x[1] - c->t[1], x[2] - c->t[2]};
+  double xc[3];
+  for (int a = 0; a < 3; ++a) xc[a] = c->R[a] * d[0] + c->R[3 + a] * d[1] + c->R[6 + a] * d[2];
+  if (!(xc[2] >= c->zmin && xc[2] <= c->zmax)) return 0;
+  double u = c->fx * xc[0] / xc[2] + c->cx, v = c->fy * xc[1] / xc[2] + c->cy;
+  double mu = c->margin * (double)c->W, mv = c->margin * (double)c->H;
+  return u >= -mu && u <= (double)(c->W - 1) + mu && v >= -mv && v <= (double)(c->H - 1) + mv;
+}
+
+typedef struct {
+  int valid;    /* S > 0 */
+  double sdf;   /* sum W phi / S */
+  double S;     /* sum W: the combined voxel's weight */
+  double rgb[3];/* sum W c_D / S (reals) */
+  int mask;     /* bit D: W_D > 0 */
+} ocvox;
+
+/* R34: the combined value of the voxel at integer position (i,j,k) ("calculating the combined
+ * SDF for every voxel in the view frustum") with the combination weights of
+ * eq:combine_weight / eq:combine_tsdf_weight; the gradient
+ * n^D from "the SDF values stored in the 6 neighboring voxels", i.e. central
+ * differences (phi(i+e_a) - phi(i-e_a)) / 2s; r = the normalised ray from the source camera
+ * centre to the voxel.  Directions, gradient presence and the regime choice as O3 (R8-R10). */
+static void combine_voxel(const ovol *v, const ocam *c, int64_t i, int64_t j, int64_t k, ocvox *o) {
+  memset(o, 0, sizeof(*o));
+  if (!in_frustum(c, v->s, i, j, k)) return;
+  double x[3] = {(double)i * v->s, (double)j * v->s, (double)k * v->s};
+  double r[3] = {x[0] - c->t[0], x[1] - c->t[1], x[2] - c->t[2]};
+  double rl = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (!(rl > 0.0)) return;
+  for (int a = 0; a < 3; ++a) r[a] /= rl;
+  const int64_t vi[3] = {i, j, k};
+  double phi[6], om[6], n[6][3];
+  int64_t rec[6];
+  int data[6], hg[6], any_grad = 0;
+  for (int D = 0; D < 6; ++D) {
+    data[D] = hg[D] = 0;
+    rec[D] = record_of(v, D, i, j, k);
+    if (rec[D] < 0) continue;
+    phi[D] = (double)v->sdf[rec[D]];
+    om[D] = (double)v->weight[rec[D]];
+    data[D] = om[D] > 0.0;
+    if (!data[D]) continue;
+    double g[3];
+    int ok = 1;
+    for (int a = 0; a < 3 && ok; ++a) {
+      int64_t p[3] = {vi[0], vi[1], vi[2]}, m[3] = {vi[0], vi[1], vi[2]};
+      p[a] += 1;
+      m[a] -= 1;
+      int64_t rp = record_of(v, D, p[0], p[1], p[2]), rm = record_of(v, D, m[0], m[1], m[2]);
+      if (rp < 0 || rm < 0) { ok = 0; break; }
+      g[a] = ((double)v->sdf[rp] - (double)v->sdf[rm]) / (2.0 * v->s);
+    }
+    if (!ok) continue;
+    double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (gn > OR_EPS_GRAD) {
+      hg[D] = 1;
+      any_grad = 1;
+      for (int a = 0; a < 3; ++a) n[D][a] = g[a] / gn;
+    }
+  }
+  double S = 0.0, F = 0.0, C[3] = {0, 0, 0};
+  int m = 0;
+  for (int D = 0; D < 6; ++D) {
+    double W = 0.0;
+    if (any_grad) {
+      if (hg[D]) {
+        double nv = n[D][0] * VDIR[D][0] + n[D][1] * VDIR[D][1] + n[D][2] * VDIR[D][2];
+        double nr = -(n[D][0] * r[0] + n[D][1] * r[1] + n[D][2] * r[2]);
+        W = oracle_w_dir(nv, v->theta) * (nr > 0.0 ? nr : 0.0) * om[D]; /* eq:combine_weight */
+      }
+    } else if (data[D]) {
+      double vr = -(VDIR[D][0] * r[0] + VDIR[D][1] * r[1] + VDIR[D][2] * r[2]);
+      W = om[D] * (vr > 0.0 ? vr : 0.0); /* eq:combine_tsdf_weight */
+    }
+    if (!(W > 0.0)) continue;
+    m |= 1 << D;
+    S += W;
+    F += W * phi[D];
+    if (v->rgb)
+      for (int a = 0; a < 3; ++a) C[a] += W * (double)v->rgb[3 * rec[D] + a];
+  }
+  if (!(S > 0.0)) return;
+  o->valid = 1;
+  o->S = S;
+  o->sdf = F / S;
+  for (int a = 0; a < 3; ++a) o->rgb[a] = C[a] / S;
+  o->mask = m;
+}
+
+/* R35: the stored colour of a combined voxel is the u8 value min(255, floor(c + 1/2)) */
+static uint8_t u8_round(double c) {
+  double q = floor(c + 0.5);
+  return (uint8_t)(q > 255.0 ? 255.0 : (q < 0.0 ? 0.0 : q));
+}
+
+/* Combined voxels of a list of integer positions (element-wise parity / pins).
+ * ijk [n][3]; outputs valid[n], sdf[n], S[n], rgb[n][3] (u8 after R35), mask[n]. */
+void oracle_combined_voxels(void *p, const double pose[16], const double intr[8], double margin, int64_t n,
+                            const int64_t *ijk, int32_t *valid, double *sdf, double *S, uint8_t *rgb, uint8_t *mask) {
+  const ovol *v = (const ovol *)p;
+  ocam c;
+  cam_from(&c, pose, intr, margin);
+  for (int64_t q = 0; q < n; ++q) {
+    ocvox o;
+    combine_voxel(v, &c, ijk[3 * q], ijk[3 * q + 1], ijk[3 * q + 2], &o);
+    valid[q] = o.valid;
+    sdf[q] = o.valid ? o.sdf : 0.0;
+    S[q] = o.S;
+    for (int a = 0; a < 3; ++a) rgb[3 * q + a] = o.valid ? u8_round(o.rgb[a]) : 0;
+    mask[q] = (uint8_t)o.mask;
+  }
+}
+
+/* R36: the combined field is a regular TSDF ("can then be used like a regular
+ * TSDF"): plain trilinear of the combined sdf over the 8 cell corners, valid iff all 8 corners
+ * are valid combined voxels. */
+static int ccell(const ovol *v, const ocam *c, const int64_t cc[3], const double fr[3], double *phi, ocvox corner[8]) {
+  double ph = 0.0;
+  for (int q = 0; q < 8; ++q) {
+    int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+    ocvox o;
+    combine_voxel(v, c, cc[0] + dx, cc[1] + dy, cc[2] + dz, &o);
+    if (!o.valid) return 0;
+    double wt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
+    ph += wt * o.sdf;
+    if (corner) corner[q] = o;
+  }
+  *phi = ph;
+  return 1;
+}
+
+/* R37: shading of a combined-TSDF hit at the bracket end b (as R32):
+ *   normal = normalised central-difference gradient of the trilinear combined field at +-s
+ *            (R7 on the combined field) when the six shifted cells are valid and |g| > 1e-3;
+ *            otherwise the gradient of the cell's own trilinear interpolant when |g| > 1e-3;
+ *            otherwise 0;
+ *   colour = min(255, floor(trilinear of the corners' u8 colours + 1/2));
+ *   mask   = OR of the 8 corners' direction masks. */
+static void cshade(const ovol *v, const ocam *c, const int64_t cc[3], const double fr[3], double *nrm, uint8_t *col,
+                   uint8_t *msk) {
+  ocvox cor[8];
+  double ph;
+  nrm[0] = nrm[1] = nrm[2] = 0.0;
+  col[0] = col[1] = col[2] = 0;
+  *msk = 0;
+  if (!ccell(v, c, cc, fr, &ph, cor)) return;
+  double g[3];
+  int ok = 1;
+  for (int a = 0; a < 3 && ok; ++a) {
+    int64_t cp[3] = {cc[0], cc[1], cc[2]}, cm[3] = {cc[0], cc[1], cc[2]};
+    cp[a] += 1;
+    cm[a] -= 1;
+    double pp, pm;
+    if (!ccell(v, c, cp, fr, &pp, NULL) || !ccell(v, c, cm, fr, &pm, NULL)) { ok = 0; break; }
+    g[a] = (pp - pm) / (2.0 * v->s);
+  }
+  double gn = ok ? sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]) : 0.0;
+  if (!(gn > OR_EPS_GRAD)) {
+    /* d/dx_a of sum_q wt_q(fr) phi_q, with d fr_a / d x_a = 1/s */
+    for (int a = 0; a < 3; ++a) {
+      double acc = 0.0;
+      for (int q = 0; q < 8; ++q) {
+        int bit[3] = {q & 1, (q >> 1) & 1, (q >> 2) & 1};
+        double wt = 1.0;
+        for (int e = 0; e < 3; ++e) {
+          if (e == a) wt *= bit[e] ? 1.0 : -1.0;
+          else wt *= bit[e] ? fr[e] : 1.0 - fr[e];
+        }
+        acc += wt * cor[q].sdf;
+      }
+      g[a] = acc / v->s;
+    }
+    gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  }
+  if (gn > OR_EPS_GRAD)
+    for (int a = 0; a < 3; ++a) nrm[a] = g[a] / gn;
+  double cs[3] = {0, 0, 0};
+  int m = 0;
+  for (int q = 0; q < 8; ++q) {
+    int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+    double wt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
+    for (int a = 0; a < 3; ++a) cs[a] += wt * (double)u8_round(cor[q].rgb[a]);
+    m |= cor[q].mask;
+  }
+  for (int a = 0; a < 3; ++a) col[a] = u8_round(cs[a]);
+  *msk = (uint8_t)m;
+}
+
+typedef struct {
+  const ovol *v;
+  ocam src;          /* camera the combined TSDF was computed for */
+  ojob J;            /* rendering camera, pixels and outputs */
+} ocjob;
+
+/* O1-O6 on the combined field (same lattice, crossing rule and bisection as the direct path,
+ * PAPER.md:178), R37 shading */
+static void render_pixel_combined(ocjob *C, int u, int vrow, int64_t out) {
+  ojob *J = &C->J;
+  const ovol *v = C->v;
+  double dt[3] = {(u - J->cx) / J->fx, (vrow - J->cy) / J->fy, 1.0};
+  double L = sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]);
+  double r[3], o[3] = {J->t[0], J->t[1], J->t[2]};
+  for (int a = 0; a < 3; ++a) r[a] = (J->R[3 * a] * dt[0] + J->R[3 * a + 1] * dt[1] + J->R[3 * a + 2] * dt[2]) / L;
+  int64_t k0 = (int64_t)ceil(J->zmin * L / v->delta), k1 = (int64_t)floor(J->zmax * L / v->delta);
+  int prev_valid = 0;
+  double prev_f = 0.0;
+  J->depth[out] = 0.0;
+  for (int a = 0; a < 3; ++a) { J->normal[3 * out + a] = 0.0; J->color[3 * out + a] = 0; }
+  J->mask[out] = 0;
+  for (int64_t k = k0; k <= k1; ++k) {
+    double t = (double)k * v->delta;
+    double x[3] = {o[0] + t * r[0], o[1] + t * r[1], o[2] + t * r[2]};
+    int64_t cc[3];
+    double fr[3], f = 0.0;
+    locate(v, x, cc, fr);
+    int valid = ccell(v, &C->src, cc, fr, &f, NULL);
+    if (valid && prev_valid && prev_f > 0.0 && f <= 0.0) {
+      double a = t - v->delta, b = t;
+      for (int it = 0; it < 60; ++it) {
+        double m = 0.5 * (a + b);
+        if (!(m > a && m < b)) break;
+        double xm[3] = {o[0] + m * r[0], o[1] + m * r[1], o[2] + m * r[2]};
+        int64_t cm[3];
+        double fm[3], ff = 0.0;
+        locate(v, xm, cm, fm);
+        int vm = ccell(v, &C->src, cm, fm, &ff, NULL);
+        if (!vm || ff > 0.0) a = m; else b = m;
+      }
+      J->depth[out] = 0.5 * (a + b) / L;
+      double xb[3] = {o[0] + b * r[0], o[1] + b * r[1], o[2] + b * r[2]};
+      int64_t cb[3];
+      double fb[3];
+      locate(v, xb, cb, fb);
+      cshade(v, &C->src, cb, fb, &J->normal[3 * out], &J->color[3 * out], &J->mask[out]);
+      break;
+    }
+    prev_valid = valid;
+    prev_f = f;
+  }
+}
+
+static void *worker_combined(void *arg) {
+  ocjob *C = (ocjob *)arg;
+  ojob *J = &C->J;
+  const int64_t chunk = 16;
+  for (;;) {
+    int64_t i0 = __atomic_fetch_add(&J->next, chunk, __ATOMIC_RELAXED);
+    if (i0 >= J->npix) break;
+    int64_t i1 = i0 + chunk < J->npix ? i0 + chunk : J->npix;
+    for (int64_t i = i0; i < i1; ++i) {
+      int u, vr;
+      if (J->uv) { u = J->uv[2 * i]; vr = J->uv[2 * i + 1]; }
+      else { u = (int)(i % J->W); vr = J->row0 + (int)(i / J->W); }
+      render_pixel_combined(C, u, vr, i);
+    }
+  }
+  return NULL;
+}
+
+/* Render npix pixels of the view (pose, intr) from the combined TSDF of the source camera
+ * (src_pose, src_intr, margin).  Argument conventions as oracle_render. */
+void oracle_render_combined(void *p, const double src_pose[16], const double src_intr[8], double margin,
+                            const double pose[16], const double intr[8], int64_t npix, const int32_t *uv, int row0,
+                            int nthreads, double *depth, double *normal, uint8_t *color, uint8_t *mask) {
+  ocjob C;
+  memset(&C, 0, sizeof(C));
+  C.v = (const ovol *)p;
+  cam_from(&C.src, src_pose, src_intr, margin);
+  ojob *J = &C.J;
+  J->v = C.v;
+  for (int a = 0; a < 3; ++a) {
+    for (int b = 0; b < 3; ++b) J->R[3 * a + b] = pose[4 * a + b];
+    J->t[a] = pose[4 * a + 3];
+  }
+  J->fx = intr[0]; J->fy = intr[1]; J->cx = intr[2]; J->cy = intr[3];
+  J->W = (int)intr[4]; J->H = (int)intr[5]; J->zmin = intr[6]; J->zmax = intr[7];
+  J->npix = npix; J->uv = uv; J->row0 = row0;
+  J->depth = depth; J->normal = normal; J->color = color; J->mask = mask;
+  if (nthreads <= 1) { worker_combined(&C); return; }
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, worker_combined, &C);
+  for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
+  free(th);
+}
+
+/* Conditional combination (eqs. condition_1-4): recombine iff
+ *   framesSinceStart < boot  OR  framesSinceLastUpdate > stale  OR
+ *   ||t - t_last|| > trans   OR  angle(R_last^T R) > rot.
+ * R38: frame indices count from 0 (framesSinceStart = frame), framesSinceLastUpdate = frame - last;
+ * the rotation distance is the angle of the relative rotation, acos((trace - 1) / 2). */
+int oracle_should_recombine(int64_t frame, int64_t last, const double pose[16], const double last_pose[16],
+                            int64_t boot, int64_t stale, double trans, double rot) {
+  if (frame < boot) return 1;
+  if (frame - last > stale) return 1;
+  double dt[3] = {pose[3] - last_pose[3], pose[7] - last_pose[7], pose[11] - last_pose[11]};
+  if (sqrt(dt[0] * dt[0] + dt[1] * dt[1] + dt[2] * dt[2]) > trans) return 1;
+  double tr = 0.0; /* trace(R_last^T R) = sum_ab R_last[a][b] R[a][b] */
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) tr += last_pose[4 * a + b] * pose[4 * a + b];
+  double cs = (tr - 1.0) / 2.0;
+  cs = cs > 1.0 ? 1.0 : (cs < -1.0 ? -1.0 : cs);
+  return acos(cs) > rot;
+}
