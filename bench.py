@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle time for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--mode", choices=["direct", "combined"], default="direct",
+                    help="direct: per-sample combination (the north-star path); combined: the paper's "
+                         "view-dependent combined TSDF (NEXT-1), recombined per eqs. 10-13 inside the timed loop")
     return ap.parse_args()
 
 
@@ -251,12 +254,32 @@ def run_dtsdf(args):
     out = R.render(poses, K)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
+    # combined mode (NEXT-1): every view is one frame of a sequence; before rendering it the
+    # recombination conditions (eqs. 10-13) decide whether the combined TSDF is
+    # recomputed at its pose.  The state runs on across warm-up and timed steps.
+    from paper_2301_12796_b200.dtsdf import should_recombine
+    seq = {"frame": 0, "last": 0, "last_pose": None, "combines": 0}
+
+    def step(d, n, c, m, host=False):
+        if args.mode == "direct":
+            R.render_into(poses, K, d, n, c, m, stream=stream)
+            return
+        for i in range(len(poses)):
+            f = seq["frame"]
+            if seq["last_pose"] is None or should_recombine(f, seq["last"], poses[i], seq["last_pose"]):
+                R.combine(poses[i], K, stream=stream)
+                seq["last"], seq["last_pose"] = f, poses[i]
+                seq["combines"] += 1
+            sl = slice(i, i + 1)
+            R.render_combined_into(poses[sl], K, d[sl], n[sl], c[sl], m[sl], stream=stream)
+            seq["frame"] = f + 1
+
     clocks = ClockSampler(local)
     clocks.start()
     for _ in range(args.warmup):
         if not args.no_flush:
             flush.fill_(1.0)
-        R.render_into(poses, K, out["depth"], out["normal"], out["color"], out["mask"], stream=stream)
+        step(out["depth"], out["normal"], out["color"], out["mask"])
     torch.cuda.synchronize()
     R.reset_kernel_times()
     R.set_profiling(True)
@@ -266,16 +289,18 @@ def run_dtsdf(args):
         dist.barrier()
     torch.cuda.synchronize()
     n_launch0 = R.launch_count()
+    combines0 = seq["combines"]
     for i in range(args.steps):
         if not args.no_flush:
             flush.fill_(1.0)
         starts[i].record(stream)
-        R.render_into(poses, K, out["depth"], out["normal"], out["color"], out["mask"], stream=stream)
+        step(out["depth"], out["normal"], out["color"], out["mask"])
         ends[i].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = R.launch_count() - n_launch0
+    combines = seq["combines"] - combines0
     clk = clocks.stop()
     R.set_profiling(False)
     kt = R.kernel_times()
@@ -286,17 +311,20 @@ def run_dtsdf(args):
     # ---- roofline of the dominant kernel (raycast) ----
     ray_ms = kt["raycast_ms"] / max(kt["raycast_launches"], 1)
     balg = load_json(os.path.join(ROOT, "profiles", "b_alg.json")) or {}
-    b_ray = balg.get(w.name, {}).get("bytes_per_ray")
+    b_ray = balg.get(w.name, {}).get("bytes_per_ray") if args.mode == "direct" else None
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     peak = peaks.get("hbm_gbs", 6650.0)
     ncu = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
-    traffic = ncu.get(w.name, {}).get("raycast_dram_bytes_per_launch")
+    traffic = ncu.get(w.name, {}).get("raycast_dram_bytes_per_launch") if args.mode == "direct" else None
     achieved = (b_ray * rays_per_step / (ray_ms / 1e3) / 1e9) if b_ray else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": "k_raycast", "kernel_ms": ray_ms, "bytes_per_ray_alg": b_ray,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
             "range_pass_ms": kt["range_ms"] / max(kt["range_launches"], 1)}
+    if args.mode == "combined":
+        roof["combine_ms_per_step"] = kt["combine_ms"] / args.steps
+        roof["recombinations_per_step"] = combines / args.steps
 
     # ---- end to end through the C ABI with pinned HOST outputs (copies inside the timing) ----
     H, W = K.height, K.width
@@ -308,7 +336,7 @@ def run_dtsdf(args):
     pose_host = torch.from_numpy(np.ascontiguousarray(poses)).pin_memory()
     e2e_steps = min(args.e2e_steps, args.steps)
     for _ in range(3):
-        R.render_into(pose_host.numpy(), K, hd, hn, hc, hm, stream=stream)
+        step(hd, hn, hc, hm)
     e2e_tot = 0.0
     if world > 1:
         dist.barrier()
@@ -317,7 +345,7 @@ def run_dtsdf(args):
             flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        R.render_into(pose_host.numpy(), K, hd, hn, hc, hm, stream=stream)  # synchronizes (host outputs)
+        step(hd, hn, hc, hm)  # synchronizes (host outputs)
         e2e_tot += time.perf_counter() - t0
     e2e_max = pdist.max_over_ranks(dist, e2e_tot, dev) if world > 1 else e2e_tot
     e2e = {"value": world * rays_per_step * e2e_steps / e2e_max / 1e6, "unit": UNIT,
@@ -333,7 +361,7 @@ def run_dtsdf(args):
     # ---- CPU oracle baseline (rank 0, N = 1 only) + a sampled parity check of this run ----
     cpu = None
     parity = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.mode == "direct":
         cpu, px, ora = cpu_baseline(w, args.cpu_seconds)
         g = {k: v[0].cpu().numpy()[px[:, 1], px[:, 0]] for k, v in out.items()}
         sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -344,7 +372,7 @@ def run_dtsdf(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scene, DESIGN.md §3)",
-        "config": describe(w, args.views),
+        "config": dict(describe(w, args.views), mode=args.mode),
         "frames_per_s": world * args.views * args.steps / (max_ms / 1e3),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,

@@ -53,6 +53,7 @@ extern "C" {
 #define DTSDF_ERR_NO_VOLUME (-3)        /* render before a successful commit */
 #define DTSDF_ERR_OUT_OF_MEMORY (-4)    /* device allocation failed */
 #define DTSDF_ERR_CUDA (-5)             /* CUDA runtime error (sticky) */
+#define DTSDF_ERR_NO_COMBINED (-6)      /* render_combined / combined query before dtsdf_combine */
 
 /* block coordinates must lie in [-2^20, 2^20) (21-bit packed index key) */
 #define DTSDF_MAX_BLOCK_COORD (1 << 20)
@@ -137,12 +138,56 @@ DTSDF_API int dtsdf_render_batch(dtsdf_ctx *ctx, int32_t n_views, const float *p
 /* Current volume: N blocks, U distinct block locations, device bytes held by the context. */
 DTSDF_API int dtsdf_volume_stats(dtsdf_ctx *ctx, int64_t *n_blocks, int64_t *n_locations, int64_t *bytes);
 
-/* Kernel timing (tracing).  While enabled, every range-pass and raycast launch is
- * bracketed by CUDA events on its stream.  dtsdf_kernel_times synchronizes those events and
- * returns the summed milliseconds and launch counts since the last reset: times_ms[0] range
- * pass, [1] raycast, [2] other (index build, memsets); counts[0..2] likewise. */
+/* ---- view-dependent combined TSDF --------------------
+ * Lemma 1: for a fixed camera the six directions combine into one conflict-free
+ * regular TSDF.  dtsdf_combine computes it "for every voxel in the view frustum",
+ * widened by margin x image size on every side (1/8), at integer voxel positions
+ * with the 6-neighbour gradient and the weights eq:combine_weight /
+ * eq:combine_tsdf_weight; readings R33-R35.  A voxel with no positive
+ * combination weight, or outside the widened frustum, is invalid.
+ *   pose_w_c, intr: the source camera (host); margin in [0, 16] (0.125 in the paper).
+ * Replaces the previous combined TSDF.  Runs on cuda_stream and synchronizes it (the number of
+ * combined block locations is read back).  Errors: INVALID_ARGUMENT, NO_VOLUME, OUT_OF_MEMORY, CUDA. */
+DTSDF_API int dtsdf_combine(dtsdf_ctx *ctx, const float pose_w_c[16], const dtsdf_intrinsics *intr, float margin,
+                            void *cuda_stream);
+
+/* Raycast the current combined TSDF "like a regular TSDF" (readings R36-R37) from
+ * n_views poses: same lattice, crossing rule, refinement, argument layout, host/device output
+ * handling and errors as dtsdf_render_batch, plus NO_COMBINED.  Valid for poses near the source
+ * pose (the recombination conditions below keep them near). */
+DTSDF_API int dtsdf_render_combined(dtsdf_ctx *ctx, int32_t n_views, const float *poses_w_c,
+                                    const dtsdf_intrinsics *intr, int32_t row0, int32_t row1, float *out_depth,
+                                    float *out_normal, uint8_t *out_color, uint8_t *out_dirmask, void *cuda_stream);
+
+/* Combined block locations (those with at least one valid voxel) and device bytes held. */
+DTSDF_API int dtsdf_combined_stats(dtsdf_ctx *ctx, int64_t *n_locations, int64_t *bytes);
+
+/* Export the combined TSDF to HOST buffers (synchronous; for checks and external consumers):
+ * locs int32 [n][3] block coordinates, sdf f32 [n][512] (NaN = invalid voxel), weight f32 [n][512]
+ * (sum of the combination weights, 0 = invalid), rgb u8 [n][512][3], mask u8 [n][512] (bit D:
+ * direction D contributed).  *n_out = n always; INVALID_ARGUMENT if capacity < n.  Location order
+ * is unspecified. */
+DTSDF_API int dtsdf_get_combined(dtsdf_ctx *ctx, int64_t capacity, int32_t *locs, float *sdf, float *weight,
+                                 uint8_t *rgb, uint8_t *mask, int64_t *n_out);
+
+/* Conditional combination (eqs. condition_1-4; reading R38): recombine iff
+ * frame < boot_frames OR frame - last > stale_frames OR |t - t_last| > translation (metres) OR
+ * angle(R_last^T R) > rotation (radians).  Frames count from 0; last = frame of the last combine.
+ * Returns 1 (recombine), 0, or INVALID_ARGUMENT (NULL, last > frame, non-positive thresholds). */
+typedef struct {
+  int32_t boot_frames, stale_frames; /* 5, 50 */
+  float translation, rotation;       /* 0.05 m, 0.05 * pi / 2 */
+} dtsdf_combine_policy;
+DTSDF_API void dtsdf_default_policy(dtsdf_combine_policy *policy);
+DTSDF_API int dtsdf_should_recombine(const dtsdf_combine_policy *policy, int64_t frame, int64_t last,
+                                     const float pose_w_c[16], const float last_pose_w_c[16]);
+
+/* Kernel timing (tracing).  While enabled, every range-pass, raycast and combine
+ * launch is bracketed by CUDA events on its stream.  dtsdf_kernel_times synchronizes those events
+ * and returns the summed milliseconds and launch counts since the last reset: times_ms[0] range
+ * pass, [1] raycast, [2] other (index build, memsets), [3] combine; counts[0..3] likewise. */
 DTSDF_API int dtsdf_set_profiling(dtsdf_ctx *ctx, int enable);
-DTSDF_API int dtsdf_kernel_times(dtsdf_ctx *ctx, double times_ms[3], int64_t counts[3]);
+DTSDF_API int dtsdf_kernel_times(dtsdf_ctx *ctx, double times_ms[4], int64_t counts[4]);
 DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
 
 /* Exact accelerations that can be switched off to check they are result-invisible:

@@ -178,7 +178,7 @@ def combined_voxels(ov: "OracleVolume", pose, K, ijk, margin: float = MARGIN):
     sdf, S = np.zeros(n), np.zeros(n)
     rgb = np.zeros((n, 3), np.uint8)
     mask = np.zeros(n, np.uint8)
-    lib().oracle_combined_voxels(ov.h, _ptr(_pose32(pose)), _ptr(_intr32(K)), float(margin), n, _ptr(ijk),
+    lib().oracle_combined_voxels(ov.h, _ptr(_pose32(pose)), _ptr(_intr32(K)), float(np.float32(margin)), n, _ptr(ijk),
                                  _ptr(valid), _ptr(sdf), _ptr(S), _ptr(rgb), _ptr(mask))
     return dict(valid=valid.astype(bool), sdf=sdf, weight=S, rgb=rgb, mask=mask)
 
@@ -201,7 +201,7 @@ def render_combined(ov: "OracleVolume", src_pose, src_K, pose, K, pixels=None, r
     color = np.zeros((npix, 3), np.uint8)
     mask = np.zeros(npix, np.uint8)
     threads = threads or os.cpu_count() or 1
-    lib().oracle_render_combined(ov.h, _ptr(_pose32(src_pose)), _ptr(_intr32(src_K)), float(margin),
+    lib().oracle_render_combined(ov.h, _ptr(_pose32(src_pose)), _ptr(_intr32(src_K)), float(np.float32(margin)),
                                  _ptr(_pose32(pose)), _ptr(_intr32(K)), npix, _ptr(uv), row0, threads, _ptr(depth),
                                  _ptr(normal), _ptr(color), _ptr(mask))
     return dict(depth=depth.reshape(shape), normal=normal.reshape(shape + (3,)), color=color.reshape(shape + (3,)),

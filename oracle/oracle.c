@@ -601,7 +601,10 @@ static int ccell(const ovol *v, const ocam *c, const int64_t cc[3], const double
  *            otherwise the gradient of the cell's own trilinear interpolant when |g| > 1e-3;
  *            otherwise 0;
  *   colour = min(255, floor(trilinear of the corners' u8 colours + 1/2));
- *   mask   = OR of the 8 corners' direction masks. */
+ *   mask   = OR of the direction masks of the corners whose trilinear weight is >= 1/8 (at least
+ *            one corner qualifies, so a hit has a nonempty mask; a plain OR over all 8 corners
+ *            would depend on which side of a voxel plane a root lying on that plane -- e.g. a
+ *            floor at z = 0 -- is refined to). */
 static void cshade(const ovol *v, const ocam *c, const int64_t cc[3], const double fr[3], double *nrm, uint8_t *col,
                    uint8_t *msk) {
   ocvox cor[8];
@@ -646,7 +649,7 @@ static void cshade(const ovol *v, const ocam *c, const int64_t cc[3], const doub
     int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
     double wt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
     for (int a = 0; a < 3; ++a) cs[a] += wt * (double)u8_round(cor[q].rgb[a]);
-    m |= cor[q].mask;
+    if (wt >= 0.125) m |= cor[q].mask;
   }
   for (int a = 0; a < 3; ++a) col[a] = u8_round(cs[a]);
   *msk = (uint8_t)m;

@@ -62,6 +62,16 @@ struct VolumeView {
   float delta, inv_delta;
 };
 
+// Device view of the view-dependent combined TSDF (NEXT-1, combine.cu): one combined brick per
+// selected block location, in the apron layout of the directional bricks.
+struct CombinedView {
+  const int *slot_of_entry;        // [table_cap] combined slot of a hash entry, -1 = not combined
+  const float *apron;              // [cap][kApronStride] combined sdf of voxels -1..9, NaN = invalid
+  const uchar4 *rgb;               // [cap][kRgbApronStride] u8 colour (xyz) + direction mask (w), voxels 0..8
+  const unsigned int *cell_pos;    // [cap][16] bit l: no valid corner of base cell l has sdf <= 0
+  const unsigned char *surf;       // [cap] 1 unless every base cell is certainly positive / invalid
+};
+
 // Per-view camera: world-from-camera rotation (row-major) and camera centre.
 struct ViewPose {
   float r[9];
@@ -85,7 +95,28 @@ struct RenderLaunch {
   unsigned char *out_color;        // [n_views][rows][W][3] or null
   unsigned char *out_mask;         // [n_views][rows][W] or null
   unsigned long long *dbg_timeline;  // DTSDF_STATS builds only: per-pixel start/end/smid
+  int combined;                    // 1: march the combined TSDF (comb) instead of the six directions
+  CombinedView comb;
   ViewPose pose[kViewsPerLaunch];
+};
+
+// Combine launch (combine.cu): the source camera in fp64 (from the float32 ABI values) for the
+// frustum test of reading R33, evaluated with the oracle's operation order and roundings.
+struct CombineLaunch {
+  VolumeView vol;
+  const int4 *locations;           // [U] (bx, by, bz, hash entry)
+  long long n_loc;
+  double R[9], t[3];
+  double fx, fy, cx, cy, z_min, z_max;
+  double mu, mv, umax, vmax;       // u in [-mu, umax], v in [-mv, vmax]
+  int *slot_of_entry;              // [table_cap], -1 on entry
+  int4 *comb_loc;                  // [cap] location + hash entry of each combined slot
+  unsigned int *n_sel;             // combined slots handed out
+  float *apron;                    // [cap][kApronStride]
+  uchar4 *rgb;                     // [cap][kRgbApronStride]
+  float *weight;                   // [cap][512] S = sum_D W_D of each interior voxel
+  unsigned int *cell_pos;          // [cap][16]
+  unsigned char *surf;             // [cap]
 };
 
 struct RangeLaunch {
@@ -104,6 +135,10 @@ struct RangeLaunch {
 // host launchers (render.cu)
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
 cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s);
+
+// host launchers (combine.cu)
+cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s);                  // interiors + slots
+cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s);  // aprons, masks
 
 // host launchers (volume.cu); all run on stream s and return the first launch error
 struct CommitScratch {

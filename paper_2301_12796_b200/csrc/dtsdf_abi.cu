@@ -27,7 +27,7 @@ int fail(int code, const std::string &msg) {
 
 struct TimedLaunch {
   cudaEvent_t start, stop;
-  int kind;  // 0 range, 1 raycast, 2 other
+  int kind;  // 0 range, 1 raycast, 2 other, 3 combine
 };
 
 }  // namespace
@@ -66,11 +66,21 @@ struct dtsdf_ctx {
   size_t host_stage_cap = 0;
   int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1;
   int *tile_counter = nullptr;
+  // view-dependent combined TSDF (NEXT-1, combine.cu)
+  bool combined = false;
+  int64_t n_comb = 0, comb_cap = 0;
+  unsigned int comb_entries = 0;  // slot_of_entry length (table capacity at allocation)
+  int *comb_slot = nullptr;
+  int4 *comb_loc = nullptr;
+  float *comb_apron = nullptr, *comb_weight = nullptr;
+  uchar4 *comb_rgb = nullptr;
+  unsigned int *comb_cell_pos = nullptr, *comb_count = nullptr;
+  unsigned char *comb_surf = nullptr;
   // tracing
   bool profiling = false;
   std::vector<TimedLaunch> timed;
-  double times_ms[3] = {0, 0, 0};
-  int64_t counts[3] = {0, 0, 0};
+  double times_ms[4] = {0, 0, 0, 0};
+  int64_t counts[4] = {0, 0, 0, 0};
   int64_t launches = 0;
 };
 
@@ -93,7 +103,22 @@ void dfree(T *&p) {
   p = nullptr;
 }
 
+void free_combined(dtsdf_ctx *c) {
+  dfree(c->comb_slot);
+  dfree(c->comb_loc);
+  dfree(c->comb_apron);
+  dfree(c->comb_weight);
+  dfree(c->comb_rgb);
+  dfree(c->comb_cell_pos);
+  dfree(c->comb_surf);
+  dfree(c->comb_count);
+  c->combined = false;
+  c->n_comb = c->comb_cap = 0;
+  c->comb_entries = 0;
+}
+
 void free_volume(dtsdf_ctx *c) {
+  free_combined(c);
   dfree(c->keys);
   dfree(c->sdf);
   dfree(c->weight);
@@ -241,6 +266,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   cudaSetDevice(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   c->committed = false;
+  free_combined(c);
   dfree(c->table);
   dfree(c->bitmap);
   dfree(c->surface);
@@ -367,7 +393,8 @@ int dtsdf_upload_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, const int32_
 }
 
 static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
-                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, cudaStream_t s) {
+                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, cudaStream_t s,
+                       bool comb) {
   const int W = K->width;
   const int rows = row1 - row0;
   const int tiles_x = (W + kRangeTile - 1) / kRangeTile, tiles_y = (rows + kRangeTile - 1) / kRangeTile;
@@ -406,8 +433,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   for (int v0 = 0; v0 < n_views; v0 += kViewsPerLaunch) {
     const int nv = std::min(kViewsPerLaunch, n_views - v0);
     rl.vol = V;
-    rl.locations = c->locations;
-    rl.n_locations = c->n_loc;
+    rl.locations = comb ? c->comb_loc : c->locations;  // combined: only the combined locations bound rays
+    rl.n_locations = comb ? c->n_comb : c->n_loc;
     rl.fx = K->fx; rl.fy = K->fy; rl.cx = K->cx; rl.cy = K->cy; rl.z_min = K->z_min; rl.z_max = K->z_max;
     rl.width = W; rl.height = K->height; rl.row0 = row0; rl.row1 = row1;
     rl.n_views = nv; rl.tiles_x = tiles_x; rl.tiles_y = tiles_y;
@@ -425,7 +452,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     CK(c, cudaMemsetAsync(c->z_near, 0x7F, vt * 4, s), "range init");  // 0x7F7F7F7F = 3.4e38
     CK(c, cudaMemsetAsync(c->z_far, 0x00, vt * 4, s), "range init");
     end_timed(c, s, &tl);
-    begin_timed(c, 0, s, &tl, c->n_loc > 0 ? 1 : 0);
+    begin_timed(c, 0, s, &tl, rl.n_locations > 0 ? 1 : 0);
     CK(c, launch_range(rl, s), "range pass");
     end_timed(c, s, &tl);
     pl.vol = V;
@@ -445,6 +472,12 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.out_color = color ? color + 3 * px : nullptr;
     pl.out_mask = mask ? mask + px : nullptr;
     pl.dbg_timeline = nullptr;
+    pl.combined = comb ? 1 : 0;
+    pl.comb.slot_of_entry = c->comb_slot;
+    pl.comb.apron = c->comb_apron;
+    pl.comb.rgb = c->comb_rgb;
+    pl.comb.cell_pos = c->comb_cell_pos;
+    pl.comb.surf = c->comb_surf;
 #ifdef DTSDF_STATS
     {
       static unsigned long long *tl_buf = nullptr;
@@ -468,8 +501,9 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   return DTSDF_OK;
 }
 
-int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
-                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, void *stream) {
+static int render_batch_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K,
+                             int32_t row0, int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask,
+                             void *stream, bool comb) {
   if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
   int rc = check_intr(K);
@@ -480,13 +514,14 @@ int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   for (int64_t i = 0; i < 16 * (int64_t)n_views; ++i)
     if (!std::isfinite(poses[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
   if (!c->committed) return fail(DTSDF_ERR_NO_VOLUME, "no committed volume");
+  if (comb && !c->combined) return fail(DTSDF_ERR_NO_COMBINED, "no combined TSDF (call dtsdf_combine)");
   cudaSetDevice(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool dev = is_device_ptr(depth);
   if ((normal && is_device_ptr(normal) != dev) || (color && is_device_ptr(color) != dev) ||
       (mask && is_device_ptr(mask) != dev))
     return fail(DTSDF_ERR_INVALID_ARGUMENT, "outputs must be all device or all host pointers");
-  if (dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s);
+  if (dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s, comb);
   // host outputs: render into device scratch, copy back, synchronize
   const size_t px = (size_t)n_views * (row1 - row0) * K->width;
   const size_t need = px * (4 + 12 + 3 + 1) + 64;
@@ -505,7 +540,7 @@ int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   float *dn = normal ? (float *)(base + px * 4) : nullptr;
   uint8_t *dc = color ? (uint8_t *)(base + px * 16) : nullptr;
   uint8_t *dm = mask ? (uint8_t *)(base + px * 19) : nullptr;
-  rc = render_impl(c, n_views, poses, K, row0, row1, dd, dn, dc, dm, s);
+  rc = render_impl(c, n_views, poses, K, row0, row1, dd, dn, dc, dm, s, comb);
   if (rc) return rc;
   CK(c, cudaMemcpyAsync(depth, dd, px * 4, cudaMemcpyDeviceToHost, s), "d2h depth");
   if (normal) CK(c, cudaMemcpyAsync(normal, dn, px * 12, cudaMemcpyDeviceToHost, s), "d2h normal");
@@ -513,6 +548,170 @@ int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   if (mask) CK(c, cudaMemcpyAsync(mask, dm, px, cudaMemcpyDeviceToHost, s), "d2h mask");
   CK(c, cudaStreamSynchronize(s), "render sync");
   return DTSDF_OK;
+}
+
+int dtsdf_render_batch(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
+                       int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, void *stream) {
+  return render_batch_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, stream, false);
+}
+
+int dtsdf_render_combined(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
+                          int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, void *stream) {
+  return render_batch_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, stream, true);
+}
+
+int dtsdf_combine(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float margin, void *stream) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  if (!pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is NULL");
+  for (int i = 0; i < 16; ++i)
+    if (!std::isfinite(pose[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
+  if (!(margin >= 0.f) || !(margin <= 16.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "margin must lie in [0, 16]");
+  if (!c->committed) return fail(DTSDF_ERR_NO_VOLUME, "no committed volume");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  c->combined = false;
+  // capacity: every allocated location (kept across combines of the same volume)
+  const int64_t cap = std::max<int64_t>(c->n_loc, 1);
+  if (c->comb_cap < cap || c->comb_entries != c->table_cap) {
+    free_combined(c);
+    if (dalloc(c->comb_slot, (size_t)c->table_cap * 4) != cudaSuccess ||
+        dalloc(c->comb_loc, (size_t)cap * sizeof(int4)) != cudaSuccess ||
+        dalloc(c->comb_apron, (size_t)cap * kApronStride * 4) != cudaSuccess ||
+        dalloc(c->comb_weight, (size_t)cap * kVoxPerBlock * 4) != cudaSuccess ||
+        dalloc(c->comb_rgb, (size_t)cap * kRgbApronStride * sizeof(uchar4)) != cudaSuccess ||
+        dalloc(c->comb_cell_pos, (size_t)cap * 64) != cudaSuccess || dalloc(c->comb_surf, (size_t)cap) != cudaSuccess ||
+        dalloc(c->comb_count, 16) != cudaSuccess) {
+      cudaGetLastError();
+      free_combined(c);
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "combined TSDF buffers");
+    }
+    c->comb_cap = cap;
+    c->comb_entries = c->table_cap;
+  }
+  CombineLaunch L;
+  L.vol.table = c->table;
+  L.vol.table_mask = c->table_cap - 1;
+  L.vol.loc_grid = c->use_grid ? c->loc_grid : nullptr;
+  L.vol.lo_x = c->lo[0]; L.vol.lo_y = c->lo[1]; L.vol.lo_z = c->lo[2];
+  L.vol.dim_x = c->dim[0]; L.vol.dim_y = c->dim[1]; L.vol.dim_z = c->dim[2];
+  L.vol.apron = c->apron;
+  L.vol.rgb_apron = c->rgb_apron;
+  L.vol.voxel_size = c->params.voxel_size;
+  L.vol.inv_voxel = 1.0f / c->params.voxel_size;
+  L.vol.theta = c->params.theta;
+  L.vol.cos_theta = cosf(c->params.theta);
+  L.vol.sin_theta = sinf(c->params.theta);
+  L.vol.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
+  L.locations = c->locations;
+  L.n_loc = c->n_loc;
+  for (int a = 0; a < 3; ++a) {
+    for (int b = 0; b < 3; ++b) L.R[3 * a + b] = (double)pose[4 * a + b];
+    L.t[a] = (double)pose[4 * a + 3];
+  }
+  L.fx = K->fx; L.fy = K->fy; L.cx = K->cx; L.cy = K->cy; L.z_min = K->z_min; L.z_max = K->z_max;
+  L.mu = (double)margin * (double)K->width;
+  L.mv = (double)margin * (double)K->height;
+  L.umax = (double)(K->width - 1) + L.mu;
+  L.vmax = (double)(K->height - 1) + L.mv;
+  L.slot_of_entry = c->comb_slot;
+  L.comb_loc = c->comb_loc;
+  L.n_sel = c->comb_count;
+  L.apron = c->comb_apron;
+  L.rgb = c->comb_rgb;
+  L.weight = c->comb_weight;
+  L.cell_pos = c->comb_cell_pos;
+  L.surf = c->comb_surf;
+  TimedLaunch tl{};
+  CK(c, cudaMemsetAsync(c->comb_slot, 0xFF, (size_t)c->table_cap * 4, s), "combine init");
+  CK(c, cudaMemsetAsync(c->comb_count, 0, 16, s), "combine init");
+  begin_timed(c, 3, s, &tl, c->n_loc > 0 ? 1 : 0);
+  CK(c, launch_combine(L, s), "combine");
+  end_timed(c, s, &tl);
+  unsigned int nsel = 0;
+  CK(c, cudaMemcpyAsync(&nsel, c->comb_count, 4, cudaMemcpyDeviceToHost, s), "combine readback");
+  CK(c, cudaStreamSynchronize(s), "combine sync");
+  begin_timed(c, 3, s, &tl, nsel > 0 ? 2 : 0);
+  CK(c, launch_combine_finish(L, (long long)nsel, s), "combine finish");
+  end_timed(c, s, &tl);
+  c->n_comb = nsel;
+  c->combined = true;
+  return DTSDF_OK;
+}
+
+int dtsdf_combined_stats(dtsdf_ctx *c, int64_t *n_locations, int64_t *bytes) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (!c->combined) return fail(DTSDF_ERR_NO_COMBINED, "no combined TSDF");
+  if (n_locations) *n_locations = c->n_comb;
+  if (bytes)
+    *bytes = (int64_t)c->comb_entries * 4 +
+             c->comb_cap * (int64_t)(sizeof(int4) + kApronStride * 4 + kVoxPerBlock * 4 + kRgbApronStride * 4 + 64 + 1);
+  return DTSDF_OK;
+}
+
+int dtsdf_get_combined(dtsdf_ctx *c, int64_t capacity, int32_t *locs, float *sdf, float *weight, uint8_t *rgb,
+                       uint8_t *mask, int64_t *n_out) {
+  if (!c || !n_out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx/n_out is NULL");
+  if (!c->combined) return fail(DTSDF_ERR_NO_COMBINED, "no combined TSDF");
+  *n_out = c->n_comb;
+  if (capacity < c->n_comb) return fail(DTSDF_ERR_INVALID_ARGUMENT, "capacity smaller than the combined locations");
+  if (c->n_comb == 0) return DTSDF_OK;
+  if (!locs || !sdf || !weight || !rgb || !mask) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL output");
+  cudaSetDevice(c->device);
+  const size_t n = (size_t)c->n_comb;
+  std::vector<int4> hl(n);
+  std::vector<float> ha(n * kApronStride), hw(n * kVoxPerBlock);
+  std::vector<uchar4> hr(n * kRgbApronStride);
+  CK(c, cudaDeviceSynchronize(), "get_combined sync");
+  CK(c, cudaMemcpy(hl.data(), c->comb_loc, n * sizeof(int4), cudaMemcpyDeviceToHost), "get_combined");
+  CK(c, cudaMemcpy(ha.data(), c->comb_apron, n * kApronStride * 4, cudaMemcpyDeviceToHost), "get_combined");
+  CK(c, cudaMemcpy(hw.data(), c->comb_weight, n * kVoxPerBlock * 4, cudaMemcpyDeviceToHost), "get_combined");
+  CK(c, cudaMemcpy(hr.data(), c->comb_rgb, n * kRgbApronStride * sizeof(uchar4), cudaMemcpyDeviceToHost), "get_combined");
+  for (size_t i = 0; i < n; ++i) {
+    locs[3 * i + 0] = hl[i].x;
+    locs[3 * i + 1] = hl[i].y;
+    locs[3 * i + 2] = hl[i].z;
+    for (int l = 0; l < kVoxPerBlock; ++l) {
+      const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+      sdf[i * kVoxPerBlock + l] = ha[i * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1)];
+      weight[i * kVoxPerBlock + l] = hw[i * kVoxPerBlock + l];
+      const uchar4 q = hr[i * kRgbApronStride + lx + kRgbApron * ly + kRgbApron * kRgbApron * lz];
+      rgb[3 * (i * kVoxPerBlock + l) + 0] = q.x;
+      rgb[3 * (i * kVoxPerBlock + l) + 1] = q.y;
+      rgb[3 * (i * kVoxPerBlock + l) + 2] = q.z;
+      mask[i * kVoxPerBlock + l] = q.w;
+    }
+  }
+  return DTSDF_OK;
+}
+
+void dtsdf_default_policy(dtsdf_combine_policy *p) {
+  if (!p) return;
+  p->boot_frames = 5;
+  p->stale_frames = 50;
+  p->translation = 0.05f;
+  p->rotation = (float)(0.05 * 3.14159265358979323846 / 2.0);
+}
+
+int dtsdf_should_recombine(const dtsdf_combine_policy *p, int64_t frame, int64_t last, const float pose[16],
+                           const float last_pose[16]) {
+  if (!p || !pose || !last_pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (frame < 0 || last < 0 || last > frame) return fail(DTSDF_ERR_INVALID_ARGUMENT, "need 0 <= last <= frame");
+  if (!(p->translation > 0.f) || !(p->rotation > 0.f) || p->boot_frames < 0 || p->stale_frames < 0)
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "policy thresholds must be positive");
+  if (frame < p->boot_frames) return 1;                 // eq. condition_1: boot up
+  if (frame - last > p->stale_frames) return 1;         // eq. condition_2: stale state
+  double d2 = 0.0, tr = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    const double d = (double)pose[4 * a + 3] - (double)last_pose[4 * a + 3];
+    d2 += d * d;
+    for (int b = 0; b < 3; ++b) tr += (double)last_pose[4 * a + b] * (double)pose[4 * a + b];
+  }
+  if (std::sqrt(d2) > (double)p->translation) return 1;  // eq. condition_3: translation
+  const double cs = std::min(1.0, std::max(-1.0, (tr - 1.0) / 2.0));
+  return std::acos(cs) > (double)p->rotation ? 1 : 0;   // eq. condition_4: rotation
 }
 
 int dtsdf_render(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float *depth, float *normal,
@@ -535,7 +734,7 @@ int dtsdf_set_profiling(dtsdf_ctx *c, int enable) {
   return DTSDF_OK;
 }
 
-int dtsdf_kernel_times(dtsdf_ctx *c, double times_ms[3], int64_t counts[3]) {
+int dtsdf_kernel_times(dtsdf_ctx *c, double times_ms[4], int64_t counts[4]) {
   if (!c || !times_ms || !counts) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
   for (auto &t : c->timed) {
     cudaError_t e = cudaEventSynchronize(t.stop);
@@ -548,7 +747,7 @@ int dtsdf_kernel_times(dtsdf_ctx *c, double times_ms[3], int64_t counts[3]) {
     cudaEventDestroy(t.stop);
   }
   c->timed.clear();
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     times_ms[i] = c->times_ms[i];
     counts[i] = c->counts[i];
   }
@@ -557,10 +756,10 @@ int dtsdf_kernel_times(dtsdf_ctx *c, double times_ms[3], int64_t counts[3]) {
 
 int dtsdf_reset_kernel_times(dtsdf_ctx *c) {
   if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
-  double t[3];
-  int64_t n[3];
+  double t[4];
+  int64_t n[4];
   int rc = dtsdf_kernel_times(c, t, n);
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     c->times_ms[i] = 0;
     c->counts[i] = 0;
   }

@@ -171,8 +171,8 @@ struct Cursor {
 };
 
 // cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (k_cell_pos)
-__device__ __forceinline__ bool cell_positive(const VolumeView &V, const Cursor &cur, int l) {
-  return (__ldg(&V.cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;
+__device__ __forceinline__ bool cell_positive(const unsigned int *cell_pos, const Cursor &cur, int l) {
+  return (__ldg(&cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;
 }
 
 __device__ __forceinline__ int pick6(const int s[6], int d) {
@@ -313,6 +313,86 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   return res;
 }
 
+// NEXT-1: sample of the combined TSDF (readings R36-R37): plain trilinear of the combined sdf
+// over the 8 cell corners, invalid if any corner is (NaN); with shade = true the normal (central
+// differences of the trilinear field at +-s, else the cell's own trilinear gradient), the
+// trilinear u8 colour and the OR of the direction masks of the corners with weight >= 1/8.
+__device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const CombinedView &C, int slot, int lx, int ly,
+                                                  int lz, float fx, float fy, float fz, bool shade, ShadeResult *sh) {
+  const float *br = C.apron + (size_t)slot * kApronStride + (lx + kApron * ly + kApron * kApron * lz);
+  const float c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
+  const float c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
+  const float c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
+  const float c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
+  const float e00 = lerpf(c000, c100, fx), e10 = lerpf(c010, c110, fx);
+  const float e01 = lerpf(c001, c101, fx), e11 = lerpf(c011, c111, fx);
+  const float R0 = lerpf(e00, e10, fy), R1 = lerpf(e01, e11, fy);
+  const float phi = lerpf(R0, R1, fz);
+  SampleResult res;
+  res.valid = !isnan(phi);
+  res.f = res.valid ? phi : 0.0f;
+  if (shade && res.valid) {
+    const float xm00 = __ldg(br + APRON_IDX(-1, 0, 0)), xm10 = __ldg(br + APRON_IDX(-1, 1, 0));
+    const float xm01 = __ldg(br + APRON_IDX(-1, 0, 1)), xm11 = __ldg(br + APRON_IDX(-1, 1, 1));
+    const float xp00 = __ldg(br + APRON_IDX(2, 0, 0)), xp10 = __ldg(br + APRON_IDX(2, 1, 0));
+    const float xp01 = __ldg(br + APRON_IDX(2, 0, 1)), xp11 = __ldg(br + APRON_IDX(2, 1, 1));
+    const float ym00 = __ldg(br + APRON_IDX(0, -1, 0)), ym10 = __ldg(br + APRON_IDX(1, -1, 0));
+    const float ym01 = __ldg(br + APRON_IDX(0, -1, 1)), ym11 = __ldg(br + APRON_IDX(1, -1, 1));
+    const float yp00 = __ldg(br + APRON_IDX(0, 2, 0)), yp10 = __ldg(br + APRON_IDX(1, 2, 0));
+    const float yp01 = __ldg(br + APRON_IDX(0, 2, 1)), yp11 = __ldg(br + APRON_IDX(1, 2, 1));
+    const float zm00 = __ldg(br + APRON_IDX(0, 0, -1)), zm10 = __ldg(br + APRON_IDX(1, 0, -1));
+    const float zm01 = __ldg(br + APRON_IDX(0, 1, -1)), zm11 = __ldg(br + APRON_IDX(1, 1, -1));
+    const float zp00 = __ldg(br + APRON_IDX(0, 0, 2)), zp10 = __ldg(br + APRON_IDX(1, 0, 2));
+    const float zp01 = __ldg(br + APRON_IDX(0, 1, 2)), zp11 = __ldg(br + APRON_IDX(1, 1, 2));
+    // bilinear interpolants of the stencil layers (as eval_sample): P over (y,z) at x = -1,0,1,2
+    const float P0 = lerpf(lerpf(c000, c010, fy), lerpf(c001, c011, fy), fz);
+    const float P1 = lerpf(lerpf(c100, c110, fy), lerpf(c101, c111, fy), fz);
+    const float Pm = lerpf(lerpf(xm00, xm10, fy), lerpf(xm01, xm11, fy), fz);
+    const float Pp = lerpf(lerpf(xp00, xp10, fy), lerpf(xp01, xp11, fy), fz);
+    const float Q0 = lerpf(e00, e01, fz), Q1 = lerpf(e10, e11, fz);
+    const float Qm = lerpf(lerpf(ym00, ym10, fx), lerpf(ym01, ym11, fx), fz);
+    const float Qp = lerpf(lerpf(yp00, yp10, fx), lerpf(yp01, yp11, fx), fz);
+    const float Rm = lerpf(lerpf(zm00, zm10, fx), lerpf(zm01, zm11, fx), fy);
+    const float Rp = lerpf(lerpf(zp00, zp10, fx), lerpf(zp01, zp11, fx), fy);
+    const float half_inv_s = 0.5f * V.inv_voxel;
+    float gx = lerpf(P1 - Pm, Pp - P0, fx) * half_inv_s;
+    float gy = lerpf(Q1 - Qm, Qp - Q0, fy) * half_inv_s;
+    float gz = lerpf(R1 - Rm, Rp - R0, fz) * half_inv_s;
+    float gn = sqrtf(gx * gx + gy * gy + gz * gz);
+    if (!(gn > 1e-3f)) {  // stencil incomplete (NaN) or flat: the cell's own trilinear gradient
+      gx = (P1 - P0) * V.inv_voxel;
+      gy = (Q1 - Q0) * V.inv_voxel;
+      gz = (R1 - R0) * V.inv_voxel;
+      gn = sqrtf(gx * gx + gy * gy + gz * gz);
+    }
+    const float ig = gn > 1e-3f ? 1.0f / gn : 0.0f;
+    sh->n[0] = gx * ig; sh->n[1] = gy * ig; sh->n[2] = gz * ig;
+    const uchar4 *cb = C.rgb + (size_t)slot * kRgbApronStride + (lx + kRgbApron * ly + kRgbApron * kRgbApron * lz);
+    const uchar4 q000 = cb[RGB_IDX(0, 0, 0)], q100 = cb[RGB_IDX(1, 0, 0)], q010 = cb[RGB_IDX(0, 1, 0)],
+                 q110 = cb[RGB_IDX(1, 1, 0)], q001 = cb[RGB_IDX(0, 0, 1)], q101 = cb[RGB_IDX(1, 0, 1)],
+                 q011 = cb[RGB_IDX(0, 1, 1)], q111 = cb[RGB_IDX(1, 1, 1)];
+#define TRI_CH(ch)                                                                                              \
+  lerpf(lerpf(lerpf((float)q000.ch, (float)q100.ch, fx), lerpf((float)q010.ch, (float)q110.ch, fx), fy),        \
+        lerpf(lerpf((float)q001.ch, (float)q101.ch, fx), lerpf((float)q011.ch, (float)q111.ch, fx), fy), fz)
+    sh->c[0] = TRI_CH(x); sh->c[1] = TRI_CH(y); sh->c[2] = TRI_CH(z);
+#undef TRI_CH
+    sh->S = 1.0f;
+    // R37: OR of the masks of the corners with trilinear weight >= 1/8
+    const float ux = 1.f - fx, uy = 1.f - fy, uz = 1.f - fz;
+    int m = 0;
+    m |= (ux * uy * uz >= 0.125f) ? q000.w : 0;
+    m |= (fx * uy * uz >= 0.125f) ? q100.w : 0;
+    m |= (ux * fy * uz >= 0.125f) ? q010.w : 0;
+    m |= (fx * fy * uz >= 0.125f) ? q110.w : 0;
+    m |= (ux * uy * fz >= 0.125f) ? q001.w : 0;
+    m |= (fx * uy * fz >= 0.125f) ? q101.w : 0;
+    m |= (ux * fy * fz >= 0.125f) ? q011.w : 0;
+    m |= (fx * fy * fz >= 0.125f) ? q111.w : 0;
+    sh->mask = m;
+  }
+  return res;
+}
+
 // ------------------------------------------------------------------------------------------
 // a4-a7: the raycast kernel, one state machine per ray so that a warp's rays -- marching,
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
@@ -323,7 +403,8 @@ constexpr int kLookahead = 8;  // lattice points tested per certainly-positive s
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
 // a warp -- whatever phase each is in -- run the evaluation code together.
-struct Ray {
+template <bool kComb>
+struct RayT {
   int view, u, vrel;
   float r[3], o[3], ir[3], iLf;
   int k, k1;
@@ -398,7 +479,7 @@ struct Ray {
 #endif
   }
 
-  __device__ __forceinline__ void locate(const VolumeView &V, float tt) {
+  __device__ __forceinline__ void locate(const VolumeView &V, const CombinedView &C, float tt) {
     const float gx = fmaf(tt, rsx, g0x), gy = fmaf(tt, rsy, g0y), gz = fmaf(tt, rsz, g0z);
     const float flx = floorf(gx), fly = floorf(gy), flz = floorf(gz);
     frx = gx - flx; fry = gy - fly; frz = gz - flz;
@@ -434,6 +515,22 @@ struct Ray {
 #pragma unroll
         for (int d = 0; d < 6; ++d) cur.present |= (cur.slots[d] >= 0) << d;
       }
+      if constexpr (kComb) {  // NEXT-1: the location's combined brick (entry -> combined slot)
+        if (cur.occ) {
+          const int cs = __ldg(&C.slot_of_entry[cur.entry]);
+          if (cs >= 0) {
+            cur.entry = cs;
+            cur.surf = __ldg(&C.surf[cs]) != 0;
+            cur.present = 1;
+            cur.slots[0] = cs;
+          } else {  // allocated but not combined: invalid like an unallocated location
+            cur.occ = false;
+            cur.dist = 1;
+            cur.present = 0;
+            cur.entry = -1;
+          }
+        }
+      }
     }
   }
 
@@ -465,7 +562,7 @@ struct Ray {
       for (;;) {
         if (k > k1) return true;  // no crossing: a miss
         t = (float)k * V.delta;
-        locate(V, t);
+        locate(V, p.comb, t);
 #ifdef DTSDF_STATS
         ++st_skip;
 #endif
@@ -518,7 +615,7 @@ struct Ray {
             continue;
           }
         }
-        if (p.use_skip && cell_positive(V, cur, (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7))) {
+        if (p.use_skip && cell_positive(kComb ? p.comb.cell_pos : V.cell_pos, cur, (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7))) {
           // look ahead over the next lattice points of this location at once (independent
           // loads): in a run of certainly-positive points only the last one needs evaluating
           unsigned run = 1u;
@@ -528,7 +625,7 @@ struct Ray {
             const int jx = ibx + (int)floorf(fmaf(tj, rsx, g0x)), jy = iby + (int)floorf(fmaf(tj, rsy, g0y)),
                       jz = ibz + (int)floorf(fmaf(tj, rsz, g0z));
             const bool ok = (jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz &&
-                            cell_positive(V, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7));
+                            cell_positive(kComb ? p.comb.cell_pos : V.cell_pos, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7));
             run |= (unsigned)ok << j;
           }
           const int n = __ffs(~run) - 1;  // leading certainly-positive points (>= 1)
@@ -540,13 +637,13 @@ struct Ray {
             k += n - 1;
             if (n == kLookahead) continue;  // the run may go on: scan again from its last point
             t = (float)k * V.delta;
-            locate(V, t);  // the run's last point: evaluate it (prev for the next point)
+            locate(V, p.comb, t);  // the run's last point: evaluate it (prev for the next point)
           }
         }
         break;
       }
     } else {
-      locate(V, t);
+      locate(V, p.comb, t);
     }
     SampleResult s;
 #ifdef DTSDF_STATS
@@ -555,7 +652,10 @@ struct Ray {
     cy_adv += c1 - c0;
 #endif
     if (cur.occ) {
-      s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh);
+      if constexpr (kComb)
+        s = eval_comb(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, mode == kShade, &sh);
+      else
+        s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh);
     } else {
       s.valid = false;
       s.f = 0.f;
@@ -689,12 +789,13 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
 #ifndef DTSDF_CTA
 #define DTSDF_CTA 256
 #endif
+template <bool kComb>
 __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
   const int vrel = blockIdx.y * (DTSDF_CTA / 16) + (warp >> 1) * 4 + (lane >> 3);
   if (u >= p.width || p.row0 + vrel >= p.row1) return;
-  Ray ray;
+  RayT<kComb> ray;
 #ifdef DTSDF_STATS
   unsigned long long g_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
@@ -720,6 +821,7 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
 
 // persistent schedule: resident warps pull 8x4-pixel warp tiles (view-major, row-major) from an
 // atomic counter until the batch is done -- no CTA-granularity tail, uneven tiles balance out
+template <bool kComb>
 __global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_constant__ RenderLaunch p) {
   const int lane = threadIdx.x & 31;
   const int wx = (p.width + 7) >> 3, wy = (p.row1 - p.row0 + 3) >> 2;
@@ -733,7 +835,7 @@ __global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_cons
     const int ty = rr / wx, tx = rr - ty * wx;
     const int u = tx * 8 + (lane & 7), vrel = ty * 4 + (lane >> 3);
     if (u < p.width && p.row0 + vrel < p.row1) {
-      Ray ray;
+      RayT<kComb> ray;
       ray.init(p, view, u, vrel);
       while (!ray.step(p)) {
       }
@@ -742,15 +844,15 @@ __global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_cons
   }
 }
 
-cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s) {
-  if (p.n_views == 0) return cudaSuccess;
+template <bool kComb>
+static cudaError_t launch_raycast_t(const RenderLaunch &p, cudaStream_t s) {
   if (p.schedule == 1) {
     static int blocks_per_sm = 0, sms = 0;
     if (!blocks_per_sm) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raycast_persistent, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raycast_persistent<kComb>, 256, 0);
       if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     cudaError_t e = cudaMemsetAsync(p.tile_counter, 0, sizeof(int), s);
@@ -758,14 +860,19 @@ cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s) {
     const long long tiles = (long long)((p.width + 7) >> 3) * ((p.row1 - p.row0 + 3) >> 2) * p.n_views;
     long long grid = (long long)blocks_per_sm * sms;
     grid = grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8;
-    k_raycast_persistent<<<(unsigned)grid, 256, 0, s>>>(p);
+    k_raycast_persistent<kComb><<<(unsigned)grid, 256, 0, s>>>(p);
     return cudaGetLastError();
   }
   const int rows_per_cta = DTSDF_CTA / 16;
   dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.row1 - p.row0 + rows_per_cta - 1) / rows_per_cta),
             (unsigned)p.n_views);
-  k_raycast<<<grid, DTSDF_CTA, 0, s>>>(p);
+  k_raycast<kComb><<<grid, DTSDF_CTA, 0, s>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s) {
+  if (p.n_views == 0) return cudaSuccess;
+  return p.combined ? launch_raycast_t<true>(p, s) : launch_raycast_t<false>(p, s);
 }
 
 }  // namespace dtsdf

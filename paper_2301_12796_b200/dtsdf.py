@@ -15,14 +15,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DTSDF_LIB") or os.path.join(_HERE, "libdtsdf.so")
 
-OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR = 0, -1, -2, -3, -4, -5
+OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR, NO_COMBINED = 0, -1, -2, -3, -4, -5, -6
 VIEWS_PER_LAUNCH = 256
 
 EXPORTS = [
     "dtsdf_create", "dtsdf_destroy", "dtsdf_alloc_volume", "dtsdf_commit_volume", "dtsdf_upload_volume",
     "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
     "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
+    "dtsdf_combine", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
+    "dtsdf_should_recombine",
 ]
+MARGIN = 0.125  # PAPER.md:262 "(±1/8 image size)"
 OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID = 1, 2, 3, 4, 5
 
 
@@ -40,6 +43,11 @@ class Intrinsics(C.Structure):
 class VolumeParams(C.Structure):
     _fields_ = [("voxel_size", C.c_float), ("truncation", C.c_float), ("theta", C.c_float), ("step", C.c_float),
                 ("n_blocks", C.c_int64)]
+
+
+class CombinePolicy(C.Structure):
+    _fields_ = [("boot_frames", C.c_int32), ("stale_frames", C.c_int32), ("translation", C.c_float),
+                ("rotation", C.c_float)]
 
 
 class VolumeBuffers(C.Structure):
@@ -72,6 +80,13 @@ def lib():
         L.dtsdf_set_option.argtypes = [P, C.c_int, C.c_int]
         L.dtsdf_launch_count.argtypes = [P]
         L.dtsdf_launch_count.restype = I64
+        L.dtsdf_combine.argtypes = [P, P, C.POINTER(Intrinsics), C.c_float, P]
+        L.dtsdf_render_combined.argtypes = [P, I32, P, C.POINTER(Intrinsics), I32, I32, P, P, P, P, P]
+        L.dtsdf_combined_stats.argtypes = [P, C.POINTER(I64), C.POINTER(I64)]
+        L.dtsdf_get_combined.argtypes = [P, I64, P, P, P, P, P, C.POINTER(I64)]
+        L.dtsdf_default_policy.argtypes = [C.POINTER(CombinePolicy)]
+        L.dtsdf_default_policy.restype = None
+        L.dtsdf_should_recombine.argtypes = [C.POINTER(CombinePolicy), I64, I64, P, P]
         L.dtsdf_last_error.argtypes = []
         L.dtsdf_last_error.restype = C.c_char_p
         _lib = L
@@ -169,8 +184,10 @@ class Renderer:
         _check(lib().dtsdf_render_batch(self._h, poses.shape[0], poses.ctypes.data, C.byref(k), int(row0), int(row1),
                                         _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask), _stream_ptr(stream)))
 
-    def render(self, poses, K, row0=0, row1=None, stream=None, outputs=("normal", "color", "mask")):
-        """Allocate device outputs and render; returns dict of torch tensors [V, rows, W, ...]."""
+    def render(self, poses, K, row0=0, row1=None, stream=None, outputs=("normal", "color", "mask"),
+               combined=False):
+        """Allocate device outputs and render (the combined TSDF if combined=True); returns dict of
+        torch tensors [V, rows, W, ...]."""
         import torch
         poses = np.asarray(poses, np.float32).reshape(-1, 4, 4)
         row1 = K.height if row1 is None else row1
@@ -183,8 +200,41 @@ class Renderer:
             out["color"] = torch.empty((V, rows, W, 3), dtype=torch.uint8, device=dev)
         if "mask" in outputs:
             out["mask"] = torch.empty((V, rows, W), dtype=torch.uint8, device=dev)
-        self.render_into(poses, K, out["depth"], out.get("normal"), out.get("color"), out.get("mask"), row0, row1,
-                         stream)
+        fn = self.render_combined_into if combined else self.render_into
+        fn(poses, K, out["depth"], out.get("normal"), out.get("color"), out.get("mask"), row0, row1, stream)
+        return out
+
+    # -- combined TSDF (NEXT-1) -----------------------------------------------------------
+    def combine(self, pose, K, margin=MARGIN, stream=None):
+        """dtsdf_combine: the view-dependent combined TSDF of the source camera (pose, K)."""
+        pose = np.ascontiguousarray(np.asarray(pose, np.float32).reshape(16))
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_combine(self._h, pose.ctypes.data, C.byref(k), float(margin), _stream_ptr(stream)))
+
+    def render_combined_into(self, poses, K, depth, normal=None, color=None, mask=None, row0=0, row1=None,
+                             stream=None):
+        """dtsdf_render_combined into caller-owned outputs (layout as render_into)."""
+        poses = np.ascontiguousarray(np.asarray(poses, np.float32).reshape(-1, 16))
+        row1 = K.height if row1 is None else row1
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_render_combined(self._h, poses.shape[0], poses.ctypes.data, C.byref(k), int(row0),
+                                           int(row1), _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask),
+                                           _stream_ptr(stream)))
+
+    def combined_stats(self):
+        u, b = C.c_int64(), C.c_int64()
+        _check(lib().dtsdf_combined_stats(self._h, C.byref(u), C.byref(b)))
+        return {"n_locations": u.value, "bytes": b.value}
+
+    def get_combined(self):
+        """dtsdf_get_combined -> dict(locs [n,3], sdf [n,512], weight [n,512], rgb [n,512,3], mask [n,512])."""
+        n = self.combined_stats()["n_locations"]
+        out = {"locs": np.zeros((n, 3), np.int32), "sdf": np.zeros((n, 512), np.float32),
+               "weight": np.zeros((n, 512), np.float32), "rgb": np.zeros((n, 512, 3), np.uint8),
+               "mask": np.zeros((n, 512), np.uint8)}
+        got = C.c_int64()
+        _check(lib().dtsdf_get_combined(self._h, n, _ptr(out["locs"]), _ptr(out["sdf"]), _ptr(out["weight"]),
+                                        _ptr(out["rgb"]), _ptr(out["mask"]), C.byref(got)))
         return out
 
     # -- tracing ------------------------------------------------------------------------
@@ -192,11 +242,12 @@ class Renderer:
         _check(lib().dtsdf_set_profiling(self._h, int(bool(enable))))
 
     def kernel_times(self):
-        t = np.zeros(3, np.float64)
-        n = np.zeros(3, np.int64)
+        t = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
         _check(lib().dtsdf_kernel_times(self._h, t.ctypes.data, n.ctypes.data))
-        return {"range_ms": t[0], "raycast_ms": t[1], "other_ms": t[2], "range_launches": int(n[0]),
-                "raycast_launches": int(n[1]), "other_launches": int(n[2])}
+        return {"range_ms": t[0], "raycast_ms": t[1], "other_ms": t[2], "combine_ms": t[3],
+                "range_launches": int(n[0]), "raycast_launches": int(n[1]), "other_launches": int(n[2]),
+                "combine_launches": int(n[3])}
 
     def reset_kernel_times(self):
         _check(lib().dtsdf_reset_kernel_times(self._h))
@@ -206,6 +257,23 @@ class Renderer:
 
     def launch_count(self) -> int:
         return int(lib().dtsdf_launch_count(self._h))
+
+
+def default_policy() -> CombinePolicy:
+    p = CombinePolicy()
+    lib().dtsdf_default_policy(C.byref(p))
+    return p
+
+
+def should_recombine(frame: int, last: int, pose, last_pose, policy: Optional[CombinePolicy] = None) -> bool:
+    """dtsdf_should_recombine: eqs. condition_1-4 (PAPER.md:256-259)."""
+    policy = policy or default_policy()
+    a = np.ascontiguousarray(np.asarray(pose, np.float32).reshape(16))
+    b = np.ascontiguousarray(np.asarray(last_pose, np.float32).reshape(16))
+    rc = lib().dtsdf_should_recombine(C.byref(policy), int(frame), int(last), a.ctypes.data, b.ctypes.data)
+    if rc < 0:
+        _check(rc)
+    return bool(rc)
 
 
 def _wrap_device(ptr, shape, dtype, device):

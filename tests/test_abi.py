@@ -63,3 +63,31 @@ def test_null_context_errors_without_gpu(lib):
     assert b"NULL" in lib.dtsdf_last_error()
     assert lib.dtsdf_set_option(None, 1, 0) == -1
     assert lib.dtsdf_destroy(None) == 0
+
+
+def test_should_recombine_matches_oracle_conditions():
+    """dtsdf_should_recombine (host code of the C ABI, no GPU call) agrees with the oracle's
+    eqs. condition_1-4 on random pose pairs around the thresholds."""
+    import numpy as np
+
+    import oracle
+    from paper_2301_12796_b200.dtsdf import should_recombine
+    rng = np.random.default_rng(11)
+    for _ in range(400):
+        frame = int(rng.integers(0, 120))
+        last = int(rng.integers(0, frame + 1))
+        ax = rng.normal(size=3)
+        ax /= np.linalg.norm(ax)
+        ang = rng.uniform(0, 0.16)
+        Kx = np.array([[0, -ax[2], ax[1]], [ax[2], 0, -ax[0]], [-ax[1], ax[0], 0]])
+        Rr = np.eye(3) + np.sin(ang) * Kx + (1 - np.cos(ang)) * Kx @ Kx
+        A = np.eye(4)
+        A[:3, 3] = rng.normal(size=3)
+        B = np.eye(4)
+        B[:3, :3] = Rr
+        B[:3, 3] = A[:3, 3] + rng.normal(size=3) / np.sqrt(3) * rng.uniform(0, 0.1)
+        a = should_recombine(frame, last, B, A)
+        b = oracle.should_recombine(frame, last, B, A)
+        tdist = np.linalg.norm(B[:3, 3] - A[:3, 3])
+        if abs(tdist - 0.05) > 1e-5 and abs(ang - 0.05 * np.pi / 2) > 1e-4:  # float32 poses at the edges
+            assert a == b, (frame, last, tdist, ang)
