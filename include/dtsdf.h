@@ -159,7 +159,7 @@ DTSDF_API int dtsdf_render_combined(dtsdf_ctx *ctx, int32_t n_views, const float
                                     const dtsdf_intrinsics *intr, int32_t row0, int32_t row1, float *out_depth,
                                     float *out_normal, uint8_t *out_color, uint8_t *out_dirmask, void *cuda_stream);
 
-/* Combined block locations (those with at least one valid voxel) and device bytes held. */
+/* Combined block locations (those with at least one voxel in the widened frustum) and device bytes held. */
 DTSDF_API int dtsdf_combined_stats(dtsdf_ctx *ctx, int64_t *n_locations, int64_t *bytes);
 
 /* Export the combined TSDF to HOST buffers (synchronous; for checks and external consumers):
