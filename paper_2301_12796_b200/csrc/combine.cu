@@ -132,27 +132,6 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
     d[2] = __dsub_rn(__dmul_rn((double)k, s), p.t[2]);
   }
   const int off = CAPRON(lx, ly, lz), coff = lx + kRgbApron * ly + kRgbApron * kRgbApron * lz;
-  float2 c[6];
-  float nb[6][6];
-  uchar4 q[6];
-#pragma unroll
-  for (int D = 0; D < 6; ++D) {
-    c[D] = make_float2(0.f, 0.f);
-    q[D] = make_uchar4(0, 0, 0, 0);
-#pragma unroll
-    for (int a = 0; a < 6; ++a) nb[D][a] = 0.f;
-    if (sl[D] >= 0 && in) {
-      const float2 *br = V.apron + (size_t)sl[D] * kApronStride + off;
-      c[D] = __ldg(br);
-      nb[D][0] = __ldg(&br[1].x);
-      nb[D][1] = __ldg(&br[-1].x);
-      nb[D][2] = __ldg(&br[kApron].x);
-      nb[D][3] = __ldg(&br[-kApron].x);
-      nb[D][4] = __ldg(&br[kApron * kApron].x);
-      nb[D][5] = __ldg(&br[-kApron * kApron].x);
-      q[D] = __ldg(V.rgb_apron + (size_t)sl[D] * kRgbApronStride + coff);
-    }
-  }
   // r in fp32 from the fp64 offset (its rounding is far below the tolerance of the weights)
   const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
   const float dd = dx * dx + dy * dy + dz * dz;
@@ -163,38 +142,75 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
   float C1[3] = {0.f, 0.f, 0.f}, C2[3] = {0.f, 0.f, 0.f};
   int m1 = 0, m2 = 0;
   bool any_grad = false;
+  // present directions, two at a time: both directions' loads are in flight together
+  unsigned present = 0;
 #pragma unroll
-  for (int D = 0; D < 6; ++D) {
-    if (!(c[D].y > 0.0f)) continue;  // absent, or D holds no data at the voxel (reading R8)
-    const float gx = (nb[D][0] - nb[D][1]) * half_inv_s;
-    const float gy = (nb[D][2] - nb[D][3]) * half_inv_s;
-    const float gz = (nb[D][4] - nb[D][5]) * half_inv_s;
-    const float gn = sqrtf(gx * gx + gy * gy + gz * gz);
-    const int axis = D >> 1;
-    const float sign = (D & 1) ? -1.0f : 1.0f;
-    const float r_axis = axis == 0 ? rx : (axis == 1 ? ry : rz);
-    const float cr = (float)q[D].x, cg = (float)q[D].y, cb = (float)q[D].z;
-    // eq:combine_tsdf_weight: omega <v^D, -r>^+
-    const float W2 = c[D].y * fmaxf(-sign * r_axis, 0.0f);
-    if (W2 > 0.0f) {
-      S2 += W2;
-      F2 = fmaf(W2, c[D].x, F2);
-      C2[0] = fmaf(W2, cr, C2[0]); C2[1] = fmaf(W2, cg, C2[1]); C2[2] = fmaf(W2, cb, C2[2]);
-      m2 |= 1 << D;
+  for (int D = 0; D < 6; ++D) present |= (unsigned)(sl[D] >= 0) << D;
+  if (!in) present = 0;
+#pragma unroll 1
+  while (present) {
+    int Dp[2];
+    float2 c[2];
+    float nb[2][6];
+    uchar4 q[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      Dp[h] = present ? __ffs(present) - 1 : -1;
+      present &= present - 1;
+      c[h] = make_float2(0.f, 0.f);
+      q[h] = make_uchar4(0, 0, 0, 0);
+#pragma unroll
+      for (int a = 0; a < 6; ++a) nb[h][a] = 0.f;
+      if (Dp[h] >= 0) {
+        int slot_d = sl[0];
+#pragma unroll
+        for (int D = 1; D < 6; ++D) slot_d = Dp[h] == D ? sl[D] : slot_d;  // register select
+        const float2 *br = V.apron + (size_t)slot_d * kApronStride + off;
+        c[h] = __ldg(br);
+        nb[h][0] = __ldg(&br[1].x);
+        nb[h][1] = __ldg(&br[-1].x);
+        nb[h][2] = __ldg(&br[kApron].x);
+        nb[h][3] = __ldg(&br[-kApron].x);
+        nb[h][4] = __ldg(&br[kApron * kApron].x);
+        nb[h][5] = __ldg(&br[-kApron * kApron].x);
+        q[h] = __ldg(V.rgb_apron + (size_t)slot_d * kRgbApronStride + coff);
+      }
     }
-    if (gn > 1e-3f) {  // reading R8 (NaN -> false)
-      any_grad = true;
-      const float ig = 1.0f / gn;
-      const float nx = gx * ig, ny = gy * ig, nz = gz * ig;
-      const float n_axis = axis == 0 ? nx : (axis == 1 ? ny : nz);
-      const float nr = -(nx * rx + ny * ry + nz * rz);
-      // eq:combine_weight: w_dir(<n,v>) <n,-r>^+ omega
-      const float W1 = w_dir_c(sign * n_axis, V) * fmaxf(nr, 0.0f) * c[D].y;
-      if (W1 > 0.0f) {
-        S1 += W1;
-        F1 = fmaf(W1, c[D].x, F1);
-        C1[0] = fmaf(W1, cr, C1[0]); C1[1] = fmaf(W1, cg, C1[1]); C1[2] = fmaf(W1, cb, C1[2]);
-        m1 |= 1 << D;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int D = Dp[h];
+      if (D < 0 || !(c[h].y > 0.0f)) continue;  // D holds no data at the voxel (reading R8)
+      // the gradient from the 6 neighbouring voxels (NaN where unallocated)
+      const float gx = (nb[h][0] - nb[h][1]) * half_inv_s;
+      const float gy = (nb[h][2] - nb[h][3]) * half_inv_s;
+      const float gz = (nb[h][4] - nb[h][5]) * half_inv_s;
+      const float gn = sqrtf(gx * gx + gy * gy + gz * gz);
+      const int axis = D >> 1;
+      const float sign = (D & 1) ? -1.0f : 1.0f;
+      const float r_axis = axis == 0 ? rx : (axis == 1 ? ry : rz);
+      const float cr = (float)q[h].x, cg = (float)q[h].y, cb = (float)q[h].z;
+      // eq:combine_tsdf_weight: omega <v^D, -r>^+
+      const float W2 = c[h].y * fmaxf(-sign * r_axis, 0.0f);
+      if (W2 > 0.0f) {
+        S2 += W2;
+        F2 = fmaf(W2, c[h].x, F2);
+        C2[0] = fmaf(W2, cr, C2[0]); C2[1] = fmaf(W2, cg, C2[1]); C2[2] = fmaf(W2, cb, C2[2]);
+        m2 |= 1 << D;
+      }
+      if (gn > 1e-3f) {  // reading R8 (NaN -> false)
+        any_grad = true;
+        const float ig = 1.0f / gn;
+        const float nx = gx * ig, ny = gy * ig, nz = gz * ig;
+        const float n_axis = axis == 0 ? nx : (axis == 1 ? ny : nz);
+        const float nr = -(nx * rx + ny * ry + nz * rz);
+        // eq:combine_weight: w_dir(<n,v>) <n,-r>^+ omega
+        const float W1 = w_dir_c(sign * n_axis, V) * fmaxf(nr, 0.0f) * c[h].y;
+        if (W1 > 0.0f) {
+          S1 += W1;
+          F1 = fmaf(W1, c[h].x, F1);
+          C1[0] = fmaf(W1, cr, C1[0]); C1[1] = fmaf(W1, cg, C1[1]); C1[2] = fmaf(W1, cb, C1[2]);
+          m1 |= 1 << D;
+        }
       }
     }
   }
