@@ -4,7 +4,8 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 ``--impl reference`` legs may import this package.  The product path
 (``paper_2301_12796_b200``) never imports it, and it never imports the product path.
 
-``liboracle.so`` is plain C in fp64 (``oracle.c``); this module only marshals arguments.
+``liboracle.so`` is plain C in fp64 (``oracle.c`` raycast and combined TSDF, ``fusion.c``
+voxel-projection fusion); this module only marshals arguments.
 Every function cites the passage it follows in ``oracle.c``; DESIGN.md §4 lists the readings.
 """
 from __future__ import annotations
@@ -16,7 +17,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "fusion.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -26,9 +27,10 @@ CFLAGS = ["-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fno-fast-ma
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (no -ffast-math, no FMA contraction)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB_PATH) or any(os.path.getmtime(_LIB_PATH) < os.path.getmtime(s)
+                                                     for s in _SRCS):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-lm", "-o", tmp])
+        subprocess.check_call(["gcc", *CFLAGS, *_SRCS, "-lm", "-o", tmp])
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH
 
@@ -57,6 +59,17 @@ def lib():
         L.oracle_render_combined.restype = None
         L.oracle_should_recombine.argtypes = [I64, I64, P, P, I64, I64, D, D]
         L.oracle_should_recombine.restype = I32
+        L.oracle_fuse_create.argtypes = [D, D, D, I64, I64, P, P, P, P, C.POINTER(P)]
+        L.oracle_fuse_create.restype = I32
+        L.oracle_fuse_destroy.argtypes = [P]
+        L.oracle_fuse_count.argtypes = [P]
+        L.oracle_fuse_count.restype = I64
+        L.oracle_fuse_get.argtypes = [P, P, P, P, P, P]
+        L.oracle_fuse_get.restype = None
+        L.oracle_fuse_frame.argtypes = [P, P, P, P, P, P, P]
+        L.oracle_fuse_frame.restype = I64
+        L.oracle_depth_normals.argtypes = [P, P, P]
+        L.oracle_depth_normals.restype = None
         _lib = L
     return _lib
 
@@ -229,3 +242,69 @@ def ray_dirs(pose, K, pixels=None):
     L = np.linalg.norm(dt, axis=-1)
     r = (dt / L[:, None]) @ pose[:3, :3].T
     return pose[:3, 3], r, L
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT-2: voxel-projection fusion (fusion.c, readings R39-R46)
+# ------------------------------------------------------------------------------------------
+W_MAX, CARVE_WEIGHT, CARVE_RADIUS = 128.0, 1.0, 2
+
+
+def depth_normals(depth, K):
+    """Camera-frame normals of a depth map (fusion.c oracle_depth_normals, reading R39)."""
+    depth = np.ascontiguousarray(depth, np.float32)
+    out = np.zeros(depth.shape + (3,), np.float32)
+    lib().oracle_depth_normals(_ptr(depth), _ptr(_intr32(K)), _ptr(out))
+    return out
+
+
+class OracleFusion:
+    """A growable DTSDF fused from depth frames (fusion.c).  Parameters as the float32 values the
+    C ABI receives."""
+
+    def __init__(self, voxel_size, truncation, theta, capacity, vol=None):
+        f32 = lambda a: float(np.float32(a))  # noqa: E731
+        h = C.c_void_p()
+        n0 = 0 if vol is None else vol.n_blocks
+        self._init = None
+        if vol is not None:
+            self._init = (np.ascontiguousarray(vol.keys, np.int32), np.ascontiguousarray(vol.sdf, np.float32),
+                          np.ascontiguousarray(vol.weight, np.float32), np.ascontiguousarray(vol.rgb, np.uint8))
+        args = [_ptr(a) for a in self._init] if self._init else [None] * 4
+        rc = lib().oracle_fuse_create(f32(voxel_size), f32(truncation), f32(theta), int(capacity), int(n0), *args,
+                                      C.byref(h))
+        if rc != 0:
+            raise ValueError(f"oracle_fuse_create failed: {rc}")
+        self.h = h
+        self.voxel_size, self.truncation, self.theta = voxel_size, truncation, theta
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and _lib is not None:
+            _lib.oracle_fuse_destroy(h)
+            self.h = None
+
+    def fuse(self, depth, normal, color, pose, K, w_max=W_MAX, carve_weight=CARVE_WEIGHT, carve_radius=CARVE_RADIUS):
+        """Allocate + fuse one frame; returns the number of new blocks (raises when full)."""
+        depth = np.ascontiguousarray(depth, np.float32)
+        normal = np.ascontiguousarray(normal, np.float32)
+        color = None if color is None else np.ascontiguousarray(color, np.uint8)
+        prm = np.array([np.float32(w_max), np.float32(carve_weight), carve_radius], np.float64)
+        n = lib().oracle_fuse_frame(self.h, _ptr(depth), _ptr(normal), _ptr(color), _ptr(_pose32(pose)),
+                                    _ptr(_intr32(K)), _ptr(prm))
+        if n < 0:
+            raise MemoryError("oracle fusion capacity exhausted")
+        return int(n)
+
+    def volume(self, with_color_weight=False):
+        """The fused blocks as a scenes.BlockVolume (insertion order)."""
+        from scenes import BlockVolume
+        n = int(lib().oracle_fuse_count(self.h))
+        keys = np.zeros((n, 4), np.int32)
+        sdf = np.zeros((n, 512), np.float32)
+        w = np.zeros((n, 512), np.float32)
+        rgb = np.zeros((n, 512, 3), np.uint8)
+        cw = np.zeros((n, 512), np.float32)
+        lib().oracle_fuse_get(self.h, _ptr(keys), _ptr(sdf), _ptr(w), _ptr(rgb), _ptr(cw))
+        vol = BlockVolume(self.voxel_size, self.truncation, self.theta, keys, sdf, w, rgb, 0.0)
+        return (vol, cw) if with_color_weight else vol
