@@ -37,23 +37,25 @@ typedef struct {
   int32_t *keys; /* [cap][4] */
   float *sdf, *w, *cw;
   uint8_t *rgb;
-  int64_t hcap; /* open addressing over packed keys */
+  int64_t hcap; /* open addressing over (packed location, direction) */
   uint64_t *hkey;
+  int8_t *hdir;
   int64_t *hval;
 } ofuse;
 
-static uint64_t fu_pack(int64_t x, int64_t y, int64_t z, int64_t D) {
+/* 3 x 21-bit block coordinates (63 bits); the direction is kept beside it */
+static uint64_t fu_pack(int64_t x, int64_t y, int64_t z) {
   const uint64_t m = (1ull << 21) - 1;
   return ((uint64_t)(x + (1 << 20)) & m) | (((uint64_t)(y + (1 << 20)) & m) << 21) |
-         (((uint64_t)(z + (1 << 20)) & m) << 42) | ((uint64_t)D << 61);
+         (((uint64_t)(z + (1 << 20)) & m) << 42);
 }
 
-static int64_t fu_find(const ofuse *F, uint64_t k) {
-  uint64_t h = (k * 0x9E3779B97F4A7C15ull) >> 7;
+static int64_t fu_find(const ofuse *F, uint64_t k, int D) {
+  uint64_t h = ((k + (uint64_t)D * 0x632BE59BD9B4E019ull) * 0x9E3779B97F4A7C15ull) >> 7;
   for (int64_t i = 0; i < F->hcap; ++i) {
     int64_t slot = (int64_t)((h + (uint64_t)i) % (uint64_t)F->hcap);
     if (F->hval[slot] < 0) return -1 - slot; /* free slot, encoded */
-    if (F->hkey[slot] == k) return F->hval[slot];
+    if (F->hkey[slot] == k && F->hdir[slot] == D) return F->hval[slot];
   }
   return -1 - F->hcap;
 }
@@ -62,12 +64,13 @@ static int64_t floordiv8(int64_t i) { return (i >= 0) ? i / 8 : -((-i + 7) / 8);
 
 /* returns 0, -1 bad key, -2 duplicate, -4 capacity */
 static int fu_insert(ofuse *F, int64_t bx, int64_t by, int64_t bz, int64_t D, int init) {
-  uint64_t k = fu_pack(bx, by, bz, D);
-  int64_t r = fu_find(F, k);
+  uint64_t k = fu_pack(bx, by, bz);
+  int64_t r = fu_find(F, k, (int)D);
   if (r >= 0) return init ? -2 : 0;
   if (r == -1 - F->hcap || F->n >= F->cap) return -4;
   int64_t slot = -1 - r, b = F->n++;
   F->hkey[slot] = k;
+  F->hdir[slot] = (int8_t)D;
   F->hval[slot] = b;
   F->keys[4 * b + 0] = (int32_t)bx; F->keys[4 * b + 1] = (int32_t)by;
   F->keys[4 * b + 2] = (int32_t)bz; F->keys[4 * b + 3] = (int32_t)D;
@@ -84,7 +87,7 @@ static int fu_insert(ofuse *F, int64_t bx, int64_t by, int64_t bz, int64_t D, in
 void oracle_fuse_destroy(void *p) {
   ofuse *F = (ofuse *)p;
   if (!F) return;
-  free(F->keys); free(F->sdf); free(F->w); free(F->cw); free(F->rgb); free(F->hkey); free(F->hval);
+  free(F->keys); free(F->sdf); free(F->w); free(F->cw); free(F->rgb); free(F->hkey); free(F->hdir); free(F->hval);
   free(F);
 }
 
@@ -106,8 +109,12 @@ int oracle_fuse_create(double s, double tau, double theta, int64_t cap, int64_t 
   F->rgb = (uint8_t *)calloc(c * FU_VPB * 3, 1);
   F->hcap = 2 * (int64_t)c + 1;
   F->hkey = (uint64_t *)calloc((size_t)F->hcap, sizeof(uint64_t));
+  F->hdir = (int8_t *)calloc((size_t)F->hcap, 1);
   F->hval = (int64_t *)malloc(sizeof(int64_t) * (size_t)F->hcap);
-  if (!F->keys || !F->sdf || !F->w || !F->cw || !F->rgb || !F->hkey || !F->hval) { oracle_fuse_destroy(F); return -4; }
+  if (!F->keys || !F->sdf || !F->w || !F->cw || !F->rgb || !F->hkey || !F->hdir || !F->hval) {
+    oracle_fuse_destroy(F);
+    return -4;
+  }
   for (int64_t i = 0; i < F->hcap; ++i) F->hval[i] = -1;
   for (int64_t b = 0; b < n0; ++b) {
     if (keys[4 * b + 3] < 0 || keys[4 * b + 3] > 5) { oracle_fuse_destroy(F); return -1; }

@@ -158,6 +158,27 @@ def test_blending_band_splits_membership():
     assert pairs > 100
 
 
+def test_every_admitted_direction_is_allocated_at_any_height():
+    """A plane whose normal (cos 38.7 deg to +x, cos 51.3 deg to +y) admits X+ and Y+, placed above
+    z = 0: both directions are allocated over the same block locations (a direction must never
+    alias another one's key)."""
+    n = np.array([0.78, 0.625, 0.0])
+    n /= np.linalg.norm(n)
+    c = np.array([0.0, 0.0, 1.3])
+    pat = scenes.Patches.empty()
+    u = np.cross(n, [0, 0, 1.0])
+    pat.extend(c, n, u / np.linalg.norm(u), np.array([0, 0, 1.0]), 0.6, 0.6, [5, 6, 7])
+    K = pinhole(40, 30, 30.0)
+    pose = look_at(c + 0.9 * n, c)
+    fr = scenes.analytic_frame(pat, pose, K)
+    F = oracle.OracleFusion(S, TAU, TH, 40000)
+    F.fuse(fr.depth, fr.normal, fr.color, pose, K)
+    keys = F.volume().keys
+    assert set(keys[:, 3]) == {0, 2}
+    assert {tuple(k[:3]) for k in keys if k[3] == 0} == {tuple(k[:3]) for k in keys if k[3] == 2}
+    assert (keys[:, 2] > 0).all()
+
+
 # ---------------------------------------------------------------------------------------
 # R43: free-space carving and its depth-edge guard (PAPER.md:123-133)
 # ---------------------------------------------------------------------------------------
