@@ -182,6 +182,55 @@ DTSDF_API void dtsdf_default_policy(dtsdf_combine_policy *policy);
 DTSDF_API int dtsdf_should_recombine(const dtsdf_combine_policy *policy, int64_t frame, int64_t last,
                                      const float pose_w_c[16], const float last_pose_w_c[16]);
 
+/* ---- voxel-projection fusion --------------------------
+ * every allocated voxel in the frame's view is projected into the depth frame,
+ * associated with the nearest pixel and updated as a weighted running average with the
+ * point-to-plane distance d = <x - p, n>/tau (positive in front, reading R6), the weight
+ * w_d = w_ICP(z) <n,-ray>^+ w_dir^D(n) (eq:combined_fusion_weight; w_ICP eq:ICP_weight) and the
+ * colour weight w_c = w_d (1 - min(1, |p - x|/tau)) (eq:color_weight); d > 1 carves towards +1 with
+ * a constant weight unless a depth within carve_radius pixels differs by more than tau; weights are
+ * capped at max_weight.  Blocks are allocated first: for every valid pixel and every direction its
+ * normal admits (eq:angular_threshold), the blocks holding p + t n, t in [-tau, tau] sampled at
+ * <= voxel/2 (readings R39-R45). */
+typedef struct {
+  float max_weight;     /* 128 */
+  float carve_weight;   /* 1 */
+  int32_t carve_radius; /* 2 pixels */
+  int32_t reserved;     /* 0 */
+} dtsdf_fusion_params;
+DTSDF_API void dtsdf_default_fusion_params(dtsdf_fusion_params *params);
+
+/* Make room for `capacity` blocks (keeping the current ones; with no volume yet, create an empty
+ * one with `params`, which is otherwise ignored) and commit.  The library-owned buffers move
+ * (pointers from dtsdf_alloc_volume become invalid).  Colour weights of existing blocks start at
+ * their depth weights (R45).  Synchronous.  Errors: INVALID_ARGUMENT (capacity < current blocks),
+ * OUT_OF_MEMORY, CUDA. */
+DTSDF_API int dtsdf_fusion_reserve(dtsdf_ctx *ctx, const dtsdf_volume_params *params, int64_t capacity);
+
+/* Camera-frame normals of a depth map ("cross product of neighboring pixels in x- and
+ * y direction"; no bilateral filter, R39): depth f32 [H][W] camera z (0 = missing), out f32
+ * [H][W][3] unit normals facing the camera, 0 on the border and next to missing depth.  Host or
+ * device pointers (host output -> synchronous). */
+DTSDF_API int dtsdf_depth_normals(dtsdf_ctx *ctx, const float *depth, const dtsdf_intrinsics *intr, float *out_normal,
+                                  void *cuda_stream);
+
+/* Allocate and fuse one frame: depth f32 [H][W] (camera z, 0 = missing; valid in [z_min, z_max]),
+ * normal f32 [H][W][3] (camera frame, facing the camera, 0 = invalid), color u8 [H][W][3] or NULL,
+ * pose world-from-camera (host), params NULL -> defaults.  Frames may be host or device memory.
+ * Re-commits the volume (the combined TSDF is dropped).  *new_blocks (may be NULL) receives the
+ * number of blocks allocated.  Synchronous.  Errors: INVALID_ARGUMENT, NO_VOLUME (no
+ * dtsdf_fusion_reserve), OUT_OF_MEMORY (capacity reached: the blocks allocated so far are kept and
+ * initialised, the frame is not fused), CUDA. */
+DTSDF_API int dtsdf_fuse(dtsdf_ctx *ctx, const float *depth, const float *normal, const uint8_t *color,
+                         const float pose_w_c[16], const dtsdf_intrinsics *intr, const dtsdf_fusion_params *params,
+                         int64_t *new_blocks, void *cuda_stream);
+
+/* Copy the current blocks to HOST buffers (synchronous): keys int32 [n][4], sdf/weight f32
+ * [n][512], rgb u8 [n][512][3]; *n_out = n always; INVALID_ARGUMENT if capacity < n.  Block order
+ * is the pool order (fusion appends in allocation order). */
+DTSDF_API int dtsdf_get_volume(dtsdf_ctx *ctx, int64_t capacity, int32_t *keys, float *sdf, float *weight, uint8_t *rgb,
+                               int64_t *n_out);
+
 /* Kernel timing (tracing).  While enabled, every range-pass, raycast and combine
  * launch is bracketed by CUDA events on its stream.  dtsdf_kernel_times synchronizes those events
  * and returns the summed milliseconds and launch counts since the last reset: times_ms[0] range

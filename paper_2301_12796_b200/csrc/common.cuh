@@ -136,6 +136,33 @@ struct RangeLaunch {
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
 cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s);
 
+// Fusion launch (fusion.cu): one depth frame against the raw block pool.  The doubles are the
+// float32 ABI values, used where both sides must take the same discrete decision (R40, R41).
+struct FuseLaunch {
+  HashEntry *table;
+  unsigned int table_mask;
+  int *keys;                       // [capacity][4]
+  float *sdf, *weight, *cweight;   // [capacity][512]
+  unsigned char *rgb;              // [capacity][512][3]
+  unsigned long long *n_blocks;    // pool size (grows during allocation)
+  long long capacity;
+  int *flags;                      // 1 pool full, 2 table full
+  const float *depth, *normal;     // [H][W], [H][W][3] camera frame
+  const unsigned char *color;      // [H][W][3] or null
+  double R[9], t[3], fx, fy, cx, cy, z_min, z_max;
+  int width, height;
+  double s, tau, step, cos_theta;  // voxel size, truncation, allocation sample step, cos(theta)
+  int M;                           // allocation samples per segment: M + 1
+  float theta_f, cos_theta_f, sin_theta_f, inv_blend;
+  float max_weight, carve_weight;
+  int carve_radius;
+};
+
+// host launchers (fusion.cu)
+cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s);
+cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s);
+cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, cudaStream_t s);
+
 // host launchers (combine.cu)
 cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s);                  // interiors + slots
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s);  // aprons, masks

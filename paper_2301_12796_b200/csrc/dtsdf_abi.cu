@@ -46,6 +46,10 @@ struct dtsdf_ctx {
   float *sdf = nullptr, *weight = nullptr;
   uint8_t *rgb = nullptr;
   int64_t n = 0;
+  int64_t cap = 0;            // pool capacity in blocks (>= n; fusion grows n up to it)
+  float *cweight = nullptr;   // fusion: colour weights [cap][512] (eq:color_weight accumulator)
+  void *fuse_stage = nullptr; // fusion: device staging of host frames
+  size_t fuse_stage_cap = 0;
   // index
   HashEntry *table = nullptr;
   unsigned int table_cap = 0;
@@ -119,6 +123,7 @@ void free_combined(dtsdf_ctx *c) {
 
 void free_volume(dtsdf_ctx *c) {
   free_combined(c);
+  dfree(c->cweight);
   dfree(c->keys);
   dfree(c->sdf);
   dfree(c->weight);
@@ -132,7 +137,7 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->apron);
   dfree(c->rgb_apron);
   c->allocated = c->committed = false;
-  c->n = c->n_loc = 0;
+  c->n = c->n_loc = c->cap = 0;
   c->index_bytes = 0;
 }
 
@@ -223,6 +228,7 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   free_volume(c);
   dfree(c->scratch);
   dfree(c->tile_counter);
+  if (c->fuse_stage) cudaFree(c->fuse_stage);
   dfree(c->z_near);
   dfree(c->z_far);
   if (c->host_stage) cudaFree(c->host_stage);
@@ -251,6 +257,7 @@ int dtsdf_alloc_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, dtsdf_volume_
   }
   c->params = *p;
   c->n = (int64_t)n;
+  c->cap = (int64_t)n;
   c->allocated = true;
   out->keys = c->keys;
   out->sdf = c->sdf;
@@ -293,7 +300,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   if (host[0]) return fail(DTSDF_ERR_INVALID_ARGUMENT, "block key with D outside 0..5 or coordinate out of range");
   // hash table: capacity = next power of two >= 2N (load factor <= 1/2 over locations)
   unsigned int cap = 64;
-  while ((long long)cap < 2 * n) cap <<= 1;
+  while ((long long)cap < 2 * std::max<long long>(n, c->cap)) cap <<= 1;  // room for fusion to grow into
   c->table_cap = cap;
   int lo[3] = {0, 0, 0}, hi[3] = {-1, -1, -1};
   if (n > 0)
@@ -712,6 +719,210 @@ int dtsdf_should_recombine(const dtsdf_combine_policy *p, int64_t frame, int64_t
   if (std::sqrt(d2) > (double)p->translation) return 1;  // eq. condition_3: translation
   const double cs = std::min(1.0, std::max(-1.0, (tr - 1.0) / 2.0));
   return std::acos(cs) > (double)p->rotation ? 1 : 0;   // eq. condition_4: rotation
+}
+
+// ---- fusion (NEXT-2, fusion.cu) ----------------------------------------------------------
+void dtsdf_default_fusion_params(dtsdf_fusion_params *p) {
+  if (!p) return;
+  p->max_weight = 128.0f;
+  p->carve_weight = 1.0f;
+  p->carve_radius = 2;
+  p->reserved = 0;
+}
+
+int dtsdf_fusion_reserve(dtsdf_ctx *c, const dtsdf_volume_params *p, int64_t capacity) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  if (capacity < 1 || capacity > (int64_t)INT32_MAX / 2) return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad capacity");
+  cudaSetDevice(c->device);
+  if (!c->allocated) {
+    int rc = check_params(p);
+    if (rc) return rc;
+    dtsdf_volume_params q = *p;
+    q.n_blocks = 0;
+    dtsdf_volume_buffers b;
+    if ((rc = dtsdf_alloc_volume(c, &q, &b))) return rc;
+  }
+  if (capacity < c->n) return fail(DTSDF_ERR_INVALID_ARGUMENT, "capacity below the current block count");
+  CK(c, cudaDeviceSynchronize(), "reserve sync");
+  const size_t n = (size_t)c->n, cp = (size_t)capacity;
+  int32_t *keys = nullptr;
+  float *sdf = nullptr, *weight = nullptr, *cw = nullptr;
+  uint8_t *rgb = nullptr;
+  if (dalloc(keys, cp * 16) != cudaSuccess || dalloc(sdf, cp * 512 * 4) != cudaSuccess ||
+      dalloc(weight, cp * 512 * 4) != cudaSuccess || dalloc(rgb, cp * 512 * 3) != cudaSuccess ||
+      dalloc(cw, cp * 512 * 4) != cudaSuccess) {
+    cudaGetLastError();
+    dfree(keys); dfree(sdf); dfree(weight); dfree(rgb); dfree(cw);
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion pool");
+  }
+  if (n > 0) {
+    CK(c, cudaMemcpy(keys, c->keys, n * 16, cudaMemcpyDeviceToDevice), "reserve copy");
+    CK(c, cudaMemcpy(sdf, c->sdf, n * 512 * 4, cudaMemcpyDeviceToDevice), "reserve copy");
+    CK(c, cudaMemcpy(weight, c->weight, n * 512 * 4, cudaMemcpyDeviceToDevice), "reserve copy");
+    CK(c, cudaMemcpy(rgb, c->rgb, n * 512 * 3, cudaMemcpyDeviceToDevice), "reserve copy");
+    // reading R45: blocks that were not fused here count their colour as observed with the depth weight
+    CK(c, cudaMemcpy(cw, c->cweight ? c->cweight : c->weight, n * 512 * 4, cudaMemcpyDeviceToDevice), "reserve copy");
+  }
+  dfree(c->keys); dfree(c->sdf); dfree(c->weight); dfree(c->rgb); dfree(c->cweight);
+  c->keys = keys; c->sdf = sdf; c->weight = weight; c->rgb = rgb; c->cweight = cw;
+  c->cap = capacity;
+  c->params.n_blocks = c->n;
+  return dtsdf_commit_volume(c, nullptr);
+}
+
+static void fuse_launch_common(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, FuseLaunch &L) {
+  std::memset(&L, 0, sizeof(L));
+  for (int a = 0; a < 3; ++a) {
+    for (int b = 0; b < 3; ++b) L.R[3 * a + b] = (double)pose[4 * a + b];
+    L.t[a] = (double)pose[4 * a + 3];
+  }
+  L.fx = K->fx; L.fy = K->fy; L.cx = K->cx; L.cy = K->cy; L.z_min = K->z_min; L.z_max = K->z_max;
+  L.width = K->width;
+  L.height = K->height;
+}
+
+static const void *to_device(dtsdf_ctx *c, const void *src, size_t bytes, size_t offset, cudaStream_t s, bool *ok) {
+  *ok = true;
+  if (!src || is_device_ptr(src)) return src;
+  char *dst = (char *)c->fuse_stage + offset;
+  if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess) *ok = false;
+  return dst;
+}
+
+static int ensure_stage(dtsdf_ctx *c, size_t need) {
+  if (need <= c->fuse_stage_cap) return DTSDF_OK;
+  if (c->fuse_stage) cudaFree(c->fuse_stage);
+  c->fuse_stage = nullptr;
+  c->fuse_stage_cap = 0;
+  if (cudaMalloc(&c->fuse_stage, need) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "frame staging");
+  }
+  c->fuse_stage_cap = need;
+  return DTSDF_OK;
+}
+
+int dtsdf_depth_normals(dtsdf_ctx *c, const float *depth, const dtsdf_intrinsics *K, float *out_normal, void *stream) {
+  if (!c || !depth || !out_normal) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t px = (size_t)K->width * K->height;
+  const bool host_out = !is_device_ptr(out_normal);
+  if ((rc = ensure_stage(c, px * 16 + 256))) return rc;
+  bool ok;
+  const float *dd = (const float *)to_device(c, depth, px * 4, 0, s, &ok);
+  if (!ok) return cuda_fail(c, cudaGetLastError(), "stage depth");
+  float *on = host_out ? (float *)((char *)c->fuse_stage + ((px * 4 + 255) & ~size_t(255))) : out_normal;
+  FuseLaunch L;
+  const float I[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};
+  fuse_launch_common(c, I, K, L);
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_depth_normals(dd, L, on, s), "depth normals");
+  end_timed(c, s, &tl);
+  if (host_out) {
+    CK(c, cudaMemcpyAsync(out_normal, on, px * 12, cudaMemcpyDeviceToHost, s), "normals d2h");
+    CK(c, cudaStreamSynchronize(s), "normals sync");
+  }
+  return DTSDF_OK;
+}
+
+int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint8_t *color, const float pose[16],
+               const dtsdf_intrinsics *K, const dtsdf_fusion_params *fp, int64_t *new_blocks, void *stream) {
+  if (!c || !depth || !normal || !pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  for (int i = 0; i < 16; ++i)
+    if (!std::isfinite(pose[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
+  dtsdf_fusion_params prm;
+  dtsdf_default_fusion_params(&prm);
+  if (fp) prm = *fp;
+  if (!(prm.max_weight > 0.f) || !(prm.carve_weight >= 0.f) || prm.carve_radius < 0 || prm.carve_radius > 16)
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad fusion parameters");
+  if (!c->committed || !c->cweight) return fail(DTSDF_ERR_NO_VOLUME, "no fusion volume (call dtsdf_fusion_reserve)");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t px = (size_t)K->width * K->height;
+  const size_t o_n = (px * 4 + 255) & ~size_t(255), o_c = o_n + ((px * 12 + 255) & ~size_t(255));
+  if ((rc = ensure_stage(c, o_c + px * 3 + 256))) return rc;
+  bool ok1, ok2, ok3;
+  FuseLaunch L;
+  fuse_launch_common(c, pose, K, L);
+  L.depth = (const float *)to_device(c, depth, px * 4, 0, s, &ok1);
+  L.normal = (const float *)to_device(c, normal, px * 12, o_n, s, &ok2);
+  L.color = (const unsigned char *)to_device(c, color, px * 3, o_c, s, &ok3);
+  if (!ok1 || !ok2 || !ok3) return cuda_fail(c, cudaGetLastError(), "stage frame");
+  L.table = c->table;
+  L.table_mask = c->table_cap - 1;
+  L.keys = c->keys;
+  L.sdf = c->sdf;
+  L.weight = c->weight;
+  L.cweight = c->cweight;
+  L.rgb = c->rgb;
+  L.capacity = c->cap;
+  L.s = (double)c->params.voxel_size;
+  L.tau = (double)c->params.truncation;
+  L.M = (int)std::ceil(4.0 * L.tau / L.s);
+  L.step = 2.0 * L.tau / (double)L.M;
+  L.cos_theta = std::cos((double)c->params.theta);
+  L.theta_f = c->params.theta;
+  L.cos_theta_f = cosf(c->params.theta);
+  L.sin_theta_f = sinf(c->params.theta);
+  L.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
+  L.max_weight = prm.max_weight;
+  L.carve_weight = prm.carve_weight;
+  L.carve_radius = prm.carve_radius;
+  // scratch: flags (int) + pool counter (u64)
+  L.flags = c->scratch;
+  L.n_blocks = reinterpret_cast<unsigned long long *>(c->scratch + 12);
+  int init[14] = {0};
+  const unsigned long long n0 = (unsigned long long)c->n;
+  std::memcpy(&init[12], &n0, 8);
+  CK(c, cudaMemcpyAsync(c->scratch, init, sizeof(init), cudaMemcpyHostToDevice, s), "fuse init");
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_fuse_alloc(L, s), "fuse alloc");
+  end_timed(c, s, &tl);
+  int host[14];
+  CK(c, cudaMemcpyAsync(host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, s), "fuse readback");
+  CK(c, cudaStreamSynchronize(s), "fuse sync");
+  unsigned long long n1;
+  std::memcpy(&n1, &host[12], 8);
+  const int64_t n_new = std::min<int64_t>((int64_t)n1, c->cap);
+  const bool full = host[0] != 0;
+  begin_timed(c, 2, s, &tl, full ? (n_new > c->n ? 1 : 0) : 2);
+  CK(c, launch_fuse(L, c->n, n_new, !full, s), "fuse");  // when full: new blocks initialised, not fused
+  end_timed(c, s, &tl);
+  if (new_blocks) *new_blocks = n_new - c->n;
+  c->n = n_new;
+  c->params.n_blocks = n_new;
+  rc = dtsdf_commit_volume(c, stream);
+  if (rc) return rc;
+  if (full) return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion capacity exhausted (blocks allocated so far are kept)");
+  return DTSDF_OK;
+}
+
+int dtsdf_get_volume(dtsdf_ctx *c, int64_t capacity, int32_t *keys, float *sdf, float *weight, uint8_t *rgb,
+                     int64_t *n_out) {
+  if (!c || !n_out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx/n_out is NULL");
+  if (!c->allocated) return fail(DTSDF_ERR_NO_VOLUME, "no volume");
+  *n_out = c->n;
+  if (capacity < c->n) return fail(DTSDF_ERR_INVALID_ARGUMENT, "capacity smaller than the block count");
+  if (c->n == 0) return DTSDF_OK;
+  if (!keys || !sdf || !weight || !rgb) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL output");
+  cudaSetDevice(c->device);
+  const size_t n = (size_t)c->n;
+  CK(c, cudaDeviceSynchronize(), "get_volume sync");
+  CK(c, cudaMemcpy(keys, c->keys, n * 16, cudaMemcpyDeviceToHost), "get_volume");
+  CK(c, cudaMemcpy(sdf, c->sdf, n * 512 * 4, cudaMemcpyDeviceToHost), "get_volume");
+  CK(c, cudaMemcpy(weight, c->weight, n * 512 * 4, cudaMemcpyDeviceToHost), "get_volume");
+  CK(c, cudaMemcpy(rgb, c->rgb, n * 512 * 3, cudaMemcpyDeviceToHost), "get_volume");
+  return DTSDF_OK;
 }
 
 int dtsdf_render(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float *depth, float *normal,

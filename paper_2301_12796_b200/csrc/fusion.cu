@@ -1,0 +1,265 @@
+// fusion.cu -- voxel-projection fusion of depth frames into the DTSDF (
+// DESIGN.md §12).
+//
+//   k_depth_normals  one thread per pixel: camera-frame normal from the cross product of the
+//                    neighbouring back-projected pixels in x and y, facing the camera (R39)
+//   k_fuse_alloc     one thread per pixel: for every direction the pixel's normal admits
+//                    (eq:angular_threshold) the blocks holding the points p + t n,
+//                    t = -tau + j 2tau/M (R40), computed in fp64 with the oracle's roundings so
+//                    both sides allocate the same key set; a new (location, D) key claims its
+//                    direction slot in the location hash (CAS) and takes the next pool index
+//   k_fuse_init      new blocks: free space of weight 0
+//   k_fuse           one CTA per block, 2 voxels per thread: the voxel is projected into the frame
+//                    (nearest pixel, association in fp64), d = <x - p, n> / tau (eq:point-to-plane
+//                    with the sign of R6), then carving (d > 1, 2-pixel depth-edge guard)
+//                    or the weighted running average with w_d = w_ICP(z) <n,-ray>^+ w_dir^D(n)
+//                    (eq:combined_fusion_weight) and w_c = w_d (1 - min(1, |p - x| / tau))
+//                    (eq:color_weight); weights capped at w_max (R41-R45)
+//
+// Every voxel is updated at most once per frame and only from frame data, so the result does not
+// depend on thread order; the pool order of new blocks does (keys are compared as a set).
+#include <climits>
+
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace dtsdf {
+
+__device__ __forceinline__ bool depth_ok(const FuseLaunch &p, float z) {
+  return z > 0.0f && (double)z >= p.z_min && (double)z <= p.z_max;
+}
+
+// camera point of pixel (u, v) at depth z, ((u - cx) / fx) z, one rounding per operation
+__device__ __forceinline__ void backproject(const FuseLaunch &p, int u, int v, double z, double P[3]) {
+  P[0] = __dmul_rn(__ddiv_rn(__dsub_rn((double)u, p.cx), p.fx), z);
+  P[1] = __dmul_rn(__ddiv_rn(__dsub_rn((double)v, p.cy), p.fy), z);
+  P[2] = z;
+}
+
+// ((R0 a0 + R1 a1) + R2 a2) (+ t): the oracle's evaluation order, no contraction
+__device__ __forceinline__ void rotate(const FuseLaunch &p, const double a[3], double o[3]) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    o[r] = __dadd_rn(__dadd_rn(__dmul_rn(p.R[3 * r], a[0]), __dmul_rn(p.R[3 * r + 1], a[1])),
+                     __dmul_rn(p.R[3 * r + 2], a[2]));
+}
+
+__global__ void __launch_bounds__(256) k_depth_normals(const float *__restrict__ depth, FuseLaunch p,
+                                                       float *__restrict__ out) {
+  const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (u >= p.width || v >= p.height) return;
+  float *o = out + 3 * ((size_t)v * p.width + u);
+  float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+  if (u >= 1 && v >= 1 && u < p.width - 1 && v < p.height - 1) {
+    const size_t i = (size_t)v * p.width + u;
+    const float zc = depth[i], zl = depth[i - 1], zr = depth[i + 1], zu = depth[i - p.width], zd = depth[i + p.width];
+    if (depth_ok(p, zc) && depth_ok(p, zl) && depth_ok(p, zr) && depth_ok(p, zu) && depth_ok(p, zd)) {
+      // fp64: the neighbour differences cancel metre-scale coordinates to centimetres
+      double L[3], Rr[3], U[3], Dn[3], P[3];
+      backproject(p, u - 1, v, zl, L);
+      backproject(p, u + 1, v, zr, Rr);
+      backproject(p, u, v - 1, zu, U);
+      backproject(p, u, v + 1, zd, Dn);
+      backproject(p, u, v, zc, P);
+      const double ax = Rr[0] - L[0], ay = Rr[1] - L[1], az = Rr[2] - L[2];
+      const double bx = Dn[0] - U[0], by = Dn[1] - U[1], bz = Dn[2] - U[2];
+      const double cxn = ay * bz - az * by, cyn = az * bx - ax * bz, czn = ax * by - ay * bx;
+      const double nn = sqrt(cxn * cxn + cyn * cyn + czn * czn);
+      if (nn > 0.0) {
+        const double sgn = (cxn * P[0] + cyn * P[1] + czn * P[2]) > 0.0 ? -1.0 : 1.0;  // face the camera
+        n0 = (float)(sgn * cxn / nn); n1 = (float)(sgn * cyn / nn); n2 = (float)(sgn * czn / nn);
+      }
+    }
+  }
+  o[0] = n0; o[1] = n1; o[2] = n2;
+}
+
+__device__ __forceinline__ long long floordiv8(long long i) { return i >= 0 ? i / 8 : -((-i + 7) / 8); }
+
+// insert (block, D): returns 0 present or inserted, 1 capacity / table exhausted
+__device__ int alloc_key(const FuseLaunch &p, int bx, int by, int bz, int D) {
+  const unsigned long long key = pack_key(bx, by, bz);
+  unsigned int h = hash_key(key) & p.table_mask;
+  for (unsigned int probe = 0; probe <= p.table_mask; ++probe) {
+    unsigned long long k = p.table[h].key;
+    if (k != key) {
+      if (k != kEmptyKey) { h = (h + 1) & p.table_mask; continue; }
+      k = atomicCAS(&p.table[h].key, kEmptyKey, key);
+      if (k != kEmptyKey && k != key) { h = (h + 1) & p.table_mask; continue; }
+    }
+    int *slot = &p.table[h].slot[D];
+    if (*((volatile int *)slot) != -1) return 0;
+    if (atomicCAS(slot, -1, -2) != -1) return 0;  // another thread claimed it
+    const unsigned long long idx = atomicAdd(p.n_blocks, 1ull);
+    if ((long long)idx >= p.capacity) {
+      atomicExch(slot, -1);
+      atomicExch(p.flags, 1);
+      return 1;
+    }
+    reinterpret_cast<int4 *>(p.keys)[idx] = make_int4(bx, by, bz, D);
+    atomicExch(slot, (int)idx);
+    return 0;
+  }
+  atomicExch(p.flags, 2);
+  return 1;
+}
+
+__global__ void __launch_bounds__(256) k_fuse_alloc(const __grid_constant__ FuseLaunch p) {
+  const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (u >= p.width || v >= p.height) return;
+  const size_t i = (size_t)v * p.width + u;
+  const float z = p.depth[i];
+  const float n0 = p.normal[3 * i], n1 = p.normal[3 * i + 1], n2 = p.normal[3 * i + 2];
+  if (!depth_ok(p, z) || (n0 == 0.f && n1 == 0.f && n2 == 0.f)) return;
+  double P[3], X[3], nc[3] = {n0, n1, n2}, n[3];
+  backproject(p, u, v, (double)z, P);
+  rotate(p, P, X);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) X[a] = __dadd_rn(X[a], p.t[a]);
+  rotate(p, nc, n);
+  for (int D = 0; D < 6; ++D) {
+    const double dot = (D & 1) ? -n[D >> 1] : n[D >> 1];
+    if (!(dot > p.cos_theta)) continue;
+    long long pb[3] = {LLONG_MIN, 0, 0};
+    for (int j = 0; j <= p.M; ++j) {
+      const double tj = __dadd_rn(-p.tau, __dmul_rn((double)j, p.step));
+      long long b[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        b[a] = floordiv8((long long)floor(__ddiv_rn(__dadd_rn(X[a], __dmul_rn(tj, n[a])), p.s)));
+      if (b[0] == pb[0] && b[1] == pb[1] && b[2] == pb[2]) continue;
+      pb[0] = b[0]; pb[1] = b[1]; pb[2] = b[2];
+      if (alloc_key(p, (int)b[0], (int)b[1], (int)b[2], D)) return;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_fuse_init(FuseLaunch p, long long n0, long long n1) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long b = n0 + (g >> 9);
+  if (b >= n1) return;
+  const size_t r = (size_t)b * kVoxPerBlock + (g & 511);
+  p.sdf[r] = 1.0f;
+  p.weight[r] = 0.0f;
+  p.cweight[r] = 0.0f;
+  p.rgb[3 * r] = p.rgb[3 * r + 1] = p.rgb[3 * r + 2] = 0;
+}
+
+__device__ __forceinline__ float w_dir_f(float c, const FuseLaunch &p) {
+  if (c <= p.cos_theta_f) return 0.0f;
+  if (c >= p.sin_theta_f) return 1.0f;
+  const float a = acosf(fminf(c, 1.0f));
+  return fminf(fmaxf((p.theta_f - a) * p.inv_blend, 0.0f), 1.0f);
+}
+
+__global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch p) {
+  const long long b = blockIdx.x;
+  const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
+  const int D = key.w;
+  const int axis = D >> 1;
+  const float sgnD = (D & 1) ? -1.0f : 1.0f;
+  const float tau = (float)p.tau;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int l = threadIdx.x + 256 * h;
+    const int i = kBlock * key.x + (l & 7), j = kBlock * key.y + ((l >> 3) & 7), k = kBlock * key.z + (l >> 6);
+    // association (R41): projection and nearest pixel in fp64 with the oracle's roundings
+    const double x0 = __dmul_rn((double)i, p.s), x1 = __dmul_rn((double)j, p.s), x2 = __dmul_rn((double)k, p.s);
+    const double d0 = __dsub_rn(x0, p.t[0]), d1 = __dsub_rn(x1, p.t[1]), d2 = __dsub_rn(x2, p.t[2]);
+    double xc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      xc[a] = __dadd_rn(__dadd_rn(__dmul_rn(p.R[a], d0), __dmul_rn(p.R[3 + a], d1)), __dmul_rn(p.R[6 + a], d2));
+    if (!(xc[2] > 0.0)) continue;
+    const double uu = __dadd_rn(__ddiv_rn(__dmul_rn(p.fx, xc[0]), xc[2]), p.cx);
+    const double vv = __dadd_rn(__ddiv_rn(__dmul_rn(p.fy, xc[1]), xc[2]), p.cy);
+    const double fu = floor(__dadd_rn(uu, 0.5)), fv = floor(__dadd_rn(vv, 0.5));
+    if (!(fu >= 0.0 && fu <= (double)(p.width - 1) && fv >= 0.0 && fv <= (double)(p.height - 1))) continue;
+    const int iu = (int)fu, iv = (int)fv;
+    const size_t pi = (size_t)iv * p.width + iu;
+    const float z = p.depth[pi];
+    const float nc0 = p.normal[3 * pi], nc1 = p.normal[3 * pi + 1], nc2 = p.normal[3 * pi + 2];
+    if (!depth_ok(p, z) || (nc0 == 0.f && nc1 == 0.f && nc2 == 0.f)) continue;
+    // the band decisions (|d| <= 1, d > 1) sit exactly on lattice planes for axis-aligned
+    // surfaces (a voxel tau from a floor at z = 0), so d is formed in fp64 with the oracle's
+    // operation order -- both sides take the same decision
+    double P[3], X[3], ncd[3] = {nc0, nc1, nc2}, nd[3];
+    backproject(p, iu, iv, (double)z, P);
+    rotate(p, P, X);
+    rotate(p, ncd, nd);
+    const double ex = __dsub_rn(x0, __dadd_rn(X[0], p.t[0])), ey = __dsub_rn(x1, __dadd_rn(X[1], p.t[1])),
+                 ez = __dsub_rn(x2, __dadd_rn(X[2], p.t[2]));
+    const double ddd =
+        __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(ex, nd[0]), __dmul_rn(ey, nd[1])), __dmul_rn(ez, nd[2])), p.tau);
+    const float dd = (float)ddd;  // eq:point-to-plane, sign of reading R6
+    const float nx = (float)nd[0], ny = (float)nd[1], nz = (float)nd[2];
+    const size_t r = (size_t)b * kVoxPerBlock + l;
+    if (ddd < -1.0) continue;  // behind the surface beyond the band: untouched
+    if (ddd > 1.0) {
+      // R43: free space, unless a depth within the guard radius differs by more than tau
+      bool edge = false;
+      for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
+        for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
+          const int qu = iu + du, qv = iv + dv;
+          if (qu < 0 || qv < 0 || qu >= p.width || qv >= p.height) continue;
+          const float zq = p.depth[(size_t)qv * p.width + qu];
+          if (!depth_ok(p, zq)) continue;
+          if (fabs((double)zq - (double)z) > p.tau) { edge = true; break; }
+        }
+      if (edge) continue;
+      const float W0 = p.weight[r];
+      p.sdf[r] = (W0 * p.sdf[r] + p.carve_weight) / (W0 + p.carve_weight);
+      p.weight[r] = fminf(W0 + p.carve_weight, p.max_weight);
+      continue;
+    }
+    const float wdir = w_dir_f(sgnD * (axis == 0 ? nx : (axis == 1 ? ny : nz)), p);
+    const float rx = (float)X[0], ry = (float)X[1], rz = (float)X[2];  // ray = p - camera centre
+    const float rl = sqrtf(rx * rx + ry * ry + rz * rz);
+    const float ca = rl > 0.f ? -(nx * rx + ny * ry + nz * rz) / rl : 0.f;
+    const float zz = z + (1.0f - (float)p.z_min);
+    const float wn = (1.0f / (zz * zz)) * fmaxf(ca, 0.0f) * wdir;  // w_ICP(z) w_angle w_dir
+    if (!(wn > 0.0f)) continue;
+    const float W0 = p.weight[r];
+    p.sdf[r] = (W0 * p.sdf[r] + wn * dd) / (W0 + wn);
+    p.weight[r] = fminf(W0 + wn, p.max_weight);
+    if (p.color) {
+      const float dist = (float)sqrt(ex * ex + ey * ey + ez * ez);
+      const float wc = wn * (1.0f - fminf(1.0f, dist / tau));  // eq:color_weight
+      if (wc > 0.0f) {
+        const float C0 = p.cweight[r];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float c = (C0 * (float)p.rgb[3 * r + a] + wc * (float)p.color[3 * pi + a]) / (C0 + wc);
+          p.rgb[3 * r + a] = (unsigned char)fminf(fmaxf(floorf(c + 0.5f), 0.f), 255.f);
+        }
+        p.cweight[r] = fminf(C0 + wc, p.max_weight);
+      }
+    }
+  }
+}
+
+cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s) {
+  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
+  k_depth_normals<<<grid, 256, 0, s>>>(depth, p, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s) {
+  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
+  k_fuse_alloc<<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, cudaStream_t s) {
+  if (n_new > n_old) {
+    k_fuse_init<<<(unsigned)(((n_new - n_old) * kVoxPerBlock + 255) / 256), 256, 0, s>>>(p, n_old, n_new);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (n_new == 0 || !fuse) return cudaSuccess;
+  k_fuse<<<(unsigned)n_new, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace dtsdf

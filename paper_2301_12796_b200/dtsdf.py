@@ -23,7 +23,8 @@ EXPORTS = [
     "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
     "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
     "dtsdf_combine", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
-    "dtsdf_should_recombine",
+    "dtsdf_should_recombine", "dtsdf_default_fusion_params", "dtsdf_fusion_reserve", "dtsdf_depth_normals",
+    "dtsdf_fuse", "dtsdf_get_volume",
 ]
 MARGIN = 0.125  # PAPER.md:262 "(±1/8 image size)"
 OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID = 1, 2, 3, 4, 5
@@ -48,6 +49,11 @@ class VolumeParams(C.Structure):
 class CombinePolicy(C.Structure):
     _fields_ = [("boot_frames", C.c_int32), ("stale_frames", C.c_int32), ("translation", C.c_float),
                 ("rotation", C.c_float)]
+
+
+class FusionParams(C.Structure):
+    _fields_ = [("max_weight", C.c_float), ("carve_weight", C.c_float), ("carve_radius", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class VolumeBuffers(C.Structure):
@@ -87,6 +93,12 @@ def lib():
         L.dtsdf_default_policy.argtypes = [C.POINTER(CombinePolicy)]
         L.dtsdf_default_policy.restype = None
         L.dtsdf_should_recombine.argtypes = [C.POINTER(CombinePolicy), I64, I64, P, P]
+        L.dtsdf_default_fusion_params.argtypes = [C.POINTER(FusionParams)]
+        L.dtsdf_default_fusion_params.restype = None
+        L.dtsdf_fusion_reserve.argtypes = [P, C.POINTER(VolumeParams), I64]
+        L.dtsdf_depth_normals.argtypes = [P, P, C.POINTER(Intrinsics), P, P]
+        L.dtsdf_fuse.argtypes = [P, P, P, P, P, C.POINTER(Intrinsics), C.POINTER(FusionParams), C.POINTER(I64), P]
+        L.dtsdf_get_volume.argtypes = [P, I64, P, P, P, P, C.POINTER(I64)]
         L.dtsdf_last_error.argtypes = []
         L.dtsdf_last_error.restype = C.c_char_p
         _lib = L
@@ -203,6 +215,43 @@ class Renderer:
         fn = self.render_combined_into if combined else self.render_into
         fn(poses, K, out["depth"], out.get("normal"), out.get("color"), out.get("mask"), row0, row1, stream)
         return out
+
+    # -- fusion (NEXT-2) --------------------------------------------------------------------
+    def fusion_reserve(self, capacity, voxel_size=0.01, truncation=0.04, theta=None, step=0.0):
+        """dtsdf_fusion_reserve: room for `capacity` blocks (an empty volume if none is loaded)."""
+        theta = float(np.deg2rad(65.0)) if theta is None else theta
+        p = VolumeParams(voxel_size, truncation, theta, step, 0)
+        _check(lib().dtsdf_fusion_reserve(self._h, C.byref(p), int(capacity)))
+
+    def depth_normals(self, depth, K, out=None, stream=None):
+        """dtsdf_depth_normals: camera-frame normals [H, W, 3] of a depth map (host or device)."""
+        if out is None:
+            out = np.zeros(tuple(depth.shape) + (3,), np.float32) if isinstance(depth, np.ndarray) else \
+                depth.new_zeros(tuple(depth.shape) + (3,))
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_depth_normals(self._h, _ptr(depth), C.byref(k), _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def fuse(self, depth, normal, color, pose, K, params: Optional[FusionParams] = None, stream=None) -> int:
+        """dtsdf_fuse: allocate + fuse one frame (host or device buffers); returns new blocks."""
+        pose = np.ascontiguousarray(np.asarray(pose, np.float32).reshape(16))
+        k = make_intrinsics(K)
+        nb = C.c_int64()
+        prm = C.byref(params) if params is not None else None
+        _check(lib().dtsdf_fuse(self._h, _ptr(depth), _ptr(normal), _ptr(color), pose.ctypes.data, C.byref(k), prm,
+                                C.byref(nb), _stream_ptr(stream)))
+        return nb.value
+
+    def get_volume(self):
+        """dtsdf_get_volume -> (keys [n,4], sdf [n,512], weight [n,512], rgb [n,512,3]) host arrays."""
+        n = self.stats()["n_blocks"]
+        keys = np.zeros((n, 4), np.int32)
+        sdf = np.zeros((n, 512), np.float32)
+        w = np.zeros((n, 512), np.float32)
+        rgb = np.zeros((n, 512, 3), np.uint8)
+        got = C.c_int64()
+        _check(lib().dtsdf_get_volume(self._h, n, _ptr(keys), _ptr(sdf), _ptr(w), _ptr(rgb), C.byref(got)))
+        return keys, sdf, w, rgb
 
     # -- combined TSDF (NEXT-1) -----------------------------------------------------------
     def combine(self, pose, K, margin=MARGIN, stream=None):
