@@ -61,6 +61,10 @@ struct dtsdf_ctx {
   float2 *apron = nullptr;
   uchar4 *rgb_apron = nullptr;
   size_t index_bytes = 0;
+  // allocated sizes of the index buffers: a re-commit (e.g. after every fused frame) reuses them
+  size_t cap_table = 0, cap_locations = 0, cap_bitmap = 0, cap_surface = 0, cap_cell_pos = 0, cap_apron = 0,
+         cap_rgb_apron = 0, cap_loc_grid = 0, cap_dist = 0;
+  unsigned char *dist_tmp = nullptr;
   // commit scratch
   int *scratch = nullptr;  // flags[4] + aabb[6] + n_loc(u64)
   // render scratch
@@ -136,6 +140,9 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
+  dfree(c->dist_tmp);
+  c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_apron =
+      c->cap_rgb_apron = c->cap_loc_grid = c->cap_dist = 0;
   c->allocated = c->committed = false;
   c->n = c->n_loc = c->cap = 0;
   c->index_bytes = 0;
@@ -177,6 +184,19 @@ int check_intr(const dtsdf_intrinsics *K) {
 template <typename T>
 cudaError_t dalloc(T *&p, size_t bytes) {
   return cudaMalloc((void **)&p, std::max<size_t>(bytes, 16));
+}
+
+// grow-only device buffer: keeps the allocation when it is large enough
+template <typename T>
+cudaError_t ensure(T *&p, size_t &cap, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 16);
+  if (p && cap >= bytes) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc((void **)&p, bytes);
+  if (e == cudaSuccess) cap = bytes;
+  return e;
 }
 
 // kernels: number of this library's kernels the bracketed region launches (memsets: 0)
@@ -274,14 +294,6 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   c->committed = false;
   free_combined(c);
-  dfree(c->table);
-  dfree(c->bitmap);
-  dfree(c->surface);
-  dfree(c->cell_pos);
-  dfree(c->loc_grid);
-  dfree(c->locations);
-  dfree(c->apron);
-  dfree(c->rgb_apron);
   const long long n = c->n;
   // scratch: flags[4] | aabb[6] | pad[2] | n_loc (8 B aligned at int offset 12)
   CommitScratch sc;
@@ -308,12 +320,13 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   for (int a = 0; a < 3; ++a) { c->lo[a] = lo[a]; c->dim[a] = hi[a] - lo[a] + 1; }
   const size_t cells = (size_t)c->dim[0] * c->dim[1] * c->dim[2];
   const size_t bm_words = (cells + 31) / 32;
-  if (dalloc(c->table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
-      dalloc(c->locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
-      dalloc(c->bitmap, (bm_words + 1) * 4) != cudaSuccess || dalloc(c->surface, (bm_words + 1) * 4) != cudaSuccess ||
-      dalloc(c->cell_pos, (size_t)cap * 64) != cudaSuccess ||
-      dalloc(c->apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
-      dalloc(c->rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
+  if (ensure(c->table, c->cap_table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
+      ensure(c->locations, c->cap_locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
+      ensure(c->bitmap, c->cap_bitmap, (bm_words + 1) * 4) != cudaSuccess ||
+      ensure(c->surface, c->cap_surface, (bm_words + 1) * 4) != cudaSuccess ||
+      ensure(c->cell_pos, c->cap_cell_pos, (size_t)cap * 64) != cudaSuccess ||
+      ensure(c->apron, c->cap_apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
+      ensure(c->rgb_apron, c->cap_rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
   }
@@ -350,7 +363,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
   // raycast resolves locations through the bitmaps and the hash table
   if (cells > 0 && cells <= (size_t(1) << 28)) {
-    if (dalloc(c->loc_grid, cells * 4) != cudaSuccess) {
+    if (ensure(c->loc_grid, c->cap_loc_grid, cells * 4) != cudaSuccess) {
       cudaGetLastError();
       c->loc_grid = nullptr;
     } else {
@@ -361,17 +374,18 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
                             c->dim[1], s),
          "loc_grid");
       end_timed(c, s, &tl);
-      unsigned char *tmp = nullptr;
-      if (dalloc(tmp, 2 * cells) == cudaSuccess) {
+      if (ensure(c->dist_tmp, c->cap_dist, 2 * cells) == cudaSuccess) {
         begin_timed(c, 2, s, &tl, 4);
-        CK(c, launch_empty_distance(c->loc_grid, tmp, tmp + cells, c->dim[0], c->dim[1], c->dim[2], s), "distance");
+        CK(c, launch_empty_distance(c->loc_grid, c->dist_tmp, c->dist_tmp + cells, c->dim[0], c->dim[1], c->dim[2], s),
+           "distance");
         end_timed(c, s, &tl);
-        CK(c, cudaStreamSynchronize(s), "distance sync");
-        cudaFree(tmp);
       } else {
         cudaGetLastError();
       }
     }
+  } else {
+    dfree(c->loc_grid);  // AABB too large for the dense grid: the hash-probe path
+    c->cap_loc_grid = 0;
   }
   CK(c, cudaStreamSynchronize(s), "commit sync");
   c->committed = true;

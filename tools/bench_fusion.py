@@ -1,0 +1,46 @@
+"""Fusion throughput on the GPU: configs[1] room scanned by seeded 640x480 ideal depth frames,
+fused frame by frame through dtsdf_fuse (allocation + fusion + re-commit of the index).
+
+    python tools/bench_fusion.py [--frames 30]
+Prints one JSON line: wall ms per frame (host clock around the synchronous call) and the summed
+kernel times of the last frames (dtsdf_kernel_times, CUDA events)."""
+import argparse, json, os, sys, time
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa
+import scenes  # noqa
+from paper_2301_12796_b200 import Renderer  # noqa
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--frames", type=int, default=30)
+ap.add_argument("--warmup", type=int, default=5)
+args = ap.parse_args()
+w = scenes.c1_room()
+K = w.intrinsics
+poses = scenes.room_scan_poses(np.random.default_rng([9, 0]), args.frames + args.warmup)
+frames = [scenes.analytic_frame(w.patches, P, K) for P in poses]
+dev = [{k: torch.from_numpy(getattr(f, k)).cuda() for k in ("depth", "normal", "color")} for f in frames]
+R = Renderer(0)
+R.upload(0.01, 0.04, scenes.THETA, np.zeros((0, 4), np.int32), np.zeros((0, 512), np.float32),
+         np.zeros((0, 512), np.float32))
+R.fusion_reserve(80000)
+for i in range(args.warmup):
+    R.fuse(dev[i]["depth"], dev[i]["normal"], dev[i]["color"], poses[i], K)
+torch.cuda.synchronize()
+R.reset_kernel_times()
+R.set_profiling(True)
+t = []
+new = 0
+for i in range(args.warmup, args.warmup + args.frames):
+    t0 = time.perf_counter()
+    new += R.fuse(dev[i]["depth"], dev[i]["normal"], dev[i]["color"], poses[i], K)
+    t.append(time.perf_counter() - t0)
+R.set_profiling(False)
+kt = R.kernel_times()
+st = R.stats()
+print(json.dumps({"what": "fusion", "config": "C1 room, 640x480 ideal depth frames, 1 cm voxels, tau 4 cm",
+                  "frames": args.frames, "ms_per_frame_median": 1e3 * float(np.median(t)),
+                  "frames_per_s": 1.0 / float(np.median(t)), "kernel_ms_per_frame": kt["other_ms"] / args.frames,
+                  "kernel_launches_per_frame": kt["other_launches"] / args.frames, "new_blocks": new,
+                  "blocks": st["n_blocks"], "device": torch.cuda.get_device_name(0)}))
