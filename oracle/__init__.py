@@ -5,7 +5,7 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 (``paper_2301_12796_b200``) never imports it, and it never imports the product path.
 
 ``liboracle.so`` is plain C in fp64 (``oracle.c`` raycast and combined TSDF, ``fusion.c``
-voxel-projection fusion); this module only marshals arguments.
+voxel-projection fusion, ``icp.c`` point-to-plane ICP); this module only marshals arguments.
 Every function cites the passage it follows in ``oracle.c``; DESIGN.md §4 lists the readings.
 """
 from __future__ import annotations
@@ -17,7 +17,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "fusion.c")]
+_SRCS = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "fusion.c"), os.path.join(_HERE, "icp.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -70,6 +70,14 @@ def lib():
         L.oracle_fuse_frame.restype = I64
         L.oracle_depth_normals.argtypes = [P, P, P]
         L.oracle_depth_normals.restype = None
+        L.oracle_se3_exp.argtypes = [P, P]
+        L.oracle_se3_exp.restype = None
+        L.oracle_icp_normal_equations.argtypes = [P, P, P, P, P, P, D, P, P, P]
+        L.oracle_icp_normal_equations.restype = None
+        L.oracle_cholesky_solve6.argtypes = [P, P, P]
+        L.oracle_cholesky_solve6.restype = I32
+        L.oracle_icp.argtypes = [P, P, P, P, P, D, I32, D, P, P]
+        L.oracle_icp.restype = I32
         _lib = L
     return _lib
 
@@ -308,3 +316,51 @@ class OracleFusion:
         lib().oracle_fuse_get(self.h, _ptr(keys), _ptr(sdf), _ptr(w), _ptr(rgb), _ptr(cw))
         vol = BlockVolume(self.voxel_size, self.truncation, self.theta, keys, sdf, w, rgb, 0.0)
         return (vol, cw) if with_color_weight else vol
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT-3: weighted geometric point-to-plane ICP (icp.c, readings R47-R52)
+# ------------------------------------------------------------------------------------------
+ICP_MAX_ITERS, ICP_MIN_STEP, ICP_OUTLIER = 50, 1e-6, 0.005  # PAPER.md:626-628 (fine level)
+
+
+def se3_exp(xi):
+    xi = np.ascontiguousarray(xi, np.float64)
+    T = np.zeros(16)
+    lib().oracle_se3_exp(_ptr(xi), _ptr(T))
+    return T.reshape(4, 4)
+
+
+def _icp_inputs(depth, ref_depth, ref_normal):
+    return (np.ascontiguousarray(depth, np.float32), np.ascontiguousarray(ref_depth, np.float32),
+            np.ascontiguousarray(ref_normal, np.float32))
+
+
+def icp_normal_equations(depth, ref_depth, ref_normal, ref_pose, K, delta=None, outlier=ICP_OUTLIER):
+    """(H [6,6], g [6], inliers, sum w r^2) of eq:ICP_Hessian at DeltaT = delta."""
+    d, rd, rn = _icp_inputs(depth, ref_depth, ref_normal)
+    delta = np.ascontiguousarray(np.eye(4) if delta is None else delta, np.float64).reshape(16)
+    H, g, st = np.zeros(36), np.zeros(6), np.zeros(2)
+    lib().oracle_icp_normal_equations(_ptr(d), _ptr(rd), _ptr(rn), _ptr(_pose32(ref_pose)), _ptr(_intr32(K)),
+                                      _ptr(delta), float(np.float32(outlier)), _ptr(H), _ptr(g), _ptr(st))
+    return H.reshape(6, 6), g, int(st[0]), float(st[1])
+
+
+def cholesky_solve6(H, b):
+    x = np.zeros(6)
+    rc = lib().oracle_cholesky_solve6(_ptr(np.ascontiguousarray(H, np.float64).reshape(36)),
+                                      _ptr(np.ascontiguousarray(b, np.float64)), _ptr(x))
+    return x if rc == 0 else None
+
+
+def icp(depth, ref_depth, ref_normal, ref_pose, K, delta=None, outlier=ICP_OUTLIER, max_iters=ICP_MAX_ITERS,
+        min_step=ICP_MIN_STEP):
+    """Gauss-Newton ICP (eq:ICP_solution / eq:deltaT_update).  Returns (DeltaT [4,4] mapping the
+    frame's camera into the rendered view's camera, dict(iterations, step, inliers, residual, ok))."""
+    d, rd, rn = _icp_inputs(depth, ref_depth, ref_normal)
+    delta = np.ascontiguousarray(np.eye(4) if delta is None else delta, np.float64).reshape(16).copy()
+    out = np.zeros(4)
+    rc = lib().oracle_icp(_ptr(d), _ptr(rd), _ptr(rn), _ptr(_pose32(ref_pose)), _ptr(_intr32(K)),
+                          float(np.float32(outlier)), int(max_iters), float(min_step), _ptr(delta), _ptr(out))
+    return delta.reshape(4, 4), dict(iterations=int(out[0]), step=out[1], inliers=int(out[2]), residual=out[3],
+                                     ok=rc == 0)
