@@ -54,6 +54,7 @@ extern "C" {
 #define DTSDF_ERR_OUT_OF_MEMORY (-4)    /* device allocation failed */
 #define DTSDF_ERR_CUDA (-5)             /* CUDA runtime error (sticky) */
 #define DTSDF_ERR_NO_COMBINED (-6)      /* render_combined / combined query before dtsdf_combine */
+#define DTSDF_ERR_SINGULAR (-7)         /* ICP normal equations not positive definite (tracking failure) */
 
 /* block coordinates must lie in [-2^20, 2^20) (21-bit packed index key) */
 #define DTSDF_MAX_BLOCK_COORD (1 << 20)
@@ -230,6 +231,47 @@ DTSDF_API int dtsdf_fuse(dtsdf_ctx *ctx, const float *depth, const float *normal
  * is the pool order (fusion appends in allocation order). */
 DTSDF_API int dtsdf_get_volume(dtsdf_ctx *ctx, int64_t capacity, int32_t *keys, float *sdf, float *weight, uint8_t *rgb,
                                int64_t *n_out);
+
+/* ---- geometric point-to-plane ICP against a rendered view
+ * the frame's points p_i (depth back-projected) are mapped by DeltaT into the
+ * camera of a view rendered at ref_pose and associated projectively with the nearest rendered pixel
+ * (q_i, n_i); E = sum w_i <q_i - exp(xi) DeltaT p_i, n_i>^2 with w_i = w_ICP(z_i) =
+ * 1/(z + 1 - z_min)^2; H = 2 sum w J J^T, g = 2 sum w J r with J = (-n, -DeltaT p x n), summed by a
+ * fixed-topology (deterministic) tree; H xi = -g by Cholesky; DeltaT <- exp(xi) DeltaT
+ * until |xi| < min_step or max_iters; residuals above `outlier` metres are rejected. */
+typedef struct {
+  int32_t max_iters; /* 50 (fine level) */
+  float min_step;    /* 1e-6 */
+  float outlier;     /* 0.005 m (fine level; 0.05 coarse) */
+  int32_t reserved;
+} dtsdf_icp_params;
+typedef struct {
+  float delta[16];       /* DeltaT, row-major: frame camera -> rendered view camera; new pose = ref_pose DeltaT */
+  double delta64[16];    /* the same in fp64 */
+  int32_t iterations;    /* Gauss-Newton steps taken */
+  int32_t status;        /* 0 ok, 1 singular */
+  int64_t inliers;       /* associated, non-outlier pixels of the last linearisation */
+  double step;           /* |xi| of the last step */
+  double residual;       /* sum w r^2 of the last linearisation */
+} dtsdf_icp_result;
+DTSDF_API void dtsdf_default_icp_params(dtsdf_icp_params *params);
+
+/* Register a depth frame against a rendered view.  depth f32 [H][W] (camera z, 0 = missing),
+ * ref_depth f32 [H][W] and ref_normal f32 [H][W][3] (world frame) as dtsdf_render outputs at
+ * ref_pose; shared intrinsics; init_delta (NULL = identity).  Host or device buffers.  All
+ * iterations are enqueued on cuda_stream; the call synchronizes once.  Errors: INVALID_ARGUMENT,
+ * SINGULAR (the result holds the last DeltaT), OUT_OF_MEMORY, CUDA. */
+DTSDF_API int dtsdf_icp(dtsdf_ctx *ctx, const float *depth, const float *ref_depth, const float *ref_normal,
+                        const float ref_pose[16], const dtsdf_intrinsics *intr, const float init_delta[16],
+                        const dtsdf_icp_params *params, dtsdf_icp_result *out, void *cuda_stream);
+
+/* One linearisation at DeltaT = delta (fp64, row-major): H [36] (full symmetric), g [6], inliers,
+ * sum w r^2 -- the deterministic reduction exposed for checks.  Synchronous. */
+DTSDF_API int dtsdf_icp_normal_equations(dtsdf_ctx *ctx, const float *depth, const float *ref_depth,
+                                         const float *ref_normal, const float ref_pose[16],
+                                         const dtsdf_intrinsics *intr, const double delta[16], float outlier,
+                                         double H[36], double g[6], int64_t *inliers, double *residual,
+                                         void *cuda_stream);
 
 /* Kernel timing (tracing).  While enabled, every range-pass, raycast and combine
  * launch is bracketed by CUDA events on its stream.  dtsdf_kernel_times synchronizes those events

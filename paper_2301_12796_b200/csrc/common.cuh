@@ -158,6 +158,32 @@ struct FuseLaunch {
   int carve_radius;
 };
 
+// ICP state in device memory (icp.cu): written by k_icp_solve, read back once per call
+struct IcpState {
+  double delta[16];                // DeltaT: frame camera -> rendered view camera (row-major)
+  double sums[29];                 // last linearisation: upper H (21), g (6), inliers, sum w r^2
+  double step, residual;
+  long long inliers;
+  int iterations, done, status;    // status 1: singular system
+  int pad;
+};
+
+struct IcpLaunch {
+  const float *depth;              // [H][W] frame camera z
+  const float *ref_depth;          // [H][W] rendered view camera z
+  const float *ref_normal;         // [H][W][3] rendered world normals
+  double ref_R[9];                 // rendered view rotation (world-from-camera, row-major)
+  double fx, fy, cx, cy, z_min, z_max, outlier, min_step;
+  int width, height, max_iters;
+  double *partials;                // [n_partials][29]
+  IcpState *state;
+};
+
+// host launchers (icp.cu)
+int icp_partials(int width, int height);
+cudaError_t launch_icp_reduce(const IcpLaunch &p, cudaStream_t s);
+cudaError_t launch_icp_solve(const IcpLaunch &p, cudaStream_t s);
+
 // host launchers (fusion.cu)
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s);
 cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s);

@@ -48,7 +48,10 @@ struct dtsdf_ctx {
   int64_t n = 0;
   int64_t cap = 0;            // pool capacity in blocks (>= n; fusion grows n up to it)
   float *cweight = nullptr;   // fusion: colour weights [cap][512] (eq:color_weight accumulator)
-  void *fuse_stage = nullptr; // fusion: device staging of host frames
+  void *fuse_stage = nullptr; // fusion / ICP: device staging of host frames
+  double *icp_partials = nullptr;
+  IcpState *icp_state = nullptr;
+  size_t cap_icp_partials = 0, cap_icp_state = 0;
   size_t fuse_stage_cap = 0;
   // index
   HashEntry *table = nullptr;
@@ -249,6 +252,8 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   dfree(c->scratch);
   dfree(c->tile_counter);
   if (c->fuse_stage) cudaFree(c->fuse_stage);
+  dfree(c->icp_partials);
+  dfree(c->icp_state);
   dfree(c->z_near);
   dfree(c->z_far);
   if (c->host_stage) cudaFree(c->host_stage);
@@ -918,6 +923,126 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   rc = dtsdf_commit_volume(c, stream);
   if (rc) return rc;
   if (full) return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion capacity exhausted (blocks allocated so far are kept)");
+  return DTSDF_OK;
+}
+
+// ---- ICP (NEXT-3, icp.cu) -----------------------------------------------------------------
+void dtsdf_default_icp_params(dtsdf_icp_params *p) {
+  if (!p) return;
+  p->max_iters = 50;
+  p->min_step = 1e-6f;
+  p->outlier = 0.005f;
+  p->reserved = 0;
+}
+
+// stage the three ICP inputs on the device; fills L's input pointers and geometry
+static int icp_prepare(dtsdf_ctx *c, const float *depth, const float *ref_depth, const float *ref_normal,
+                       const float ref_pose[16], const dtsdf_intrinsics *K, float outlier, cudaStream_t s,
+                       IcpLaunch &L) {
+  if (!depth || !ref_depth || !ref_normal || !ref_pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  for (int i = 0; i < 16; ++i)
+    if (!std::isfinite(ref_pose[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
+  if (!(outlier > 0.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "outlier threshold must be > 0");
+  const size_t px = (size_t)K->width * K->height;
+  const size_t o_r = (px * 4 + 255) & ~size_t(255), o_n = o_r + o_r;
+  if ((rc = ensure_stage(c, o_n + px * 12 + 256))) return rc;
+  bool ok1, ok2, ok3;
+  std::memset(&L, 0, sizeof(L));
+  L.depth = (const float *)to_device(c, depth, px * 4, 0, s, &ok1);
+  L.ref_depth = (const float *)to_device(c, ref_depth, px * 4, o_r, s, &ok2);
+  L.ref_normal = (const float *)to_device(c, ref_normal, px * 12, o_n, s, &ok3);
+  if (!ok1 || !ok2 || !ok3) return cuda_fail(c, cudaGetLastError(), "stage ICP inputs");
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) L.ref_R[3 * a + b] = (double)ref_pose[4 * a + b];
+  L.fx = K->fx; L.fy = K->fy; L.cx = K->cx; L.cy = K->cy; L.z_min = K->z_min; L.z_max = K->z_max;
+  L.outlier = (double)outlier;
+  L.width = K->width;
+  L.height = K->height;
+  const size_t np = (size_t)icp_partials(K->width, K->height);
+  if (ensure(c->icp_partials, c->cap_icp_partials, np * 29 * sizeof(double)) != cudaSuccess ||
+      ensure(c->icp_state, c->cap_icp_state, sizeof(IcpState)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "ICP scratch");
+  }
+  L.partials = c->icp_partials;
+  L.state = c->icp_state;
+  return DTSDF_OK;
+}
+
+int dtsdf_icp(dtsdf_ctx *c, const float *depth, const float *ref_depth, const float *ref_normal,
+              const float ref_pose[16], const dtsdf_intrinsics *K, const float init_delta[16],
+              const dtsdf_icp_params *params, dtsdf_icp_result *out, void *stream) {
+  if (!c || !out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx/out is NULL");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  dtsdf_icp_params prm;
+  dtsdf_default_icp_params(&prm);
+  if (params) prm = *params;
+  if (prm.max_iters < 1 || prm.max_iters > 1000 || !(prm.min_step >= 0.f))
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad ICP parameters");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  IcpLaunch L;
+  int rc = icp_prepare(c, depth, ref_depth, ref_normal, ref_pose, K, prm.outlier, s, L);
+  if (rc) return rc;
+  L.min_step = prm.min_step;
+  L.max_iters = prm.max_iters;
+  IcpState init;
+  std::memset(&init, 0, sizeof(init));
+  for (int i = 0; i < 16; ++i) init.delta[i] = init_delta ? (double)init_delta[i] : ((i % 5) == 0 ? 1.0 : 0.0);
+  CK(c, cudaMemcpyAsync(c->icp_state, &init, sizeof(init), cudaMemcpyHostToDevice, s), "ICP init");
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl, 2 * prm.max_iters);
+  for (int it = 0; it < prm.max_iters; ++it) {
+    CK(c, launch_icp_reduce(L, s), "ICP reduce");
+    CK(c, launch_icp_solve(L, s), "ICP solve");
+  }
+  end_timed(c, s, &tl);
+  IcpState fin;
+  CK(c, cudaMemcpyAsync(&fin, c->icp_state, sizeof(fin), cudaMemcpyDeviceToHost, s), "ICP readback");
+  CK(c, cudaStreamSynchronize(s), "ICP sync");
+  for (int i = 0; i < 16; ++i) out->delta[i] = (float)fin.delta[i];
+  for (int i = 0; i < 16; ++i) out->delta64[i] = fin.delta[i];
+  out->iterations = fin.iterations;
+  out->inliers = fin.inliers;
+  out->step = fin.step;
+  out->residual = fin.residual;
+  out->status = fin.status;
+  return fin.status ? fail(DTSDF_ERR_SINGULAR, "singular ICP system (no or degenerate inliers)") : DTSDF_OK;
+}
+
+int dtsdf_icp_normal_equations(dtsdf_ctx *c, const float *depth, const float *ref_depth, const float *ref_normal,
+                               const float ref_pose[16], const dtsdf_intrinsics *K, const double delta[16],
+                               float outlier, double H[36], double g[6], int64_t *inliers, double *residual,
+                               void *stream) {
+  if (!c || !delta || !H || !g) return fail(DTSDF_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  IcpLaunch L;
+  int rc = icp_prepare(c, depth, ref_depth, ref_normal, ref_pose, K, outlier, s, L);
+  if (rc) return rc;
+  L.min_step = 0.0;
+  L.max_iters = 1;
+  IcpState init;
+  std::memset(&init, 0, sizeof(init));
+  for (int i = 0; i < 16; ++i) init.delta[i] = delta[i];
+  CK(c, cudaMemcpyAsync(c->icp_state, &init, sizeof(init), cudaMemcpyHostToDevice, s), "ICP init");
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl, 2);
+  CK(c, launch_icp_reduce(L, s), "ICP reduce");
+  CK(c, launch_icp_solve(L, s), "ICP solve");
+  end_timed(c, s, &tl);
+  IcpState fin;
+  CK(c, cudaMemcpyAsync(&fin, c->icp_state, sizeof(fin), cudaMemcpyDeviceToHost, s), "ICP readback");
+  CK(c, cudaStreamSynchronize(s), "ICP sync");
+  int k = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b) { H[6 * a + b] = H[6 * b + a] = fin.sums[k]; ++k; }
+  for (int a = 0; a < 6; ++a) g[a] = fin.sums[21 + a];
+  if (inliers) *inliers = (int64_t)fin.sums[27];
+  if (residual) *residual = fin.sums[28];
   return DTSDF_OK;
 }
 

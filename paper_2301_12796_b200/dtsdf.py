@@ -15,7 +15,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DTSDF_LIB") or os.path.join(_HERE, "libdtsdf.so")
 
-OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR, NO_COMBINED = 0, -1, -2, -3, -4, -5, -6
+OK, INVALID_ARGUMENT, DUPLICATE_KEY, NO_VOLUME, OUT_OF_MEMORY, CUDA_ERROR, NO_COMBINED, SINGULAR = \
+    0, -1, -2, -3, -4, -5, -6, -7
 VIEWS_PER_LAUNCH = 256
 
 EXPORTS = [
@@ -24,7 +25,7 @@ EXPORTS = [
     "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
     "dtsdf_combine", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
     "dtsdf_should_recombine", "dtsdf_default_fusion_params", "dtsdf_fusion_reserve", "dtsdf_depth_normals",
-    "dtsdf_fuse", "dtsdf_get_volume",
+    "dtsdf_fuse", "dtsdf_get_volume", "dtsdf_default_icp_params", "dtsdf_icp", "dtsdf_icp_normal_equations",
 ]
 MARGIN = 0.125  # PAPER.md:262 "(±1/8 image size)"
 OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID = 1, 2, 3, 4, 5
@@ -54,6 +55,15 @@ class CombinePolicy(C.Structure):
 class FusionParams(C.Structure):
     _fields_ = [("max_weight", C.c_float), ("carve_weight", C.c_float), ("carve_radius", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class IcpParams(C.Structure):
+    _fields_ = [("max_iters", C.c_int32), ("min_step", C.c_float), ("outlier", C.c_float), ("reserved", C.c_int32)]
+
+
+class IcpResult(C.Structure):
+    _fields_ = [("delta", C.c_float * 16), ("delta64", C.c_double * 16), ("iterations", C.c_int32),
+                ("status", C.c_int32), ("inliers", C.c_int64), ("step", C.c_double), ("residual", C.c_double)]
 
 
 class VolumeBuffers(C.Structure):
@@ -99,6 +109,11 @@ def lib():
         L.dtsdf_depth_normals.argtypes = [P, P, C.POINTER(Intrinsics), P, P]
         L.dtsdf_fuse.argtypes = [P, P, P, P, P, C.POINTER(Intrinsics), C.POINTER(FusionParams), C.POINTER(I64), P]
         L.dtsdf_get_volume.argtypes = [P, I64, P, P, P, P, C.POINTER(I64)]
+        L.dtsdf_default_icp_params.argtypes = [C.POINTER(IcpParams)]
+        L.dtsdf_default_icp_params.restype = None
+        L.dtsdf_icp.argtypes = [P, P, P, P, P, C.POINTER(Intrinsics), P, C.POINTER(IcpParams), C.POINTER(IcpResult), P]
+        L.dtsdf_icp_normal_equations.argtypes = [P, P, P, P, P, C.POINTER(Intrinsics), P, C.c_float, P, P,
+                                                 C.POINTER(I64), C.POINTER(C.c_double), P]
         L.dtsdf_last_error.argtypes = []
         L.dtsdf_last_error.restype = C.c_char_p
         _lib = L
@@ -252,6 +267,38 @@ class Renderer:
         got = C.c_int64()
         _check(lib().dtsdf_get_volume(self._h, n, _ptr(keys), _ptr(sdf), _ptr(w), _ptr(rgb), C.byref(got)))
         return keys, sdf, w, rgb
+
+    # -- ICP (NEXT-3) -----------------------------------------------------------------------
+    def icp(self, depth, ref_depth, ref_normal, ref_pose, K, init_delta=None, max_iters=50, min_step=1e-6,
+            outlier=0.005, stream=None, raise_singular=True):
+        """dtsdf_icp: DeltaT (frame camera -> rendered view camera, float64 [4,4]) and a result dict."""
+        prm = IcpParams(int(max_iters), float(min_step), float(outlier), 0)
+        res = IcpResult()
+        ref_pose = np.ascontiguousarray(np.asarray(ref_pose, np.float32).reshape(16))
+        init = None if init_delta is None else np.ascontiguousarray(np.asarray(init_delta, np.float32).reshape(16))
+        k = make_intrinsics(K)
+        rc = lib().dtsdf_icp(self._h, _ptr(depth), _ptr(ref_depth), _ptr(ref_normal), ref_pose.ctypes.data,
+                             C.byref(k), None if init is None else init.ctypes.data, C.byref(prm), C.byref(res),
+                             _stream_ptr(stream))
+        if rc != OK and (rc != SINGULAR or raise_singular):
+            _check(rc)
+        info = dict(iterations=res.iterations, status=res.status, inliers=res.inliers, step=res.step,
+                    residual=res.residual)
+        return np.array(res.delta64[:], np.float64).reshape(4, 4), info
+
+    def icp_normal_equations(self, depth, ref_depth, ref_normal, ref_pose, K, delta=None, outlier=0.005,
+                             stream=None):
+        """dtsdf_icp_normal_equations -> (H [6,6], g [6], inliers, sum w r^2)."""
+        delta = np.ascontiguousarray(np.eye(4) if delta is None else delta, np.float64).reshape(16)
+        ref_pose = np.ascontiguousarray(np.asarray(ref_pose, np.float32).reshape(16))
+        H, g = np.zeros(36), np.zeros(6)
+        n, r = C.c_int64(), C.c_double()
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_icp_normal_equations(self._h, _ptr(depth), _ptr(ref_depth), _ptr(ref_normal),
+                                                ref_pose.ctypes.data, C.byref(k), delta.ctypes.data,
+                                                float(outlier), H.ctypes.data, g.ctypes.data, C.byref(n),
+                                                C.byref(r), _stream_ptr(stream)))
+        return H.reshape(6, 6), g, n.value, r.value
 
     # -- combined TSDF (NEXT-1) -----------------------------------------------------------
     def combine(self, pose, K, margin=MARGIN, stream=None):
