@@ -445,6 +445,8 @@ typedef struct {
   double fx, fy, cx, cy, zmin, zmax;
   int W, H;
   double margin; /* fraction of the image size added on every side (1/8) */
+  int mode;      /* 0: eq:combine_weight / eq:combine_tsdf_weight (R34); 1: Algorithm 1 (R53-R57) */
+  double w_floor;/* Algorithm 1: directions need a stored weight above this (R53) */
 } ocam;
 
 static void cam_from(ocam *c, const double pose[16], const double intr[8], double margin) {
@@ -455,6 +457,8 @@ static void cam_from(ocam *c, const double pose[16], const double intr[8], doubl
   c->fx = intr[0]; c->fy = intr[1]; c->cx = intr[2]; c->cy = intr[3];
   c->W = (int)intr[4]; c->H = (int)intr[5]; c->zmin = intr[6]; c->zmax = intr[7];
   c->margin = margin;
+  c->mode = 0;
+  c->w_floor = 0.0;
 }
 
 /* R33: voxel (i,j,k) lies in the source view frustum widened by margin*W / margin*H pixels on
@@ -486,7 +490,10 @@ typedef struct {
  * n^D from "the SDF values stored in the 6 neighboring voxels", i.e. central
  * differences (phi(i+e_a) - phi(i-e_a)) / 2s; r = the normalised ray from the source camera
  * centre to the voxel.  Directions, gradient presence and the regime choice as O3 (R8-R10). */
+static void combine_voxel_alg1(const ovol *v, const ocam *c, int64_t i, int64_t j, int64_t k, ocvox *o);
+
 static void combine_voxel(const ovol *v, const ocam *c, int64_t i, int64_t j, int64_t k, ocvox *o) {
+  if (c->mode == 1) { combine_voxel_alg1(v, c, i, j, k, o); return; }
   memset(o, 0, sizeof(*o));
   if (!in_frustum(c, v->s, i, j, k)) return;
   double x[3] = {(double)i * v->s, (double)j * v->s, (double)k * v->s};
@@ -553,6 +560,135 @@ static void combine_voxel(const ovol *v, const ocam *c, int64_t i, int64_t j, in
   o->mask = m;
 }
 
+
+/* ---------------------------------------------------------------------------------------
+ * NEXT-4: Algorithm 1 "Compute Combined TSDF" (prose P:217-226) at an integer
+ * voxel position, readings R53-R57:
+ *   R53 a direction D takes part iff allocated at the voxel, its stored weight exceeds w_floor
+ *       (0 by default: ">0"), its 6-neighbour gradient exists (|g| > 1e-3) and is valid w.r.t.
+ *       the direction vector, w_dir(<n^D, v^D>) > 0 ("ignoring information from points with
+ *       invalid gradients")
+ *   R54 F = taking-part directions with phi_D(p) > 0 (free), O = those with phi_D(p) <= 0
+ *   R55 for D in F: q = first zero transition of Phi^D from p towards the camera (-r): samples
+ *       p - k s r, k = 1 .. floor(|p - c| / s), the march ends without a transition (q = none) at
+ *       the first sample where D is absent; bisection in the bracket (invalid midpoints positive)
+ *   R56 D's free space stands iff q = none or no other direction D~ has Phi^D~(q) < 0 with a
+ *       gradient n^D~(q) (central differences, R7) and <n^D~(q), -r> > 0; freespace = OR over F
+ *   R57 freespace -> the stored-weight average of the F directions; else of the O directions;
+ *       else invalid ("all congruent directions are combined as weighted sum using the fused voxel
+ *       weights")
+ * ------------------------------------------------------------------------------------- */
+static int dir_value(const ovol *v, int D, const double x[3], double *phi) {
+  int64_t cc[3];
+  double fr[3], om;
+  locate(v, x, cc, fr);
+  return cell_interp(v, D, cc, fr, phi, &om, 0, NULL);
+}
+
+static int dir_normal(const ovol *v, int D, const double x[3], double n[3]) {
+  int64_t cc[3];
+  double fr[3], g[3];
+  locate(v, x, cc, fr);
+  if (!cell_gradient(v, D, cc, fr, g)) return 0;
+  double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  if (!(gn > OR_EPS_GRAD)) return 0;
+  for (int a = 0; a < 3; ++a) n[a] = g[a] / gn;
+  return 1;
+}
+
+static void combine_voxel_alg1(const ovol *v, const ocam *c, int64_t i, int64_t j, int64_t k, ocvox *o) {
+  memset(o, 0, sizeof(*o));
+  if (!in_frustum(c, v->s, i, j, k)) return;
+  double x[3] = {(double)i * v->s, (double)j * v->s, (double)k * v->s};
+  double r[3] = {x[0] - c->t[0], x[1] - c->t[1], x[2] - c->t[2]};
+  double dist = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (!(dist > 0.0)) return;
+  for (int a = 0; a < 3; ++a) r[a] /= dist;
+  const int64_t vi[3] = {i, j, k};
+  double phi[6], om[6];
+  int64_t rec[6];
+  int part[6];
+  for (int D = 0; D < 6; ++D) {
+    part[D] = 0;
+    rec[D] = record_of(v, D, i, j, k);
+    if (rec[D] < 0) continue;
+    phi[D] = (double)v->sdf[rec[D]];
+    om[D] = (double)v->weight[rec[D]];
+    if (!(om[D] > c->w_floor)) continue;
+    double g[3];
+    int ok = 1;
+    for (int a = 0; a < 3 && ok; ++a) {
+      int64_t pp[3] = {vi[0], vi[1], vi[2]}, mm[3] = {vi[0], vi[1], vi[2]};
+      pp[a] += 1;
+      mm[a] -= 1;
+      int64_t rp = record_of(v, D, pp[0], pp[1], pp[2]), rm = record_of(v, D, mm[0], mm[1], mm[2]);
+      if (rp < 0 || rm < 0) { ok = 0; break; }
+      g[a] = ((double)v->sdf[rp] - (double)v->sdf[rm]) / (2.0 * v->s);
+    }
+    if (!ok) continue;
+    double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+    if (!(gn > OR_EPS_GRAD)) continue;
+    double nv = (g[0] * VDIR[D][0] + g[1] * VDIR[D][1] + g[2] * VDIR[D][2]) / gn;
+    if (!(oracle_w_dir(nv, v->theta) > 0.0)) continue;
+    part[D] = 1;
+  }
+  int freespace = 0, any_free = 0, any_occ = 0;
+  const int64_t K = (int64_t)floor(dist / v->s);
+  for (int D = 0; D < 6; ++D) {
+    if (!part[D]) continue;
+    if (!(phi[D] > 0.0)) { any_occ = 1; continue; }
+    any_free = 1;
+    if (freespace) continue;
+    /* R55: back-march towards the camera in Phi^D */
+    double prev_t = 0.0, qt = -1.0;
+    for (int64_t kk = 1; kk <= K; ++kk) {
+      double t = (double)kk * v->s, y[3] = {x[0] - t * r[0], x[1] - t * r[1], x[2] - t * r[2]}, f;
+      if (!dir_value(v, D, y, &f)) break; /* D absent: no transition observed */
+      if (f <= 0.0) {
+        double a = prev_t, b = t;
+        for (int it = 0; it < 50; ++it) {
+          double m = 0.5 * (a + b), ym[3] = {x[0] - m * r[0], x[1] - m * r[1], x[2] - m * r[2]}, fm;
+          if (!(m > a && m < b)) break;
+          if (!dir_value(v, D, ym, &fm) || fm > 0.0) a = m; else b = m;
+        }
+        qt = 0.5 * (a + b);
+        break;
+      }
+      prev_t = t;
+    }
+    if (qt < 0.0) { freespace = 1; continue; }
+    double q[3] = {x[0] - qt * r[0], x[1] - qt * r[1], x[2] - qt * r[2]};
+    int conflict = 0;
+    for (int E = 0; E < 6 && !conflict; ++E) {
+      if (E == D) continue;
+      double fe, ne[3];
+      if (!dir_value(v, E, q, &fe) || !(fe < 0.0)) continue;
+      if (!dir_normal(v, E, q, ne)) continue;
+      if (-(ne[0] * r[0] + ne[1] * r[1] + ne[2] * r[2]) > 0.0) conflict = 1;
+    }
+    if (!conflict) freespace = 1;
+  }
+  if (!any_free && !any_occ) return;
+  const int use_free = freespace;
+  if (!use_free && !any_occ) return;
+  double S = 0.0, F = 0.0, C[3] = {0, 0, 0};
+  int m = 0;
+  for (int D = 0; D < 6; ++D) {
+    if (!part[D] || ((phi[D] > 0.0) != (use_free != 0))) continue;
+    S += om[D];
+    F += om[D] * phi[D];
+    if (v->rgb)
+      for (int a = 0; a < 3; ++a) C[a] += om[D] * (double)v->rgb[3 * rec[D] + a];
+    m |= 1 << D;
+  }
+  if (!(S > 0.0)) return;
+  o->valid = 1;
+  o->S = S;
+  o->sdf = F / S;
+  for (int a = 0; a < 3; ++a) o->rgb[a] = C[a] / S;
+  o->mask = m;
+}
+
 /* R35: the stored colour of a combined voxel is the u8 value min(255, floor(c + 1/2)) */
 static uint8_t u8_round(double c) {
   double q = floor(c + 0.5);
@@ -561,11 +697,14 @@ static uint8_t u8_round(double c) {
 
 /* Combined voxels of a list of integer positions (element-wise parity / pins).
  * ijk [n][3]; outputs valid[n], sdf[n], S[n], rgb[n][3] (u8 after R35), mask[n]. */
-void oracle_combined_voxels(void *p, const double pose[16], const double intr[8], double margin, int64_t n,
-                            const int64_t *ijk, int32_t *valid, double *sdf, double *S, uint8_t *rgb, uint8_t *mask) {
+void oracle_combined_voxels_mode(void *p, const double pose[16], const double intr[8], double margin, int mode,
+                                 double w_floor, int64_t n, const int64_t *ijk, int32_t *valid, double *sdf, double *S,
+                                 uint8_t *rgb, uint8_t *mask) {
   const ovol *v = (const ovol *)p;
   ocam c;
   cam_from(&c, pose, intr, margin);
+  c.mode = mode;
+  c.w_floor = w_floor;
   for (int64_t q = 0; q < n; ++q) {
     ocvox o;
     combine_voxel(v, &c, ijk[3 * q], ijk[3 * q + 1], ijk[3 * q + 2], &o);
@@ -728,13 +867,16 @@ static void *worker_combined(void *arg) {
 
 /* Render npix pixels of the view (pose, intr) from the combined TSDF of the source camera
  * (src_pose, src_intr, margin).  Argument conventions as oracle_render. */
-void oracle_render_combined(void *p, const double src_pose[16], const double src_intr[8], double margin,
-                            const double pose[16], const double intr[8], int64_t npix, const int32_t *uv, int row0,
-                            int nthreads, double *depth, double *normal, uint8_t *color, uint8_t *mask) {
+void oracle_render_combined_mode(void *p, const double src_pose[16], const double src_intr[8], double margin,
+                                 int mode, double w_floor, const double pose[16], const double intr[8], int64_t npix,
+                                 const int32_t *uv, int row0, int nthreads, double *depth, double *normal,
+                                 uint8_t *color, uint8_t *mask) {
   ocjob C;
   memset(&C, 0, sizeof(C));
   C.v = (const ovol *)p;
   cam_from(&C.src, src_pose, src_intr, margin);
+  C.src.mode = mode;
+  C.src.w_floor = w_floor;
   ojob *J = &C.J;
   J->v = C.v;
   for (int a = 0; a < 3; ++a) {
