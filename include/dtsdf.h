@@ -152,6 +152,19 @@ DTSDF_API int dtsdf_volume_stats(dtsdf_ctx *ctx, int64_t *n_blocks, int64_t *n_l
 DTSDF_API int dtsdf_combine(dtsdf_ctx *ctx, const float pose_w_c[16], const dtsdf_intrinsics *intr, float margin,
                             void *cuda_stream);
 
+/* Same with a choice of combination rule:
+ *   DTSDF_COMBINE_WEIGHTED    eq:combine_weight / eq:combine_tsdf_weight (the paper's method; dtsdf_combine)
+ *   DTSDF_COMBINE_ALGORITHM1  Algorithm 1 "Compute Combined TSDF" (readings R53-R57): a
+ *                             direction takes part iff its stored weight exceeds w_floor and its gradient is
+ *                             valid for it; a free direction's free space stands unless its first zero
+ *                             transition towards the camera lies in another direction's visible occupied
+ *                             space; stored-weight average of the free (else occupied) directions.  The paper
+ *                             reports it underperforms on real data; w_floor >= 0 (0 in the paper). */
+#define DTSDF_COMBINE_WEIGHTED 0
+#define DTSDF_COMBINE_ALGORITHM1 1
+DTSDF_API int dtsdf_combine_mode(dtsdf_ctx *ctx, const float pose_w_c[16], const dtsdf_intrinsics *intr, float margin,
+                                 int32_t mode, float w_floor, void *cuda_stream);
+
 /* Raycast the current combined TSDF "like a regular TSDF" (readings R36-R37) from
  * n_views poses: same lattice, crossing rule, refinement, argument layout, host/device output
  * handling and errors as dtsdf_render_batch, plus NO_COMBINED.  Valid for poses near the source

@@ -231,6 +231,212 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
   p.weight[slot * kVoxPerBlock + l] = valid ? S : 0.f;
 }
 
+
+// ------------------------------------------------------------------------------------------
+// NEXT-4: Algorithm 1 "Compute Combined TSDF", readings R53-R57 (oracle.c
+// combine_voxel_alg1): per voxel, the directions taking part (valid gradient w.r.t. the
+// direction, stored weight above the floor) split into free (phi > 0) and occupied; a free
+// direction's free space stands unless its first zero transition towards the camera lies in the
+// occupied space of another direction whose surface faces the camera; the result is the stored-
+// weight average of the free directions if any free space stands, else of the occupied ones.
+// Sample positions are fp64 (the oracle's formulas), interpolation fp32.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ long long floordiv8_ll(long long i) { return i >= 0 ? i / 8 : -((-i + 7) / 8); }
+
+// direction D's apron brick for the base cell of world point y, and the cell's local offset and
+// fractions; false when D is not allocated at that location
+__device__ bool dir_cell(const CombineLaunch &p, int D, const double y[3], const float2 **br, double fr[3]) {
+  const VolumeView &V = p.vol;
+  long long ci[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double g = y[a] / (double)V.voxel_size;
+    const double fl = floor(g);
+    ci[a] = (long long)fl;
+    fr[a] = g - fl;
+  }
+  const long long b0 = floordiv8_ll(ci[0]), b1 = floordiv8_ll(ci[1]), b2 = floordiv8_ll(ci[2]);
+  int e = -1;
+  if (V.loc_grid) {
+    const long long x = b0 - V.lo_x, yy = b1 - V.lo_y, z = b2 - V.lo_z;
+    if (x < 0 || yy < 0 || z < 0 || x >= V.dim_x || yy >= V.dim_y || z >= V.dim_z) return false;
+    const int gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + yy) * V.dim_x + x]);
+    if (gv < 0) return false;
+    e = gv & 0x3fffffff;
+  } else {
+    const unsigned long long key = pack_key((int)b0, (int)b1, (int)b2);
+    unsigned int h = hash_key(key) & V.table_mask;
+    for (unsigned int probe = 0; probe <= V.table_mask; ++probe) {
+      const unsigned long long k = V.table[h].key;
+      if (k == key) { e = (int)h; break; }
+      if (k == kEmptyKey) return false;
+      h = (h + 1) & V.table_mask;
+    }
+    if (e < 0) return false;
+  }
+  const int slot = V.table[e].slot[D];
+  if (slot < 0) return false;
+  const int lx = (int)(ci[0] - 8 * b0), ly = (int)(ci[1] - 8 * b1), lz = (int)(ci[2] - 8 * b2);
+  *br = V.apron + (size_t)slot * kApronStride + lx + kApron * ly + kApron * kApron * lz;
+  return true;
+}
+
+// Algorithm 1 takes discrete decisions from these values (free / occupied, first transition,
+// conflicting direction), so they are evaluated in fp64 like the oracle's (float voxel values,
+// fp64 fractions): a decision can only differ where the oracle's value itself is ~1e-16 from it.
+__device__ __forceinline__ double tri64(const float2 *c, const double f[3]) {
+  const double c000 = c[CAPRON(0, 0, 0)].x, c100 = c[CAPRON(1, 0, 0)].x, c010 = c[CAPRON(0, 1, 0)].x,
+               c110 = c[CAPRON(1, 1, 0)].x, c001 = c[CAPRON(0, 0, 1)].x, c101 = c[CAPRON(1, 0, 1)].x,
+               c011 = c[CAPRON(0, 1, 1)].x, c111 = c[CAPRON(1, 1, 1)].x;
+  const double e00 = c000 + f[0] * (c100 - c000), e10 = c010 + f[0] * (c110 - c010);
+  const double e01 = c001 + f[0] * (c101 - c001), e11 = c011 + f[0] * (c111 - c011);
+  const double r0 = e00 + f[1] * (e10 - e00), r1 = e01 + f[1] * (e11 - e01);
+  return r0 + f[2] * (r1 - r0);
+}
+
+// trilinear phi_D at y (NaN: absent -- a corner in an unallocated block)
+__device__ double dir_value(const CombineLaunch &p, int D, const double y[3]) {
+  const float2 *b;
+  double f[3];
+  if (!dir_cell(p, D, y, &b, f)) return CUDART_NAN;
+  return tri64(b, f);
+}
+
+// unit normal of phi_D at y: central differences of the trilinear field at +-s (R7); false if
+// the stencil is incomplete or |g| <= 1e-3
+__device__ bool dir_normal(const CombineLaunch &p, int D, const double y[3], double n[3]) {
+  const float2 *b;
+  double f[3];
+  if (!dir_cell(p, D, y, &b, f)) return false;
+  double g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int e = a == 0 ? 1 : (a == 1 ? kApron : kApron * kApron);
+    g[a] = (tri64(b + e, f) - tri64(b - e, f)) / (2.0 * (double)p.vol.voxel_size);
+  }
+  const double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
+  if (!(gn > 1e-3)) return false;  // NaN (incomplete stencil) -> false
+  n[0] = g[0] / gn; n[1] = g[1] / gn; n[2] = g[2] / gn;
+  return true;
+}
+
+__global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p,
+                                                      const unsigned char *__restrict__ cls_in) {
+  const VolumeView &V = p.vol;
+  const size_t slot = blockIdx.x;
+  const int l = blockIdx.y * 128 + threadIdx.x;
+  const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+  const int4 b = p.comb_loc[slot];
+  const int4 *ent = reinterpret_cast<const int4 *>(&V.table[b.w]);
+  const int4 ea = __ldg(ent), eb = __ldg(ent + 1);
+  const int sl[6] = {ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
+  const int i = kBlock * b.x + lx, j = kBlock * b.y + ly, k = kBlock * b.z + lz;
+  double d[3];
+  bool in = true;
+  if (cls_in[slot] == 2) {
+    in = in_frustum(p, (double)V.voxel_size, i, j, k, d);
+  } else {
+    const double s = (double)V.voxel_size;
+    d[0] = __dsub_rn(__dmul_rn((double)i, s), p.t[0]);
+    d[1] = __dsub_rn(__dmul_rn((double)j, s), p.t[1]);
+    d[2] = __dsub_rn(__dmul_rn((double)k, s), p.t[2]);
+  }
+  const double dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  const double x[3] = {(double)i * (double)V.voxel_size, (double)j * (double)V.voxel_size,
+                       (double)k * (double)V.voxel_size};
+  const double r[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+  const int off = CAPRON(lx, ly, lz), coff = lx + kRgbApron * ly + kRgbApron * kRgbApron * lz;
+  float phi[6], om[6];
+  unsigned part = 0, free_m = 0;
+  if (in && dist > 0.0) {
+#pragma unroll
+    for (int D = 0; D < 6; ++D) {
+      if (sl[D] < 0) continue;
+      const float2 *br = V.apron + (size_t)sl[D] * kApronStride + off;
+      const float2 c = __ldg(br);
+      phi[D] = c.x;
+      om[D] = c.y;
+      if (!(c.y > p.w_floor)) continue;  // R53 (decided in fp64 like the oracle)
+      const double two_s = 2.0 * (double)V.voxel_size;
+      const double gx = ((double)__ldg(&br[1].x) - (double)__ldg(&br[-1].x)) / two_s;
+      const double gy = ((double)__ldg(&br[kApron].x) - (double)__ldg(&br[-kApron].x)) / two_s;
+      const double gz = ((double)__ldg(&br[kApron * kApron].x) - (double)__ldg(&br[-kApron * kApron].x)) / two_s;
+      const double gn = sqrt(gx * gx + gy * gy + gz * gz);
+      if (!(gn > 1e-3)) continue;
+      const double nax = (D >> 1) == 0 ? gx : ((D >> 1) == 1 ? gy : gz);
+      if (!(acos(fmin(fmax(((D & 1) ? -nax : nax) / gn, -1.0), 1.0)) < p.theta64)) continue;  // w_dir > 0
+      part |= 1u << D;
+      if (c.x > 0.0f) free_m |= 1u << D;
+    }
+  }
+  // R55-R56: does any free direction's free space stand?
+  bool freespace = false;
+  const long long K = (long long)floor(dist / (double)V.voxel_size);
+  for (int D = 0; D < 6 && !freespace; ++D) {
+    if (!((free_m >> D) & 1u)) continue;
+    double prev_t = 0.0, qt = -1.0;
+    for (long long kk = 1; kk <= K; ++kk) {
+      const double t = (double)kk * (double)V.voxel_size;
+      const double y[3] = {x[0] - t * r[0], x[1] - t * r[1], x[2] - t * r[2]};
+      const double f = dir_value(p, D, y);
+      if (isnan(f)) break;  // D absent: no transition observed
+      if (f <= 0.0) {
+        double a = prev_t, bb = t;
+        for (int it = 0; it < 50; ++it) {
+          const double m = 0.5 * (a + bb);
+          if (!(m > a && m < bb)) break;
+          const double ym[3] = {x[0] - m * r[0], x[1] - m * r[1], x[2] - m * r[2]};
+          const double fm = dir_value(p, D, ym);
+          if (isnan(fm) || fm > 0.0) a = m; else bb = m;
+        }
+        qt = 0.5 * (a + bb);
+        break;
+      }
+      prev_t = t;
+    }
+    if (qt < 0.0) { freespace = true; break; }
+    const double q[3] = {x[0] - qt * r[0], x[1] - qt * r[1], x[2] - qt * r[2]};
+    bool conflict = false;
+    for (int E = 0; E < 6 && !conflict; ++E) {
+      if (E == D) continue;
+      const double fe = dir_value(p, E, q);
+      if (!(fe < -1e-6)) continue;  // strictly inside E's occupied space (R56)
+      double ne[3];
+      if (!dir_normal(p, E, q, ne)) continue;
+      if (-(ne[0] * r[0] + ne[1] * r[1] + ne[2] * r[2]) > 0.0) conflict = true;
+    }
+    if (!conflict) freespace = true;
+  }
+  // R57: stored-weight average of the chosen set.  The colour sums are fp64: stored weights are
+  // float32 and colours integers, so products and sums are exact and an average that is exactly
+  // k + 1/2 (equal weights, e.g. a plate's front and back directions) rounds as in the oracle.
+  const unsigned use = freespace ? free_m : (part & ~free_m);
+  float S = 0.f, F = 0.f;
+  double Sd = 0.0, C[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int D = 0; D < 6; ++D) {
+    if (!((use >> D) & 1u)) continue;
+    const uchar4 q = __ldg(V.rgb_apron + (size_t)sl[D] * kRgbApronStride + coff);
+    S += om[D];
+    F = fmaf(om[D], phi[D], F);
+    Sd += (double)om[D];
+    C[0] += (double)om[D] * q.x; C[1] += (double)om[D] * q.y; C[2] += (double)om[D] * q.z;
+  }
+  float sdf = CUDART_NAN_F;
+  uchar4 col = make_uchar4(0, 0, 0, 0);
+  const bool valid = use != 0 && S > 0.0f;
+  if (valid) {
+    sdf = F / S;
+    unsigned char cc[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) cc[a] = (unsigned char)fmin(fmax(floor(C[a] / Sd + 0.5), 0.0), 255.0);
+    col = make_uchar4(cc[0], cc[1], cc[2], (unsigned char)use);
+  }
+  p.apron[slot * kApronStride + off] = sdf;
+  p.rgb[slot * kRgbApronStride + coff] = col;
+  p.weight[slot * kVoxPerBlock + l] = valid ? S : 0.f;
+}
+
 // combined slot of block location (bx,by,bz), or -1
 __device__ __forceinline__ int comb_slot_of(const CombineLaunch &p, int bx, int by, int bz) {
   const VolumeView &V = p.vol;
@@ -352,7 +558,10 @@ cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s) {
 
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
-  k_combine<<<dim3((unsigned)n_sel, 4), 128, 0, s>>>(p, p.surf);
+  if (p.mode == 1)
+    k_combine_alg1<<<dim3((unsigned)n_sel, 4), 128, 0, s>>>(p, p.surf);
+  else
+    k_combine<<<dim3((unsigned)n_sel, 4), 128, 0, s>>>(p, p.surf);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_comb_finish<<<(unsigned)n_sel, kFinishThreads, 0, s>>>(p);

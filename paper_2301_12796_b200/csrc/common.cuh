@@ -117,6 +117,9 @@ struct CombineLaunch {
   float *weight;                   // [cap][512] S = sum_D W_D of each interior voxel
   unsigned int *cell_pos;          // [cap][16]
   unsigned char *surf;             // [cap]
+  int mode;                        // 0 eq:combine_weight / eq:combine_tsdf_weight, 1 Algorithm 1
+  float w_floor;                   // Algorithm 1: stored-weight floor of a taking-part direction
+  double theta64;                  // Algorithm 1: theta (fp64) for the w_dir > 0 decision
 };
 
 struct RangeLaunch {

@@ -587,7 +587,15 @@ int dtsdf_render_combined(dtsdf_ctx *c, int32_t n_views, const float *poses, con
 }
 
 int dtsdf_combine(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float margin, void *stream) {
+  return dtsdf_combine_mode(c, pose, K, margin, DTSDF_COMBINE_WEIGHTED, 0.0f, stream);
+}
+
+int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float margin, int32_t mode,
+                       float w_floor, void *stream) {
   if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (mode != DTSDF_COMBINE_WEIGHTED && mode != DTSDF_COMBINE_ALGORITHM1)
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown combination mode");
+  if (!(w_floor >= 0.f) || !std::isfinite(w_floor)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "w_floor must be >= 0");
   if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
   int rc = check_intr(K);
   if (rc) return rc;
@@ -650,6 +658,9 @@ int dtsdf_combine(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K,
   L.weight = c->comb_weight;
   L.cell_pos = c->comb_cell_pos;
   L.surf = c->comb_surf;
+  L.mode = mode;
+  L.w_floor = w_floor;
+  L.theta64 = (double)c->params.theta;
   TimedLaunch tl{};
   CK(c, cudaMemsetAsync(c->comb_slot, 0xFF, (size_t)c->table_cap * 4, s), "combine init");
   CK(c, cudaMemsetAsync(c->comb_count, 0, 16, s), "combine init");

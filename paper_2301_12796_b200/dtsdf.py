@@ -23,7 +23,7 @@ EXPORTS = [
     "dtsdf_create", "dtsdf_destroy", "dtsdf_alloc_volume", "dtsdf_commit_volume", "dtsdf_upload_volume",
     "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
     "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
-    "dtsdf_combine", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
+    "dtsdf_combine", "dtsdf_combine_mode", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
     "dtsdf_should_recombine", "dtsdf_default_fusion_params", "dtsdf_fusion_reserve", "dtsdf_depth_normals",
     "dtsdf_fuse", "dtsdf_get_volume", "dtsdf_default_icp_params", "dtsdf_icp", "dtsdf_icp_normal_equations",
 ]
@@ -97,6 +97,7 @@ def lib():
         L.dtsdf_launch_count.argtypes = [P]
         L.dtsdf_launch_count.restype = I64
         L.dtsdf_combine.argtypes = [P, P, C.POINTER(Intrinsics), C.c_float, P]
+        L.dtsdf_combine_mode.argtypes = [P, P, C.POINTER(Intrinsics), C.c_float, C.c_int32, C.c_float, P]
         L.dtsdf_render_combined.argtypes = [P, I32, P, C.POINTER(Intrinsics), I32, I32, P, P, P, P, P]
         L.dtsdf_combined_stats.argtypes = [P, C.POINTER(I64), C.POINTER(I64)]
         L.dtsdf_get_combined.argtypes = [P, I64, P, P, P, P, P, C.POINTER(I64)]
@@ -301,11 +302,13 @@ class Renderer:
         return H.reshape(6, 6), g, n.value, r.value
 
     # -- combined TSDF (NEXT-1) -----------------------------------------------------------
-    def combine(self, pose, K, margin=MARGIN, stream=None):
-        """dtsdf_combine: the view-dependent combined TSDF of the source camera (pose, K)."""
+    def combine(self, pose, K, margin=MARGIN, stream=None, mode=0, w_floor=0.0):
+        """dtsdf_combine_mode: the view-dependent combined TSDF of the source camera (pose, K);
+        mode 0 = eq:combine_weight (the paper's method), 1 = Algorithm 1."""
         pose = np.ascontiguousarray(np.asarray(pose, np.float32).reshape(16))
         k = make_intrinsics(K)
-        _check(lib().dtsdf_combine(self._h, pose.ctypes.data, C.byref(k), float(margin), _stream_ptr(stream)))
+        _check(lib().dtsdf_combine_mode(self._h, pose.ctypes.data, C.byref(k), float(margin), int(mode),
+                                        float(w_floor), _stream_ptr(stream)))
 
     def render_combined_into(self, poses, K, depth, normal=None, color=None, mask=None, row0=0, row1=None,
                              stream=None):

@@ -41,7 +41,7 @@ def _voxels(locs):
     return (locs.astype(np.int64)[:, None, :] * 8 + off[None]).reshape(-1, 3)
 
 
-def _compare_voxels(R, w, pose, budget=1e-3):
+def _compare_voxels(R, w, pose, budget=1e-3, mode=0):
     """Every exported combined voxel against the oracle's combine_voxel at the same position, and
     sampled non-exported locations hold no valid oracle voxel."""
     ex = R.get_combined()
@@ -49,7 +49,7 @@ def _compare_voxels(R, w, pose, budget=1e-3):
     assert n > 0
     ov = oracle.OracleVolume(w.volume)
     ijk = _voxels(ex["locs"])
-    o = oracle.combined_voxels(ov, pose, w.intrinsics, ijk)
+    o = oracle.combined_voxels(ov, pose, w.intrinsics, ijk, mode=mode)
     g_valid = ~np.isnan(ex["sdf"].reshape(-1))
     assert np.array_equal(g_valid, ex["weight"].reshape(-1) > 0)
     disagree = (g_valid != o["valid"]).sum()
@@ -72,7 +72,8 @@ def _compare_voxels(R, w, pose, budget=1e-3):
     if len(rest):
         rng = np.random.default_rng(0)
         pick = rest[rng.choice(len(rest), min(len(rest), 400), replace=False)]
-        assert oracle.combined_voxels(ov, pose, w.intrinsics, _voxels(pick))["valid"].sum() <= budget * both.sum()
+        assert oracle.combined_voxels(ov, pose, w.intrinsics, _voxels(pick), mode=mode)["valid"].sum() <= \
+            budget * both.sum()
     return st
 
 
@@ -184,3 +185,19 @@ def test_combined_host_outputs_equal_device(R, c1):
     R.render_combined_into(c1.poses, K, hd, hn, hc, hm)
     assert np.array_equal(hd, to_np(g["depth"])) and np.array_equal(hn, to_np(g["normal"]))
     assert np.array_equal(hc, to_np(g["color"])) and np.array_equal(hm, to_np(g["mask"]))
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_algorithm1_voxels_and_render(R, cfg, c1, c2):
+    """NEXT-4: the Algorithm-1 combined TSDF (mode 1, readings R53-R57) -- every combined voxel
+    against the oracle, then the render through it (BJ tolerances)."""
+    w = c1 if cfg == "C1" else c2
+    v = 0
+    R.upload_volume(w.volume)
+    R.combine(w.poses[v], w.intrinsics, mode=1)
+    st = _compare_voxels(R, w, w.poses[v], mode=1)
+    g = R.render(w.poses[v:v + 1], w.intrinsics, combined=True)
+    o = oracle.render_combined(oracle.OracleVolume(w.volume), w.poses[v], w.intrinsics, w.poses[v], w.intrinsics,
+                               mode=1)
+    rs = assert_parity(_sel(g, 0), o, what=f"{cfg} algorithm 1")
+    print(cfg, "algorithm 1", st, rs)
