@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--mode", choices=["direct", "combined"], default="direct",
                     help="direct: per-sample combination (the north-star path); combined: the paper's "
                          "view-dependent combined TSDF (NEXT-1), recombined per eqs. 10-13 inside the timed loop")
+    ap.add_argument("--combine-mode", type=int, default=0, choices=[0, 1],
+                    help="combined mode: 0 eq:combine_weight (the paper's method), 1 Algorithm 1 (NEXT-4)")
     return ap.parse_args()
 
 
@@ -267,7 +269,7 @@ def run_dtsdf(args):
         for i in range(len(poses)):
             f = seq["frame"]
             if seq["last_pose"] is None or should_recombine(f, seq["last"], poses[i], seq["last_pose"]):
-                R.combine(poses[i], K, stream=stream)
+                R.combine(poses[i], K, stream=stream, mode=args.combine_mode)
                 seq["last"], seq["last_pose"] = f, poses[i]
                 seq["combines"] += 1
             sl = slice(i, i + 1)
@@ -372,7 +374,8 @@ def run_dtsdf(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scene, DESIGN.md §3)",
-        "config": dict(describe(w, args.views), mode=args.mode),
+        "config": dict(describe(w, args.views), mode=args.mode,
+                       **({"combine_mode": args.combine_mode} if args.mode == "combined" else {})),
         "frames_per_s": world * args.views * args.steps / (max_ms / 1e3),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
