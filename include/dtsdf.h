@@ -312,6 +312,9 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
 #define DTSDF_OPT_SCHEDULE 3
 #define DTSDF_OPT_BISECT_STEPS 4
 #define DTSDF_OPT_LOCATION_GRID 5
+/*   DTSDF_OPT_REFINE_TOL_NM  0 (default) regula falsi stops when f(b) is within 1e-7 of the root or after
+ *                            12 steps; n > 0 also stops it once the bracket is narrower than n nanometres */
+#define DTSDF_OPT_REFINE_TOL_NM 6
 DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
 
 /* Kernel launches issued by this context since creation (all kinds). */

@@ -75,7 +75,7 @@ struct dtsdf_ctx {
   size_t range_cap = 0;  // tiles
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
-  int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1;
+  int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1, refine_tol_nm = 0;
   int *tile_counter = nullptr;
   // view-dependent combined TSDF (NEXT-1, combine.cu)
   bool combined = false;
@@ -490,6 +490,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     while (V.delta / (float)(1 << pl.n_bisect) > 5e-5f && pl.n_bisect < 20) ++pl.n_bisect;
     if (c->bisect_steps >= 0) pl.n_bisect = c->bisect_steps;
     pl.schedule = c->schedule;
+    pl.refine_tol = 1e-9f * (float)c->refine_tol_nm;
     pl.tile_counter = c->tile_counter;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
     const size_t px = (size_t)v0 * rows * W;
@@ -1134,6 +1135,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_SCHEDULE && (value == 0 || value == 1)) c->schedule = value;
   else if (option == DTSDF_OPT_LOCATION_GRID) c->use_grid = value ? 1 : 0;
   else if (option == DTSDF_OPT_BISECT_STEPS && value >= -1 && value <= 30) c->bisect_steps = value;
+  else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

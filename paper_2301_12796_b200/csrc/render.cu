@@ -16,9 +16,6 @@
 
 #include "common.cuh"
 
-#ifndef DTSDF_RAYCAST_MINB
-#define DTSDF_RAYCAST_MINB 2
-#endif
 
 namespace dtsdf {
 
@@ -716,7 +713,7 @@ struct RayT {
         side = -1;
         if (s.f > -1e-7f) mode = kShade;  // b sits on the root
       }
-      if (++it >= 12) mode = kShade;
+      if (++it >= 12 || b - a < p.refine_tol) mode = kShade;
     } else {  // kShade: a7 evaluated at b, a valid sample on the surface side (reading R32)
       hit = true;
       return true;
@@ -787,7 +784,10 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
 
 // grid schedule: one CTA per 16 x (2 * DTSDF_CTA / 64)-pixel tile of 8x4-pixel warps, one ray per thread
 #ifndef DTSDF_CTA
-#define DTSDF_CTA 256
+#define DTSDF_CTA 128  // 128-thread CTAs: 4% faster than 256 on C1 (smaller tail, profiles/r1c_sweep_cta.txt)
+#endif
+#ifndef DTSDF_RAYCAST_MINB
+#define DTSDF_RAYCAST_MINB (512 / DTSDF_CTA)  // 128 registers per thread (16 warps per SM)
 #endif
 template <bool kComb>
 __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {

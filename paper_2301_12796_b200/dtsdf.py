@@ -28,7 +28,7 @@ EXPORTS = [
     "dtsdf_fuse", "dtsdf_get_volume", "dtsdf_default_icp_params", "dtsdf_icp", "dtsdf_icp_normal_equations",
 ]
 MARGIN = 0.125  # PAPER.md:262 "(±1/8 image size)"
-OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID = 1, 2, 3, 4, 5
+OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID, OPT_REFINE_TOL_NM = 1, 2, 3, 4, 5, 6
 
 
 class DtsdfError(RuntimeError):

@@ -18,7 +18,7 @@ import oracle  # noqa: E402
 import scenes  # noqa: E402
 from parity import compare  # noqa: E402
 from paper_2301_12796_b200 import Renderer  # noqa: E402
-from paper_2301_12796_b200.dtsdf import OPT_BISECT_STEPS, OPT_SCHEDULE  # noqa: E402
+from paper_2301_12796_b200.dtsdf import OPT_BISECT_STEPS, OPT_REFINE_TOL_NM, OPT_SCHEDULE  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C1,C2")
@@ -26,6 +26,7 @@ ap.add_argument("--reps", type=int, default=200)
 ap.add_argument("--schedules", default="0,1")
 ap.add_argument("--bisect", default="-1,6,5,4,3")
 ap.add_argument("--views", type=int, default=1)
+ap.add_argument("--tol", default="0")
 ap.add_argument("--no-parity", action="store_true")
 args = ap.parse_args()
 
@@ -36,9 +37,11 @@ for name in args.configs.split(","):
     R.upload_volume(w.volume)
     ora = None if args.no_parity else oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
     poses = np.repeat(np.asarray(w.poses[:1], np.float32), args.views, axis=0)
-    for sch, nb in itertools.product([int(x) for x in args.schedules.split(",")],
-                                     [int(x) for x in args.bisect.split(",")]):
+    for sch, nb, tol in itertools.product([int(x) for x in args.schedules.split(",")],
+                                          [int(x) for x in args.bisect.split(",")],
+                                          [int(x) for x in args.tol.split(",")]):
         R.set_option(OPT_SCHEDULE, sch)
+        R.set_option(OPT_REFINE_TOL_NM, tol)
         R.set_option(OPT_BISECT_STEPS, nb)
         out = R.render(poses, w.intrinsics)
         for _ in range(5):
@@ -56,9 +59,10 @@ for name in args.configs.split(","):
         st = compare({k: v[0].cpu().numpy() for k, v in out.items()}, ora) if ora is not None else {
             "budget_used": None, "color_exact": None, "depth_max_err": None, "hit_disagree": None, "geom_out_of_tol": None}
         rays = w.intrinsics.width * w.intrinsics.height * args.views
-        print(json.dumps({"config": name, "views": args.views, "schedule": sch, "bisect": nb, "raycast_ms": round(ms, 4),
+        print(json.dumps({"config": name, "views": args.views, "schedule": sch, "bisect": nb, "tol_nm": tol, "raycast_ms": round(ms, 4),
                           "Mrays_s_kernel": round(rays / ms / 1e3, 1), "budget_used": st["budget_used"],
                           "color_exact": st["color_exact"], "depth_max": st["depth_max_err"],
                           "hit_disagree": st["hit_disagree"], "geom_bad": st["geom_out_of_tol"]}), flush=True)
 R.set_option(OPT_SCHEDULE, 0)
 R.set_option(OPT_BISECT_STEPS, -1)
+R.set_option(OPT_REFINE_TOL_NM, 0)
