@@ -324,6 +324,17 @@ def run_dtsdf(args):
             "kernel": "k_raycast", "kernel_ms": ray_ms, "bytes_per_ray_alg": b_ray,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
             "range_pass_ms": kt["range_ms"] / max(kt["range_launches"], 1)}
+    # what actually bounds k_raycast: instruction issue.  Warp instructions per launch
+    # from the committed ncu capture of this config (a property of the workload), divided by this
+    # run's live kernel time, against 148 SMs x 4 schedulers x 1 instruction per clock.
+    ins = ncu.get(w.name, {}).get("raycast_warp_insts_per_launch") if args.mode == "direct" and args.views == 1 else None
+    if ins:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = (clk.get("sm_mhz") if isinstance(clk, dict) else None) or 1965.0
+        ach = ins / (ray_ms / 1e3) / 1e12
+        pk = sms * 4 * mhz * 1e6 / 1e12
+        roof["issue"] = {"achieved": ach, "peak": pk, "unit": "Tinst/s (warp instructions)", "frac": ach / pk,
+                         "insts_per_launch": ins, "source": ncu.get(w.name, {}).get("source")}
     if args.mode == "combined":
         roof["combine_ms_per_step"] = kt["combine_ms"] / args.steps
         roof["recombinations_per_step"] = combines / args.steps

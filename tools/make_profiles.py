@@ -61,8 +61,10 @@ def main():
             rd = float(s[rk[0]]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
         path = os.path.join(PROF, "ncu_summary.json")
         js = json.load(open(path)) if os.path.exists(path) else {}
+        ins = s.get("Executed Instructions [inst]")
         js[cfg] = {"raycast_dram_bytes_per_launch": (rd or 0) + (wr or 0), "source": f"profiles/{tag}_ncu_k_raycast.txt",
-                   "duration_us": float(s.get("Duration [us]", "nan"))}
+                   "duration_us": float(s.get("Duration [us]", "nan")),
+                   "raycast_warp_insts_per_launch": float(ins.replace(",", "")) if ins else None}
         json.dump(js, open(path, "w"), indent=1)
     lc = os.path.join(OUT, f"launches_{tag}.csv")
     if os.path.exists(lc):
