@@ -325,13 +325,15 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   for (int a = 0; a < 3; ++a) { c->lo[a] = lo[a]; c->dim[a] = hi[a] - lo[a] + 1; }
   const size_t cells = (size_t)c->dim[0] * c->dim[1] * c->dim[2];
   const size_t bm_words = (cells + 31) / 32;
+  // per-block buffers sized for the pool capacity, so a volume growing by fusion keeps them
+  const size_t nb = (size_t)std::max<long long>(std::max<long long>(n, c->cap), 1);
   if (ensure(c->table, c->cap_table, (size_t)cap * sizeof(HashEntry)) != cudaSuccess ||
-      ensure(c->locations, c->cap_locations, (size_t)std::max<long long>(n, 1) * sizeof(int4)) != cudaSuccess ||
+      ensure(c->locations, c->cap_locations, nb * sizeof(int4)) != cudaSuccess ||
       ensure(c->bitmap, c->cap_bitmap, (bm_words + 1) * 4) != cudaSuccess ||
       ensure(c->surface, c->cap_surface, (bm_words + 1) * 4) != cudaSuccess ||
       ensure(c->cell_pos, c->cap_cell_pos, (size_t)cap * 64) != cudaSuccess ||
-      ensure(c->apron, c->cap_apron, (size_t)n * kApronStride * sizeof(float2)) != cudaSuccess ||
-      ensure(c->rgb_apron, c->cap_rgb_apron, (size_t)n * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
+      ensure(c->apron, c->cap_apron, nb * kApronStride * sizeof(float2)) != cudaSuccess ||
+      ensure(c->rgb_apron, c->cap_rgb_apron, nb * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
   }
