@@ -231,7 +231,9 @@ DTSDF_API int dtsdf_depth_normals(dtsdf_ctx *ctx, const float *depth, const dtsd
 /* Allocate and fuse one frame: depth f32 [H][W] (camera z, 0 = missing; valid in [z_min, z_max]),
  * normal f32 [H][W][3] (camera frame, facing the camera, 0 = invalid), color u8 [H][W][3] or NULL,
  * pose world-from-camera (host), params NULL -> defaults.  Frames may be host or device memory.
- * Re-commits the volume (the combined TSDF is dropped).  *new_blocks (may be NULL) receives the
+ * Re-commits the volume; a combined TSDF is kept, stale, until the next dtsdf_combine (the paper's
+ * conditional recombination: blocks allocated since are invalid in it).  *new_blocks
+ * (may be NULL) receives the
  * number of blocks allocated.  Synchronous.  Errors: INVALID_ARGUMENT, NO_VOLUME (no
  * dtsdf_fusion_reserve), OUT_OF_MEMORY (capacity reached: the blocks allocated so far are kept and
  * initialised, the frame is not fused), CUDA. */

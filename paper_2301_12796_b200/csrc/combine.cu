@@ -550,6 +550,37 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
   if (tid == 0) p.surf[slot] = (unsigned char)any_neg;
 }
 
+// After a re-commit (e.g. a fused frame) the hash entries move: re-point the kept combined slots
+// (stale by design until the next recombination) at their locations' new entries.
+__global__ void k_comb_remap(const HashEntry *__restrict__ table, unsigned int mask, int4 *comb_loc, long long n,
+                             int *slot_of_entry) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 b = comb_loc[i];
+  const unsigned long long key = pack_key(b.x, b.y, b.z);
+  unsigned int h = hash_key(key) & mask;
+  for (unsigned int probe = 0; probe <= mask; ++probe) {
+    const unsigned long long k = table[h].key;
+    if (k == key) {
+      b.w = (int)h;
+      comb_loc[i] = b;
+      slot_of_entry[h] = (int)i;
+      return;
+    }
+    if (k == kEmptyKey) break;
+    h = (h + 1) & mask;
+  }
+  b.w = -1;  // the location left the volume: the slot is kept but unreachable
+  comb_loc[i] = b;
+}
+
+cudaError_t launch_comb_remap(const HashEntry *table, unsigned int mask, int4 *comb_loc, long long n,
+                              int *slot_of_entry, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_comb_remap<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(table, mask, comb_loc, n, slot_of_entry);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s) {
   if (p.n_loc == 0) return cudaSuccess;
   k_comb_select<<<(unsigned)((p.n_loc * 32 + 255) / 256), 256, 0, s>>>(p, p.surf);

@@ -196,6 +196,8 @@ cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, b
 // host launchers (combine.cu)
 cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s);                  // interiors + slots
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s);  // aprons, masks
+cudaError_t launch_comb_remap(const HashEntry *table, unsigned int mask, int4 *comb_loc, long long n,
+                              int *slot_of_entry, cudaStream_t s);
 
 // host launchers (volume.cu); all run on stream s and return the first launch error
 struct CommitScratch {

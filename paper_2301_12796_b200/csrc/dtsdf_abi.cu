@@ -298,7 +298,8 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   cudaSetDevice(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   c->committed = false;
-  free_combined(c);
+  // a combined TSDF survives a re-commit of the same volume (stale until recombined);
+  // its slots are re-pointed at the rebuilt hash entries below
   const long long n = c->n;
   // scratch: flags[4] | aabb[6] | pad[2] | n_loc (8 B aligned at int offset 12)
   CommitScratch sc;
@@ -393,6 +394,23 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   } else {
     dfree(c->loc_grid);  // AABB too large for the dense grid: the hash-probe path
     c->cap_loc_grid = 0;
+  }
+  if (c->combined) {
+    if (c->comb_entries != c->table_cap) {
+      dfree(c->comb_slot);
+      if (dalloc(c->comb_slot, (size_t)c->table_cap * 4) != cudaSuccess) {
+        cudaGetLastError();
+        free_combined(c);
+      } else {
+        c->comb_entries = c->table_cap;
+      }
+    }
+    if (c->combined) {
+      CK(c, cudaMemsetAsync(c->comb_slot, 0xFF, (size_t)c->table_cap * 4, s), "combined remap init");
+      begin_timed(c, 3, s, &tl, c->n_comb > 0 ? 1 : 0);
+      CK(c, launch_comb_remap(c->table, c->table_cap - 1, c->comb_loc, c->n_comb, c->comb_slot, s), "combined remap");
+      end_timed(c, s, &tl);
+    }
   }
   CK(c, cudaStreamSynchronize(s), "commit sync");
   c->committed = true;
