@@ -113,8 +113,10 @@ __global__ void __launch_bounds__(256) k_comb_select(const __grid_constant__ Com
 __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ CombineLaunch p,
                                                  const unsigned char *__restrict__ cls_in) {
   const VolumeView &V = p.vol;
-  const size_t slot = blockIdx.x;
-  const int l = blockIdx.y * 128 + threadIdx.x;
+  // the 4 CTAs of a slot are adjacent in launch order (x = quarter, y = slot): they share the
+  // slot's bricks in L2 while they run
+  const size_t slot = blockIdx.y;
+  const int l = blockIdx.x * 128 + threadIdx.x;
   const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
   const int4 b = p.comb_loc[slot];
   const int4 *e = reinterpret_cast<const int4 *>(&V.table[b.w]);
@@ -323,8 +325,8 @@ __device__ bool dir_normal(const CombineLaunch &p, int D, const double y[3], dou
 __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p,
                                                       const unsigned char *__restrict__ cls_in) {
   const VolumeView &V = p.vol;
-  const size_t slot = blockIdx.x;
-  const int l = blockIdx.y * 128 + threadIdx.x;
+  const size_t slot = blockIdx.y;
+  const int l = blockIdx.x * 128 + threadIdx.x;
   const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
   const int4 b = p.comb_loc[slot];
   const int4 *ent = reinterpret_cast<const int4 *>(&V.table[b.w]);
@@ -590,9 +592,9 @@ cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s) {
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
   if (p.mode == 1)
-    k_combine_alg1<<<dim3((unsigned)n_sel, 4), 128, 0, s>>>(p, p.surf);
+    k_combine_alg1<<<dim3(4, (unsigned)n_sel), 128, 0, s>>>(p, p.surf);
   else
-    k_combine<<<dim3((unsigned)n_sel, 4), 128, 0, s>>>(p, p.surf);
+    k_combine<<<dim3(4, (unsigned)n_sel), 128, 0, s>>>(p, p.surf);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_comb_finish<<<(unsigned)n_sel, kFinishThreads, 0, s>>>(p);
