@@ -303,6 +303,16 @@ def run_dtsdf(args):
         dist.barrier()
     launches = R.launch_count() - n_launch0
     combines = seq["combines"] - combines0
+    # the shards are checked against each other -- ranks that rendered the same poses
+    # (configs[1] has one) must produce bit-identical outputs; a 64-bit checksum per rank is gathered
+    out_sum = pdist.checksum({"keys": out["depth"], "sdf": out["normal"], "weight": out["color"], "rgb": out["mask"]})
+    if world > 1:
+        sums = [None] * world
+        dist.all_gather_object(sums, (out_sum, [int(i) for i in idx]))
+        same = [s for s, v in sums if v == [int(i) for i in idx]]
+        replicas_equal = len(set(same)) == 1
+    else:
+        replicas_equal = None
     clk = clocks.stop()
     R.set_profiling(False)
     kt = R.kernel_times()
@@ -391,6 +401,7 @@ def run_dtsdf(args):
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
         "extra": {"upload_and_index_ms": upload_ms, "broadcast_ms": bcast_ms, "n_locations": st["n_locations"],
+                  "output_checksum": out_sum, "ranks_with_same_views_bit_identical": replicas_equal,
                   "device_bytes": st["bytes"], "parity_sample_vs_oracle": parity,
                   "device": torch.cuda.get_device_name(dev)},
     }
