@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
   const int l = blockIdx.x * 128 + threadIdx.x;
   const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
   const int4 b = p.comb_loc[slot];
+  DTSDF_CHECK(b.w >= 0 && (long long)b.w < V.table_cap);
   const int4 *e = reinterpret_cast<const int4 *>(&V.table[b.w]);
   const int4 ea = __ldg(e), eb = __ldg(e + 1);
   const int sl[6] = {ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
@@ -278,6 +279,7 @@ __device__ bool dir_cell(const CombineLaunch &p, int D, const double y[3], const
   }
   const int slot = V.table[e].slot[D];
   if (slot < 0) return false;
+  DTSDF_CHECK(slot < V.n_blocks);
   const int lx = (int)(ci[0] - 8 * b0), ly = (int)(ci[1] - 8 * b1), lz = (int)(ci[2] - 8 * b2);
   *br = V.apron + (size_t)slot * kApronStride + lx + kApron * ly + kApron * kApron * lz;
   return true;
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
       int nbi, src;
       apron_src(a, &nbi, &src);
       const int ns = s_nb[nbi];
+      DTSDF_CHECK(ns < (int)gridDim.x && src >= 0 && src < kApronVox);
       if (ns >= 0) v[k] = __ldg(apin + (size_t)ns * kApronStride + src);
     }
   }

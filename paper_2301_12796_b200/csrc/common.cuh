@@ -6,6 +6,21 @@
 
 namespace dtsdf {
 
+// Bounds checks of the debug build (-DDTSDF_CHECKS, tools/build_checked.sh): every brick, mask and
+// output index is checked before it is used and a violation traps the kernel.  compute-sanitizer
+// is not available on the GPU pool, so this build plus the oracle comparisons is the memory-safety
+// gate.  Compiled out of the product build.
+#ifdef DTSDF_CHECKS
+#define DTSDF_CHECK(cond) \
+  do {                    \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define DTSDF_CHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
 constexpr int kBlock = 8;          // 8^3 voxel blocks
 constexpr int kVoxPerBlock = 512;
 constexpr int kApron = 11;         // apron brick: voxels -1..9 of the block per axis
@@ -60,11 +75,14 @@ struct VolumeView {
   float theta, inv_blend;      // 1 / (2 theta - pi/2)
   float cos_theta, sin_theta;  // membership band edges: w_dir = 0 below cos(theta), 1 above sin(theta)
   float delta, inv_delta;
+  long long n_blocks;          // bricks in the pool (bounds checks)
+  long long table_cap;         // hash entries (bounds checks)
 };
 
 // Device view of the view-dependent combined TSDF (NEXT-1, combine.cu): one combined brick per
 // selected block location, in the apron layout of the directional bricks.
 struct CombinedView {
+  long long n_slots;               // combined slots (bounds checks)
   const int *slot_of_entry;        // [table_cap] combined slot of a hash entry, -1 = not combined
   const float *apron;              // [cap][kApronStride] combined sdf of voxels -1..9, NaN = invalid
   const uchar4 *rgb;               // [cap][kRgbApronStride] u8 colour (xyz) + direction mask (w), voxels 0..8

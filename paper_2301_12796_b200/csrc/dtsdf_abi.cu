@@ -474,6 +474,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
   V.delta = c->params.step > 0.f ? c->params.step : c->params.voxel_size;
   V.inv_delta = 1.0f / V.delta;
+  V.n_blocks = c->n;
+  V.table_cap = c->table_cap;
   static thread_local RangeLaunch rl;
   static thread_local RenderLaunch pl;
   for (int v0 = 0; v0 < n_views; v0 += kViewsPerLaunch) {
@@ -520,6 +522,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.out_mask = mask ? mask + px : nullptr;
     pl.dbg_timeline = nullptr;
     pl.combined = comb ? 1 : 0;
+    pl.comb.n_slots = c->n_comb;
     pl.comb.slot_of_entry = c->comb_slot;
     pl.comb.apron = c->comb_apron;
     pl.comb.rgb = c->comb_rgb;
@@ -660,6 +663,8 @@ int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsic
   L.vol.cos_theta = cosf(c->params.theta);
   L.vol.sin_theta = sinf(c->params.theta);
   L.vol.inv_blend = (float)(1.0 / (2.0 * (double)c->params.theta - 3.14159265358979323846 / 2.0));
+  L.vol.n_blocks = c->n;
+  L.vol.table_cap = c->table_cap;
   L.locations = c->locations;
   L.n_loc = c->n_loc;
   for (int a = 0; a < 3; ++a) {

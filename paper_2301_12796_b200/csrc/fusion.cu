@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     if (!(fu >= 0.0 && fu <= (double)(p.width - 1) && fv >= 0.0 && fv <= (double)(p.height - 1))) continue;
     const int iu = (int)fu, iv = (int)fv;
     const size_t pi = (size_t)iv * p.width + iu;
+    DTSDF_CHECK(iu >= 0 && iu < p.width && iv >= 0 && iv < p.height);
     const float z = p.depth[pi];
     const float nc0 = p.normal[3 * pi], nc1 = p.normal[3 * pi + 1], nc2 = p.normal[3 * pi + 2];
     if (!depth_ok(p, z) || (nc0 == 0.f && nc1 == 0.f && nc2 == 0.f)) continue;

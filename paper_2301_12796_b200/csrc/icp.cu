@@ -40,6 +40,7 @@ __device__ __forceinline__ void icp_pixel(const IcpLaunch &p, const double *D, i
   if (!(fu >= 0.0 && fu <= (double)(p.width - 1) && fv >= 0.0 && fv <= (double)(p.height - 1))) return;
   const int iu = (int)fu, iv = (int)fv;
   const size_t j = (size_t)iv * p.width + iu;
+  DTSDF_CHECK(iu >= 0 && iu < p.width && iv >= 0 && iv < p.height);
   const float zr = p.ref_depth[j];
   const float nw0 = p.ref_normal[3 * j], nw1 = p.ref_normal[3 * j + 1], nw2 = p.ref_normal[3 * j + 2];
   if (!icp_z_ok(p, zr) || (nw0 == 0.f && nw1 == 0.f && nw2 == 0.f)) return;

@@ -169,6 +169,7 @@ struct Cursor {
 
 // cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (k_cell_pos)
 __device__ __forceinline__ bool cell_positive(const unsigned int *cell_pos, const Cursor &cur, int l) {
+  DTSDF_CHECK(cur.entry >= 0 && l >= 0 && l < 512);
   return (__ldg(&cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;
 }
 
@@ -203,6 +204,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     const int D = __ffs(present) - 1;
     present &= present - 1;
     const int slot = pick6(cur.slots, D);
+    DTSDF_CHECK(slot >= 0 && slot < V.n_blocks && lx >= 0 && lx < 8 && ly >= 0 && ly < 8 && lz >= 0 && lz < 8);
     const float2 *br = V.apron + (size_t)slot * kApronStride + off;
     // all 32 stencil voxels are issued before any test (one load round per direction; the
     // apron brick always holds them, NaN marking unallocated neighbours)
@@ -316,6 +318,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
 // trilinear u8 colour and the OR of the direction masks of the corners with weight >= 1/8.
 __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const CombinedView &C, int slot, int lx, int ly,
                                                   int lz, float fx, float fy, float fz, bool shade, ShadeResult *sh) {
+  DTSDF_CHECK(slot >= 0 && slot < C.n_slots && lx >= 0 && lx < 8 && ly >= 0 && ly < 8 && lz >= 0 && lz < 8);
   const float *br = C.apron + (size_t)slot * kApronStride + (lx + kApron * ly + kApron * kApron * lz);
   const float c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
   const float c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
@@ -493,6 +496,7 @@ struct RayT {
           gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + y) * V.dim_x + x]);
         else
           gv = -0x7fffffff;
+        DTSDF_CHECK(gv < 0 || (long long)(gv & 0x3fffffff) < V.table_cap);
         cur.occ = gv >= 0;
         cur.dist = gv == -0x7fffffff ? 0 : (gv < 0 ? -gv : 0);
         cur.surf = (gv >> 30) & 1;
@@ -500,6 +504,8 @@ struct RayT {
           cur.entry = gv & 0x3fffffff;
           const int4 *e = reinterpret_cast<const int4 *>(&V.table[cur.entry]);
           const int4 ea = __ldg(e), eb = __ldg(e + 1);
+          DTSDF_CHECK(ea.z < V.n_blocks && ea.w < V.n_blocks && eb.x < V.n_blocks && eb.y < V.n_blocks &&
+                      eb.z < V.n_blocks && eb.w < V.n_blocks);
           cur.slots[0] = ea.z; cur.slots[1] = ea.w; cur.slots[2] = eb.x;
           cur.slots[3] = eb.y; cur.slots[4] = eb.z; cur.slots[5] = eb.w;
         }
@@ -514,7 +520,9 @@ struct RayT {
       }
       if constexpr (kComb) {  // NEXT-1: the location's combined brick (entry -> combined slot)
         if (cur.occ) {
+          DTSDF_CHECK(cur.entry >= 0 && cur.entry < V.table_cap);
           const int cs = __ldg(&C.slot_of_entry[cur.entry]);
+          DTSDF_CHECK(cs < C.n_slots);
           if (cs >= 0) {
             cur.entry = cs;
             cur.surf = __ldg(&C.surf[cs]) != 0;
@@ -760,6 +768,7 @@ struct RayT {
     mask = min(st_cpi, 255) | 0;  // jumps: st_jump (not stored)
 #endif
     const size_t pix = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
+    DTSDF_CHECK(view < p.n_views && vrel >= 0 && vrel < p.row1 - p.row0 && u >= 0 && u < p.width);
     p.out_depth[pix] = depth;
     if (p.out_normal) {
       p.out_normal[3 * pix + 0] = nrm[0];
