@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--mode", choices=["direct", "combined"], default="direct",
                     help="direct: per-sample combination (the north-star path); combined: the paper's "
                          "view-dependent combined TSDF (NEXT-1), recombined per eqs. 10-13 inside the timed loop")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU code path (NCCL process group, volume broadcast into library buffers, "
+                         "checksum all-gather, max over ranks) even at world size 1")
     ap.add_argument("--combine-mode", type=int, default=0, choices=[0, 1],
                     help="combined mode: 0 eq:combine_weight (the paper's method), 1 Algorithm 1 (NEXT-4)")
     return ap.parse_args()
@@ -207,7 +210,12 @@ def run_dtsdf(args):
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
     w = workload(args.config) if rank == 0 else None
     R = Renderer(local)
@@ -215,7 +223,7 @@ def run_dtsdf(args):
 
     # ---- replicate the volume: rank 0 fills its buffers, NCCL broadcast into the others' ----
     t_up = time.perf_counter()
-    if world > 1:
+    if use_dist:
         meta = None
         if rank == 0:
             v = w.volume
@@ -287,7 +295,7 @@ def run_dtsdf(args):
     R.set_profiling(True)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     n_launch0 = R.launch_count()
@@ -299,14 +307,14 @@ def run_dtsdf(args):
         step(out["depth"], out["normal"], out["color"], out["mask"])
         ends[i].record(stream)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     launches = R.launch_count() - n_launch0
     combines = seq["combines"] - combines0
     # the shards are checked against each other -- ranks that rendered the same poses
     # (configs[1] has one) must produce bit-identical outputs; a 64-bit checksum per rank is gathered
     out_sum = pdist.checksum({"keys": out["depth"], "sdf": out["normal"], "weight": out["color"], "rgb": out["mask"]})
-    if world > 1:
+    if use_dist:
         sums = [None] * world
         dist.all_gather_object(sums, (out_sum, [int(i) for i in idx]))
         same = [s for s, v in sums if v == [int(i) for i in idx]]
@@ -317,7 +325,7 @@ def run_dtsdf(args):
     R.set_profiling(False)
     kt = R.kernel_times()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    max_ms = pdist.max_over_ranks(dist, total_ms, dev) if world > 1 else total_ms
+    max_ms = pdist.max_over_ranks(dist, total_ms, dev) if use_dist else total_ms
     value = world * rays_per_step * args.steps / (max_ms / 1e3) / 1e6
 
     # ---- roofline of the dominant kernel (raycast) ----
@@ -361,7 +369,7 @@ def run_dtsdf(args):
     for _ in range(3):
         step(hd, hn, hc, hm)
     e2e_tot = 0.0
-    if world > 1:
+    if use_dist:
         dist.barrier()
     for _ in range(e2e_steps):
         if not args.no_flush:
@@ -370,15 +378,15 @@ def run_dtsdf(args):
         t0 = time.perf_counter()
         step(hd, hn, hc, hm)  # synchronizes (host outputs)
         e2e_tot += time.perf_counter() - t0
-    e2e_max = pdist.max_over_ranks(dist, e2e_tot, dev) if world > 1 else e2e_tot
+    e2e_max = pdist.max_over_ranks(dist, e2e_tot, dev) if use_dist else e2e_tot
     e2e = {"value": world * rays_per_step * e2e_steps / e2e_max / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(pose_host.numel() * 4 + 32),
            "d2h_bytes_per_step": int(hd.numel() * 4 + hn.numel() * 4 + hc.numel() + hm.numel()),
            "timing": "host wall clock per dtsdf_render_batch call with host outputs (D2H inside)"}
 
     if rank != 0:
-        dist.barrier() if world > 1 else None
-        dist.destroy_process_group() if world > 1 else None
+        dist.barrier() if use_dist else None
+        dist.destroy_process_group() if use_dist else None
         return 0
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) + a sampled parity check of this run ----
@@ -406,7 +414,7 @@ def run_dtsdf(args):
                   "device": torch.cuda.get_device_name(dev)},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
