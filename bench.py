@@ -366,23 +366,33 @@ def run_dtsdf(args):
     hm = torch.empty((V, H, W), dtype=torch.uint8).pin_memory()
     pose_host = torch.from_numpy(np.ascontiguousarray(poses)).pin_memory()
     e2e_steps = min(args.e2e_steps, args.steps)
-    for _ in range(3):
-        step(hd, hn, hc, hm)
-    e2e_tot = 0.0
-    if use_dist:
-        dist.barrier()
-    for _ in range(e2e_steps):
-        if not args.no_flush:
-            flush.fill_(1.0)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        step(hd, hn, hc, hm)  # synchronizes (host outputs)
-        e2e_tot += time.perf_counter() - t0
-    e2e_max = pdist.max_over_ranks(dist, e2e_tot, dev) if use_dist else e2e_tot
+
+    def e2e_run():
+        for _ in range(3):
+            step(hd, hn, hc, hm)
+        tot = 0.0
+        if use_dist:
+            dist.barrier()
+        for _ in range(e2e_steps):
+            if not args.no_flush:
+                flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            step(hd, hn, hc, hm)  # synchronizes (host outputs)
+            tot += time.perf_counter() - t0
+        return pdist.max_over_ranks(dist, tot, dev) if use_dist else tot
+
+    from paper_2301_12796_b200.dtsdf import OPT_HOST_WRITE
+    R.set_option(OPT_HOST_WRITE, 0)  # context: render into device scratch, then copy engine D2H
+    e2e_copy = e2e_run()
+    R.set_option(OPT_HOST_WRITE, 1)  # default: the kernel writes the pinned outputs directly
+    e2e_max = e2e_run()
     e2e = {"value": world * rays_per_step * e2e_steps / e2e_max / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(pose_host.numel() * 4 + 32),
            "d2h_bytes_per_step": int(hd.numel() * 4 + hn.numel() * 4 + hc.numel() + hm.numel()),
-           "timing": "host wall clock per dtsdf_render_batch call with host outputs (D2H inside)"}
+           "timing": "host wall clock per dtsdf_render_batch call into pinned host outputs, written by the "
+                     "raycast across the host link (DTSDF_OPT_HOST_WRITE)",
+           "copy_path_value": world * rays_per_step * e2e_steps / e2e_copy / 1e6}
 
     if rank != 0:
         dist.barrier() if use_dist else None

@@ -124,7 +124,8 @@ DTSDF_API int dtsdf_upload_volume(dtsdf_ctx *ctx, const dtsdf_volume_params *par
  *   out_color   u8  [H][W][3]   RGB, 0 = miss                      (may be NULL)
  *   out_dirmask u8  [H][W]      bit D set iff W_D > 0 at the hit    (may be NULL)
  * If all non-NULL outputs are device pointers the call is asynchronous on cuda_stream; if they
- * are host pointers the library renders into its own scratch, copies back and synchronizes. */
+ * are host pointers the call synchronizes: page-locked (pinned) host outputs are written by the
+ * kernel directly (DTSDF_OPT_HOST_WRITE), pageable ones via device scratch and a copy back. */
 DTSDF_API int dtsdf_render(dtsdf_ctx *ctx, const float pose_w_c[16], const dtsdf_intrinsics *intr, float *out_depth,
                  float *out_normal, uint8_t *out_color, uint8_t *out_dirmask, void *cuda_stream);
 
@@ -317,6 +318,13 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
 /*   DTSDF_OPT_REFINE_TOL_NM  0 (default) regula falsi stops when f(b) is within 1e-7 of the root or after
  *                            12 steps; n > 0 also stops it once the bracket is narrower than n nanometres */
 #define DTSDF_OPT_REFINE_TOL_NM 6
+/*   DTSDF_OPT_HOST_WRITE  1 (default) when every non-NULL output of a render call is page-locked host
+ *                         memory mapped into the device address space (cudaHostAlloc / cudaMallocHost /
+ *                         torch pin_memory() under unified addressing) the raycast kernel writes the
+ *                         outputs there directly, in whole 16-byte-aligned tile rows, overlapping the
+ *                         host-link transfer with the ray march; 0 renders into device scratch and
+ *                         copies back after the kernel.  Pageable host outputs always take the copy path. */
+#define DTSDF_OPT_HOST_WRITE 7
 DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
 
 /* Kernel launches issued by this context since creation (all kinds). */

@@ -114,6 +114,8 @@ struct RenderLaunch {
   unsigned char *out_color;        // [n_views][rows][W][3] or null
   unsigned char *out_mask;         // [n_views][rows][W] or null
   unsigned long long *dbg_timeline;  // DTSDF_STATS builds only: per-pixel start/end/smid
+  int staged;                      // grid schedule: outputs leave via shared memory in whole tile rows
+                                   // (mapped host outputs); 0: per-pixel stores
   int combined;                    // 1: march the combined TSDF (comb) instead of the six directions
   CombinedView comb;
   ViewPose pose[kViewsPerLaunch];

@@ -76,6 +76,7 @@ struct dtsdf_ctx {
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
   int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1, refine_tol_nm = 0;
+  int host_write = 1;          // DTSDF_OPT_HOST_WRITE: the raycast writes mapped pinned host outputs directly
   int *tile_counter = nullptr;
   // view-dependent combined TSDF (NEXT-1, combine.cu)
   bool combined = false;
@@ -440,7 +441,7 @@ int dtsdf_upload_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, const int32_
 
 static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
                        int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, cudaStream_t s,
-                       bool comb) {
+                       bool comb, bool staged = false) {
   const int W = K->width;
   const int rows = row1 - row0;
   const int tiles_x = (W + kRangeTile - 1) / kRangeTile, tiles_y = (rows + kRangeTile - 1) / kRangeTile;
@@ -521,6 +522,10 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.out_color = color ? color + 3 * px : nullptr;
     pl.out_mask = mask ? mask + px : nullptr;
     pl.dbg_timeline = nullptr;
+#ifdef DTSDF_ALWAYS_STAGED
+    staged = true;
+#endif
+    pl.staged = staged ? 1 : 0;
     pl.combined = comb ? 1 : 0;
     pl.comb.n_slots = c->n_comb;
     pl.comb.slot_of_entry = c->comb_slot;
@@ -572,7 +577,33 @@ static int render_batch_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, 
       (mask && is_device_ptr(mask) != dev))
     return fail(DTSDF_ERR_INVALID_ARGUMENT, "outputs must be all device or all host pointers");
   if (dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s, comb);
-  // host outputs: render into device scratch, copy back, synchronize
+  // host outputs in page-locked memory (mapped into the device address space under UVA, e.g.
+  // torch pin_memory()): the raycast writes its staged output rows straight into them across the
+  // host link while it runs, then the call synchronizes -- no staging copy after the kernel
+  if (c->host_write) {
+    void *dptr[4] = {depth, normal, color, mask};
+    bool mapped = true;
+    for (int i = 0; i < 4 && mapped; ++i) {
+      if (!dptr[i]) continue;
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, dptr[i]) != cudaSuccess) {
+        cudaGetLastError();
+        mapped = false;
+      } else if (a.type != cudaMemoryTypeHost || !a.devicePointer) {
+        mapped = false;
+      } else {
+        dptr[i] = a.devicePointer;
+      }
+    }
+    if (mapped) {
+      rc = render_impl(c, n_views, poses, K, row0, row1, (float *)dptr[0], (float *)dptr[1], (uint8_t *)dptr[2],
+                       (uint8_t *)dptr[3], s, comb, /*staged=*/true);
+      if (rc) return rc;
+      CK(c, cudaStreamSynchronize(s), "render sync");
+      return DTSDF_OK;
+    }
+  }
+  // pageable host outputs: render into device scratch, copy back, synchronize
   const size_t px = (size_t)n_views * (row1 - row0) * K->width;
   const size_t need = px * (4 + 12 + 3 + 1) + 64;
   if (need > c->host_stage_cap) {
@@ -1161,6 +1192,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_LOCATION_GRID) c->use_grid = value ? 1 : 0;
   else if (option == DTSDF_OPT_BISECT_STEPS && value >= -1 && value <= 30) c->bisect_steps = value;
   else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;
+  else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

@@ -130,7 +130,27 @@ __device__ __forceinline__ int lookup_slots(const VolumeView &V, int bx, int by,
 struct SampleResult {
   bool valid;
   float f;
+  bool unk;  // lazy evaluation: invalid or positive, not resolved (every direction holding data
+             // has phi_D > 0, so F > 0 whenever S > 0); valid = false
 };
+
+// Lazy evaluation (measured dead end; off): where only the sign class of F matters
+// -- march samples and bisection midpoints -- the gradients (24 of the 32 stencil voxels and most
+// of the arithmetic) can be skipped when every direction holding data at x has phi_D > 0: F is then
+// positive or invalid, and both count as "not <= 0" for the crossing test and for the bisection
+// (R21).  A march sample left unresolved is evaluated in full only if the next one ends a crossing
+// (mode kResolve).  Exact, but slower on B200 (profiles/r1f_sweep_lazy.jsonl): the second pass over
+// the corners costs more than the skipped gradients save, and skipping certainly-positive points
+// unevaluated lengthens the divergent advance loop of every step.
+#ifndef DTSDF_LAZY
+#define DTSDF_LAZY 0         // gradient-free sign class for march samples
+#endif
+#ifndef DTSDF_LAZY_BISECT
+#define DTSDF_LAZY_BISECT 0  // ... and for bisection midpoints (fa unknown -> regula falsi starts with a midpoint)
+#endif
+#ifndef DTSDF_LAZY_SKIP
+#define DTSDF_LAZY_SKIP 0    // certainly-positive points are skipped unevaluated (resolved on demand)
+#endif
 
 struct ShadeResult {
   float n[3];
@@ -189,7 +209,38 @@ __device__ __forceinline__ int pick6(const int s[6], int d) {
 // body is compiled (runtime direction loop) to keep the kernel inside the instruction cache.
 __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const Cursor &cur, int lx, int ly, int lz,
                                                  float fx, float fy, float fz, float rx, float ry, float rz,
-                                                 bool shade, ShadeResult *sh) {
+                                                 bool shade, ShadeResult *sh, bool lazy) {
+  SampleResult res;
+  res.unk = false;
+  const int off = lx + kApron * ly + kApron * kApron * lz;
+#if DTSDF_LAZY
+  if (lazy) {  // sign class from the 8 cell corners of each direction
+    bool any = false, full = false;
+    int pr = cur.present;
+#pragma unroll 1
+    while (pr) {
+      const int D = __ffs(pr) - 1;
+      pr &= pr - 1;
+      const float2 *br = V.apron + (size_t)pick6(cur.slots, D) * kApronStride + off;
+      const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
+      const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
+      const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
+      const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
+      const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
+      const float2 pw = lerp2(lerp2(lerp2(c000, c100, fx2), lerp2(c010, c110, fx2), fy2),
+                              lerp2(lerp2(c001, c101, fx2), lerp2(c011, c111, fx2), fy2), fz2);
+      if (isnan(pw.x) || !(pw.y > 0.0f)) continue;  // no data from D (as in the full evaluation)
+      any = true;
+      if (!(pw.x > 0.0f)) { full = true; break; }
+    }
+    if (!full) {
+      res.valid = false;
+      res.f = 0.0f;
+      res.unk = any;  // no data at all: invalid for certain
+      return res;
+    }
+  }
+#endif
   float S1 = 0.f, F1 = 0.f, S2 = 0.f, F2 = 0.f;
   bool any_grad = false;
   float N1x = 0.f, N1y = 0.f, N1z = 0.f, N2x = 0.f, N2y = 0.f, N2z = 0.f;
@@ -197,7 +248,6 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   int m1 = 0, m2 = 0;
   const float half_inv_s = 0.5f * V.inv_voxel;
   const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
-  const int off = lx + kApron * ly + kApron * kApron * lz;
   int present = cur.present;
 #pragma unroll 1
   while (present) {
@@ -300,7 +350,6 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   // O3(d)/(e): eq:combine_weight if any direction holding data has a gradient, else the fallback
   const float S = any_grad ? S1 : S2;
   const float F = any_grad ? F1 : F2;
-  SampleResult res;
   res.valid = S > 0.0f;
   res.f = res.valid ? F / S : 0.0f;
   if (shade) {
@@ -331,6 +380,7 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
   SampleResult res;
   res.valid = !isnan(phi);
   res.f = res.valid ? phi : 0.0f;
+  res.unk = false;
   if (shade && res.valid) {
     const float xm00 = __ldg(br + APRON_IDX(-1, 0, 0)), xm10 = __ldg(br + APRON_IDX(-1, 1, 0));
     const float xm01 = __ldg(br + APRON_IDX(-1, 0, 1)), xm11 = __ldg(br + APRON_IDX(-1, 1, 1));
@@ -397,7 +447,7 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
 // a4-a7: the raycast kernel, one state machine per ray so that a warp's rays -- marching,
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
-enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
+enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3, kResolve = 4 };
 constexpr int kLookahead = 8;  // lattice points tested per certainly-positive scan
 
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
@@ -417,7 +467,7 @@ struct RayT {
   float g0x, g0y, g0z, rsx, rsy, rsz;
   Cursor cur;
   int mode, it, side;
-  bool prev_valid, fa_valid, hit;
+  bool prev_valid, prev_unk, fa_valid, hit;
   float prev_f, a, b, t, fa, fb;
   ShadeResult sh;
   int ix, iy, iz;
@@ -466,6 +516,7 @@ struct RayT {
     for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
     mode = kMarch;
     prev_valid = false;
+    prev_unk = false;
     prev_f = 0.f;
     a = b = 0.f;
     t = (float)k * V.delta;
@@ -552,6 +603,39 @@ struct RayT {
   }
   __device__ __forceinline__ float block_exit(const VolumeView &V) const { return box_exit(V, 0); }
 
+  // a6: bracket [t_{k-1}, t_k] with F(t_{k-1}) = f_prev > 0 and F(t_k) = f_k <= 0
+  __device__ __forceinline__ void begin_bracket(const RenderLaunch &p, float f_prev, float f_k) {
+    const VolumeView &V = p.vol;
+    // re-anchor the position frame at x(t_{k-1}) in fp64
+    {
+      const ViewPose &P = p.pose[view];
+      const double ddx = ((double)u - (double)p.cx) / (double)p.fx;
+      const double ddy = ((double)(p.row0 + vrel) - (double)p.cy) / (double)p.fy;
+      const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0), inv_s = 1.0 / (double)V.voxel_size;
+      const double t0 = (double)(k - 1) * (double)V.delta;
+      double rq[3], gq[3];
+      for (int q = 0; q < 3; ++q) {
+        rq[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
+        gq[q] = fma(t0, rq[q], (double)P.t[q]) * inv_s;
+      }
+      const double fx0 = floor(gq[0]), fy0 = floor(gq[1]), fz0 = floor(gq[2]);
+      ibx = (int)fx0; iby = (int)fy0; ibz = (int)fz0;
+      g0x = (float)(gq[0] - fx0); g0y = (float)(gq[1] - fy0); g0z = (float)(gq[2] - fz0);
+      rsx = (float)(rq[0] * inv_s); rsy = (float)(rq[1] * inv_s); rsz = (float)(rq[2] * inv_s);
+    }
+    // Phase 1: bisection with the oracle's decisions (an invalid midpoint counts as positive,
+    // R21) until the bracket is <= 5e-5 m, so it keeps the oracle's root when F has several
+    // sign changes (reading R20).  Phase 2: Illinois regula falsi inside it.
+    a = 0.f;
+    b = V.delta;
+    fa = f_prev;
+    fb = f_k;
+    fa_valid = true;
+    it = 0;
+    side = 0;
+    mode = p.n_bisect > 0 ? kBisect : kIllinois;
+  }
+
   // Advance (march only), evaluate one sample, update the state.  Returns true when the ray is
   // finished (hit shaded, or no crossing in range).
   __device__ __forceinline__ bool step(const RenderLaunch &p) {
@@ -573,6 +657,7 @@ struct RayT {
 #endif
         if (!cur.occ) {
           prev_valid = false;
+          prev_unk = false;
 #ifdef DTSDF_STATS
           ++st_empty;
 #endif
@@ -617,6 +702,13 @@ struct RayT {
 #endif
             k = (kj > (float)k1) ? k1 + 1 : (int)kj;
             prev_valid = false;
+            prev_unk = false;
+#if DTSDF_LAZY_SKIP
+            // every point of the location is positive or invalid: leave the jump's landing point
+            // unresolved as well and move past it
+            prev_unk = true;
+            ++k;
+#endif
             continue;
           }
         }
@@ -634,11 +726,22 @@ struct RayT {
             run |= (unsigned)ok << j;
           }
           const int n = __ffs(~run) - 1;  // leading certainly-positive points (>= 1)
+#if DTSDF_LAZY_SKIP
+          // all n points are positive or invalid: none is evaluated; the last one stays unresolved
+#ifdef DTSDF_STATS
+          st_cpi += n;
+#endif
+          prev_valid = false;
+          prev_unk = true;
+          k += n;
+          continue;
+#endif
           if (n >= 2) {
 #ifdef DTSDF_STATS
             st_cpi += n - 1;
 #endif
             prev_valid = false;
+            prev_unk = false;
             k += n - 1;
             if (n == kLookahead) continue;  // the run may go on: scan again from its last point
             t = (float)k * V.delta;
@@ -660,10 +763,12 @@ struct RayT {
       if constexpr (kComb)
         s = eval_comb(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, mode == kShade, &sh);
       else
-        s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh);
+        s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh,
+                        mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect));
     } else {
       s.valid = false;
       s.f = 0.f;
+      s.unk = false;
     }
 #ifdef DTSDF_STATS
     {
@@ -671,41 +776,37 @@ struct RayT {
       if (mode == kMarch) cy_march += c2 - c1; else cy_refine += c2 - c1;
     }
 #endif
-    if (mode == kMarch) {
-      if (!(s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f)) {
-        prev_valid = s.valid;
-        prev_f = s.f;
-        ++k;
-        return false;
-      }
-      // a6: bracket [t_{k-1}, t_k]: re-anchor the position frame at x(t_{k-1}) in fp64
-      {
-        const ViewPose &P = p.pose[view];
-        const double ddx = ((double)u - (double)p.cx) / (double)p.fx;
-        const double ddy = ((double)(p.row0 + vrel) - (double)p.cy) / (double)p.fy;
-        const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0), inv_s = 1.0 / (double)V.voxel_size;
-        const double t0 = (double)(k - 1) * (double)V.delta;
-        double rq[3], gq[3];
-        for (int q = 0; q < 3; ++q) {
-          rq[q] = ((double)P.r[3 * q] * ddx + (double)P.r[3 * q + 1] * ddy + (double)P.r[3 * q + 2]) * iLd;
-          gq[q] = fma(t0, rq[q], (double)P.t[q]) * inv_s;
+    if (mode == kMarch || mode == kResolve) {
+      float f_prev, f_k;
+      if (mode == kMarch) {
+        if (!(s.valid && s.f <= 0.0f && (prev_unk || (prev_valid && prev_f > 0.0f)))) {
+          prev_valid = s.valid;
+          prev_unk = s.unk;
+          prev_f = s.f;
+          ++k;
+          return false;
         }
-        const double fx0 = floor(gq[0]), fy0 = floor(gq[1]), fz0 = floor(gq[2]);
-        ibx = (int)fx0; iby = (int)fy0; ibz = (int)fz0;
-        g0x = (float)(gq[0] - fx0); g0y = (float)(gq[1] - fy0); g0z = (float)(gq[2] - fz0);
-        rsx = (float)(rq[0] * inv_s); rsy = (float)(rq[1] * inv_s); rsz = (float)(rq[2] * inv_s);
+        if (prev_unk) {  // sample k ends a crossing iff the unresolved t_{k-1} is valid: evaluate it
+          mode = kResolve;
+          fb = s.f;
+          t = (float)(k - 1) * V.delta;
+          return false;
+        }
+        f_prev = prev_f;
+        f_k = s.f;
+      } else {
+        if (!(s.valid && s.f > 0.0f)) {  // no crossing ends at k; sample k (valid, <= 0) becomes prev
+          prev_valid = true;
+          prev_unk = false;
+          prev_f = fb;
+          mode = kMarch;
+          ++k;
+          return false;
+        }
+        f_prev = s.f;
+        f_k = fb;
       }
-      // Phase 1: bisection with the oracle's decisions (an invalid midpoint counts as positive,
-      // R21) until the bracket is <= 5e-5 m, so it keeps the oracle's root when F has several
-      // sign changes (reading R20).  Phase 2: Illinois regula falsi inside it.
-      a = 0.f;
-      b = V.delta;
-      fa = prev_f;
-      fb = s.f;
-      fa_valid = true;
-      it = 0;
-      side = 0;
-      mode = p.n_bisect > 0 ? kBisect : kIllinois;
+      begin_bracket(p, f_prev, f_k);
     } else if (mode == kBisect) {
       if (!s.valid || s.f > 0.0f) { a = t; fa = s.f; fa_valid = s.valid; }
       else { b = t; fb = s.f; }
@@ -740,9 +841,12 @@ struct RayT {
     return false;
   }
 
-  __device__ __forceinline__ void store(const RenderLaunch &p) const {
-    float depth = 0.f, nrm[3] = {0.f, 0.f, 0.f};
-    int col[3] = {0, 0, 0}, mask = 0;
+  // a7 outputs of this ray (zeros for a miss)
+  __device__ __forceinline__ void result(const RenderLaunch &p, float &depth, float nrm[3], int col[3], int &mask) const {
+    depth = 0.f;
+    nrm[0] = nrm[1] = nrm[2] = 0.f;
+    col[0] = col[1] = col[2] = 0;
+    mask = 0;
     if (hit) {
       depth = ((float)(k - 1) * p.vol.delta + b) * iLf;
       const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
@@ -767,6 +871,13 @@ struct RayT {
     col[0] = min(st_march, 255); col[1] = min(st_refine, 255); col[2] = min(st_empty, 255);
     mask = min(st_cpi, 255) | 0;  // jumps: st_jump (not stored)
 #endif
+  }
+
+  // per-pixel scalar stores (persistent schedule)
+  __device__ __forceinline__ void store(const RenderLaunch &p) const {
+    float depth, nrm[3];
+    int col[3], mask;
+    result(p, depth, nrm, col, mask);
     const size_t pix = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
     DTSDF_CHECK(view < p.n_views && vrel >= 0 && vrel < p.row1 - p.row0 && u >= 0 && u < p.width);
     p.out_depth[pix] = depth;
@@ -798,34 +909,98 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
 #ifndef DTSDF_RAYCAST_MINB
 #define DTSDF_RAYCAST_MINB (512 / DTSDF_CTA)  // 128 registers per thread (16 warps per SM)
 #endif
+// Copy `n` bytes of one staged output row from shared memory to global (device or mapped pinned
+// host) memory with the lanes [l0, l0 + nl) of a warp: 16-byte stores when both ends are aligned,
+// else bytes.  Whole rows of the CTA tile leave as contiguous full-width writes, which is what a
+// PCIe write to a mapped host buffer needs (strided 4-byte stores would split into 4-byte TLPs).
+__device__ __forceinline__ void copy_row(unsigned char *dst, const unsigned char *src, int n, int l, int nl) {
+  if (((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)n) & 15) == 0) {
+    for (int i = l; i < (n >> 4); i += nl)
+      reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+  } else {
+    for (int i = l; i < n; i += nl) dst[i] = src[i];
+  }
+}
+
+constexpr int kTileW = 16, kTileH = DTSDF_CTA / 16;  // CTA pixel tile
+
 template <bool kComb>
 __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
+  // a7 outputs of the CTA's tile, laid out row by row as in the output arrays (16-B aligned rows)
+  __shared__ __align__(16) float s_depth[kTileH][kTileW];
+  __shared__ __align__(16) float s_normal[kTileH][3 * kTileW];
+  __shared__ __align__(16) unsigned char s_color[kTileH][3 * kTileW];
+  __shared__ __align__(16) unsigned char s_mask[kTileH][kTileW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 16 + (warp & 1) * 8 + (lane & 7);
-  const int vrel = blockIdx.y * (DTSDF_CTA / 16) + (warp >> 1) * 4 + (lane >> 3);
-  if (u >= p.width || p.row0 + vrel >= p.row1) return;
-  RayT<kComb> ray;
+  const int tx = (warp & 1) * 8 + (lane & 7), ty = (warp >> 1) * 4 + (lane >> 3);
+  const int u0 = blockIdx.x * kTileW, v0 = blockIdx.y * kTileH;
+  const int u = u0 + tx, vrel = v0 + ty;
+  const int rows = p.row1 - p.row0;
+  if (u < p.width && vrel < rows) {
+    RayT<kComb> ray;
 #ifdef DTSDF_STATS
-  unsigned long long g_start;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+    unsigned long long g_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 #endif
-  ray.init(p, blockIdx.z, u, vrel);
+    ray.init(p, blockIdx.z, u, vrel);
 #ifdef DTSDF_STATS
-  const long long c0 = clock64();
+    const long long c0 = clock64();
 #endif
-  while (!ray.step(p)) {
+    while (!ray.step(p)) {
+    }
+#ifdef DTSDF_STATS
+    ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations
+    unsigned long long g_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    ray.g_start = g_start;
+    ray.g_end = g_end;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    ray.smid = smid;
+#endif
+    if (!p.staged) {  // device outputs: per-pixel stores straight from the ray
+      ray.store(p);
+      return;
+    }
+    float depth, nrm[3];
+    int col[3], mask;
+    ray.result(p, depth, nrm, col, mask);
+    s_depth[ty][tx] = depth;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      s_normal[ty][3 * tx + q] = nrm[q];
+      s_color[ty][3 * tx + q] = (unsigned char)col[q];
+    }
+    s_mask[ty][tx] = (unsigned char)mask;
   }
-#ifdef DTSDF_STATS
-  ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations
-  unsigned long long g_end;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-  ray.g_start = g_start;
-  ray.g_end = g_end;
-  unsigned smid;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-  ray.smid = smid;
-#endif
-  ray.store(p);
+  if (!p.staged) return;  // uniform per launch
+  __syncthreads();
+  // each warp writes kTileH / 4 rows: lanes 0-3 depth, 4-15 normal, 16-18 colour, 19 mask when the
+  // row is full width and aligned; otherwise each array of the row with all 32 lanes, bytewise
+  const int nu = min(kTileW, p.width - u0);
+  for (int row = warp; row < kTileH; row += DTSDF_CTA / 32) {
+    if (v0 + row >= rows) break;
+    const size_t pix = ((size_t)blockIdx.z * rows + v0 + row) * p.width + u0;
+    DTSDF_CHECK(blockIdx.z < p.n_views && nu > 0);
+    unsigned char *d0 = reinterpret_cast<unsigned char *>(p.out_depth + pix);
+    unsigned char *d1 = p.out_normal ? reinterpret_cast<unsigned char *>(p.out_normal + 3 * pix) : nullptr;
+    unsigned char *d2 = p.out_color ? p.out_color + 3 * pix : nullptr;
+    unsigned char *d3 = p.out_mask ? p.out_mask + pix : nullptr;
+    const bool fast = nu == kTileW &&
+                      ((reinterpret_cast<uintptr_t>(d0) | reinterpret_cast<uintptr_t>(d1) |
+                        reinterpret_cast<uintptr_t>(d2) | reinterpret_cast<uintptr_t>(d3)) & 15) == 0;
+    if (fast) {
+      if (lane < 4) copy_row(d0, reinterpret_cast<const unsigned char *>(s_depth[row]), 64, lane, 4);
+      else if (lane < 16) { if (d1) copy_row(d1, reinterpret_cast<const unsigned char *>(s_normal[row]), 192, lane - 4, 12); }
+      else if (lane < 19) { if (d2) copy_row(d2, s_color[row], 48, lane - 16, 3); }
+      else if (lane == 19) { if (d3) copy_row(d3, s_mask[row], 16, 0, 1); }
+    } else {
+      copy_row(d0, reinterpret_cast<const unsigned char *>(s_depth[row]), 4 * nu, lane, 32);
+      if (d1) copy_row(d1, reinterpret_cast<const unsigned char *>(s_normal[row]), 12 * nu, lane, 32);
+      if (d2) copy_row(d2, s_color[row], 3 * nu, lane, 32);
+      if (d3) copy_row(d3, s_mask[row], nu, lane, 32);
+    }
+  }
 }
 
 // persistent schedule: resident warps pull 8x4-pixel warp tiles (view-major, row-major) from an

@@ -175,17 +175,28 @@ def test_schedules_give_identical_bits(R, c1):
 
 
 def test_host_outputs_equal_device_outputs(R, c1):
+    """Pinned host outputs written by the kernel (DTSDF_OPT_HOST_WRITE), pinned via the copy path,
+    and pageable host outputs all equal the device render bit for bit -- full frame, and a ragged
+    width / row range / multi-view batch whose tile rows are neither full nor 16-B aligned."""
+    from paper_2301_12796_b200.dtsdf import OPT_HOST_WRITE
     R.upload_volume(c1.volume)
-    K = c1.intrinsics
-    g = R.render(c1.poses, K)
-    H, W = K.height, K.width
-    hd = torch.zeros((1, H, W), dtype=torch.float32).pin_memory()
-    hn = torch.zeros((1, H, W, 3), dtype=torch.float32).pin_memory()
-    hc = torch.zeros((1, H, W, 3), dtype=torch.uint8).pin_memory()
-    hm = torch.zeros((1, H, W), dtype=torch.uint8).pin_memory()
-    R.render_into(c1.poses, K, hd, hn, hc, hm)
-    for k, h in (("depth", hd), ("normal", hn), ("color", hc), ("mask", hm)):
-        assert torch.equal(g[k].cpu(), h), k
+    K1 = c1.intrinsics
+    Kr = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=321, height=243)
+    w3 = scenes.c3_batch(n_views=3, room=c1)
+    for poses, K, r0, r1 in ((c1.poses, K1, 0, K1.height), (w3.poses, Kr, 5, 240)):
+        g = R.render(poses, K, row0=r0, row1=r1)
+        V, H, W = len(poses), r1 - r0, K.width
+        for pinned, host_write in ((True, 1), (True, 0), (False, 1)):
+            R.set_option(OPT_HOST_WRITE, host_write)
+            mk = (lambda t: t.pin_memory()) if pinned else (lambda t: t)
+            hd = mk(torch.full((V, H, W), 7.0, dtype=torch.float32))
+            hn = mk(torch.full((V, H, W, 3), 7.0, dtype=torch.float32))
+            hc = mk(torch.full((V, H, W, 3), 7, dtype=torch.uint8))
+            hm = mk(torch.full((V, H, W), 7, dtype=torch.uint8))
+            R.render_into(poses, K, hd, hn, hc, hm, row0=r0, row1=r1)
+            for k, h in (("depth", hd), ("normal", hn), ("color", hc), ("mask", hm)):
+                assert torch.equal(g[k].cpu(), h), (k, W, pinned, host_write)
+    R.set_option(OPT_HOST_WRITE, 1)
 
 
 def test_alloc_fill_commit_equals_upload(R, c0):
