@@ -148,13 +148,24 @@ def oracle_sample_rate(w, n_pix, seed=0, threads=None):
 
 
 def cpu_baseline(w, seconds):
+    """The oracle as it stands on all host cores: a seeded pixel subset sized for `seconds` of CPU
+    work; when one whole frame takes less, the frame is traced again (same pixels, same result)
+    until `seconds` have passed, so the rate is measured over ~10-30 s as the contract asks."""
+    import oracle
     threads = os.cpu_count() or 1
     n0, dt0, _, _ = oracle_sample_rate(w, 2048, seed=1, threads=threads)
     n = int(min(w.intrinsics.width * w.intrinsics.height, max(2048, n0 * seconds / max(dt0, 1e-3))))
     n, dt, px, out = oracle_sample_rate(w, n, seed=2, threads=threads)
-    return {"value": n / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+    passes, tot = 1, dt
+    ov = oracle.OracleVolume(w.volume)
+    while tot < seconds and passes < 64:
+        t0 = time.perf_counter()
+        ov.render(w.poses[0], w.intrinsics, pixels=px, threads=threads)
+        tot += time.perf_counter() - t0
+        passes += 1
+    return {"value": n * passes / tot / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{n} of {w.intrinsics.width * w.intrinsics.height} pixel rays of the {w.name} view "
-                      f"(seeded uniform subset), fp64 brute-force march, {dt:.1f} s"}, px, out
+                      f"(seeded uniform subset) x {passes} pass(es), fp64 brute-force march, {tot:.1f} s"}, px, out
 
 
 def run_reference(args):

@@ -207,9 +207,10 @@ __device__ __forceinline__ int pick6(const int s[6], int d) {
 // F(x, r) of DESIGN.md §2 O3 for the sample at base voxel (block-local l, fractions f) of the
 // current cursor location; with shade = true also the shading sums of O7.  One instance of this
 // body is compiled (runtime direction loop) to keep the kernel inside the instruction cache.
+template <bool shade>
 __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const Cursor &cur, int lx, int ly, int lz,
                                                  float fx, float fy, float fz, float rx, float ry, float rz,
-                                                 bool shade, ShadeResult *sh, bool lazy) {
+                                                 ShadeResult *sh, bool lazy) {
   SampleResult res;
   res.unk = false;
   const int off = lx + kApron * ly + kApron * kApron * lz;
@@ -324,7 +325,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
       S1 += W1;
       F1 = fmaf(W1, phi, F1);
     }
-    if (shade) {
+    if constexpr (shade) {
       const uchar4 *cb = V.rgb_apron + (size_t)slot * kRgbApronStride + (lx + kRgbApron * ly + kRgbApron * kRgbApron * lz);
       const uchar4 q000 = cb[RGB_IDX(0, 0, 0)], q100 = cb[RGB_IDX(1, 0, 0)], q010 = cb[RGB_IDX(0, 1, 0)],
                    q110 = cb[RGB_IDX(1, 1, 0)], q001 = cb[RGB_IDX(0, 0, 1)], q101 = cb[RGB_IDX(1, 0, 1)],
@@ -352,7 +353,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   const float F = any_grad ? F1 : F2;
   res.valid = S > 0.0f;
   res.f = res.valid ? F / S : 0.0f;
-  if (shade) {
+  if constexpr (shade) {
     sh->S = S;
     sh->mask = any_grad ? m1 : m2;
     sh->n[0] = any_grad ? N1x : N2x; sh->n[1] = any_grad ? N1y : N2y; sh->n[2] = any_grad ? N1z : N2z;
@@ -365,8 +366,9 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
 // over the 8 cell corners, invalid if any corner is (NaN); with shade = true the normal (central
 // differences of the trilinear field at +-s, else the cell's own trilinear gradient), the
 // trilinear u8 colour and the OR of the direction masks of the corners with weight >= 1/8.
+template <bool shade>
 __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const CombinedView &C, int slot, int lx, int ly,
-                                                  int lz, float fx, float fy, float fz, bool shade, ShadeResult *sh) {
+                                                  int lz, float fx, float fy, float fz, ShadeResult *sh) {
   DTSDF_CHECK(slot >= 0 && slot < C.n_slots && lx >= 0 && lx < 8 && ly >= 0 && ly < 8 && lz >= 0 && lz < 8);
   const float *br = C.apron + (size_t)slot * kApronStride + (lx + kApron * ly + kApron * kApron * lz);
   const float c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
@@ -381,7 +383,7 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
   res.valid = !isnan(phi);
   res.f = res.valid ? phi : 0.0f;
   res.unk = false;
-  if (shade && res.valid) {
+  if (shade && res.valid) {  // (compile-time shade)
     const float xm00 = __ldg(br + APRON_IDX(-1, 0, 0)), xm10 = __ldg(br + APRON_IDX(-1, 1, 0));
     const float xm01 = __ldg(br + APRON_IDX(-1, 0, 1)), xm11 = __ldg(br + APRON_IDX(-1, 1, 1));
     const float xp00 = __ldg(br + APRON_IDX(2, 0, 0)), xp10 = __ldg(br + APRON_IDX(2, 1, 0));
@@ -761,10 +763,10 @@ struct RayT {
 #endif
     if (cur.occ) {
       if constexpr (kComb)
-        s = eval_comb(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, mode == kShade, &sh);
+        s = eval_comb<false>(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, nullptr);
       else
-        s = eval_sample(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], mode == kShade, &sh,
-                        mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect));
+        s = eval_sample<false>(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], nullptr,
+                               mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect));
     } else {
       s.valid = false;
       s.f = 0.f;
@@ -823,9 +825,6 @@ struct RayT {
         if (s.f > -1e-7f) mode = kShade;  // b sits on the root
       }
       if (++it >= 12 || b - a < p.refine_tol) mode = kShade;
-    } else {  // kShade: a7 evaluated at b, a valid sample on the surface side (reading R32)
-      hit = true;
-      return true;
     }
     // next position (offset from t_{k-1})
     if (mode == kBisect) {
@@ -834,11 +833,31 @@ struct RayT {
       float m = (fa_valid && fa > fb) ? fmaf(fa / (fa - fb), b - a, a) : 0.5f * (a + b);
       if (!(m > a && m < b)) m = 0.5f * (a + b);
       if (!(m > a && m < b)) mode = kShade;  // bracket at the fp32 resolution of the offset
-      t = (mode == kShade) ? b : m;
-    } else {
-      t = b;  // kShade
+      t = m;
+    }
+    if (mode == kShade) {  // the hit is b, a valid sample on the surface side (reading R32); a7 runs
+                           // after the loop (shade()), with the warp's hit lanes together
+      t = b;
+      hit = true;
+      return true;
     }
     return false;
+  }
+
+  // a7 at the hit t = b (refinement frame): the evaluation of the last step again, with the
+  // shading sums
+  __device__ __forceinline__ void shade(const RenderLaunch &p) {
+    locate(p.vol, p.comb, t);
+    sh.n[0] = sh.n[1] = sh.n[2] = 0.f;
+    sh.c[0] = sh.c[1] = sh.c[2] = 0.f;
+    sh.S = 0.f;
+    sh.mask = 0;
+    if (cur.occ) {
+      if constexpr (kComb)
+        eval_comb<true>(p.vol, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, &sh);
+      else
+        eval_sample<true>(p.vol, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], &sh, false);
+    }
   }
 
   // a7 outputs of this ray (zeros for a miss)
@@ -948,6 +967,7 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
 #endif
     while (!ray.step(p)) {
     }
+    if (ray.hit) ray.shade(p);
 #ifdef DTSDF_STATS
     ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations
     unsigned long long g_end;
@@ -1023,6 +1043,7 @@ __global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_cons
       ray.init(p, view, u, vrel);
       while (!ray.step(p)) {
       }
+      if (ray.hit) ray.shade(p);
       ray.store(p);
     }
   }

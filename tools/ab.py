@@ -1,4 +1,4 @@
-"""A/B timing of compile-time k_raycast variants on the GPU box.
+"""A/B timing of compile-time k_raycast variants on the GPU box (name:@lib.so times a prebuilt library).
 
     python tools/ab.py --variant base: --variant staged:-DDTSDF_ALWAYS_STAGED [--configs C1,C2] [--rounds 2]
 
@@ -72,6 +72,9 @@ def main():
     libs = []
     for v in args.variant or ["base:"]:
         name, _, defs = v.partition(":")
+        if defs.startswith("@"):  # a prebuilt library (e.g. an earlier build kept under gpurun_out/)
+            libs.append((name, os.path.abspath(defs[1:])))
+            continue
         lib = os.path.join(ROOT, "gpurun_out", f"ab_{name}.so")
         cus = sorted(os.path.join(B.CSRC, f) for f in os.listdir(B.CSRC) if f.endswith(".cu"))
         cmd = [B.NVCC, *B.NVCC_FLAGS, *defs.split(), *cus, "-o", lib]
