@@ -67,6 +67,9 @@ struct VolumeView {
                                // else -d with d >= 1 its empty-space distance in blocks
   const unsigned int *cell_pos;  // [table_cap][16]: bit l of location entry h = base cell l is
                                  // "certainly positive": every present direction's 8 corners > 0
+  const unsigned char *cell_dirs;  // [table_cap][512] or null: bit D of byte l of entry h = direction D
+                                   // can hold data at base cell l (present, no NaN corner, a corner
+                                   // weight > 0); the evaluation visits only these directions
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
   int dim_x, dim_y, dim_z;     // AABB extent (blocks)
   const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}
@@ -235,7 +238,7 @@ cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsign
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
 cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
-                            unsigned int *cell_pos, cudaStream_t s);
+                            unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s);
 cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,

@@ -57,6 +57,8 @@ struct dtsdf_ctx {
   HashEntry *table = nullptr;
   unsigned int table_cap = 0;
   unsigned int *bitmap = nullptr, *surface = nullptr, *cell_pos = nullptr;
+  unsigned char *cell_dirs = nullptr;  // [table cap][512] live directions per base cell
+  size_t cap_cell_dirs = 0;
   int *loc_grid = nullptr;
   int lo[3] = {0, 0, 0}, dim[3] = {0, 0, 0};
   int4 *locations = nullptr;
@@ -140,13 +142,14 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->bitmap);
   dfree(c->surface);
   dfree(c->cell_pos);
+  dfree(c->cell_dirs);
   dfree(c->loc_grid);
   dfree(c->locations);
   dfree(c->apron);
   dfree(c->rgb_apron);
   dfree(c->dist_tmp);
   c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_apron =
-      c->cap_rgb_apron = c->cap_loc_grid = c->cap_dist = 0;
+      c->cap_rgb_apron = c->cap_loc_grid = c->cap_dist = c->cap_cell_dirs = 0;
   c->allocated = c->committed = false;
   c->n = c->n_loc = c->cap = 0;
   c->index_bytes = 0;
@@ -334,12 +337,13 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
       ensure(c->bitmap, c->cap_bitmap, (bm_words + 1) * 4) != cudaSuccess ||
       ensure(c->surface, c->cap_surface, (bm_words + 1) * 4) != cudaSuccess ||
       ensure(c->cell_pos, c->cap_cell_pos, (size_t)cap * 64) != cudaSuccess ||
+      ensure(c->cell_dirs, c->cap_cell_dirs, (size_t)cap * 512) != cudaSuccess ||
       ensure(c->apron, c->cap_apron, nb * kApronStride * sizeof(float2)) != cudaSuccess ||
       ensure(c->rgb_apron, c->cap_rgb_apron, nb * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
   }
-  c->index_bytes = (size_t)cap * (sizeof(HashEntry) + 64) + (size_t)n * sizeof(int4) + 2 * bm_words * 4 +
+  c->index_bytes = (size_t)cap * (sizeof(HashEntry) + 64 + 512) + (size_t)n * sizeof(int4) + 2 * bm_words * 4 +
                    (size_t)n * kApronStride * sizeof(float2) + (size_t)n * kRgbApronStride * sizeof(uchar4);
   CK(c, cudaMemsetAsync(c->table, 0xFF, (size_t)cap * sizeof(HashEntry), s), "table init");
   CK(c, cudaMemsetAsync(c->bitmap, 0, (bm_words + 1) * 4, s), "bitmap init");
@@ -363,7 +367,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
      "apron");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
-  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->apron, c->cell_pos, s), "cell_pos");
+  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->apron, c->cell_pos, c->cell_dirs, s), "cell_pos");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
   CK(c, launch_surface(c->locations, c->n_loc, c->cell_pos, c->surface, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s),
@@ -462,6 +466,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.bitmap = c->bitmap;
   V.surface = c->surface;
   V.cell_pos = c->cell_pos;
+  V.cell_dirs = c->cell_dirs;
   V.loc_grid = c->use_grid ? c->loc_grid : nullptr;
   V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
   V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];

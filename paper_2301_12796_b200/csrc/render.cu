@@ -142,6 +142,9 @@ struct SampleResult {
 // (mode kResolve).  Exact, but slower on B200 (profiles/r1f_sweep_lazy.jsonl): the second pass over
 // the corners costs more than the skipped gradients save, and skipping certainly-positive points
 // unevaluated lengthens the divergent advance loop of every step.
+#ifndef DTSDF_CELL_DIRS
+#define DTSDF_CELL_DIRS 1    // visit only the directions live at the sample's base cell (k_cell_pos)
+#endif
 #ifndef DTSDF_LAZY
 #define DTSDF_LAZY 0         // gradient-free sign class for march samples
 #endif
@@ -249,7 +252,11 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   int m1 = 0, m2 = 0;
   const float half_inv_s = 0.5f * V.inv_voxel;
   const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
-  int present = cur.present;
+  // the directions that can hold data at this base cell (a subset of the location's, exact)
+  DTSDF_CHECK(!V.cell_dirs || cur.entry >= 0);
+  int present = DTSDF_CELL_DIRS && V.cell_dirs
+                    ? (int)__ldg(&V.cell_dirs[(size_t)cur.entry * 512 + lx + 8 * ly + 64 * lz])
+                    : cur.present;
 #pragma unroll 1
   while (present) {
     const int D = __ffs(present) - 1;

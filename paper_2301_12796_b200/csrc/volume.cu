@@ -140,11 +140,12 @@ __global__ void k_rgb_apron(const int4 *__restrict__ keys, long long n, const Ha
 // when the next lattice point is such a sample too -- start one (render.cu, exact).
 // One warp per 32 consecutive cells of a location; the ballot writes one mask word.
 __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const HashEntry *__restrict__ table,
-                           const float2 *__restrict__ apron, unsigned int *cell_pos) {
+                           const float2 *__restrict__ apron, unsigned int *cell_pos, unsigned char *cell_dirs) {
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long u = gid >> 9;
   int l = (int)(gid & 511);
   bool pos = false;
+  int live = 0;
   if (u < n_loc) {
     const int h = loc[u].w;
     const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
@@ -153,17 +154,22 @@ __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const 
       const int slot = table[h].slot[D];
       if (slot < 0) continue;
       const float2 *br = apron + (size_t)slot * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1);
-      bool absent = false, allpos = true;
+      bool absent = false, allpos = true, weighted = false;
       for (int q = 0; q < 8; ++q) {
-        const float v = br[(q & 1) + kApron * ((q >> 1) & 1) + kApron * kApron * (q >> 2)].x;
-        absent |= isnan(v);
-        allpos &= v > 0.0f;
+        const float2 v = br[(q & 1) + kApron * ((q >> 1) & 1) + kApron * kApron * (q >> 2)];
+        absent |= isnan(v.x);
+        allpos &= v.x > 0.0f;
+        weighted |= v.y > 0.0f;
       }
       if (!absent && !allpos) pos = false;
+      // a NaN corner makes the trilinear phi NaN, corner weights all <= 0 make omega <= 0: either
+      // way the evaluation drops D here (O3(a), reading R8), so it need not visit it
+      if (!absent && weighted) live |= 1 << D;
     }
   }
   const unsigned int word = __ballot_sync(0xffffffffu, pos);
   if (u < n_loc && (l & 31) == 0) cell_pos[(size_t)loc[u].w * 16 + (l >> 5)] = word;
+  if (u < n_loc && cell_dirs) cell_dirs[(size_t)loc[u].w * 512 + l] = (unsigned char)live;
 }
 
 // Dense location grid: for each allocated location, its hash entry index and surface bit, so
@@ -269,9 +275,9 @@ cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char 
 }
 
 cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
-                            unsigned int *cell_pos, cudaStream_t s) {
+                            unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s) {
   if (n_loc == 0) return cudaSuccess;
-  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, apron, cell_pos);
+  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, apron, cell_pos, cell_dirs);
   return cudaGetLastError();
 }
 

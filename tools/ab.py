@@ -39,7 +39,8 @@ def run_one(args):
         R.reset_kernel_times()
         R.set_profiling(True)
         for _ in range(args.reps):
-            flush.fill_(1.0)
+            if not args.no_flush:
+                flush.fill_(1.0)
             R.render_into(poses, w.intrinsics, out["depth"], out["normal"], out["color"], out["mask"])
         torch.cuda.synchronize()
         R.set_profiling(False)
@@ -49,7 +50,8 @@ def run_one(args):
         if not args.no_parity:
             ora = oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
             st = compare({k: v[0].cpu().numpy() for k, v in out.items()}, ora)
-        print(json.dumps({"variant": args.name, "config": name, "raycast_ms": round(ms, 4),
+        print(json.dumps({"variant": args.name, "config": name, "l2": "warm" if args.no_flush else "flushed",
+                          "raycast_ms": round(ms, 4),
                           "budget_used": st.get("budget_used"), "color_exact": st.get("color_exact"),
                           "depth_max": st.get("depth_max_err"), "hit_disagree": st.get("hit_disagree"),
                           "geom_bad": st.get("geom_out_of_tol")}), flush=True)
@@ -62,6 +64,7 @@ def main():
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between launches (an upper bound)")
     ap.add_argument("--run", action="store_true")
     ap.add_argument("--name", default="")
     args = ap.parse_args()
@@ -88,7 +91,8 @@ def main():
         for name, lib in libs:
             env = dict(os.environ, DTSDF_LIB=lib)
             cmd = [sys.executable, os.path.abspath(__file__), "--run", "--name", name, "--configs", args.configs,
-                   "--reps", str(args.reps)] + (["--no-parity"] if args.no_parity or r > 0 else [])
+                   "--reps", str(args.reps)] + (["--no-parity"] if args.no_parity or r > 0 else []) + \
+                  (["--no-flush"] if args.no_flush else [])
             subprocess.run(cmd, env=env, check=True)
 
 
