@@ -67,9 +67,10 @@ struct VolumeView {
                                // else -d with d >= 1 its empty-space distance in blocks
   const unsigned int *cell_pos;  // [table_cap][16]: bit l of location entry h = base cell l is
                                  // "certainly positive": every present direction's 8 corners > 0
-  const unsigned char *cell_dirs;  // [table_cap][512] or null: bit D of byte l of entry h = direction D
+  const unsigned char *cell_dirs;  // [table_cap][512]: bit D (0-5) of byte l of entry h = direction D
                                    // can hold data at base cell l (present, no NaN corner, a corner
-                                   // weight > 0); the evaluation visits only these directions
+                                   // weight > 0), the directions the evaluation visits; bit 7 = the
+                                   // cell is certainly positive (as cell_pos)
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
   int dim_x, dim_y, dim_z;     // AABB extent (blocks)
   const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}

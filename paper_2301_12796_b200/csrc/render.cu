@@ -196,6 +196,13 @@ __device__ __forceinline__ bool cell_positive(const unsigned int *cell_pos, cons
   return (__ldg(&cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;
 }
 
+// byte l of the cursor's location in the live-direction masks (bits 0-5 live directions, bit 7
+// certainly positive)
+__device__ __forceinline__ int cell_byte(const VolumeView &V, const Cursor &cur, int l) {
+  DTSDF_CHECK(cur.entry >= 0 && l >= 0 && l < 512);
+  return __ldg(&V.cell_dirs[(size_t)cur.entry * 512 + l]);
+}
+
 __device__ __forceinline__ int pick6(const int s[6], int d) {
   // register-resident select (a dynamic index would spill the array to local memory)
   int v = s[0];
@@ -213,7 +220,7 @@ __device__ __forceinline__ int pick6(const int s[6], int d) {
 template <bool shade>
 __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const Cursor &cur, int lx, int ly, int lz,
                                                  float fx, float fy, float fz, float rx, float ry, float rz,
-                                                 ShadeResult *sh, bool lazy) {
+                                                 ShadeResult *sh, bool lazy, int live = -1) {
   SampleResult res;
   res.unk = false;
   const int off = lx + kApron * ly + kApron * kApron * lz;
@@ -254,9 +261,10 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
   // the directions that can hold data at this base cell (a subset of the location's, exact)
   DTSDF_CHECK(!V.cell_dirs || cur.entry >= 0);
-  int present = DTSDF_CELL_DIRS && V.cell_dirs
-                    ? (int)__ldg(&V.cell_dirs[(size_t)cur.entry * 512 + lx + 8 * ly + 64 * lz])
-                    : cur.present;
+  // (live >= 0: the advance loop already read this cell's byte)
+  int present = live >= 0 ? live
+                : DTSDF_CELL_DIRS && V.cell_dirs ? (cell_byte(V, cur, lx + 8 * ly + 64 * lz) & 63)
+                                                 : cur.present;
 #pragma unroll 1
   while (present) {
     const int D = __ffs(present) - 1;
@@ -652,12 +660,14 @@ struct RayT {
 #ifdef DTSDF_STATS
     const long long c0 = clock64();
 #endif
+    int live = -1;  // live-direction byte of the point to evaluate, if the advance loop read it
     if (mode == kMarch) {
       // a4: advance to the next lattice point that needs an evaluation.  Every step skipped here
       // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
       // location without an sdf <= 0 corner, and in a certainly-positive cell followed by
       // another, no crossing can end or start.
       for (;;) {
+        live = -1;
         if (k > k1) return true;  // no crossing: a miss
         t = (float)k * V.delta;
         locate(V, p.comb, t);
@@ -721,7 +731,19 @@ struct RayT {
             continue;
           }
         }
-        if (p.use_skip && cell_positive(kComb ? p.comb.cell_pos : V.cell_pos, cur, (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7))) {
+        bool cp = false;
+        if (p.use_skip) {
+          const int l0 = (ix & 7) + 8 * (iy & 7) + 64 * (iz & 7);
+          if constexpr (kComb) {
+            cp = cell_positive(p.comb.cell_pos, cur, l0);
+          } else {
+            const int cb = cell_byte(V, cur, l0);
+            cp = (cb & 128) != 0;
+            live = DTSDF_CELL_DIRS ? (cb & 63) : -1;  // handed to the evaluation of this point
+          }
+        }
+        if (cp) {
+          live = -1;
           // look ahead over the next lattice points of this location at once (independent
           // loads): in a run of certainly-positive points only the last one needs evaluating
           unsigned run = 1u;
@@ -730,8 +752,10 @@ struct RayT {
             const float tj = (float)(k + j) * V.delta;
             const int jx = ibx + (int)floorf(fmaf(tj, rsx, g0x)), jy = iby + (int)floorf(fmaf(tj, rsy, g0y)),
                       jz = ibz + (int)floorf(fmaf(tj, rsz, g0z));
-            const bool ok = (jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz &&
-                            cell_positive(kComb ? p.comb.cell_pos : V.cell_pos, cur, (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7));
+            const int lj = (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7);
+            bool ok = (jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz;
+            if constexpr (kComb) ok = ok && cell_positive(p.comb.cell_pos, cur, lj);
+            else ok = ok && (cell_byte(V, cur, lj) & 128);
             run |= (unsigned)ok << j;
           }
           const int n = __ffs(~run) - 1;  // leading certainly-positive points (>= 1)
@@ -773,7 +797,7 @@ struct RayT {
         s = eval_comb<false>(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, nullptr);
       else
         s = eval_sample<false>(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], nullptr,
-                               mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect));
+                               mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect), live);
     } else {
       s.valid = false;
       s.f = 0.f;

@@ -169,7 +169,7 @@ __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const 
   }
   const unsigned int word = __ballot_sync(0xffffffffu, pos);
   if (u < n_loc && (l & 31) == 0) cell_pos[(size_t)loc[u].w * 16 + (l >> 5)] = word;
-  if (u < n_loc && cell_dirs) cell_dirs[(size_t)loc[u].w * 512 + l] = (unsigned char)live;
+  if (u < n_loc && cell_dirs) cell_dirs[(size_t)loc[u].w * 512 + l] = (unsigned char)(live | (pos ? 128 : 0));
 }
 
 // Dense location grid: for each allocated location, its hash entry index and surface bit, so
