@@ -303,6 +303,10 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *   DTSDF_OPT_BLOCK_SKIP  1 (default) jump over unallocated block locations; 0 step every point */
 #define DTSDF_OPT_RANGE_PASS 1
 #define DTSDF_OPT_BLOCK_SKIP 2
+/*   DTSDF_OPT_CELL_DIRS   1 (default) a sample visits only the directions that can hold data at its base
+ *                         cell (present, no NaN corner, a corner weight > 0; built at commit); 0 visits
+ *                         every direction present at the block location */
+#define DTSDF_OPT_CELL_DIRS 8
 /* Tuning (results unchanged):
  *   DTSDF_OPT_SCHEDULE    0 (default) one CTA per 16x16-pixel tile; 1 persistent warps pulling
  *                         8x4-pixel tiles from an atomic counter

@@ -71,6 +71,7 @@ struct VolumeView {
                                    // can hold data at base cell l (present, no NaN corner, a corner
                                    // weight > 0), the directions the evaluation visits; bit 7 = the
                                    // cell is certainly positive (as cell_pos)
+  int use_live;                    // 1: visit only the live directions of a cell (DTSDF_OPT_CELL_DIRS)
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
   int dim_x, dim_y, dim_z;     // AABB extent (blocks)
   const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}

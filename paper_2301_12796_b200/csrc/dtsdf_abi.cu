@@ -78,7 +78,8 @@ struct dtsdf_ctx {
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
   int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1, refine_tol_nm = 0;
-  int host_write = 1;          // DTSDF_OPT_HOST_WRITE: the raycast writes mapped pinned host outputs directly
+  int host_write = 1;
+  int use_live = 1;            // DTSDF_OPT_CELL_DIRS          // DTSDF_OPT_HOST_WRITE: the raycast writes mapped pinned host outputs directly
   int *tile_counter = nullptr;
   // view-dependent combined TSDF (NEXT-1, combine.cu)
   bool combined = false;
@@ -467,6 +468,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.surface = c->surface;
   V.cell_pos = c->cell_pos;
   V.cell_dirs = c->cell_dirs;
+  V.use_live = c->use_live;
   V.loc_grid = c->use_grid ? c->loc_grid : nullptr;
   V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
   V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];
@@ -1198,6 +1200,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_BISECT_STEPS && value >= -1 && value <= 30) c->bisect_steps = value;
   else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;
   else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
+  else if (option == DTSDF_OPT_CELL_DIRS) c->use_live = value ? 1 : 0;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

@@ -142,9 +142,6 @@ struct SampleResult {
 // (mode kResolve).  Exact, but slower on B200 (profiles/r1f_sweep_lazy.jsonl): the second pass over
 // the corners costs more than the skipped gradients save, and skipping certainly-positive points
 // unevaluated lengthens the divergent advance loop of every step.
-#ifndef DTSDF_CELL_DIRS
-#define DTSDF_CELL_DIRS 1    // visit only the directions live at the sample's base cell (k_cell_pos)
-#endif
 #ifndef DTSDF_LAZY
 #define DTSDF_LAZY 0         // gradient-free sign class for march samples
 #endif
@@ -262,9 +259,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   // the directions that can hold data at this base cell (a subset of the location's, exact)
   DTSDF_CHECK(!V.cell_dirs || cur.entry >= 0);
   // (live >= 0: the advance loop already read this cell's byte)
-  int present = live >= 0 ? live
-                : DTSDF_CELL_DIRS && V.cell_dirs ? (cell_byte(V, cur, lx + 8 * ly + 64 * lz) & 63)
-                                                 : cur.present;
+  int present = !V.use_live ? cur.present : live >= 0 ? live : (cell_byte(V, cur, lx + 8 * ly + 64 * lz) & 63);
 #pragma unroll 1
   while (present) {
     const int D = __ffs(present) - 1;
@@ -739,7 +734,7 @@ struct RayT {
           } else {
             const int cb = cell_byte(V, cur, l0);
             cp = (cb & 128) != 0;
-            live = DTSDF_CELL_DIRS ? (cb & 63) : -1;  // handed to the evaluation of this point
+            live = cb & 63;  // handed to the evaluation of this point
           }
         }
         if (cp) {

@@ -130,20 +130,25 @@ def test_row_shards_concatenate_bitexact(R, c1):
         assert torch.equal(full[k], torch.cat([a[k], b[k]], 1)), k
 
 
-def test_accelerations_are_result_invisible(R, c1):
-    """Range pass and block skipping are exact (DESIGN.md §2 O2): switching them off changes no bit."""
-    from paper_2301_12796_b200.dtsdf import OPT_BLOCK_SKIP, OPT_RANGE_PASS
-    R.upload_volume(c1.volume)
+def test_accelerations_are_result_invisible(R, c1, c2):
+    """Range pass, block skipping and the live-direction cell masks are exact (DESIGN.md §2 O2,
+    §5): switching them off changes no bit (C1 room and the C2 thin plates, where opposing
+    directions share block locations)."""
+    from paper_2301_12796_b200.dtsdf import OPT_BLOCK_SKIP, OPT_CELL_DIRS, OPT_RANGE_PASS
     K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=320, height=240)
-    ref = R.render(c1.poses, K)
-    for rng_on, skip_on in ((0, 1), (1, 0), (0, 0)):
-        R.set_option(OPT_RANGE_PASS, rng_on)
-        R.set_option(OPT_BLOCK_SKIP, skip_on)
-        g = R.render(c1.poses, K)
-        for k in ref:
-            assert torch.equal(ref[k], g[k]), (rng_on, skip_on, k)
-    R.set_option(OPT_RANGE_PASS, 1)
-    R.set_option(OPT_BLOCK_SKIP, 1)
+    for w in (c1, c2):
+        R.upload_volume(w.volume)
+        ref = R.render(w.poses[:2], K)
+        for rng_on, skip_on, live_on in ((0, 1, 1), (1, 0, 1), (0, 0, 1), (1, 1, 0), (0, 0, 0)):
+            R.set_option(OPT_RANGE_PASS, rng_on)
+            R.set_option(OPT_BLOCK_SKIP, skip_on)
+            R.set_option(OPT_CELL_DIRS, live_on)
+            g = R.render(w.poses[:2], K)
+            for k in ref:
+                assert torch.equal(ref[k], g[k]), (w.name, rng_on, skip_on, live_on, k)
+        R.set_option(OPT_RANGE_PASS, 1)
+        R.set_option(OPT_BLOCK_SKIP, 1)
+        R.set_option(OPT_CELL_DIRS, 1)
 
 
 def test_location_grid_and_hash_paths_agree(R, c1):

@@ -1,0 +1,15 @@
+#!/usr/bin/env bash
+# Bench lines for every config and mode on the current build (evidence for profiles/<tag>_*):
+#   gpurun --timeout 2400 -- 'bash tools/gpu_configs.sh r1f'
+TAG=${1:-r1}
+OUT=gpurun_out
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+B="python bench.py --no-cpu-baseline"
+run() { local name=$1; shift; timeout 900 "$@" > $OUT/cfg_${TAG}_$name.log 2>&1; echo "$name rc=$?"; tail -1 $OUT/cfg_${TAG}_$name.log | cut -c1-200; }
+run c2_views20 $B --config C2 --views 20 --steps 20 --warmup 3 --e2e-steps 5
+run c3_views256 $B --config C3 --views 256 --steps 10 --warmup 3 --e2e-steps 3
+run c1_combined $B --mode combined --steps 200 --warmup 10 --e2e-steps 20
+run c3_combined $B --config C3 --views 256 --mode combined --steps 5 --warmup 3 --e2e-steps 2
+timeout 1200 python -m pytest tests/test_gpu_large.py -x -q -s > $OUT/cfg_${TAG}_c4_pytest.log 2>&1; echo "c4 parity rc=$?"; tail -4 $OUT/cfg_${TAG}_c4_pytest.log
+run c4_views64 $B --config C4 --views 64 --steps 10 --warmup 3 --e2e-steps 3
