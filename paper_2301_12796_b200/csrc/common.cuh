@@ -112,8 +112,9 @@ struct RenderLaunch {
   float refine_tol;                // regula falsi also stops once the bracket is narrower (m)
   int schedule;                    // 0 grid of 16x16 CTAs, 1 persistent warps + tile counter
   int *tile_counter;               // persistent schedule work counter (reset per launch)
-  const unsigned int *z_near;      // [n_views][tiles_y][tiles_x] float bits
-  const unsigned int *z_far;
+  const unsigned long long *z_near;  // [n_views][tiles_y][tiles_x] range keys of k_range (epoch-tagged
+  const unsigned long long *z_far;   // float bits, range_key_*)
+  unsigned int epoch;                // range-pass epoch of this launch
   float *out_depth;                // [n_views][rows][W]
   float *out_normal;               // [n_views][rows][W][3] or null
   unsigned char *out_color;        // [n_views][rows][W][3] or null
@@ -156,10 +157,22 @@ struct RangeLaunch {
   int width, height, row0, row1;
   int n_views;
   int tiles_x, tiles_y;
-  unsigned int *z_near;
-  unsigned int *z_far;
+  unsigned long long *z_near;      // epoch-tagged keys (range_key_near / range_key_far): entries of
+  unsigned long long *z_far;       // older epochs lose every atomic and read as "no block", so the
+                                   // buffers never need clearing between calls
+  unsigned int epoch;              // >= 1, advanced per range pass
   ViewPose pose[kViewsPerLaunch];
 };
+
+// Range-pass keys: the high word tags the epoch so that atomicMin / atomicMax of the current pass
+// always beat stale entries of earlier passes (z_near: smaller tag for newer epochs; z_far: larger),
+// the low word holds the float bits of a positive camera z (ordered like the floats).
+__host__ __device__ __forceinline__ unsigned long long range_key_near(unsigned int epoch, unsigned int zbits) {
+  return ((unsigned long long)(0xFFFFFFFFu - epoch) << 32) | zbits;
+}
+__host__ __device__ __forceinline__ unsigned long long range_key_far(unsigned int epoch, unsigned int zbits) {
+  return ((unsigned long long)epoch << 32) | zbits;
+}
 
 // host launchers (render.cu)
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);

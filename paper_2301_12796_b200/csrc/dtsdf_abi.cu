@@ -73,7 +73,8 @@ struct dtsdf_ctx {
   // commit scratch
   int *scratch = nullptr;  // flags[4] + aabb[6] + n_loc(u64)
   // render scratch
-  unsigned int *z_near = nullptr, *z_far = nullptr;
+  unsigned long long *z_near = nullptr, *z_far = nullptr;  // range keys (epoch-tagged)
+  unsigned int range_epoch = 0;  // last epoch used; 0 = buffers need clearing
   size_t range_cap = 0;  // tiles
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
@@ -455,11 +456,12 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     dfree(c->z_near);
     dfree(c->z_far);
     c->range_cap = 0;
-    if (dalloc(c->z_near, tiles * 4) != cudaSuccess || dalloc(c->z_far, tiles * 4) != cudaSuccess) {
+    if (dalloc(c->z_near, tiles * 8) != cudaSuccess || dalloc(c->z_far, tiles * 8) != cudaSuccess) {
       cudaGetLastError();
       return fail(DTSDF_ERR_OUT_OF_MEMORY, "range buffers");
     }
     c->range_cap = tiles;
+    c->range_epoch = 0;
   }
   VolumeView V;
   V.table = c->table;
@@ -502,12 +504,17 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
         rl.pose[i].t[a] = T[4 * a + 3];
       }
     }
-    const size_t vt = (size_t)tiles_x * tiles_y * nv;
     TimedLaunch tl{};
-    begin_timed(c, 2, s, &tl, 0);
-    CK(c, cudaMemsetAsync(c->z_near, 0x7F, vt * 4, s), "range init");  // 0x7F7F7F7F = 3.4e38
-    CK(c, cudaMemsetAsync(c->z_far, 0x00, vt * 4, s), "range init");
-    end_timed(c, s, &tl);
+    if (c->range_epoch == 0 || c->range_epoch >= 0xFFFFFFF0u) {
+      // fresh buffers (or the epoch counter wrapping): keys of epoch 0, which loses every atomic
+      // of an epoch >= 1 (near tag 0xFFFFFFFF, far tag 0)
+      begin_timed(c, 2, s, &tl, 0);
+      CK(c, cudaMemsetAsync(c->z_near, 0xFF, c->range_cap * 8, s), "range init");
+      CK(c, cudaMemsetAsync(c->z_far, 0x00, c->range_cap * 8, s), "range init");
+      end_timed(c, s, &tl);
+      c->range_epoch = 0;
+    }
+    rl.epoch = ++c->range_epoch;
     begin_timed(c, 0, s, &tl, rl.n_locations > 0 ? 1 : 0);
     CK(c, launch_range(rl, s), "range pass");
     end_timed(c, s, &tl);
@@ -523,6 +530,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.refine_tol = 1e-9f * (float)c->refine_tol_nm;
     pl.tile_counter = c->tile_counter;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
+    pl.epoch = rl.epoch;
     const size_t px = (size_t)v0 * rows * W;
     pl.out_depth = depth + px;
     pl.out_normal = normal ? normal + 3 * px : nullptr;

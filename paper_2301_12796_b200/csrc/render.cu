@@ -82,9 +82,10 @@ __global__ void __launch_bounds__(256) k_range(const __grid_constant__ RangeLaun
   if (!(fu0 <= fu1) || !(fv0 <= fv1)) return;
   const int tx0 = (int)fu0 / kRangeTile, tx1 = (int)fu1 / kRangeTile;
   const int ty0 = ((int)fv0 - p.row0) / kRangeTile, ty1 = ((int)fv1 - p.row0) / kRangeTile;
-  const unsigned int zn = __float_as_uint(zmin), zf = __float_as_uint(zmax);
-  unsigned int *zn_v = p.z_near + (size_t)view * p.tiles_x * p.tiles_y;
-  unsigned int *zf_v = p.z_far + (size_t)view * p.tiles_x * p.tiles_y;
+  const unsigned long long zn = range_key_near(p.epoch, __float_as_uint(zmin));
+  const unsigned long long zf = range_key_far(p.epoch, __float_as_uint(zmax));
+  unsigned long long *zn_v = p.z_near + (size_t)view * p.tiles_x * p.tiles_y;
+  unsigned long long *zf_v = p.z_far + (size_t)view * p.tiles_x * p.tiles_y;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
       atomicMin(&zn_v[ty * p.tiles_x + tx], zn);
@@ -507,7 +508,10 @@ struct RayT {
     }
     // O2 lattice bounds, narrowed to the tile's block range (a3)
     const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
-    const float zn = __uint_as_float(__ldg(&p.z_near[tile])), zf = __uint_as_float(__ldg(&p.z_far[tile]));
+    const unsigned long long kn = __ldg(&p.z_near[tile]), kf = __ldg(&p.z_far[tile]);
+    // a tile no block of this pass projected onto still holds keys of an earlier epoch: empty
+    const bool covered = (kn >> 32) == (0xFFFFFFFFu - p.epoch) && (kf >> 32) == p.epoch;
+    const float zn = covered ? __uint_as_float((unsigned)kn) : 1.0f, zf = covered ? __uint_as_float((unsigned)kf) : 0.0f;
     const int kmin = (int)ceilf(p.z_min * Lf * V.inv_delta), kmax = (int)floorf(p.z_max * Lf * V.inv_delta);
     k = kmin;
     k1 = kmax;
