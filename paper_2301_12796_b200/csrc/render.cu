@@ -149,6 +149,10 @@ struct SampleResult {
 #ifndef DTSDF_LAZY_BISECT
 #define DTSDF_LAZY_BISECT 0  // ... and for bisection midpoints (fa unknown -> regula falsi starts with a midpoint)
 #endif
+#ifndef DTSDF_ADV_BUDGET
+#define DTSDF_ADV_BUDGET 0   // > 0: at most this many advance iterations (locates) per step (measured
+                             // slower with and without DTSDF_LAZY_SKIP, profiles/r1f_sweep_lazy.jsonl)
+#endif
 #ifndef DTSDF_LAZY_SKIP
 #define DTSDF_LAZY_SKIP 0    // certainly-positive points are skipped unevaluated (resolved on demand)
 #endif
@@ -665,9 +669,17 @@ struct RayT {
       // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
       // location without an sdf <= 0 corner, and in a certainly-positive cell followed by
       // another, no crossing can end or start.
+#if DTSDF_ADV_BUDGET > 0
+      int adv = 0;
+#endif
       for (;;) {
         live = -1;
         if (k > k1) return true;  // no crossing: a miss
+#if DTSDF_ADV_BUDGET > 0
+        // bounded advance per step: a lane with a long skip sits out this step's evaluation
+        // (its warp evaluates without it) and goes on advancing in the next
+        if (++adv > DTSDF_ADV_BUDGET) return false;
+#endif
         t = (float)k * V.delta;
         locate(V, p.comb, t);
 #ifdef DTSDF_STATS
