@@ -1,6 +1,6 @@
 // render.cu -- the per-pixel DTSDF raycast.
 //
-//   k_range    (a3) block-bounds range pass: every allocated block location's AABB, clipped
+//   k_range_*  (a3) block-bounds range pass: every allocated block location's AABB, clipped
 //              to z >= z_min, is projected into each view; per 8x8 pixel tile the min/max
 //              camera z of the covering blocks is kept with order-independent atomics.
 //   k_raycast  (a2, a4-a7) one thread per pixel, 8x4-pixel warps: lattice march t_k = k*Delta
@@ -22,7 +22,8 @@ namespace dtsdf {
 // ------------------------------------------------------------------------------------------
 // a3: range pass
 // ------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_range(const __grid_constant__ RangeLaunch p) {
+// One thread per (block location, view): enough parallelism for view batches.
+__global__ void __launch_bounds__(256) k_range_thread(const __grid_constant__ RangeLaunch p) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int view = blockIdx.y;
   if (i >= p.n_locations) return;
@@ -91,6 +92,93 @@ __global__ void __launch_bounds__(256) k_range(const __grid_constant__ RangeLaun
       atomicMin(&zn_v[ty * p.tiles_x + tx], zn);
       atomicMax(&zf_v[ty * p.tiles_x + tx], zf);
     }
+}
+
+// One warp per (block location, view), for small launches (a single view): lanes 0-7 project the
+// 8 AABB corners, lanes 8-19 clip the 12 edges against the near plane, warp reductions give the
+// pixel bbox and z-range, and the covered tiles are shared out over the lanes (with one thread per
+// location, the few near blocks covering dozens of tiles serialise a one-view pass).  Both kernels
+// compute the same keys with the same operations.
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_range_warp(const __grid_constant__ RangeLaunch p) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int view = blockIdx.y;
+  if (i >= p.n_locations) return;  // warp-uniform
+  const int4 b = p.locations[i];
+  const ViewPose &P = p.pose[view];
+  const float bs = kBlock * p.vol.voxel_size;
+  // camera coordinates of the block corners: Xc = R^T (X - t)
+  const float wx = b.x * bs - P.t[0], wy = b.y * bs - P.t[1], wz = b.z * bs - P.t[2];
+  float c0[3], e[3][3];
+  for (int a = 0; a < 3; ++a) {
+    c0[a] = P.r[0 * 3 + a] * wx + P.r[1 * 3 + a] * wy + P.r[2 * 3 + a] * wz;
+    for (int ax = 0; ax < 3; ++ax) e[ax][a] = P.r[ax * 3 + a] * bs;  // camera coords of world axis ax * bs
+  }
+  // lane < 8: corner q = lane; 8 <= lane < 20: edge (q, q | 1 << ax) with bit ax of q clear
+  int q = lane & 7, q2 = q;
+  if (lane >= 8 && lane < 20) {
+    const int ed = lane - 8, ax = ed >> 2, low = ed & 3;  // the 4 corners with bit ax clear
+    q = ax == 0 ? (low << 1) : ax == 1 ? ((low & 1) | ((low & 2) << 1)) : low;
+    q2 = q | (1 << ax);
+  }
+  auto corner = [&](int c, float &x, float &y, float &z) {
+    const float dx = (c & 1), dy = ((c >> 1) & 1), dz = ((c >> 2) & 1);
+    x = c0[0] + dx * e[0][0] + dy * e[1][0] + dz * e[2][0];
+    y = c0[1] + dx * e[0][1] + dy * e[1][1] + dz * e[2][1];
+    z = c0[2] + dx * e[0][2] + dy * e[1][2] + dz * e[2][2];
+  };
+  float x1, y1, z1, x2, y2, z2;
+  corner(q, x1, y1, z1);
+  corner(q2, x2, y2, z2);
+  const float zmax = warp_max(lane < 8 ? z1 : -CUDART_INF_F);
+  if (zmax < p.z_min) return;  // entirely in front of the near plane (warp-uniform)
+  float umin = CUDART_INF_F, umax = -CUDART_INF_F, vmin = CUDART_INF_F, vmax = -CUDART_INF_F;
+  float zmin = CUDART_INF_F;
+  if (lane < 8 && z1 >= p.z_min) {
+    const float iz = 1.0f / z1;
+    const float u = p.fx * x1 * iz + p.cx, v = p.fy * y1 * iz + p.cy;
+    umin = umax = u;
+    vmin = vmax = v;
+    zmin = z1;
+  } else if (lane >= 8 && lane < 20 && (z1 >= p.z_min) != (z2 >= p.z_min)) {
+    // an edge crossing the near plane contributes its intersection point
+    const float s = (p.z_min - z1) / (z2 - z1);
+    const float x = x1 + s * (x2 - x1), y = y1 + s * (y2 - y1);
+    const float u = p.fx * x / p.z_min + p.cx, v = p.fy * y / p.z_min + p.cy;
+    umin = umax = u;
+    vmin = vmax = v;
+    zmin = p.z_min;
+  }
+  umin = warp_min(umin); umax = warp_max(umax);
+  vmin = warp_min(vmin); vmax = warp_max(vmax);
+  zmin = warp_min(zmin);
+  // conservative pixel range (+1 px), clipped to the image / row shard
+  const float fu0 = fmaxf(floorf(umin) - 1.0f, 0.0f), fu1 = fminf(ceilf(umax) + 1.0f, (float)(p.width - 1));
+  const float fv0 = fmaxf(floorf(vmin) - 1.0f, (float)p.row0), fv1 = fminf(ceilf(vmax) + 1.0f, (float)(p.row1 - 1));
+  if (!(fu0 <= fu1) || !(fv0 <= fv1)) return;
+  const int tx0 = (int)fu0 / kRangeTile, tx1 = (int)fu1 / kRangeTile;
+  const int ty0 = ((int)fv0 - p.row0) / kRangeTile, ty1 = ((int)fv1 - p.row0) / kRangeTile;
+  const unsigned long long zn = range_key_near(p.epoch, __float_as_uint(zmin));
+  const unsigned long long zf = range_key_far(p.epoch, __float_as_uint(zmax));
+  unsigned long long *zn_v = p.z_near + (size_t)view * p.tiles_x * p.tiles_y;
+  unsigned long long *zf_v = p.z_far + (size_t)view * p.tiles_x * p.tiles_y;
+  const int nx = tx1 - tx0 + 1, n = nx * (ty1 - ty0 + 1);
+  for (int j = lane; j < n; j += 32) {
+    const int tile = (ty0 + j / nx) * p.tiles_x + tx0 + j % nx;
+    atomicMin(&zn_v[tile], zn);
+    atomicMax(&zf_v[tile], zf);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -958,8 +1046,13 @@ struct RayT {
 
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
   if (p.n_locations == 0 || p.n_views == 0) return cudaSuccess;
-  dim3 grid((unsigned)((p.n_locations + 255) / 256), (unsigned)p.n_views);
-  k_range<<<grid, 256, 0, s>>>(p);
+  if (p.n_locations * p.n_views < (1 << 18)) {  // a warp per location while a thread each would fill < 1 wave
+    dim3 grid((unsigned)((p.n_locations * 32 + 255) / 256), (unsigned)p.n_views);
+    k_range_warp<<<grid, 256, 0, s>>>(p);
+  } else {
+    dim3 grid((unsigned)((p.n_locations + 255) / 256), (unsigned)p.n_views);
+    k_range_thread<<<grid, 256, 0, s>>>(p);
+  }
   return cudaGetLastError();
 }
 
