@@ -27,6 +27,9 @@ def run_one(args):
     from paper_2301_12796_b200 import Renderer
 
     R = Renderer(0)
+    for kv in args.set:  # DTSDF_OPT_* settings "option=value"
+        o, v = kv.split("=")
+        R.set_option(int(o), int(v))
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     for name in args.configs.split(","):
         w = scenes.CONFIGS[name]()
@@ -51,6 +54,7 @@ def run_one(args):
             ora = oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
             st = compare({k: v[0].cpu().numpy() for k, v in out.items()}, ora)
         print(json.dumps({"variant": args.name, "config": name, "l2": "warm" if args.no_flush else "flushed",
+                          "options": args.set,
                           "raycast_ms": round(ms, 4),
                           "budget_used": st.get("budget_used"), "color_exact": st.get("color_exact"),
                           "depth_max": st.get("depth_max_err"), "hit_disagree": st.get("hit_disagree"),
@@ -66,6 +70,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between launches (an upper bound)")
     ap.add_argument("--run", action="store_true")
+    ap.add_argument("--set", action="append", default=[], help="dtsdf_set_option for the --run process: opt=value")
     ap.add_argument("--name", default="")
     args = ap.parse_args()
     if args.run:
@@ -73,8 +78,12 @@ def main():
     from paper_2301_12796_b200 import build as B
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     libs = []
+    name_opts = {}
     for v in args.variant or ["base:"]:
         name, _, defs = v.partition(":")
+        if "|" in defs:  # name:defines|opt=value,opt=value -> runtime options too
+            defs, _, opts = defs.partition("|")
+            name_opts[name] = [o for o in opts.split(",") if o]
         if defs.startswith("@"):  # a prebuilt library (e.g. an earlier build kept under gpurun_out/)
             libs.append((name, os.path.abspath(defs[1:])))
             continue
@@ -92,7 +101,7 @@ def main():
             env = dict(os.environ, DTSDF_LIB=lib)
             cmd = [sys.executable, os.path.abspath(__file__), "--run", "--name", name, "--configs", args.configs,
                    "--reps", str(args.reps)] + (["--no-parity"] if args.no_parity or r > 0 else []) + \
-                  (["--no-flush"] if args.no_flush else [])
+                  (["--no-flush"] if args.no_flush else []) + sum((["--set", o] for o in name_opts.get(name, [])), [])
             subprocess.run(cmd, env=env, check=True)
 
 
