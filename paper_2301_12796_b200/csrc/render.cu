@@ -553,7 +553,10 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
 enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3, kResolve = 4 };
-constexpr int kLookahead = 8;  // lattice points tested per certainly-positive scan
+#ifndef DTSDF_LOOKAHEAD
+#define DTSDF_LOOKAHEAD 8
+#endif
+constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certainly-positive scan
 
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
