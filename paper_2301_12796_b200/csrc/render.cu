@@ -1063,6 +1063,9 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
 #ifndef DTSDF_CTA
 #define DTSDF_CTA 128  // 128-thread CTAs: 4% faster than 256 on C1 (smaller tail, profiles/r1c_sweep_cta.txt)
 #endif
+#ifndef DTSDF_CARVEOUT
+#define DTSDF_CARVEOUT -1  // >= 0: preferred shared-memory carveout (percent) of k_raycast; -1 driver default
+#endif
 #ifndef DTSDF_RAYCAST_MINB
 #define DTSDF_RAYCAST_MINB (512 / DTSDF_CTA)  // 128 registers per thread (16 warps per SM)
 #endif
@@ -1206,6 +1209,13 @@ static cudaError_t launch_raycast_t(const RenderLaunch &p, cudaStream_t s) {
     k_raycast_persistent<kComb><<<(unsigned)grid, 256, 0, s>>>(p);
     return cudaGetLastError();
   }
+#if DTSDF_CARVEOUT >= 0
+  static bool carve = false;
+  if (!carve) {  // L1 / shared-memory split of the SM's unified array (percent shared)
+    cudaFuncSetAttribute(k_raycast<kComb>, cudaFuncAttributePreferredSharedMemoryCarveout, DTSDF_CARVEOUT);
+    carve = true;
+  }
+#endif
   const int rows_per_cta = DTSDF_CTA / 16;
   dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.row1 - p.row0 + rows_per_cta - 1) / rows_per_cta),
             (unsigned)p.n_views);
