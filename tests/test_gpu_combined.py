@@ -201,3 +201,25 @@ def test_algorithm1_voxels_and_render(R, cfg, c1, c2):
                                mode=1)
     rs = assert_parity(_sel(g, 0), o, what=f"{cfg} algorithm 1")
     print(cfg, "algorithm 1", st, rs)
+
+
+def test_combined_host_outputs_equal_device_outputs(R, c1):
+    """The combined raycast into pinned host outputs (written by the kernel, DTSDF_OPT_HOST_WRITE)
+    and via the copy path equals the device render bit for bit, on a ragged row range."""
+    from paper_2301_12796_b200.dtsdf import OPT_HOST_WRITE
+    R.upload_volume(c1.volume)
+    K = c1.intrinsics
+    R.combine(c1.poses[0], K)
+    r0, r1 = 3, 470
+    g = R.render(c1.poses, K, row0=r0, row1=r1, combined=True)
+    H, W = r1 - r0, K.width
+    for host_write in (1, 0):
+        R.set_option(OPT_HOST_WRITE, host_write)
+        hd = torch.full((1, H, W), 7.0, dtype=torch.float32).pin_memory()
+        hn = torch.full((1, H, W, 3), 7.0, dtype=torch.float32).pin_memory()
+        hc = torch.full((1, H, W, 3), 7, dtype=torch.uint8).pin_memory()
+        hm = torch.full((1, H, W), 7, dtype=torch.uint8).pin_memory()
+        R.render_combined_into(c1.poses, K, hd, hn, hc, hm, row0=r0, row1=r1)
+        for k, h in (("depth", hd), ("normal", hn), ("color", hc), ("mask", hm)):
+            assert torch.equal(g[k].cpu(), h), (k, host_write)
+    R.set_option(OPT_HOST_WRITE, 1)

@@ -313,3 +313,28 @@ def test_hand_built_cases_match_oracle(R):
         pose = scenes.look_at(c + side * 0.5 * n, c)
         g = R.render(pose[None], K)
         assert_parity(_sel(g, 0), ov.render(pose, K), budget=2e-3)
+
+
+def test_random_and_axis_aligned_poses_inside_the_room(R, c1):
+    """Cameras inside the volume's AABB at seeded random positions and directions (looking up,
+    down, along the floor), plus exactly axis-aligned views whose central rays have components
+    that are exactly 0 (the empty-space and AABB-entry skips divide by them): full-frame parity."""
+    R.upload_volume(c1.volume)
+    rng = np.random.default_rng([7, 1])
+    poses = []
+    for _ in range(6):
+        p = np.array([rng.uniform(-1.8, 1.8), rng.uniform(-1.8, 1.8), rng.uniform(0.05, 1.6)])
+        d = rng.normal(size=3)
+        d[2] = -abs(d[2]) if len(poses) % 3 else abs(d[2])  # mostly towards the floor and boxes
+        poses.append(scenes.look_at(p, p + d / np.linalg.norm(d)))
+    poses.append(scenes.look_at((0.013, -0.021, 1.5), (0.013, -0.021, 0.0)))   # straight down
+    poses.append(scenes.look_at((-1.9, 0.0, 0.3), (1.0, 0.0, 0.3)))            # along +x
+    poses.append(scenes.look_at((0.4, 1.9, 0.25), (0.4, -1.0, 0.25)))          # along -y
+    ov = oracle.OracleVolume(c1.volume)
+    for K in (scenes.Intrinsics(fx=131.25, fy=131.25, cx=80.0, cy=60.0, width=160, height=120),
+              scenes.Intrinsics(fx=131.25, fy=131.25, cx=79.5, cy=59.5, width=161, height=121)):
+        g = R.render(np.stack(poses), K)
+        for i, P in enumerate(poses):
+            o = ov.render(P, K)
+            st = assert_parity(_sel(g, i), o, what=f"pose {i} {K.width}x{K.height}")
+            print("inside-room pose", i, K.width, st["hits_gpu"], st["budget_used"], st["depth_max_err"])
