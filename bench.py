@@ -352,7 +352,8 @@ def run_dtsdf(args):
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": "k_raycast", "kernel_ms": ray_ms, "bytes_per_ray_alg": b_ray,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s",
-            "range_pass_ms": kt["range_ms"] / max(kt["range_launches"], 1)}
+            "range_pass_ms": kt["range_ms"] / max(kt["range_launches"], 1),  # k_range + k_order
+            "range_pass_note": "range pass + tile order (k_range_*, k_order), per launch"}
     # what actually bounds k_raycast: instruction issue.  Warp instructions per launch
     # from the committed ncu capture of this config (a property of the workload), divided by this
     # run's live kernel time, against 148 SMs x 4 schedulers x 1 instruction per clock.

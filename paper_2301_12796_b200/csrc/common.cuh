@@ -115,6 +115,8 @@ struct RenderLaunch {
   const unsigned long long *z_near;  // [n_views][tiles_y][tiles_x] range keys of k_range (epoch-tagged
   const unsigned long long *z_far;   // float bits, range_key_*)
   unsigned int epoch;                // range-pass epoch of this launch
+  const int *order;                  // [n_views][ct_x * ct_y] CTA tiles, longest predicted first, or null
+  int ct_x;                          // CTA tiles per image row
   float *out_depth;                // [n_views][rows][W]
   float *out_normal;               // [n_views][rows][W][3] or null
   unsigned char *out_color;        // [n_views][rows][W][3] or null
@@ -161,6 +163,8 @@ struct RangeLaunch {
   unsigned long long *z_far;       // older epochs lose every atomic and read as "no block", so the
                                    // buffers never need clearing between calls
   unsigned int epoch;              // >= 1, advanced per range pass
+  unsigned int *count;             // [n_views][tiles] block locations covering each tile (cost proxy of
+                                   // the tile order; zero between passes -- k_order clears it), or null
   ViewPose pose[kViewsPerLaunch];
 };
 
@@ -176,6 +180,12 @@ __host__ __device__ __forceinline__ unsigned long long range_key_far(unsigned in
 
 // host launchers (render.cu)
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
+// raycast CTA tiles (kTileW x kTileH pixels) of a width x rows image
+void raycast_tiles(int width, int rows, int *ct_x, int *ct_y);
+// CTA tile order of each view from the range-pass counts (longest predicted first); clears the counts
+cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, const unsigned long long *z_far,
+                         unsigned int epoch, float voxel_size, int *order, int tiles_x, int tiles_y, int width,
+                         int rows, int n_views, cudaStream_t s);
 cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s);
 
 // Fusion launch (fusion.cu): one depth frame against the raw block pool.  The doubles are the

@@ -75,6 +75,10 @@ struct dtsdf_ctx {
   // render scratch
   unsigned long long *z_near = nullptr, *z_far = nullptr;  // range keys (epoch-tagged)
   unsigned int range_epoch = 0;  // last epoch used; 0 = buffers need clearing
+  unsigned int *tile_count = nullptr;  // range-pass block counts per tile (zero between passes)
+  int *tile_order = nullptr;           // CTA tile order per view
+  size_t order_cap = 0;
+  int use_order = 1;                   // DTSDF_OPT_TILE_ORDER
   size_t range_cap = 0;  // tiles
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
@@ -262,6 +266,8 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   dfree(c->icp_state);
   dfree(c->z_near);
   dfree(c->z_far);
+  dfree(c->tile_count);
+  dfree(c->tile_order);
   if (c->host_stage) cudaFree(c->host_stage);
   for (auto &t : c->timed) {
     cudaEventDestroy(t.start);
@@ -455,14 +461,30 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   if (tiles > c->range_cap) {
     dfree(c->z_near);
     dfree(c->z_far);
+    dfree(c->tile_count);
     c->range_cap = 0;
-    if (dalloc(c->z_near, tiles * 8) != cudaSuccess || dalloc(c->z_far, tiles * 8) != cudaSuccess) {
+    if (dalloc(c->z_near, tiles * 8) != cudaSuccess || dalloc(c->z_far, tiles * 8) != cudaSuccess ||
+        dalloc(c->tile_count, tiles * 4) != cudaSuccess) {
       cudaGetLastError();
       return fail(DTSDF_ERR_OUT_OF_MEMORY, "range buffers");
     }
+    CK(c, cudaMemsetAsync(c->tile_count, 0, tiles * 4, s), "tile counts");
     c->range_cap = tiles;
     c->range_epoch = 0;
   }
+  int ct_x = 0, ct_y = 0;
+  raycast_tiles(W, rows, &ct_x, &ct_y);
+  const size_t cts = (size_t)ct_x * ct_y * std::min(n_views, kViewsPerLaunch);
+  if (cts > c->order_cap) {
+    dfree(c->tile_order);
+    c->order_cap = 0;
+    if (dalloc(c->tile_order, cts * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "tile order");
+    }
+    c->order_cap = cts;
+  }
+  const bool order = c->use_order && c->schedule == 0;
   VolumeView V;
   V.table = c->table;
   V.table_mask = c->table_cap - 1;
@@ -515,8 +537,12 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
       c->range_epoch = 0;
     }
     rl.epoch = ++c->range_epoch;
-    begin_timed(c, 0, s, &tl, rl.n_locations > 0 ? 1 : 0);
+    rl.count = order ? c->tile_count : nullptr;
+    begin_timed(c, 0, s, &tl, (rl.n_locations > 0 ? 1 : 0) + (order ? 1 : 0));
     CK(c, launch_range(rl, s), "range pass");
+    if (order)
+      CK(c, launch_order(c->tile_count, c->z_near, c->z_far, rl.epoch, V.voxel_size, c->tile_order, tiles_x, tiles_y,
+                         W, rows, nv, s), "tile order");
     end_timed(c, s, &tl);
     pl.vol = V;
     pl.fx = K->fx; pl.fy = K->fy; pl.cx = K->cx; pl.cy = K->cy; pl.z_min = K->z_min; pl.z_max = K->z_max;
@@ -531,6 +557,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.tile_counter = c->tile_counter;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
     pl.epoch = rl.epoch;
+    pl.order = order ? c->tile_order : nullptr;
+    pl.ct_x = ct_x;
     const size_t px = (size_t)v0 * rows * W;
     pl.out_depth = depth + px;
     pl.out_normal = normal ? normal + 3 * px : nullptr;
@@ -1209,6 +1237,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;
   else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
   else if (option == DTSDF_OPT_CELL_DIRS) c->use_live = value ? 1 : 0;
+  else if (option == DTSDF_OPT_TILE_ORDER) c->use_order = value ? 1 : 0;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

@@ -14,16 +14,48 @@
 // in an unallocated block location has no present direction and is invalid (DESIGN.md §2 O2).
 #include <math_constants.h>
 
+#include <utility>
+
 #include "common.cuh"
 
 
 namespace dtsdf {
+
+// grid schedule of the raycast: one CTA per kTileW x kTileH-pixel tile of 8x4-pixel warps
+#ifndef DTSDF_CTA
+#define DTSDF_CTA 128  // 128-thread CTAs: 4% faster than 256 on C1 (smaller tail, profiles/r1c_sweep_cta.txt)
+#endif
+constexpr int kTileW = 16, kTileH = DTSDF_CTA / 16;  // CTA pixel tile
+static_assert(kTileW % kRangeTile == 0 && kTileH % kRangeTile == 0, "CTA tiles cover whole range tiles");
+
+// Programmatic dependent launch: the range pass -> tile order -> raycast chain is launched with
+// programmatic stream serialisation, so each grid is set up while its predecessor runs; the
+// dependent waits for the predecessor's completion (and memory) at griddepcontrol.wait.  Without
+// the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------------------------------
 // a3: range pass
 // ------------------------------------------------------------------------------------------
 // One thread per (block location, view): enough parallelism for view batches.
 __global__ void __launch_bounds__(256) k_range_thread(const __grid_constant__ RangeLaunch p) {
+  griddep_launch_dependents();
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int view = blockIdx.y;
   if (i >= p.n_locations) return;
@@ -87,10 +119,12 @@ __global__ void __launch_bounds__(256) k_range_thread(const __grid_constant__ Ra
   const unsigned long long zf = range_key_far(p.epoch, __float_as_uint(zmax));
   unsigned long long *zn_v = p.z_near + (size_t)view * p.tiles_x * p.tiles_y;
   unsigned long long *zf_v = p.z_far + (size_t)view * p.tiles_x * p.tiles_y;
+  unsigned int *cnt_v = p.count ? p.count + (size_t)view * p.tiles_x * p.tiles_y : nullptr;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) {
       atomicMin(&zn_v[ty * p.tiles_x + tx], zn);
       atomicMax(&zf_v[ty * p.tiles_x + tx], zf);
+      if (cnt_v) atomicAdd(&cnt_v[ty * p.tiles_x + tx], 1u);
     }
 }
 
@@ -111,6 +145,7 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 __global__ void __launch_bounds__(256) k_range_warp(const __grid_constant__ RangeLaunch p) {
+  griddep_launch_dependents();
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int view = blockIdx.y;
@@ -174,11 +209,101 @@ __global__ void __launch_bounds__(256) k_range_warp(const __grid_constant__ Rang
   unsigned long long *zn_v = p.z_near + (size_t)view * p.tiles_x * p.tiles_y;
   unsigned long long *zf_v = p.z_far + (size_t)view * p.tiles_x * p.tiles_y;
   const int nx = tx1 - tx0 + 1, n = nx * (ty1 - ty0 + 1);
+  unsigned int *cnt_v = p.count ? p.count + (size_t)view * p.tiles_x * p.tiles_y : nullptr;
   for (int j = lane; j < n; j += 32) {
     const int tile = (ty0 + j / nx) * p.tiles_x + tx0 + j % nx;
     atomicMin(&zn_v[tile], zn);
     atomicMax(&zf_v[tile], zf);
+    if (cnt_v) atomicAdd(&cnt_v[tile], 1u);
   }
+}
+
+// Tile order (one CTA per view): the raycast's cost is dominated by a few long-running warp tiles
+// (rays grazing the floor, threading between boxes), and a tile launched late stretches the end of
+// the kernel while the SMs drain (profiles/r1f_timeline.txt).  Longest-predicted-first: the cost
+// proxy of a CTA tile is the number of block locations whose projection covers its range tiles;
+// a counting sort on a log2 key (64 buckets) orders the CTA tiles by decreasing count.  The order
+// changes only when a tile runs, never what it computes.  Clears the counts for the next pass.
+constexpr int kOrderKeys = 64;
+#ifndef DTSDF_ORDER_PROXY
+#define DTSDF_ORDER_PROXY 0  // cost proxy: 0 covering block count, 1 depth span of the covering blocks, 2 both
+#endif
+struct OrderLaunch {
+  unsigned int *count;               // [views][tiles]
+  const unsigned long long *z_near;  // [views][tiles] range keys of this pass
+  const unsigned long long *z_far;
+  int *order;                        // [views][ct_x * ct_y]
+  int tiles_x, tiles_y, ct_x, ct_y;
+  unsigned int epoch;
+  float inv_voxel;
+};
+
+__device__ __forceinline__ int order_key(const OrderLaunch &p, int view, int t) {
+  const int tx = t % p.ct_x, ty = t / p.ct_x;
+  const size_t vo = (size_t)view * p.tiles_x * p.tiles_y;
+  float c = 0.f, span = 0.f;
+  for (int ry = ty * (kTileH / kRangeTile); ry < min(p.tiles_y, (ty + 1) * (kTileH / kRangeTile)); ++ry)
+    for (int rx = tx * (kTileW / kRangeTile); rx < min(p.tiles_x, (tx + 1) * (kTileW / kRangeTile)); ++rx) {
+      const size_t i = vo + ry * p.tiles_x + rx;
+      c += (float)p.count[i];
+      if (DTSDF_ORDER_PROXY) {
+        const unsigned long long kn = p.z_near[i], kf = p.z_far[i];
+        if ((kn >> 32) == (0xFFFFFFFFu - p.epoch) && (kf >> 32) == p.epoch)
+          span = fmaxf(span, (__uint_as_float((unsigned)kf) - __uint_as_float((unsigned)kn)) * p.inv_voxel);
+      }
+    }
+  const float cost = DTSDF_ORDER_PROXY == 0 ? c : DTSDF_ORDER_PROXY == 1 ? span : c * span;
+  const int lg = cost > 0.f ? (int)(8.0f * __log2f(cost + 1.0f)) : 0;  // 8 keys per doubling
+  return kOrderKeys - 1 - min(lg, kOrderKeys - 1);                   // ascending key = descending cost
+}
+
+__global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLaunch p) {
+  __shared__ unsigned int hist[kOrderKeys];
+  griddep_launch_dependents();  // the raycast may be set up now; it waits for this grid to finish
+  griddep_wait();               // the range pass's counts and keys
+  const int view = blockIdx.x;
+  unsigned int *cnt = p.count + (size_t)view * p.tiles_x * p.tiles_y;
+  int *ord = p.order + (size_t)view * p.ct_x * p.ct_y;
+  const int n = p.ct_x * p.ct_y;
+  if (threadIdx.x < kOrderKeys) hist[threadIdx.x] = 0;
+  __syncthreads();
+  // warp-aggregated shared atomics: the lanes of a warp holding the same key add once (most tiles
+  // share a handful of keys, and per-lane atomics on one bucket serialise)
+  const int n_round = (n + (int)blockDim.x - 1) / (int)blockDim.x * (int)blockDim.x;
+  for (int t = threadIdx.x; t < n_round; t += blockDim.x) {
+    const int key = t < n ? order_key(p, view, t) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], (unsigned)__popc(same));
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan of the 64 bucket sizes (two per lane)
+    const unsigned int a = hist[2 * threadIdx.x], b = hist[2 * threadIdx.x + 1];
+    unsigned int incl = a + b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)threadIdx.x >= o) incl += v;
+    }
+    const unsigned int excl = incl - a - b;
+    hist[2 * threadIdx.x] = excl;
+    hist[2 * threadIdx.x + 1] = excl + a;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_round; t += blockDim.x) {
+    const int key = t < n ? order_key(p, view, t) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
+    unsigned base = 0;
+    if (key >= 0 && lane == leader) base = atomicAdd(&hist[key], (unsigned)__popc(same));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (key >= 0) {
+      const unsigned pos = base + __popc(same & ((1u << lane) - 1u));
+      DTSDF_CHECK(pos < (unsigned)n);
+      ord[pos] = t;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < p.tiles_x * p.tiles_y; i += blockDim.x) cnt[i] = 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -558,12 +683,16 @@ enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3, kResolve = 4 };
 #endif
 constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certainly-positive scan
 
+// per-thread pixel of the ray (u | vrel << 16), read back only when a bracket starts and at the end
+__shared__ int ray_pix[256];
+
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
 // a warp -- whatever phase each is in -- run the evaluation code together.
 template <bool kComb>
 struct RayT {
-  int view, u, vrel;
+  int view;  // the pixel (u | vrel << 16) waits in shared memory (ray_pix): no register through the march
+  __device__ __forceinline__ int pix() const { return ray_pix[threadIdx.x]; }
   float r[3], o[3], ir[3], iLf;
   int k, k1;
   // sample positions in voxel units g = g0 + t * rs relative to the integer cell ib of a frame:
@@ -588,7 +717,9 @@ struct RayT {
 #endif
 
   __device__ __forceinline__ void init(const RenderLaunch &p, int view_, int u_, int vrel_) {
-    view = view_; u = u_; vrel = vrel_;
+    view = view_;
+    ray_pix[threadIdx.x] = u_ | (vrel_ << 16);
+    const int u = u_, vrel = vrel_;
     const VolumeView &V = p.vol;
     const ViewPose &P = p.pose[view];
     const int v = p.row0 + vrel;
@@ -720,8 +851,9 @@ struct RayT {
     // re-anchor the position frame at x(t_{k-1}) in fp64
     {
       const ViewPose &P = p.pose[view];
-      const double ddx = ((double)u - (double)p.cx) / (double)p.fx;
-      const double ddy = ((double)(p.row0 + vrel) - (double)p.cy) / (double)p.fy;
+      const int px = pix();
+      const double ddx = ((double)(px & 0xffff) - (double)p.cx) / (double)p.fx;
+      const double ddy = ((double)(p.row0 + (px >> 16)) - (double)p.cy) / (double)p.fy;
       const double iLd = 1.0 / sqrt(ddx * ddx + ddy * ddy + 1.0), inv_s = 1.0 / (double)V.voxel_size;
       const double t0 = (double)(k - 1) * (double)V.delta;
       double rq[3], gq[3];
@@ -1012,7 +1144,7 @@ struct RayT {
     }
 #ifdef DTSDF_STATS
     if (p.dbg_timeline) {
-      const size_t pid = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
+      const size_t pid = ((size_t)view * (p.row1 - p.row0) + (pix() >> 16)) * p.width + (pix() & 0xffff);
       p.dbg_timeline[3 * pid + 0] = g_start;
       p.dbg_timeline[3 * pid + 1] = g_end;
       p.dbg_timeline[3 * pid + 2] = smid;
@@ -1030,20 +1162,21 @@ struct RayT {
     float depth, nrm[3];
     int col[3], mask;
     result(p, depth, nrm, col, mask);
-    const size_t pix = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
+    const int u = pix() & 0xffff, vrel = pix() >> 16;
+    const size_t px = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
     DTSDF_CHECK(view < p.n_views && vrel >= 0 && vrel < p.row1 - p.row0 && u >= 0 && u < p.width);
-    p.out_depth[pix] = depth;
+    p.out_depth[px] = depth;
     if (p.out_normal) {
-      p.out_normal[3 * pix + 0] = nrm[0];
-      p.out_normal[3 * pix + 1] = nrm[1];
-      p.out_normal[3 * pix + 2] = nrm[2];
+      p.out_normal[3 * px + 0] = nrm[0];
+      p.out_normal[3 * px + 1] = nrm[1];
+      p.out_normal[3 * px + 2] = nrm[2];
     }
     if (p.out_color) {
-      p.out_color[3 * pix + 0] = (unsigned char)col[0];
-      p.out_color[3 * pix + 1] = (unsigned char)col[1];
-      p.out_color[3 * pix + 2] = (unsigned char)col[2];
+      p.out_color[3 * px + 0] = (unsigned char)col[0];
+      p.out_color[3 * px + 1] = (unsigned char)col[1];
+      p.out_color[3 * px + 2] = (unsigned char)col[2];
     }
-    if (p.out_mask) p.out_mask[pix] = (unsigned char)mask;
+    if (p.out_mask) p.out_mask[px] = (unsigned char)mask;
   }
 };
 
@@ -1059,10 +1192,26 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+void raycast_tiles(int width, int rows, int *ct_x, int *ct_y) {
+  *ct_x = (width + kTileW - 1) / kTileW;
+  *ct_y = (rows + kTileH - 1) / kTileH;
+}
+
+cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, const unsigned long long *z_far,
+                         unsigned int epoch, float voxel_size, int *order, int tiles_x, int tiles_y, int width,
+                         int rows, int n_views, cudaStream_t s) {
+  if (n_views == 0) return cudaSuccess;
+  OrderLaunch p;
+  p.count = count; p.z_near = z_near; p.z_far = z_far; p.order = order;
+  p.tiles_x = tiles_x; p.tiles_y = tiles_y;
+  raycast_tiles(width, rows, &p.ct_x, &p.ct_y);
+  p.epoch = epoch;
+  p.inv_voxel = 1.0f / voxel_size;
+  return launch_pdl(k_order, dim3((unsigned)n_views), dim3(1024), s, p);
+  return cudaGetLastError();
+}
+
 // grid schedule: one CTA per 16 x (2 * DTSDF_CTA / 64)-pixel tile of 8x4-pixel warps, one ray per thread
-#ifndef DTSDF_CTA
-#define DTSDF_CTA 128  // 128-thread CTAs: 4% faster than 256 on C1 (smaller tail, profiles/r1c_sweep_cta.txt)
-#endif
 #ifndef DTSDF_CARVEOUT
 #define DTSDF_CARVEOUT -1  // >= 0: preferred shared-memory carveout (percent) of k_raycast; -1 driver default
 #endif
@@ -1082,7 +1231,6 @@ __device__ __forceinline__ void copy_row(unsigned char *dst, const unsigned char
   }
 }
 
-constexpr int kTileW = 16, kTileH = DTSDF_CTA / 16;  // CTA pixel tile
 
 template <bool kComb>
 __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const __grid_constant__ RenderLaunch p) {
@@ -1093,7 +1241,17 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   __shared__ __align__(16) unsigned char s_mask[kTileH][kTileW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tx = (warp & 1) * 8 + (lane & 7), ty = (warp >> 1) * 4 + (lane >> 3);
-  const int u0 = blockIdx.x * kTileW, v0 = blockIdx.y * kTileH;
+  griddep_wait();  // launched programmatically after the range pass / tile order: their outputs
+  // CTA tile: in the view's tile order (longest predicted first, k_order) when there is one; its
+  // origin is parked in shared memory for the epilogue instead of a register through the march
+  __shared__ int s_origin[2];
+  int u0, v0;
+  {
+    const int ct = p.order ? __ldg(&p.order[(size_t)blockIdx.z * gridDim.x + blockIdx.x]) : blockIdx.x;
+    u0 = (ct % p.ct_x) * kTileW;
+    v0 = (ct / p.ct_x) * kTileH;
+    if (threadIdx.x == 0) { s_origin[0] = u0; s_origin[1] = v0; }
+  }
   const int u = u0 + tx, vrel = v0 + ty;
   const int rows = p.row1 - p.row0;
   if (u < p.width && vrel < rows) {
@@ -1136,6 +1294,8 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   }
   if (!p.staged) return;  // uniform per launch
   __syncthreads();
+  u0 = s_origin[0];
+  v0 = s_origin[1];
   // each warp writes kTileH / 4 rows: lanes 0-3 depth, 4-15 normal, 16-18 colour, 19 mask when the
   // row is full width and aligned; otherwise each array of the row with all 32 lanes, bytewise
   const int nu = min(kTileW, p.width - u0);
@@ -1216,10 +1376,9 @@ static cudaError_t launch_raycast_t(const RenderLaunch &p, cudaStream_t s) {
     carve = true;
   }
 #endif
-  const int rows_per_cta = DTSDF_CTA / 16;
-  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.row1 - p.row0 + rows_per_cta - 1) / rows_per_cta),
-            (unsigned)p.n_views);
-  k_raycast<kComb><<<grid, DTSDF_CTA, 0, s>>>(p);
+  const int ct_y = (p.row1 - p.row0 + kTileH - 1) / kTileH;
+  dim3 grid((unsigned)(p.ct_x * ct_y), 1u, (unsigned)p.n_views);
+  return launch_pdl(k_raycast<kComb>, grid, dim3(DTSDF_CTA), s, p);
   return cudaGetLastError();
 }
 

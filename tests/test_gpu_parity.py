@@ -131,24 +131,27 @@ def test_row_shards_concatenate_bitexact(R, c1):
 
 
 def test_accelerations_are_result_invisible(R, c1, c2):
-    """Range pass, block skipping and the live-direction cell masks are exact (DESIGN.md §2 O2,
-    §5): switching them off changes no bit (C1 room and the C2 thin plates, where opposing
+    """Range pass, block skipping, the live-direction cell masks and the tile order are exact
+    (DESIGN.md §2 O2, §5, §6): switching them off changes no bit (C1 room and the C2 thin plates, where opposing
     directions share block locations)."""
-    from paper_2301_12796_b200.dtsdf import OPT_BLOCK_SKIP, OPT_CELL_DIRS, OPT_RANGE_PASS
+    from paper_2301_12796_b200.dtsdf import OPT_BLOCK_SKIP, OPT_CELL_DIRS, OPT_RANGE_PASS, OPT_TILE_ORDER
     K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=320, height=240)
     for w in (c1, c2):
         R.upload_volume(w.volume)
         ref = R.render(w.poses[:2], K)
-        for rng_on, skip_on, live_on in ((0, 1, 1), (1, 0, 1), (0, 0, 1), (1, 1, 0), (0, 0, 0)):
+        for rng_on, skip_on, live_on, order_on in ((0, 1, 1, 1), (1, 0, 1, 1), (0, 0, 1, 1), (1, 1, 0, 1),
+                                                   (1, 1, 1, 0), (0, 0, 0, 0)):
             R.set_option(OPT_RANGE_PASS, rng_on)
             R.set_option(OPT_BLOCK_SKIP, skip_on)
             R.set_option(OPT_CELL_DIRS, live_on)
+            R.set_option(OPT_TILE_ORDER, order_on)
             g = R.render(w.poses[:2], K)
             for k in ref:
-                assert torch.equal(ref[k], g[k]), (w.name, rng_on, skip_on, live_on, k)
+                assert torch.equal(ref[k], g[k]), (w.name, rng_on, skip_on, live_on, order_on, k)
         R.set_option(OPT_RANGE_PASS, 1)
         R.set_option(OPT_BLOCK_SKIP, 1)
         R.set_option(OPT_CELL_DIRS, 1)
+        R.set_option(OPT_TILE_ORDER, 1)
 
 
 def test_location_grid_and_hash_paths_agree(R, c1):
@@ -278,7 +281,7 @@ def test_batch_larger_than_one_launch(R, c1):
     R.upload_volume(w.volume)
     n0 = R.launch_count()
     g = R.render(w.poses, K)
-    assert R.launch_count() - n0 == 4  # 2 x (range pass + raycast)
+    assert R.launch_count() - n0 == 6  # 2 x (range pass + tile order + raycast)
     for v in (0, 255, 256, 299):
         s = R.render(w.poses[v:v + 1], K)
         for k in g:

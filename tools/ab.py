@@ -49,13 +49,14 @@ def run_one(args):
         R.set_profiling(False)
         kt = R.kernel_times()
         ms = kt["raycast_ms"] / kt["raycast_launches"]
+        pre_ms = kt["range_ms"] / max(kt["range_launches"], 1)  # range pass + tile order
         st = {}
         if not args.no_parity:
             ora = oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
             st = compare({k: v[0].cpu().numpy() for k, v in out.items()}, ora)
         print(json.dumps({"variant": args.name, "config": name, "l2": "warm" if args.no_flush else "flushed",
                           "options": args.set,
-                          "raycast_ms": round(ms, 4),
+                          "raycast_ms": round(ms, 4), "range_order_ms": round(pre_ms, 4),
                           "budget_used": st.get("budget_used"), "color_exact": st.get("color_exact"),
                           "depth_max": st.get("depth_max_err"), "hit_disagree": st.get("hit_disagree"),
                           "geom_bad": st.get("geom_out_of_tol")}), flush=True)

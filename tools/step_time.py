@@ -1,0 +1,42 @@
+"""Whole-step time of dtsdf_render_batch (range pass + tile order + raycast) with CUDA events around
+each call and the library's own tracing OFF (its per-kernel events would sit between the launches).
+
+    DTSDF_LIB=... python tools/step_time.py [--configs C1,C2] [--reps 200]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import scenes  # noqa: E402
+from paper_2301_12796_b200 import Renderer  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="C1,C2")
+ap.add_argument("--reps", type=int, default=200)
+ap.add_argument("--name", default=os.path.basename(os.environ.get("DTSDF_LIB", "libdtsdf.so")))
+args = ap.parse_args()
+R = Renderer(0)
+flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+for name in args.configs.split(","):
+    w = scenes.CONFIGS[name]()
+    R.upload_volume(w.volume)
+    poses = np.asarray(w.poses[:1], np.float32)
+    out = R.render(poses, w.intrinsics)
+    ts = []
+    for i in range(args.reps + 5):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        R.render_into(poses, w.intrinsics, out["depth"], out["normal"], out["color"], out["mask"])
+        b.record()
+        ts.append((a, b))
+    torch.cuda.synchronize()
+    ms = np.array([a.elapsed_time(b) for a, b in ts[5:]])
+    print(json.dumps({"lib": args.name, "config": name, "step_ms_mean": round(float(ms.mean()), 4),
+                      "step_ms_median": round(float(np.median(ms)), 4)}), flush=True)

@@ -9,7 +9,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["DTSDF_LIB"] = os.path.join(ROOT, "paper_2301_12796_b200", "libdtsdf_stats.so")
+os.environ.setdefault("DTSDF_LIB", os.path.join(ROOT, "paper_2301_12796_b200", "libdtsdf_stats.so"))
 import scenes  # noqa: E402
 from paper_2301_12796_b200 import Renderer, dtsdf  # noqa: E402
 
