@@ -25,8 +25,9 @@ namespace dtsdf {
 #ifndef DTSDF_CTA
 #define DTSDF_CTA 128  // 128-thread CTAs: 4% faster than 256 on C1 (smaller tail, profiles/r1c_sweep_cta.txt)
 #endif
-constexpr int kTileW = 16, kTileH = DTSDF_CTA / 16;  // CTA pixel tile
-static_assert(kTileW % kRangeTile == 0 && kTileH % kRangeTile == 0, "CTA tiles cover whole range tiles");
+// CTA pixel tile: 8x4-pixel warps, two across when the CTA has two or more warps
+constexpr int kTileW = DTSDF_CTA >= 64 ? 16 : 8, kTileH = DTSDF_CTA / kTileW;
+static_assert(DTSDF_CTA % 32 == 0 && DTSDF_CTA <= 256, "whole warps, at most 8 per CTA (ray_pix)");
 
 // Programmatic dependent launch: the range pass -> tile order -> raycast chain is launched with
 // programmatic stream serialisation, so each grid is set up while its predecessor runs; the
@@ -242,8 +243,9 @@ __device__ __forceinline__ int order_key(const OrderLaunch &p, int view, int t) 
   const int tx = t % p.ct_x, ty = t / p.ct_x;
   const size_t vo = (size_t)view * p.tiles_x * p.tiles_y;
   float c = 0.f, span = 0.f;
-  for (int ry = ty * (kTileH / kRangeTile); ry < min(p.tiles_y, (ty + 1) * (kTileH / kRangeTile)); ++ry)
-    for (int rx = tx * (kTileW / kRangeTile); rx < min(p.tiles_x, (tx + 1) * (kTileW / kRangeTile)); ++rx) {
+  // the range tiles overlapping the CTA tile (a CTA tile may be smaller than a range tile)
+  for (int ry = ty * kTileH / kRangeTile; ry <= min(p.tiles_y - 1, ((ty + 1) * kTileH - 1) / kRangeTile); ++ry)
+    for (int rx = tx * kTileW / kRangeTile; rx <= min(p.tiles_x - 1, ((tx + 1) * kTileW - 1) / kRangeTile); ++rx) {
       const size_t i = vo + ry * p.tiles_x + rx;
       c += (float)p.count[i];
       if (DTSDF_ORDER_PROXY) {
@@ -1218,17 +1220,22 @@ cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, 
 #ifndef DTSDF_RAYCAST_MINB
 #define DTSDF_RAYCAST_MINB (512 / DTSDF_CTA)  // 128 registers per thread (16 warps per SM)
 #endif
-// Copy `n` bytes of one staged output row from shared memory to global (device or mapped pinned
-// host) memory with the lanes [l0, l0 + nl) of a warp: 16-byte stores when both ends are aligned,
-// else bytes.  Whole rows of the CTA tile leave as contiguous full-width writes, which is what a
-// PCIe write to a mapped host buffer needs (strided 4-byte stores would split into 4-byte TLPs).
-__device__ __forceinline__ void copy_row(unsigned char *dst, const unsigned char *src, int n, int l, int nl) {
-  if (((reinterpret_cast<uintptr_t>(dst) | (uintptr_t)n) & 15) == 0) {
-    for (int i = l; i < (n >> 4); i += nl)
-      reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
-  } else {
-    for (int i = l; i < n; i += nl) dst[i] = src[i];
-  }
+// Copy `n` bytes of one staged output row from shared memory (16-B aligned) to global (device or
+// mapped pinned host) memory with the lanes of a warp, in the widest stores (16, 8, 4, 2 or 1 B) that
+// the destination alignment and n allow.  Whole rows of the CTA tile leave as contiguous writes,
+// which is what a PCIe write to a mapped host buffer needs (strided 4-byte stores would split into
+// 4-byte TLPs).
+template <typename T>
+__device__ __forceinline__ void copy_row_t(unsigned char *dst, const unsigned char *src, int n, int lane) {
+  for (int i = lane; i < n / (int)sizeof(T); i += 32)
+    reinterpret_cast<T *>(dst)[i] = reinterpret_cast<const T *>(src)[i];
+}
+__device__ __forceinline__ void copy_row(unsigned char *dst, const unsigned char *src, int n, int lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | (uintptr_t)n;
+  if ((a & 15) == 0) copy_row_t<uint4>(dst, src, n, lane);
+  else if ((a & 7) == 0) copy_row_t<uint2>(dst, src, n, lane);
+  else if ((a & 3) == 0) copy_row_t<unsigned int>(dst, src, n, lane);
+  else copy_row_t<unsigned char>(dst, src, n, lane);
 }
 
 
@@ -1240,7 +1247,8 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   __shared__ __align__(16) unsigned char s_color[kTileH][3 * kTileW];
   __shared__ __align__(16) unsigned char s_mask[kTileH][kTileW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tx = (warp & 1) * 8 + (lane & 7), ty = (warp >> 1) * 4 + (lane >> 3);
+  const int tx = (kTileW == 16 ? (warp & 1) * 8 : 0) + (lane & 7);
+  const int ty = (kTileW == 16 ? (warp >> 1) : warp) * 4 + (lane >> 3);
   griddep_wait();  // launched programmatically after the range pass / tile order: their outputs
   // CTA tile: in the view's tile order (longest predicted first, k_order) when there is one; its
   // origin is parked in shared memory for the epilogue instead of a register through the march
@@ -1296,8 +1304,7 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   __syncthreads();
   u0 = s_origin[0];
   v0 = s_origin[1];
-  // each warp writes kTileH / 4 rows: lanes 0-3 depth, 4-15 normal, 16-18 colour, 19 mask when the
-  // row is full width and aligned; otherwise each array of the row with all 32 lanes, bytewise
+  // each warp writes whole rows of the tile, array by array
   const int nu = min(kTileW, p.width - u0);
   for (int row = warp; row < kTileH; row += DTSDF_CTA / 32) {
     if (v0 + row >= rows) break;
@@ -1307,20 +1314,10 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
     unsigned char *d1 = p.out_normal ? reinterpret_cast<unsigned char *>(p.out_normal + 3 * pix) : nullptr;
     unsigned char *d2 = p.out_color ? p.out_color + 3 * pix : nullptr;
     unsigned char *d3 = p.out_mask ? p.out_mask + pix : nullptr;
-    const bool fast = nu == kTileW &&
-                      ((reinterpret_cast<uintptr_t>(d0) | reinterpret_cast<uintptr_t>(d1) |
-                        reinterpret_cast<uintptr_t>(d2) | reinterpret_cast<uintptr_t>(d3)) & 15) == 0;
-    if (fast) {
-      if (lane < 4) copy_row(d0, reinterpret_cast<const unsigned char *>(s_depth[row]), 64, lane, 4);
-      else if (lane < 16) { if (d1) copy_row(d1, reinterpret_cast<const unsigned char *>(s_normal[row]), 192, lane - 4, 12); }
-      else if (lane < 19) { if (d2) copy_row(d2, s_color[row], 48, lane - 16, 3); }
-      else if (lane == 19) { if (d3) copy_row(d3, s_mask[row], 16, 0, 1); }
-    } else {
-      copy_row(d0, reinterpret_cast<const unsigned char *>(s_depth[row]), 4 * nu, lane, 32);
-      if (d1) copy_row(d1, reinterpret_cast<const unsigned char *>(s_normal[row]), 12 * nu, lane, 32);
-      if (d2) copy_row(d2, s_color[row], 3 * nu, lane, 32);
-      if (d3) copy_row(d3, s_mask[row], nu, lane, 32);
-    }
+    copy_row(d0, reinterpret_cast<const unsigned char *>(s_depth[row]), 4 * nu, lane);
+    if (d1) copy_row(d1, reinterpret_cast<const unsigned char *>(s_normal[row]), 12 * nu, lane);
+    if (d2) copy_row(d2, s_color[row], 3 * nu, lane);
+    if (d3) copy_row(d3, s_mask[row], nu, lane);
   }
 }
 
