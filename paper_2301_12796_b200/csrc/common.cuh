@@ -182,6 +182,7 @@ __host__ __device__ __forceinline__ unsigned long long range_key_far(unsigned in
 cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
 // raycast CTA tiles (kTileW x kTileH pixels) of a width x rows image
 void raycast_tiles(int width, int rows, int *ct_x, int *ct_y);
+bool tile_order_fits(int width, int rows);  // the order kernel holds one key byte per CTA tile in shared memory
 // CTA tile order of each view from the range-pass counts (longest predicted first); clears the counts
 cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, const unsigned long long *z_far,
                          unsigned int epoch, float voxel_size, int *order, int tiles_x, int tiles_y, int width,

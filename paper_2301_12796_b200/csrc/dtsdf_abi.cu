@@ -484,7 +484,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     }
     c->order_cap = cts;
   }
-  const bool order = c->use_order && c->schedule == 0;
+  const bool order = c->use_order && c->schedule == 0 && tile_order_fits(W, rows);
   VolumeView V;
   V.table = c->table;
   V.table_mask = c->table_cap - 1;

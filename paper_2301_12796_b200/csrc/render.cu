@@ -259,8 +259,11 @@ __device__ __forceinline__ int order_key(const OrderLaunch &p, int view, int t) 
   return kOrderKeys - 1 - min(lg, kOrderKeys - 1);                   // ascending key = descending cost
 }
 
+constexpr int kOrderMaxTiles = 160 * 1024;  // CTA tiles per view whose keys fit the shared bytes below
+
 __global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLaunch p) {
   __shared__ unsigned int hist[kOrderKeys];
+  extern __shared__ unsigned char keys[];  // [n] the sort key of every CTA tile of the view
   griddep_launch_dependents();  // the raycast may be set up now; it waits for this grid to finish
   griddep_wait();               // the range pass's counts and keys
   const int view = blockIdx.x;
@@ -268,15 +271,20 @@ __global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLau
   int *ord = p.order + (size_t)view * p.ct_x * p.ct_y;
   const int n = p.ct_x * p.ct_y;
   if (threadIdx.x < kOrderKeys) hist[threadIdx.x] = 0;
+  // keys first, with independent loads (no sync intrinsics in this loop)
+#pragma unroll 4
+  for (int t = threadIdx.x; t < n; t += blockDim.x) keys[t] = (unsigned char)order_key(p, view, t);
   __syncthreads();
   // warp-aggregated shared atomics: the lanes of a warp holding the same key add once (most tiles
   // share a handful of keys, and per-lane atomics on one bucket serialise)
   const int n_round = (n + (int)blockDim.x - 1) / (int)blockDim.x * (int)blockDim.x;
   for (int t = threadIdx.x; t < n_round; t += blockDim.x) {
-    const int key = t < n ? order_key(p, view, t) : -1;
+    const int key = t < n ? keys[t] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     if (key >= 0 && (threadIdx.x & 31) == __ffs(same) - 1) atomicAdd(&hist[key], (unsigned)__popc(same));
   }
+  // the counts are read: clear them for the next pass
+  for (int i = threadIdx.x; i < p.tiles_x * p.tiles_y; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   if (threadIdx.x < 32) {  // exclusive scan of the 64 bucket sizes (two per lane)
     const unsigned int a = hist[2 * threadIdx.x], b = hist[2 * threadIdx.x + 1];
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLau
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n_round; t += blockDim.x) {
-    const int key = t < n ? order_key(p, view, t) : -1;
+    const int key = t < n ? keys[t] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     const int lane = threadIdx.x & 31, leader = __ffs(same) - 1;
     unsigned base = 0;
@@ -304,8 +312,6 @@ __global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLau
       ord[pos] = t;
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < p.tiles_x * p.tiles_y; i += blockDim.x) cnt[i] = 0;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1194,6 +1200,12 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+bool tile_order_fits(int width, int rows) {
+  int cx = 0, cy = 0;
+  raycast_tiles(width, rows, &cx, &cy);
+  return (long long)cx * cy <= kOrderMaxTiles;
+}
+
 void raycast_tiles(int width, int rows, int *ct_x, int *ct_y) {
   *ct_x = (width + kTileW - 1) / kTileW;
   *ct_y = (rows + kTileH - 1) / kTileH;
@@ -1209,7 +1221,22 @@ cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, 
   raycast_tiles(width, rows, &p.ct_x, &p.ct_y);
   p.epoch = epoch;
   p.inv_voxel = 1.0f / voxel_size;
-  return launch_pdl(k_order, dim3((unsigned)n_views), dim3(1024), s, p);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_order, cudaFuncAttributeMaxDynamicSharedMemorySize, kOrderMaxTiles);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)n_views);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = (size_t)p.ct_x * p.ct_y;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_order, p);
   return cudaGetLastError();
 }
 
