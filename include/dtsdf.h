@@ -329,10 +329,12 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *                         host-link transfer with the ray march; 0 renders into device scratch and
  *                         copies back after the kernel.  Pageable host outputs always take the copy path. */
 #define DTSDF_OPT_HOST_WRITE 7
-/*   DTSDF_OPT_TILE_ORDER  1 (default) the raycast runs its 16x8-pixel CTA tiles longest-predicted-first
- *                         (the range pass counts the block locations covering each tile; a counting sort
+/*   DTSDF_OPT_TILE_ORDER  1 (default) automatic: for launches of up to 65536 CTA tiles (one 640x480 view is
+ *                         2400) the raycast runs its 16x8-pixel CTA tiles longest-predicted-first (the
+ *                         range pass counts the block locations covering each tile; a counting sort
  *                         orders them), so the slow tiles do not start last and stretch the kernel's
- *                         drain; 0 row-major.  Changes only when a tile runs, never what it computes. */
+ *                         drain; longer batches stay row-major.  2 always, 0 never.  Changes only when a
+ *                         tile runs, never what it computes. */
 #define DTSDF_OPT_TILE_ORDER 9
 DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
 

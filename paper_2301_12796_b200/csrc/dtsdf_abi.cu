@@ -451,6 +451,8 @@ int dtsdf_upload_volume(dtsdf_ctx *c, const dtsdf_volume_params *p, const int32_
   return dtsdf_commit_volume(c, nullptr);
 }
 
+constexpr long long kOrderAutoMaxCtas = 65536;  // DTSDF_OPT_TILE_ORDER 1: CTA tiles per launch up to which the order is used
+
 static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const dtsdf_intrinsics *K, int32_t row0,
                        int32_t row1, float *depth, float *normal, uint8_t *color, uint8_t *mask, cudaStream_t s,
                        bool comb, bool staged = false) {
@@ -484,7 +486,10 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     }
     c->order_cap = cts;
   }
-  const bool order = c->use_order && c->schedule == 0 && tile_order_fits(W, rows);
+  // the order pays most when the launch is a few waves of CTAs (one view: C1 -12 %); by 256-view
+  // batches the drain is amortised and it is neutral (profiles/r1f_sweep_tile_order.jsonl)
+  const bool order = c->schedule == 0 && tile_order_fits(W, rows) &&
+                     (c->use_order == 2 || (c->use_order == 1 && cts <= (size_t)kOrderAutoMaxCtas));
   VolumeView V;
   V.table = c->table;
   V.table_mask = c->table_cap - 1;
@@ -1237,7 +1242,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;
   else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
   else if (option == DTSDF_OPT_CELL_DIRS) c->use_live = value ? 1 : 0;
-  else if (option == DTSDF_OPT_TILE_ORDER) c->use_order = value ? 1 : 0;
+  else if (option == DTSDF_OPT_TILE_ORDER && value >= 0 && value <= 2) c->use_order = value;
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

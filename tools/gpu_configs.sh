@@ -13,3 +13,4 @@ run c1_combined $B --mode combined --steps 200 --warmup 10 --e2e-steps 20
 run c3_combined $B --config C3 --views 256 --mode combined --steps 5 --warmup 3 --e2e-steps 2
 timeout 1200 python -m pytest tests/test_gpu_large.py -x -q -s > $OUT/cfg_${TAG}_c4_pytest.log 2>&1; echo "c4 parity rc=$?"; tail -4 $OUT/cfg_${TAG}_c4_pytest.log
 run c4_views64 $B --config C4 --views 64 --steps 10 --warmup 3 --e2e-steps 3
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29513 bench.py --gpus 1 --steps 50 --warmup 3 --dist --no-cpu-baseline --e2e-steps 5 > $OUT/cfg_${TAG}_torchrun_dist.log 2>&1; echo "torchrun dist rc=$?"; tail -1 $OUT/cfg_${TAG}_torchrun_dist.log | cut -c1-200
