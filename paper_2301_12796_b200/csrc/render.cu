@@ -261,7 +261,10 @@ __device__ __forceinline__ int order_key(const OrderLaunch &p, int view, int t) 
 
 constexpr int kOrderMaxTiles = 160 * 1024;  // CTA tiles per view whose keys fit the shared bytes below
 
-__global__ void __launch_bounds__(1024) k_order(const __grid_constant__ OrderLaunch p) {
+#ifndef DTSDF_ORDER_THREADS
+#define DTSDF_ORDER_THREADS 1024
+#endif
+__global__ void __launch_bounds__(DTSDF_ORDER_THREADS) k_order(const __grid_constant__ OrderLaunch p) {
   __shared__ unsigned int hist[kOrderKeys];
   extern __shared__ unsigned char keys[];  // [n] the sort key of every CTA tile of the view
   griddep_launch_dependents();  // the raycast may be set up now; it waits for this grid to finish
@@ -368,6 +371,10 @@ struct SampleResult {
 #define DTSDF_FAST_NORM 1    // rsqrt gradient normalisation, approximate F / S and regula-falsi quotient: one
                              // MUFU op each instead of the IEEE sequences with their special-case branches
                              // (C1 -6 %, C2 -8 %; fp32 rounding differences only, profiles/r1f_sweep_fast_norm.jsonl)
+#endif
+#ifndef DTSDF_PREFETCH
+#define DTSDF_PREFETCH 0     // 1: prefetch the next march point's brick rows into L1 (measured slower,
+                             // profiles/r1f_sweep_prefetch.jsonl)
 #endif
 #ifndef DTSDF_LAZY
 #define DTSDF_LAZY 0         // gradient-free sign class for march samples
@@ -872,6 +879,31 @@ struct RayT {
   }
   __device__ __forceinline__ float block_exit(const VolumeView &V) const { return box_exit(V, 0); }
 
+#if DTSDF_PREFETCH
+  // Prefetch into L1 the brick rows the next lattice point's evaluation will read (the 4 corner rows
+  // and the 4 outer stencil rows of each present direction), if it stays in the cursor's location,
+  // so that its loads hit while this warp is away.
+  __device__ __forceinline__ void prefetch_next(const VolumeView &V) const {
+    const float tn = (float)k * V.delta;
+    const int jx = ibx + (int)floorf(fmaf(tn, rsx, g0x)), jy = iby + (int)floorf(fmaf(tn, rsy, g0y)),
+              jz = ibz + (int)floorf(fmaf(tn, rsz, g0z));
+    if ((jx >> 3) != cur.bx || (jy >> 3) != cur.by || (jz >> 3) != cur.bz) return;
+    const int off = (jx & 7) + kApron * (jy & 7) + kApron * kApron * (jz & 7);
+    int pr = cur.present;
+#pragma unroll 1
+    while (pr) {
+      const int D = __ffs(pr) - 1;
+      pr &= pr - 1;
+      const float2 *br = V.apron + (size_t)pick6(cur.slots, D) * kApronStride + off;
+      const float2 *rows[8] = {br + APRON_IDX(0, 0, 0), br + APRON_IDX(0, 1, 0), br + APRON_IDX(0, 0, 1),
+                               br + APRON_IDX(0, 1, 1), br + APRON_IDX(0, -1, 0), br + APRON_IDX(0, 2, 0),
+                               br + APRON_IDX(0, 0, -1), br + APRON_IDX(0, 0, 2)};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(rows[q]));
+    }
+  }
+#endif
+
   // a6: bracket [t_{k-1}, t_k] with F(t_{k-1}) = f_prev > 0 and F(t_k) = f_k <= 0
   __device__ __forceinline__ void begin_bracket(const RenderLaunch &p, float f_prev, float f_k) {
     const VolumeView &V = p.vol;
@@ -1078,6 +1110,9 @@ struct RayT {
           prev_unk = s.unk;
           prev_f = s.f;
           ++k;
+#if DTSDF_PREFETCH
+          if constexpr (!kComb) prefetch_next(V);
+#endif
           return false;
         }
         if (prev_unk) {  // sample k ends a crossing iff the unresolved t_{k-1} is valid: evaluate it
@@ -1251,7 +1286,7 @@ cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)n_views);
-  cfg.blockDim = dim3(1024);
+  cfg.blockDim = dim3(DTSDF_ORDER_THREADS);
   cfg.dynamicSmemBytes = (size_t)p.ct_x * p.ct_y;
   cfg.stream = s;
   cudaLaunchAttribute la[1];
