@@ -376,6 +376,11 @@ struct SampleResult {
 #define DTSDF_PREFETCH 0     // 1: prefetch the next march point's brick rows into L1 (measured slower,
                              // profiles/r1f_sweep_prefetch.jsonl)
 #endif
+#ifndef DTSDF_EARLY_LOADS
+#define DTSDF_EARLY_LOADS 0  // 1: the 24 outer stencil loads as volatile loads, issued with the 8 corner loads
+                             // before the direction's NaN / weight test (ptxas otherwise sinks them past it);
+                             // measured equal (profiles/r1f_sweep_prefetch.jsonl), so left to the compiler
+#endif
 #ifndef DTSDF_LAZY
 #define DTSDF_LAZY 0         // gradient-free sign class for march samples
 #endif
@@ -396,6 +401,16 @@ struct ShadeResult {
   float S;
   int mask;
 };
+
+__device__ __forceinline__ float ldg_stencil(const float *ptr) {
+#if DTSDF_EARLY_LOADS
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
+  return v;
+#else
+  return __ldg(ptr);
+#endif
+}
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 // a + t (b - a) on a pair: two packed FFMA2 (a - t a, then + t b)
@@ -511,18 +526,18 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
     const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
     const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
-    const float xm00 = __ldg(&br[APRON_IDX(-1, 0, 0)].x), xm10 = __ldg(&br[APRON_IDX(-1, 1, 0)].x);
-    const float xm01 = __ldg(&br[APRON_IDX(-1, 0, 1)].x), xm11 = __ldg(&br[APRON_IDX(-1, 1, 1)].x);
-    const float xp00 = __ldg(&br[APRON_IDX(2, 0, 0)].x), xp10 = __ldg(&br[APRON_IDX(2, 1, 0)].x);
-    const float xp01 = __ldg(&br[APRON_IDX(2, 0, 1)].x), xp11 = __ldg(&br[APRON_IDX(2, 1, 1)].x);
-    const float ym00 = __ldg(&br[APRON_IDX(0, -1, 0)].x), ym10 = __ldg(&br[APRON_IDX(1, -1, 0)].x);
-    const float ym01 = __ldg(&br[APRON_IDX(0, -1, 1)].x), ym11 = __ldg(&br[APRON_IDX(1, -1, 1)].x);
-    const float yp00 = __ldg(&br[APRON_IDX(0, 2, 0)].x), yp10 = __ldg(&br[APRON_IDX(1, 2, 0)].x);
-    const float yp01 = __ldg(&br[APRON_IDX(0, 2, 1)].x), yp11 = __ldg(&br[APRON_IDX(1, 2, 1)].x);
-    const float zm00 = __ldg(&br[APRON_IDX(0, 0, -1)].x), zm10 = __ldg(&br[APRON_IDX(1, 0, -1)].x);
-    const float zm01 = __ldg(&br[APRON_IDX(0, 1, -1)].x), zm11 = __ldg(&br[APRON_IDX(1, 1, -1)].x);
-    const float zp00 = __ldg(&br[APRON_IDX(0, 0, 2)].x), zp10 = __ldg(&br[APRON_IDX(1, 0, 2)].x);
-    const float zp01 = __ldg(&br[APRON_IDX(0, 1, 2)].x), zp11 = __ldg(&br[APRON_IDX(1, 1, 2)].x);
+    const float xm00 = ldg_stencil(&br[APRON_IDX(-1, 0, 0)].x), xm10 = ldg_stencil(&br[APRON_IDX(-1, 1, 0)].x);
+    const float xm01 = ldg_stencil(&br[APRON_IDX(-1, 0, 1)].x), xm11 = ldg_stencil(&br[APRON_IDX(-1, 1, 1)].x);
+    const float xp00 = ldg_stencil(&br[APRON_IDX(2, 0, 0)].x), xp10 = ldg_stencil(&br[APRON_IDX(2, 1, 0)].x);
+    const float xp01 = ldg_stencil(&br[APRON_IDX(2, 0, 1)].x), xp11 = ldg_stencil(&br[APRON_IDX(2, 1, 1)].x);
+    const float ym00 = ldg_stencil(&br[APRON_IDX(0, -1, 0)].x), ym10 = ldg_stencil(&br[APRON_IDX(1, -1, 0)].x);
+    const float ym01 = ldg_stencil(&br[APRON_IDX(0, -1, 1)].x), ym11 = ldg_stencil(&br[APRON_IDX(1, -1, 1)].x);
+    const float yp00 = ldg_stencil(&br[APRON_IDX(0, 2, 0)].x), yp10 = ldg_stencil(&br[APRON_IDX(1, 2, 0)].x);
+    const float yp01 = ldg_stencil(&br[APRON_IDX(0, 2, 1)].x), yp11 = ldg_stencil(&br[APRON_IDX(1, 2, 1)].x);
+    const float zm00 = ldg_stencil(&br[APRON_IDX(0, 0, -1)].x), zm10 = ldg_stencil(&br[APRON_IDX(1, 0, -1)].x);
+    const float zm01 = ldg_stencil(&br[APRON_IDX(0, 1, -1)].x), zm11 = ldg_stencil(&br[APRON_IDX(1, 1, -1)].x);
+    const float zp00 = ldg_stencil(&br[APRON_IDX(0, 0, 2)].x), zp10 = ldg_stencil(&br[APRON_IDX(1, 0, 2)].x);
+    const float zp01 = ldg_stencil(&br[APRON_IDX(0, 1, 2)].x), zp11 = ldg_stencil(&br[APRON_IDX(1, 1, 2)].x);
     // The lerps run pairwise on Blackwell's packed fp32x2 FMA (FFMA2): {sdf, weight} of the
     // corners, and pairs of independent stencil layers.
     // O3(a) trilinear phi_D, omega_D over the 8 cell corners (x: rows e_yz, y: slabs R(dz), z)
