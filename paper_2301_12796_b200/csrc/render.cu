@@ -381,6 +381,11 @@ struct SampleResult {
                              // before the direction's NaN / weight test (ptxas otherwise sinks them past it);
                              // measured equal (profiles/r1f_sweep_prefetch.jsonl), so left to the compiler
 #endif
+#ifndef DTSDF_SLOTS_FROM_TABLE
+#define DTSDF_SLOTS_FROM_TABLE 1  // direction slots re-read from the hash entry (an L1 hit) per evaluated
+                                  // direction instead of six registers through the march: with them the
+                                  // kernel fits 96 registers (5 CTAs / 20 warps per SM), profiles/r1f_sweep_regs.jsonl
+#endif
 #ifndef DTSDF_LAZY
 #define DTSDF_LAZY 0         // gradient-free sign class for march samples
 #endif
@@ -437,7 +442,11 @@ struct Cursor {
   int present;   // bit D: direction D has a brick at this location
   int entry;     // hash entry index (row of cell_pos), -1 if unallocated
   int dist;      // unallocated: empty-space distance in blocks (>= 1); 0 = outside the AABB
+#if DTSDF_SLOTS_FROM_TABLE
+  int slot0;     // combined path: the location's combined slot (the direction slots stay in the table)
+#else
   int slots[6];
+#endif
 };
 
 // cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (k_cell_pos)
@@ -464,6 +473,16 @@ __device__ __forceinline__ int pick6(const int s[6], int d) {
   return v;
 }
 
+// brick slot of direction D at the cursor's location: from the cursor's registers, or re-read from
+// the location's hash entry (an L1 hit) so that the six slots need no registers through the march
+__device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, int D) {
+#if DTSDF_SLOTS_FROM_TABLE
+  return __ldg(&V.table[cur.entry].slot[D]);
+#else
+  return pick6(cur.slots, D);
+#endif
+}
+
 // F(x, r) of DESIGN.md §2 O3 for the sample at base voxel (block-local l, fractions f) of the
 // current cursor location; with shade = true also the shading sums of O7.  One instance of this
 // body is compiled (runtime direction loop) to keep the kernel inside the instruction cache.
@@ -482,7 +501,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     while (pr) {
       const int D = __ffs(pr) - 1;
       pr &= pr - 1;
-      const float2 *br = V.apron + (size_t)pick6(cur.slots, D) * kApronStride + off;
+      const float2 *br = V.apron + (size_t)dir_slot(V, cur, D) * kApronStride + off;
       const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
       const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
       const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
@@ -517,7 +536,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
   while (present) {
     const int D = __ffs(present) - 1;
     present &= present - 1;
-    const int slot = pick6(cur.slots, D);
+    const int slot = dir_slot(V, cur, D);
     DTSDF_CHECK(slot >= 0 && slot < V.n_blocks && lx >= 0 && lx < 8 && ly >= 0 && ly < 8 && lz >= 0 && lz < 8);
     const float2 *br = V.apron + (size_t)slot * kApronStride + off;
     // all 32 stencil voxels are issued before any test (one load round per direction; the
@@ -734,15 +753,23 @@ constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certai
 
 // per-thread pixel of the ray (u | vrel << 16), read back only when a bracket starts and at the end
 __shared__ int ray_pix[256];
+__shared__ int ray_view[256];
 
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
 // a warp -- whatever phase each is in -- run the evaluation code together.
 template <bool kComb>
 struct RayT {
-  int view;  // the pixel (u | vrel << 16) waits in shared memory (ray_pix): no register through the march
+  // the view and the pixel (u | vrel << 16) wait in shared memory (ray_view, ray_pix): no registers
+  // through the march
   __device__ __forceinline__ int pix() const { return ray_pix[threadIdx.x]; }
-  float r[3], o[3], ir[3], iLf;
+  __device__ __forceinline__ int view() const { return ray_view[threadIdx.x]; }
+#if DTSDF_SLOTS_FROM_TABLE
+  __device__ __forceinline__ int comb_slot() const { return cur.slot0; }
+#else
+  __device__ __forceinline__ int comb_slot() const { return cur.slots[0]; }
+#endif
+  float r[3], o[3], ir[3];
   int k, k1;
   // sample positions in voxel units g = g0 + t * rs relative to the integer cell ib of a frame:
   // the world origin during the march; re-anchored once per bracket in fp64 at x(t_{k-1}), so g
@@ -766,7 +793,8 @@ struct RayT {
 #endif
 
   __device__ __forceinline__ void init(const RenderLaunch &p, int view_, int u_, int vrel_) {
-    view = view_;
+    ray_view[threadIdx.x] = view_;
+    const int view = view_;
     ray_pix[threadIdx.x] = u_ | (vrel_ << 16);
     const int u = u_, vrel = vrel_;
     const VolumeView &V = p.vol;
@@ -775,7 +803,7 @@ struct RayT {
     // O1 ray (eq:reprojection)
     const float dxf = (u - p.cx) / p.fx, dyf = (v - p.cy) / p.fy;
     const float Lf = sqrtf(dxf * dxf + dyf * dyf + 1.0f);
-    iLf = 1.0f / Lf;
+    const float iLf = 1.0f / Lf;
     for (int q = 0; q < 3; ++q) {
       r[q] = (P.r[3 * q] * dxf + P.r[3 * q + 1] * dyf + P.r[3 * q + 2]) * iLf;
       o[q] = P.t[q];
@@ -804,7 +832,11 @@ struct RayT {
     cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
     cur.dist = 1;
 #pragma unroll
+#if DTSDF_SLOTS_FROM_TABLE
+    cur.slot0 = -1;
+#else
     for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
+#endif
     mode = kMarch;
     prev_valid = false;
     prev_unk = false;
@@ -848,18 +880,34 @@ struct RayT {
           const int4 ea = __ldg(e), eb = __ldg(e + 1);
           DTSDF_CHECK(ea.z < V.n_blocks && ea.w < V.n_blocks && eb.x < V.n_blocks && eb.y < V.n_blocks &&
                       eb.z < V.n_blocks && eb.w < V.n_blocks);
+#if DTSDF_SLOTS_FROM_TABLE
+          cur.present = (ea.z >= 0) | (ea.w >= 0) << 1 | (eb.x >= 0) << 2 | (eb.y >= 0) << 3 | (eb.z >= 0) << 4 |
+                        (eb.w >= 0) << 5;
+#else
           cur.slots[0] = ea.z; cur.slots[1] = ea.w; cur.slots[2] = eb.x;
           cur.slots[3] = eb.y; cur.slots[4] = eb.z; cur.slots[5] = eb.w;
+#endif
         }
       } else {  // a2 via occupancy bitmaps + hash probe
         cur.dist = 1;
         cur.occ = occupied(V, bx, by, bz, &cur.surf);
+#if DTSDF_SLOTS_FROM_TABLE
+        if (cur.occ) {
+          int sl[6];
+          cur.entry = lookup_slots(V, bx, by, bz, sl);
+#pragma unroll
+          for (int d = 0; d < 6; ++d) cur.present |= (sl[d] >= 0) << d;
+        }
+#else
         if (cur.occ) cur.entry = lookup_slots(V, bx, by, bz, cur.slots);
+#endif
       }
+#if !DTSDF_SLOTS_FROM_TABLE
       if (cur.occ) {
 #pragma unroll
         for (int d = 0; d < 6; ++d) cur.present |= (cur.slots[d] >= 0) << d;
       }
+#endif
       if constexpr (kComb) {  // NEXT-1: the location's combined brick (entry -> combined slot)
         if (cur.occ) {
           DTSDF_CHECK(cur.entry >= 0 && cur.entry < V.table_cap);
@@ -869,7 +917,11 @@ struct RayT {
             cur.entry = cs;
             cur.surf = __ldg(&C.surf[cs]) != 0;
             cur.present = 1;
+#if DTSDF_SLOTS_FROM_TABLE
+            cur.slot0 = cs;
+#else
             cur.slots[0] = cs;
+#endif
           } else {  // allocated but not combined: invalid like an unallocated location
             cur.occ = false;
             cur.dist = 1;
@@ -909,7 +961,7 @@ struct RayT {
     while (pr) {
       const int D = __ffs(pr) - 1;
       pr &= pr - 1;
-      const float2 *br = V.apron + (size_t)pick6(cur.slots, D) * kApronStride + off;
+      const float2 *br = V.apron + (size_t)dir_slot(V, cur, D) * kApronStride + off;
       const float2 *rows[8] = {br + APRON_IDX(0, 0, 0), br + APRON_IDX(0, 1, 0), br + APRON_IDX(0, 0, 1),
                                br + APRON_IDX(0, 1, 1), br + APRON_IDX(0, -1, 0), br + APRON_IDX(0, 2, 0),
                                br + APRON_IDX(0, 0, -1), br + APRON_IDX(0, 0, 2)};
@@ -924,7 +976,7 @@ struct RayT {
     const VolumeView &V = p.vol;
     // re-anchor the position frame at x(t_{k-1}) in fp64
     {
-      const ViewPose &P = p.pose[view];
+      const ViewPose &P = p.pose[view()];
       const int px = pix();
       const double ddx = ((double)(px & 0xffff) - (double)p.cx) / (double)p.fx;
       const double ddy = ((double)(p.row0 + (px >> 16)) - (double)p.cy) / (double)p.fy;
@@ -1102,7 +1154,7 @@ struct RayT {
 #endif
     if (cur.occ) {
       if constexpr (kComb)
-        s = eval_comb<false>(V, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, nullptr);
+        s = eval_comb<false>(V, p.comb, comb_slot(), ix & 7, iy & 7, iz & 7, frx, fry, frz, nullptr);
       else
         s = eval_sample<false>(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], nullptr,
                                mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect), live);
@@ -1200,7 +1252,7 @@ struct RayT {
     sh.mask = 0;
     if (cur.occ) {
       if constexpr (kComb)
-        eval_comb<true>(p.vol, p.comb, cur.slots[0], ix & 7, iy & 7, iz & 7, frx, fry, frz, &sh);
+        eval_comb<true>(p.vol, p.comb, comb_slot(), ix & 7, iy & 7, iz & 7, frx, fry, frz, &sh);
       else
         eval_sample<true>(p.vol, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], &sh, false);
     }
@@ -1213,6 +1265,10 @@ struct RayT {
     col[0] = col[1] = col[2] = 0;
     mask = 0;
     if (hit) {
+      // 1 / |d~| of the ray, recomputed with init's operations (the same bits)
+      const int u = pix() & 0xffff, v = p.row0 + (pix() >> 16);
+      const float dxf = (u - p.cx) / p.fx, dyf = (v - p.cy) / p.fy;
+      const float iLf = 1.0f / sqrtf(dxf * dxf + dyf * dyf + 1.0f);
       depth = ((float)(k - 1) * p.vol.delta + b) * iLf;
       const float nn = sqrtf(sh.n[0] * sh.n[0] + sh.n[1] * sh.n[1] + sh.n[2] * sh.n[2]);
       const float inn = nn > 0.f ? 1.0f / nn : 0.f;
@@ -1225,7 +1281,7 @@ struct RayT {
     }
 #ifdef DTSDF_STATS
     if (p.dbg_timeline) {
-      const size_t pid = ((size_t)view * (p.row1 - p.row0) + (pix() >> 16)) * p.width + (pix() & 0xffff);
+      const size_t pid = ((size_t)view() * (p.row1 - p.row0) + (pix() >> 16)) * p.width + (pix() & 0xffff);
       p.dbg_timeline[3 * pid + 0] = g_start;
       p.dbg_timeline[3 * pid + 1] = g_end;
       p.dbg_timeline[3 * pid + 2] = smid;
@@ -1244,8 +1300,8 @@ struct RayT {
     int col[3], mask;
     result(p, depth, nrm, col, mask);
     const int u = pix() & 0xffff, vrel = pix() >> 16;
-    const size_t px = ((size_t)view * (p.row1 - p.row0) + vrel) * p.width + u;
-    DTSDF_CHECK(view < p.n_views && vrel >= 0 && vrel < p.row1 - p.row0 && u >= 0 && u < p.width);
+    const size_t px = ((size_t)view() * (p.row1 - p.row0) + vrel) * p.width + u;
+    DTSDF_CHECK(view() < p.n_views && vrel >= 0 && vrel < p.row1 - p.row0 && u >= 0 && u < p.width);
     p.out_depth[px] = depth;
     if (p.out_normal) {
       p.out_normal[3 * px + 0] = nrm[0];
@@ -1318,7 +1374,8 @@ cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, 
 #define DTSDF_CARVEOUT -1  // >= 0: preferred shared-memory carveout (percent) of k_raycast; -1 driver default
 #endif
 #ifndef DTSDF_RAYCAST_MINB
-#define DTSDF_RAYCAST_MINB (512 / DTSDF_CTA)  // 128 registers per thread (16 warps per SM)
+#define DTSDF_RAYCAST_MINB (640 / DTSDF_CTA)  // 96 registers per thread: 20 warps per SM (128 was 16 warps:
+                                              // 4-6 % slower, profiles/r1f_sweep_regs.jsonl)
 #endif
 // Copy `n` bytes of one staged output row from shared memory (16-B aligned) to global (device or
 // mapped pinned host) memory with the lanes of a warp, in the widest stores (16, 8, 4, 2 or 1 B) that
