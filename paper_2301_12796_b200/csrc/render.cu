@@ -754,6 +754,12 @@ constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certai
 // per-thread pixel of the ray (u | vrel << 16), read back only when a bracket starts and at the end
 __shared__ int ray_pix[256];
 __shared__ int ray_view[256];
+#ifndef DTSDF_SMEM_COLD
+#define DTSDF_SMEM_COLD 0  // 1: camera centre, 1/r and the last lattice index in shared memory (more spills: off)
+#endif
+#if DTSDF_SMEM_COLD
+__shared__ float ray_cold[7][256];  // per thread: camera centre (3), 1 / ray direction (3), last lattice index
+#endif
 
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
@@ -762,15 +768,29 @@ template <bool kComb>
 struct RayT {
   // the view and the pixel (u | vrel << 16) wait in shared memory (ray_view, ray_pix): no registers
   // through the march
-  __device__ __forceinline__ int pix() const { return ray_pix[threadIdx.x]; }
-  __device__ __forceinline__ int view() const { return ray_view[threadIdx.x]; }
+  __device__ __forceinline__ int pix() const { return ((volatile int *)ray_pix)[threadIdx.x]; }
+  __device__ __forceinline__ int view() const { return ((volatile int *)ray_view)[threadIdx.x]; }
 #if DTSDF_SLOTS_FROM_TABLE
   __device__ __forceinline__ int comb_slot() const { return cur.slot0; }
 #else
   __device__ __forceinline__ int comb_slot() const { return cur.slots[0]; }
 #endif
-  float r[3], o[3], ir[3];
-  int k, k1;
+  float r[3];
+#if DTSDF_SMEM_COLD
+  // camera centre, 1 / ray direction and the last lattice index: read by the empty-space skips only,
+  // kept in shared memory (ray_cold) rather than registers through the march
+  // (volatile: re-read at each use, not hoisted out of the march loop into registers)
+  __device__ __forceinline__ float O(int q) const { return ((volatile float *)ray_cold[q])[threadIdx.x]; }
+  __device__ __forceinline__ float IR(int q) const { return ((volatile float *)ray_cold[3 + q])[threadIdx.x]; }
+  __device__ __forceinline__ int K1() const { return __float_as_int(((volatile float *)ray_cold[6])[threadIdx.x]); }
+#else
+  float o[3], ir[3];
+  int k1;
+  __device__ __forceinline__ float O(int q) const { return o[q]; }
+  __device__ __forceinline__ float IR(int q) const { return ir[q]; }
+  __device__ __forceinline__ int K1() const { return k1; }
+#endif
+  int k;
   // sample positions in voxel units g = g0 + t * rs relative to the integer cell ib of a frame:
   // the world origin during the march; re-anchored once per bracket in fp64 at x(t_{k-1}), so g
   // stays within two voxels of it and fp32 resolves the shading point to ~1e-9 m (reading R32) --
@@ -806,8 +826,13 @@ struct RayT {
     const float iLf = 1.0f / Lf;
     for (int q = 0; q < 3; ++q) {
       r[q] = (P.r[3 * q] * dxf + P.r[3 * q + 1] * dyf + P.r[3 * q + 2]) * iLf;
+#if DTSDF_SMEM_COLD
+      ray_cold[q][threadIdx.x] = P.t[q];
+      ray_cold[3 + q][threadIdx.x] = 1.0f / r[q];
+#else
       o[q] = P.t[q];
       ir[q] = 1.0f / r[q];
+#endif
     }
     // O2 lattice bounds, narrowed to the tile's block range (a3)
     const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
@@ -817,17 +842,22 @@ struct RayT {
     const float zn = covered ? __uint_as_float((unsigned)kn) : 1.0f, zf = covered ? __uint_as_float((unsigned)kf) : 0.0f;
     const int kmin = (int)ceilf(p.z_min * Lf * V.inv_delta), kmax = (int)floorf(p.z_max * Lf * V.inv_delta);
     k = kmin;
-    k1 = kmax;
+    int kl = kmax;
     if (p.use_range) {
       if (zn <= zf) {
         k = max(kmin, (int)floorf(zn * (1.0f - 1e-4f) * Lf * V.inv_delta));
-        k1 = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * Lf * V.inv_delta) + 1);
+        kl = min(kmax, (int)ceilf(zf * (1.0f + 1e-4f) * Lf * V.inv_delta) + 1);
       } else {
-        k1 = k - 1;  // no allocated block projects onto this tile
+        kl = k - 1;  // no allocated block projects onto this tile
       }
     }
+#if DTSDF_SMEM_COLD
+    ray_cold[6][threadIdx.x] = __int_as_float(kl);
+#else
+    k1 = kl;
+#endif
     ibx = iby = ibz = 0;
-    g0x = o[0] * V.inv_voxel; g0y = o[1] * V.inv_voxel; g0z = o[2] * V.inv_voxel;
+    g0x = P.t[0] * V.inv_voxel; g0y = P.t[1] * V.inv_voxel; g0z = P.t[2] * V.inv_voxel;
     rsx = r[0] * V.inv_voxel; rsy = r[1] * V.inv_voxel; rsz = r[2] * V.inv_voxel;
     cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
     cur.dist = 1;
@@ -939,8 +969,8 @@ struct RayT {
     float texit = 3.0e38f;
     const int bb[3] = {cur.bx, cur.by, cur.bz};
     for (int q = 0; q < 3; ++q) {
-      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + rad) * bsz - o[q]) * ir[q]);
-      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - rad) * bsz - o[q]) * ir[q]);
+      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + rad) * bsz - O(q)) * IR(q));
+      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - rad) * bsz - O(q)) * IR(q));
     }
     return texit;
   }
@@ -1023,7 +1053,7 @@ struct RayT {
 #endif
       for (;;) {
         live = -1;
-        if (k > k1) return true;  // no crossing: a miss
+        if (k > K1()) return true;  // no crossing: a miss
 #if DTSDF_ADV_BUDGET > 0
         // bounded advance per step: a lane with a long skip sits out this step's evaluation
         // (its warp evaluates without it) and goes on advancing in the next
@@ -1050,9 +1080,9 @@ struct RayT {
               float t0 = -3.0e38f, t1 = 3.0e38f;
               const int lo3[3] = {V.lo_x, V.lo_y, V.lo_z}, dm3[3] = {V.dim_x, V.dim_y, V.dim_z};
               for (int q = 0; q < 3; ++q) {
-                const float lo = lo3[q] * bsz - o[q], hi = (lo3[q] + dm3[q]) * bsz - o[q];
+                const float lo = lo3[q] * bsz - O(q), hi = (lo3[q] + dm3[q]) * bsz - O(q);
                 if (r[q] != 0.f) {
-                  const float ta = lo * ir[q], tb = hi * ir[q];
+                  const float ta = lo * IR(q), tb = hi * IR(q);
                   t0 = fmaxf(t0, fminf(ta, tb));
                   t1 = fminf(t1, fmaxf(ta, tb));
                 } else if (lo > 0.f || hi < 0.f) {
@@ -1060,12 +1090,12 @@ struct RayT {
                 }
               }
               texit = (t0 <= t1 && t1 > t) ? fmaxf(t0, t) : 3.0e38f;
-              if (texit >= 3.0e38f) { k = k1 + 1; continue; }
+              if (texit >= 3.0e38f) { k = K1() + 1; continue; }
             } else {
               texit = box_exit(V, cur.dist - 1);
             }
             const float kn = floorf(texit * V.inv_delta);
-            k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);
+            k = (kn > (float)K1()) ? K1() + 1 : max(k + 1, (int)kn);
           } else {
             ++k;
           }
@@ -1079,7 +1109,7 @@ struct RayT {
 #ifdef DTSDF_STATS
             ++st_jump;
 #endif
-            k = (kj > (float)k1) ? k1 + 1 : (int)kj;
+            k = (kj > (float)K1()) ? K1() + 1 : (int)kj;
             prev_valid = false;
             prev_unk = false;
 #if DTSDF_LAZY_SKIP
