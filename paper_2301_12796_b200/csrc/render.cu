@@ -768,8 +768,8 @@ template <bool kComb>
 struct RayT {
   // the view and the pixel (u | vrel << 16) wait in shared memory (ray_view, ray_pix): no registers
   // through the march
-  __device__ __forceinline__ int pix() const { return ((volatile int *)ray_pix)[threadIdx.x]; }
-  __device__ __forceinline__ int view() const { return ((volatile int *)ray_view)[threadIdx.x]; }
+  __device__ __forceinline__ int pix() const { return ray_pix[threadIdx.x]; }
+  __device__ __forceinline__ int view() const { return ray_view[threadIdx.x]; }
 #if DTSDF_SLOTS_FROM_TABLE
   __device__ __forceinline__ int comb_slot() const { return cur.slot0; }
 #else
