@@ -620,36 +620,39 @@ static int render_batch_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, 
   if (comb && !c->combined) return fail(DTSDF_ERR_NO_COMBINED, "no combined TSDF (call dtsdf_combine)");
   cudaSetDevice(c->device);
   cudaStream_t s = (cudaStream_t)stream;
-  const bool dev = is_device_ptr(depth);
-  if ((normal && is_device_ptr(normal) != dev) || (color && is_device_ptr(color) != dev) ||
-      (mask && is_device_ptr(mask) != dev))
-    return fail(DTSDF_ERR_INVALID_ARGUMENT, "outputs must be all device or all host pointers");
-  if (dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s, comb);
+  // classify every output once (one attribute query each): device, mapped page-locked host, pageable
+  void *outs[4] = {depth, normal, color, mask};
+  void *mapped_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n_dev = 0, n_host = 0, n_mapped = 0;
+  for (int i = 0; i < 4; ++i) {
+    if (!outs[i]) continue;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, outs[i]) != cudaSuccess) {
+      cudaGetLastError();
+      a.type = cudaMemoryTypeUnregistered;
+      a.devicePointer = nullptr;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+      ++n_dev;
+    } else {
+      ++n_host;
+      if (a.type == cudaMemoryTypeHost && a.devicePointer) {
+        ++n_mapped;
+        mapped_ptr[i] = a.devicePointer;
+      }
+    }
+  }
+  if (n_dev && n_host) return fail(DTSDF_ERR_INVALID_ARGUMENT, "outputs must be all device or all host pointers");
+  if (n_dev) return render_impl(c, n_views, poses, K, row0, row1, depth, normal, color, mask, s, comb);
   // host outputs in page-locked memory (mapped into the device address space under UVA, e.g.
   // torch pin_memory()): the raycast writes its staged output rows straight into them across the
   // host link while it runs, then the call synchronizes -- no staging copy after the kernel
-  if (c->host_write) {
-    void *dptr[4] = {depth, normal, color, mask};
-    bool mapped = true;
-    for (int i = 0; i < 4 && mapped; ++i) {
-      if (!dptr[i]) continue;
-      cudaPointerAttributes a;
-      if (cudaPointerGetAttributes(&a, dptr[i]) != cudaSuccess) {
-        cudaGetLastError();
-        mapped = false;
-      } else if (a.type != cudaMemoryTypeHost || !a.devicePointer) {
-        mapped = false;
-      } else {
-        dptr[i] = a.devicePointer;
-      }
-    }
-    if (mapped) {
-      rc = render_impl(c, n_views, poses, K, row0, row1, (float *)dptr[0], (float *)dptr[1], (uint8_t *)dptr[2],
-                       (uint8_t *)dptr[3], s, comb, /*staged=*/true);
-      if (rc) return rc;
-      CK(c, cudaStreamSynchronize(s), "render sync");
-      return DTSDF_OK;
-    }
+  if (c->host_write && n_mapped == n_host) {
+    rc = render_impl(c, n_views, poses, K, row0, row1, (float *)mapped_ptr[0], (float *)mapped_ptr[1],
+                     (uint8_t *)mapped_ptr[2], (uint8_t *)mapped_ptr[3], s, comb, /*staged=*/true);
+    if (rc) return rc;
+    CK(c, cudaStreamSynchronize(s), "render sync");
+    return DTSDF_OK;
   }
   // pageable host outputs: render into device scratch, copy back, synchronize
   const size_t px = (size_t)n_views * (row1 - row0) * K->width;
