@@ -184,9 +184,8 @@ cudaError_t launch_range(const RangeLaunch &p, cudaStream_t s);
 void raycast_tiles(int width, int rows, int *ct_x, int *ct_y);
 bool tile_order_fits(int width, int rows);  // the order kernel holds one key byte per CTA tile in shared memory
 // CTA tile order of each view from the range-pass counts (longest predicted first); clears the counts
-cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, const unsigned long long *z_far,
-                         unsigned int epoch, float voxel_size, int *order, int tiles_x, int tiles_y, int width,
-                         int rows, int n_views, cudaStream_t s);
+cudaError_t launch_order(unsigned int *count, int *order, int tiles_x, int tiles_y, int width, int rows, int n_views,
+                         cudaStream_t s);
 cudaError_t launch_raycast(const RenderLaunch &p, cudaStream_t s);
 
 // Fusion launch (fusion.cu): one depth frame against the raw block pool.  The doubles are the

@@ -546,8 +546,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     begin_timed(c, 0, s, &tl, (rl.n_locations > 0 ? 1 : 0) + (order ? 1 : 0));
     CK(c, launch_range(rl, s), "range pass");
     if (order)
-      CK(c, launch_order(c->tile_count, c->z_near, c->z_far, rl.epoch, V.voxel_size, c->tile_order, tiles_x, tiles_y,
-                         W, rows, nv, s), "tile order");
+      CK(c, launch_order(c->tile_count, c->tile_order, tiles_x, tiles_y, W, rows, nv, s), "tile order");
     end_timed(c, s, &tl);
     pl.vol = V;
     pl.fx = K->fx; pl.fy = K->fy; pl.cx = K->cx; pl.cy = K->cy; pl.z_min = K->z_min; pl.z_max = K->z_max;

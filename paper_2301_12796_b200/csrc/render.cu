@@ -226,37 +226,24 @@ __global__ void __launch_bounds__(256) k_range_warp(const __grid_constant__ Rang
 // a counting sort on a log2 key (64 buckets) orders the CTA tiles by decreasing count.  The order
 // changes only when a tile runs, never what it computes.  Clears the counts for the next pass.
 constexpr int kOrderKeys = 64;
-#ifndef DTSDF_ORDER_PROXY
-#define DTSDF_ORDER_PROXY 0  // cost proxy: 0 covering block count, 1 depth span of the covering blocks, 2 both
-#endif
 struct OrderLaunch {
-  unsigned int *count;               // [views][tiles]
-  const unsigned long long *z_near;  // [views][tiles] range keys of this pass
-  const unsigned long long *z_far;
-  int *order;                        // [views][ct_x * ct_y]
+  unsigned int *count;  // [views][tiles] block locations covering each range tile (k_range_*)
+  int *order;           // [views][ct_x * ct_y]
   int tiles_x, tiles_y, ct_x, ct_y;
-  unsigned int epoch;
-  float inv_voxel;
 };
 
 __device__ __forceinline__ int order_key(const OrderLaunch &p, int view, int t) {
   const int tx = t % p.ct_x, ty = t / p.ct_x;
   const size_t vo = (size_t)view * p.tiles_x * p.tiles_y;
-  float c = 0.f, span = 0.f;
+  float c = 0.f;
   // the range tiles overlapping the CTA tile (a CTA tile may be smaller than a range tile)
   for (int ry = ty * kTileH / kRangeTile; ry <= min(p.tiles_y - 1, ((ty + 1) * kTileH - 1) / kRangeTile); ++ry)
-    for (int rx = tx * kTileW / kRangeTile; rx <= min(p.tiles_x - 1, ((tx + 1) * kTileW - 1) / kRangeTile); ++rx) {
-      const size_t i = vo + ry * p.tiles_x + rx;
-      c += (float)p.count[i];
-      if (DTSDF_ORDER_PROXY) {
-        const unsigned long long kn = p.z_near[i], kf = p.z_far[i];
-        if ((kn >> 32) == (0xFFFFFFFFu - p.epoch) && (kf >> 32) == p.epoch)
-          span = fmaxf(span, (__uint_as_float((unsigned)kf) - __uint_as_float((unsigned)kn)) * p.inv_voxel);
-      }
-    }
-  const float cost = DTSDF_ORDER_PROXY == 0 ? c : DTSDF_ORDER_PROXY == 1 ? span : c * span;
-  const int lg = cost > 0.f ? (int)(8.0f * __log2f(cost + 1.0f)) : 0;  // 8 keys per doubling
-  return kOrderKeys - 1 - min(lg, kOrderKeys - 1);                   // ascending key = descending cost
+    for (int rx = tx * kTileW / kRangeTile; rx <= min(p.tiles_x - 1, ((tx + 1) * kTileW - 1) / kRangeTile); ++rx)
+      c += (float)p.count[vo + ry * p.tiles_x + rx];
+  // (the depth span of the covering blocks, alone or times the count, orders worse:
+  // profiles/r1f_sweep_tile_order.jsonl)
+  const int lg = c > 0.f ? (int)(8.0f * __log2f(c + 1.0f)) : 0;  // 8 keys per doubling
+  return kOrderKeys - 1 - min(lg, kOrderKeys - 1);              // ascending key = descending cost
 }
 
 constexpr int kOrderMaxTiles = 160 * 1024;  // CTA tiles per view whose keys fit the shared bytes below
@@ -355,49 +342,17 @@ __device__ __forceinline__ int lookup_slots(const VolumeView &V, int bx, int by,
 struct SampleResult {
   bool valid;
   float f;
-  bool unk;  // lazy evaluation: invalid or positive, not resolved (every direction holding data
-             // has phi_D > 0, so F > 0 whenever S > 0); valid = false
 };
 
-// Lazy evaluation (measured dead end; off): where only the sign class of F matters
-// -- march samples and bisection midpoints -- the gradients (24 of the 32 stencil voxels and most
-// of the arithmetic) can be skipped when every direction holding data at x has phi_D > 0: F is then
-// positive or invalid, and both count as "not <= 0" for the crossing test and for the bisection
-// (R21).  A march sample left unresolved is evaluated in full only if the next one ends a crossing
-// (mode kResolve).  Exact, but slower on B200 (profiles/r1f_sweep_lazy.jsonl): the second pass over
-// the corners costs more than the skipped gradients save, and skipping certainly-positive points
-// unevaluated lengthens the divergent advance loop of every step.
 #ifndef DTSDF_FAST_NORM
 #define DTSDF_FAST_NORM 1    // rsqrt gradient normalisation, approximate F / S and regula-falsi quotient: one
                              // MUFU op each instead of the IEEE sequences with their special-case branches
                              // (C1 -6 %, C2 -8 %; fp32 rounding differences only, profiles/r1f_sweep_fast_norm.jsonl)
 #endif
-#ifndef DTSDF_PREFETCH
-#define DTSDF_PREFETCH 0     // 1: prefetch the next march point's brick rows into L1 (measured slower,
-                             // profiles/r1f_sweep_prefetch.jsonl)
-#endif
-#ifndef DTSDF_EARLY_LOADS
-#define DTSDF_EARLY_LOADS 0  // 1: the 24 outer stencil loads as volatile loads, issued with the 8 corner loads
-                             // before the direction's NaN / weight test (ptxas otherwise sinks them past it);
-                             // measured equal (profiles/r1f_sweep_prefetch.jsonl), so left to the compiler
-#endif
 #ifndef DTSDF_SLOTS_FROM_TABLE
 #define DTSDF_SLOTS_FROM_TABLE 1  // direction slots re-read from the hash entry (an L1 hit) per evaluated
                                   // direction instead of six registers through the march: with them the
                                   // kernel fits 96 registers (5 CTAs / 20 warps per SM), profiles/r1f_sweep_regs.jsonl
-#endif
-#ifndef DTSDF_LAZY
-#define DTSDF_LAZY 0         // gradient-free sign class for march samples
-#endif
-#ifndef DTSDF_LAZY_BISECT
-#define DTSDF_LAZY_BISECT 0  // ... and for bisection midpoints (fa unknown -> regula falsi starts with a midpoint)
-#endif
-#ifndef DTSDF_ADV_BUDGET
-#define DTSDF_ADV_BUDGET 0   // > 0: at most this many advance iterations (locates) per step (measured
-                             // slower with and without DTSDF_LAZY_SKIP, profiles/r1f_sweep_lazy.jsonl)
-#endif
-#ifndef DTSDF_LAZY_SKIP
-#define DTSDF_LAZY_SKIP 0    // certainly-positive points are skipped unevaluated (resolved on demand)
 #endif
 
 struct ShadeResult {
@@ -406,16 +361,6 @@ struct ShadeResult {
   float S;
   int mask;
 };
-
-__device__ __forceinline__ float ldg_stencil(const float *ptr) {
-#if DTSDF_EARLY_LOADS
-  float v;
-  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(ptr));
-  return v;
-#else
-  return __ldg(ptr);
-#endif
-}
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 // a + t (b - a) on a pair: two packed FFMA2 (a - t a, then + t b)
@@ -489,38 +434,9 @@ __device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, 
 template <bool shade>
 __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const Cursor &cur, int lx, int ly, int lz,
                                                  float fx, float fy, float fz, float rx, float ry, float rz,
-                                                 ShadeResult *sh, bool lazy, int live = -1) {
+                                                 ShadeResult *sh, int live = -1) {
   SampleResult res;
-  res.unk = false;
   const int off = lx + kApron * ly + kApron * kApron * lz;
-#if DTSDF_LAZY
-  if (lazy) {  // sign class from the 8 cell corners of each direction
-    bool any = false, full = false;
-    int pr = cur.present;
-#pragma unroll 1
-    while (pr) {
-      const int D = __ffs(pr) - 1;
-      pr &= pr - 1;
-      const float2 *br = V.apron + (size_t)dir_slot(V, cur, D) * kApronStride + off;
-      const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
-      const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
-      const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
-      const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
-      const float2 fx2 = make_float2(fx, fx), fy2 = make_float2(fy, fy), fz2 = make_float2(fz, fz);
-      const float2 pw = lerp2(lerp2(lerp2(c000, c100, fx2), lerp2(c010, c110, fx2), fy2),
-                              lerp2(lerp2(c001, c101, fx2), lerp2(c011, c111, fx2), fy2), fz2);
-      if (isnan(pw.x) || !(pw.y > 0.0f)) continue;  // no data from D (as in the full evaluation)
-      any = true;
-      if (!(pw.x > 0.0f)) { full = true; break; }
-    }
-    if (!full) {
-      res.valid = false;
-      res.f = 0.0f;
-      res.unk = any;  // no data at all: invalid for certain
-      return res;
-    }
-  }
-#endif
   float S1 = 0.f, F1 = 0.f, S2 = 0.f, F2 = 0.f;
   bool any_grad = false;
   float N1x = 0.f, N1y = 0.f, N1z = 0.f, N2x = 0.f, N2y = 0.f, N2z = 0.f;
@@ -545,18 +461,18 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
     const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
     const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
-    const float xm00 = ldg_stencil(&br[APRON_IDX(-1, 0, 0)].x), xm10 = ldg_stencil(&br[APRON_IDX(-1, 1, 0)].x);
-    const float xm01 = ldg_stencil(&br[APRON_IDX(-1, 0, 1)].x), xm11 = ldg_stencil(&br[APRON_IDX(-1, 1, 1)].x);
-    const float xp00 = ldg_stencil(&br[APRON_IDX(2, 0, 0)].x), xp10 = ldg_stencil(&br[APRON_IDX(2, 1, 0)].x);
-    const float xp01 = ldg_stencil(&br[APRON_IDX(2, 0, 1)].x), xp11 = ldg_stencil(&br[APRON_IDX(2, 1, 1)].x);
-    const float ym00 = ldg_stencil(&br[APRON_IDX(0, -1, 0)].x), ym10 = ldg_stencil(&br[APRON_IDX(1, -1, 0)].x);
-    const float ym01 = ldg_stencil(&br[APRON_IDX(0, -1, 1)].x), ym11 = ldg_stencil(&br[APRON_IDX(1, -1, 1)].x);
-    const float yp00 = ldg_stencil(&br[APRON_IDX(0, 2, 0)].x), yp10 = ldg_stencil(&br[APRON_IDX(1, 2, 0)].x);
-    const float yp01 = ldg_stencil(&br[APRON_IDX(0, 2, 1)].x), yp11 = ldg_stencil(&br[APRON_IDX(1, 2, 1)].x);
-    const float zm00 = ldg_stencil(&br[APRON_IDX(0, 0, -1)].x), zm10 = ldg_stencil(&br[APRON_IDX(1, 0, -1)].x);
-    const float zm01 = ldg_stencil(&br[APRON_IDX(0, 1, -1)].x), zm11 = ldg_stencil(&br[APRON_IDX(1, 1, -1)].x);
-    const float zp00 = ldg_stencil(&br[APRON_IDX(0, 0, 2)].x), zp10 = ldg_stencil(&br[APRON_IDX(1, 0, 2)].x);
-    const float zp01 = ldg_stencil(&br[APRON_IDX(0, 1, 2)].x), zp11 = ldg_stencil(&br[APRON_IDX(1, 1, 2)].x);
+    const float xm00 = __ldg(&br[APRON_IDX(-1, 0, 0)].x), xm10 = __ldg(&br[APRON_IDX(-1, 1, 0)].x);
+    const float xm01 = __ldg(&br[APRON_IDX(-1, 0, 1)].x), xm11 = __ldg(&br[APRON_IDX(-1, 1, 1)].x);
+    const float xp00 = __ldg(&br[APRON_IDX(2, 0, 0)].x), xp10 = __ldg(&br[APRON_IDX(2, 1, 0)].x);
+    const float xp01 = __ldg(&br[APRON_IDX(2, 0, 1)].x), xp11 = __ldg(&br[APRON_IDX(2, 1, 1)].x);
+    const float ym00 = __ldg(&br[APRON_IDX(0, -1, 0)].x), ym10 = __ldg(&br[APRON_IDX(1, -1, 0)].x);
+    const float ym01 = __ldg(&br[APRON_IDX(0, -1, 1)].x), ym11 = __ldg(&br[APRON_IDX(1, -1, 1)].x);
+    const float yp00 = __ldg(&br[APRON_IDX(0, 2, 0)].x), yp10 = __ldg(&br[APRON_IDX(1, 2, 0)].x);
+    const float yp01 = __ldg(&br[APRON_IDX(0, 2, 1)].x), yp11 = __ldg(&br[APRON_IDX(1, 2, 1)].x);
+    const float zm00 = __ldg(&br[APRON_IDX(0, 0, -1)].x), zm10 = __ldg(&br[APRON_IDX(1, 0, -1)].x);
+    const float zm01 = __ldg(&br[APRON_IDX(0, 1, -1)].x), zm11 = __ldg(&br[APRON_IDX(1, 1, -1)].x);
+    const float zp00 = __ldg(&br[APRON_IDX(0, 0, 2)].x), zp10 = __ldg(&br[APRON_IDX(1, 0, 2)].x);
+    const float zp01 = __ldg(&br[APRON_IDX(0, 1, 2)].x), zp11 = __ldg(&br[APRON_IDX(1, 1, 2)].x);
     // The lerps run pairwise on Blackwell's packed fp32x2 FMA (FFMA2): {sdf, weight} of the
     // corners, and pairs of independent stencil layers.
     // O3(a) trilinear phi_D, omega_D over the 8 cell corners (x: rows e_yz, y: slabs R(dz), z)
@@ -678,7 +594,6 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
   SampleResult res;
   res.valid = !isnan(phi);
   res.f = res.valid ? phi : 0.0f;
-  res.unk = false;
   if (shade && res.valid) {  // (compile-time shade)
     const float xm00 = __ldg(br + APRON_IDX(-1, 0, 0)), xm10 = __ldg(br + APRON_IDX(-1, 1, 0));
     const float xm01 = __ldg(br + APRON_IDX(-1, 0, 1)), xm11 = __ldg(br + APRON_IDX(-1, 1, 1));
@@ -745,7 +660,7 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
 // a4-a7: the raycast kernel, one state machine per ray so that a warp's rays -- marching,
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
-enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3, kResolve = 4 };
+enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
 #ifndef DTSDF_LOOKAHEAD
 #define DTSDF_LOOKAHEAD 8
 #endif
@@ -754,12 +669,6 @@ constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certai
 // per-thread pixel of the ray (u | vrel << 16), read back only when a bracket starts and at the end
 __shared__ int ray_pix[256];
 __shared__ int ray_view[256];
-#ifndef DTSDF_SMEM_COLD
-#define DTSDF_SMEM_COLD 0  // 1: camera centre, 1/r and the last lattice index in shared memory (more spills: off)
-#endif
-#if DTSDF_SMEM_COLD
-__shared__ float ray_cold[7][256];  // per thread: camera centre (3), 1 / ray direction (3), last lattice index
-#endif
 
 // One ray's complete state: the march/refinement/shading state machine of DESIGN.md §2 (a4-a7).
 // step() performs the cheap advance loop plus exactly one sample evaluation, so that the lanes of
@@ -776,20 +685,8 @@ struct RayT {
   __device__ __forceinline__ int comb_slot() const { return cur.slots[0]; }
 #endif
   float r[3];
-#if DTSDF_SMEM_COLD
-  // camera centre, 1 / ray direction and the last lattice index: read by the empty-space skips only,
-  // kept in shared memory (ray_cold) rather than registers through the march
-  // (volatile: re-read at each use, not hoisted out of the march loop into registers)
-  __device__ __forceinline__ float O(int q) const { return ((volatile float *)ray_cold[q])[threadIdx.x]; }
-  __device__ __forceinline__ float IR(int q) const { return ((volatile float *)ray_cold[3 + q])[threadIdx.x]; }
-  __device__ __forceinline__ int K1() const { return __float_as_int(((volatile float *)ray_cold[6])[threadIdx.x]); }
-#else
   float o[3], ir[3];
   int k1;
-  __device__ __forceinline__ float O(int q) const { return o[q]; }
-  __device__ __forceinline__ float IR(int q) const { return ir[q]; }
-  __device__ __forceinline__ int K1() const { return k1; }
-#endif
   int k;
   // sample positions in voxel units g = g0 + t * rs relative to the integer cell ib of a frame:
   // the world origin during the march; re-anchored once per bracket in fp64 at x(t_{k-1}), so g
@@ -800,7 +697,7 @@ struct RayT {
   float g0x, g0y, g0z, rsx, rsy, rsz;
   Cursor cur;
   int mode, it, side;
-  bool prev_valid, prev_unk, fa_valid, hit;
+  bool prev_valid, fa_valid, hit;
   float prev_f, a, b, t, fa, fb;
   ShadeResult sh;
   int ix, iy, iz;
@@ -826,13 +723,8 @@ struct RayT {
     const float iLf = 1.0f / Lf;
     for (int q = 0; q < 3; ++q) {
       r[q] = (P.r[3 * q] * dxf + P.r[3 * q + 1] * dyf + P.r[3 * q + 2]) * iLf;
-#if DTSDF_SMEM_COLD
-      ray_cold[q][threadIdx.x] = P.t[q];
-      ray_cold[3 + q][threadIdx.x] = 1.0f / r[q];
-#else
       o[q] = P.t[q];
       ir[q] = 1.0f / r[q];
-#endif
     }
     // O2 lattice bounds, narrowed to the tile's block range (a3)
     const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
@@ -851,11 +743,7 @@ struct RayT {
         kl = k - 1;  // no allocated block projects onto this tile
       }
     }
-#if DTSDF_SMEM_COLD
-    ray_cold[6][threadIdx.x] = __int_as_float(kl);
-#else
     k1 = kl;
-#endif
     ibx = iby = ibz = 0;
     g0x = P.t[0] * V.inv_voxel; g0y = P.t[1] * V.inv_voxel; g0z = P.t[2] * V.inv_voxel;
     rsx = r[0] * V.inv_voxel; rsy = r[1] * V.inv_voxel; rsz = r[2] * V.inv_voxel;
@@ -869,7 +757,6 @@ struct RayT {
 #endif
     mode = kMarch;
     prev_valid = false;
-    prev_unk = false;
     prev_f = 0.f;
     a = b = 0.f;
     t = (float)k * V.delta;
@@ -969,37 +856,12 @@ struct RayT {
     float texit = 3.0e38f;
     const int bb[3] = {cur.bx, cur.by, cur.bz};
     for (int q = 0; q < 3; ++q) {
-      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + rad) * bsz - O(q)) * IR(q));
-      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - rad) * bsz - O(q)) * IR(q));
+      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + rad) * bsz - o[q]) * ir[q]);
+      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - rad) * bsz - o[q]) * ir[q]);
     }
     return texit;
   }
   __device__ __forceinline__ float block_exit(const VolumeView &V) const { return box_exit(V, 0); }
-
-#if DTSDF_PREFETCH
-  // Prefetch into L1 the brick rows the next lattice point's evaluation will read (the 4 corner rows
-  // and the 4 outer stencil rows of each present direction), if it stays in the cursor's location,
-  // so that its loads hit while this warp is away.
-  __device__ __forceinline__ void prefetch_next(const VolumeView &V) const {
-    const float tn = (float)k * V.delta;
-    const int jx = ibx + (int)floorf(fmaf(tn, rsx, g0x)), jy = iby + (int)floorf(fmaf(tn, rsy, g0y)),
-              jz = ibz + (int)floorf(fmaf(tn, rsz, g0z));
-    if ((jx >> 3) != cur.bx || (jy >> 3) != cur.by || (jz >> 3) != cur.bz) return;
-    const int off = (jx & 7) + kApron * (jy & 7) + kApron * kApron * (jz & 7);
-    int pr = cur.present;
-#pragma unroll 1
-    while (pr) {
-      const int D = __ffs(pr) - 1;
-      pr &= pr - 1;
-      const float2 *br = V.apron + (size_t)dir_slot(V, cur, D) * kApronStride + off;
-      const float2 *rows[8] = {br + APRON_IDX(0, 0, 0), br + APRON_IDX(0, 1, 0), br + APRON_IDX(0, 0, 1),
-                               br + APRON_IDX(0, 1, 1), br + APRON_IDX(0, -1, 0), br + APRON_IDX(0, 2, 0),
-                               br + APRON_IDX(0, 0, -1), br + APRON_IDX(0, 0, 2)};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) asm volatile("prefetch.global.L1 [%0];" ::"l"(rows[q]));
-    }
-  }
-#endif
 
   // a6: bracket [t_{k-1}, t_k] with F(t_{k-1}) = f_prev > 0 and F(t_k) = f_k <= 0
   __device__ __forceinline__ void begin_bracket(const RenderLaunch &p, float f_prev, float f_k) {
@@ -1048,17 +910,9 @@ struct RayT {
       // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
       // location without an sdf <= 0 corner, and in a certainly-positive cell followed by
       // another, no crossing can end or start.
-#if DTSDF_ADV_BUDGET > 0
-      int adv = 0;
-#endif
       for (;;) {
         live = -1;
-        if (k > K1()) return true;  // no crossing: a miss
-#if DTSDF_ADV_BUDGET > 0
-        // bounded advance per step: a lane with a long skip sits out this step's evaluation
-        // (its warp evaluates without it) and goes on advancing in the next
-        if (++adv > DTSDF_ADV_BUDGET) return false;
-#endif
+        if (k > k1) return true;  // no crossing: a miss
         t = (float)k * V.delta;
         locate(V, p.comb, t);
 #ifdef DTSDF_STATS
@@ -1066,7 +920,6 @@ struct RayT {
 #endif
         if (!cur.occ) {
           prev_valid = false;
-          prev_unk = false;
 #ifdef DTSDF_STATS
           ++st_empty;
 #endif
@@ -1080,9 +933,9 @@ struct RayT {
               float t0 = -3.0e38f, t1 = 3.0e38f;
               const int lo3[3] = {V.lo_x, V.lo_y, V.lo_z}, dm3[3] = {V.dim_x, V.dim_y, V.dim_z};
               for (int q = 0; q < 3; ++q) {
-                const float lo = lo3[q] * bsz - O(q), hi = (lo3[q] + dm3[q]) * bsz - O(q);
+                const float lo = lo3[q] * bsz - o[q], hi = (lo3[q] + dm3[q]) * bsz - o[q];
                 if (r[q] != 0.f) {
-                  const float ta = lo * IR(q), tb = hi * IR(q);
+                  const float ta = lo * ir[q], tb = hi * ir[q];
                   t0 = fmaxf(t0, fminf(ta, tb));
                   t1 = fminf(t1, fmaxf(ta, tb));
                 } else if (lo > 0.f || hi < 0.f) {
@@ -1090,12 +943,12 @@ struct RayT {
                 }
               }
               texit = (t0 <= t1 && t1 > t) ? fmaxf(t0, t) : 3.0e38f;
-              if (texit >= 3.0e38f) { k = K1() + 1; continue; }
+              if (texit >= 3.0e38f) { k = k1 + 1; continue; }
             } else {
               texit = box_exit(V, cur.dist - 1);
             }
             const float kn = floorf(texit * V.inv_delta);
-            k = (kn > (float)K1()) ? K1() + 1 : max(k + 1, (int)kn);
+            k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);
           } else {
             ++k;
           }
@@ -1109,15 +962,8 @@ struct RayT {
 #ifdef DTSDF_STATS
             ++st_jump;
 #endif
-            k = (kj > (float)K1()) ? K1() + 1 : (int)kj;
+            k = (kj > (float)k1) ? k1 + 1 : (int)kj;
             prev_valid = false;
-            prev_unk = false;
-#if DTSDF_LAZY_SKIP
-            // every point of the location is positive or invalid: leave the jump's landing point
-            // unresolved as well and move past it
-            prev_unk = true;
-            ++k;
-#endif
             continue;
           }
         }
@@ -1149,22 +995,11 @@ struct RayT {
             run |= (unsigned)ok << j;
           }
           const int n = __ffs(~run) - 1;  // leading certainly-positive points (>= 1)
-#if DTSDF_LAZY_SKIP
-          // all n points are positive or invalid: none is evaluated; the last one stays unresolved
-#ifdef DTSDF_STATS
-          st_cpi += n;
-#endif
-          prev_valid = false;
-          prev_unk = true;
-          k += n;
-          continue;
-#endif
           if (n >= 2) {
 #ifdef DTSDF_STATS
             st_cpi += n - 1;
 #endif
             prev_valid = false;
-            prev_unk = false;
             k += n - 1;
             if (n == kLookahead) continue;  // the run may go on: scan again from its last point
             t = (float)k * V.delta;
@@ -1186,12 +1021,10 @@ struct RayT {
       if constexpr (kComb)
         s = eval_comb<false>(V, p.comb, comb_slot(), ix & 7, iy & 7, iz & 7, frx, fry, frz, nullptr);
       else
-        s = eval_sample<false>(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], nullptr,
-                               mode == kMarch || (DTSDF_LAZY_BISECT && mode == kBisect), live);
+        s = eval_sample<false>(V, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], nullptr, live);
     } else {
       s.valid = false;
       s.f = 0.f;
-      s.unk = false;
     }
 #ifdef DTSDF_STATS
     {
@@ -1199,40 +1032,14 @@ struct RayT {
       if (mode == kMarch) cy_march += c2 - c1; else cy_refine += c2 - c1;
     }
 #endif
-    if (mode == kMarch || mode == kResolve) {
-      float f_prev, f_k;
-      if (mode == kMarch) {
-        if (!(s.valid && s.f <= 0.0f && (prev_unk || (prev_valid && prev_f > 0.0f)))) {
-          prev_valid = s.valid;
-          prev_unk = s.unk;
-          prev_f = s.f;
-          ++k;
-#if DTSDF_PREFETCH
-          if constexpr (!kComb) prefetch_next(V);
-#endif
-          return false;
-        }
-        if (prev_unk) {  // sample k ends a crossing iff the unresolved t_{k-1} is valid: evaluate it
-          mode = kResolve;
-          fb = s.f;
-          t = (float)(k - 1) * V.delta;
-          return false;
-        }
-        f_prev = prev_f;
-        f_k = s.f;
-      } else {
-        if (!(s.valid && s.f > 0.0f)) {  // no crossing ends at k; sample k (valid, <= 0) becomes prev
-          prev_valid = true;
-          prev_unk = false;
-          prev_f = fb;
-          mode = kMarch;
-          ++k;
-          return false;
-        }
-        f_prev = s.f;
-        f_k = fb;
+    if (mode == kMarch) {
+      if (!(s.valid && prev_valid && prev_f > 0.0f && s.f <= 0.0f)) {
+        prev_valid = s.valid;
+        prev_f = s.f;
+        ++k;
+        return false;
       }
-      begin_bracket(p, f_prev, f_k);
+      begin_bracket(p, prev_f, s.f);
     } else if (mode == kBisect) {
       if (!s.valid || s.f > 0.0f) { a = t; fa = s.f; fa_valid = s.valid; }
       else { b = t; fb = s.f; }
@@ -1284,7 +1091,7 @@ struct RayT {
       if constexpr (kComb)
         eval_comb<true>(p.vol, p.comb, comb_slot(), ix & 7, iy & 7, iz & 7, frx, fry, frz, &sh);
       else
-        eval_sample<true>(p.vol, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], &sh, false);
+        eval_sample<true>(p.vol, cur, ix & 7, iy & 7, iz & 7, frx, fry, frz, r[0], r[1], r[2], &sh);
     }
   }
 
@@ -1370,16 +1177,13 @@ void raycast_tiles(int width, int rows, int *ct_x, int *ct_y) {
   *ct_y = (rows + kTileH - 1) / kTileH;
 }
 
-cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, const unsigned long long *z_far,
-                         unsigned int epoch, float voxel_size, int *order, int tiles_x, int tiles_y, int width,
-                         int rows, int n_views, cudaStream_t s) {
+cudaError_t launch_order(unsigned int *count, int *order, int tiles_x, int tiles_y, int width, int rows, int n_views,
+                         cudaStream_t s) {
   if (n_views == 0) return cudaSuccess;
   OrderLaunch p;
-  p.count = count; p.z_near = z_near; p.z_far = z_far; p.order = order;
+  p.count = count; p.order = order;
   p.tiles_x = tiles_x; p.tiles_y = tiles_y;
   raycast_tiles(width, rows, &p.ct_x, &p.ct_y);
-  p.epoch = epoch;
-  p.inv_voxel = 1.0f / voxel_size;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_order, cudaFuncAttributeMaxDynamicSharedMemorySize, kOrderMaxTiles);
@@ -1400,9 +1204,6 @@ cudaError_t launch_order(unsigned int *count, const unsigned long long *z_near, 
 }
 
 // grid schedule: one CTA per 16 x (2 * DTSDF_CTA / 64)-pixel tile of 8x4-pixel warps, one ray per thread
-#ifndef DTSDF_CARVEOUT
-#define DTSDF_CARVEOUT -1  // >= 0: preferred shared-memory carveout (percent) of k_raycast; -1 driver default
-#endif
 #ifndef DTSDF_RAYCAST_MINB
 #define DTSDF_RAYCAST_MINB (640 / DTSDF_CTA)  // 96 registers per thread: 20 warps per SM (128 was 16 warps:
                                               // 4-6 % slower, profiles/r1f_sweep_regs.jsonl)
@@ -1553,13 +1354,6 @@ static cudaError_t launch_raycast_t(const RenderLaunch &p, cudaStream_t s) {
     k_raycast_persistent<kComb><<<(unsigned)grid, 256, 0, s>>>(p);
     return cudaGetLastError();
   }
-#if DTSDF_CARVEOUT >= 0
-  static bool carve = false;
-  if (!carve) {  // L1 / shared-memory split of the SM's unified array (percent shared)
-    cudaFuncSetAttribute(k_raycast<kComb>, cudaFuncAttributePreferredSharedMemoryCarveout, DTSDF_CARVEOUT);
-    carve = true;
-  }
-#endif
   const int ct_y = (p.row1 - p.row0 + kTileH - 1) / kTileH;
   dim3 grid((unsigned)(p.ct_x * ct_y), 1u, (unsigned)p.n_views);
   return launch_pdl(k_raycast<kComb>, grid, dim3(DTSDF_CTA), s, p);
