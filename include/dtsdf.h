@@ -336,6 +336,11 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *                         drain; longer batches stay row-major.  2 always, 0 never.  Changes only when a
  *                         tile runs, never what it computes. */
 #define DTSDF_OPT_TILE_ORDER 9
+/* Testing only:
+ *   DTSDF_OPT_RANGE_EPOCH  n != 0 (read as uint32): the next range pass uses epoch n + 1 (the range keys carry a per-pass
+ *                          epoch; passes at or above 0xFFFFFFF0 clear the buffers and restart at 1), to
+ *                          exercise the wrap.  No effect before the first render of the context. */
+#define DTSDF_OPT_RANGE_EPOCH 10
 DTSDF_API int dtsdf_set_option(dtsdf_ctx *ctx, int option, int value);
 
 /* Kernel launches issued by this context since creation (all kinds). */

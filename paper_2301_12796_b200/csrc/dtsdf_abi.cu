@@ -1245,6 +1245,9 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
   else if (option == DTSDF_OPT_CELL_DIRS) c->use_live = value ? 1 : 0;
   else if (option == DTSDF_OPT_TILE_ORDER && value >= 0 && value <= 2) c->use_order = value;
+  else if (option == DTSDF_OPT_RANGE_EPOCH && value != 0) {  // value: the epoch's 32 bits
+    if (c->range_epoch != 0) c->range_epoch = (unsigned int)value;  // testing: next pass uses value + 1
+  }
   else return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown option");
   return DTSDF_OK;
 }

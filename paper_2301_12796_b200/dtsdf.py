@@ -32,6 +32,7 @@ OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRI
 OPT_HOST_WRITE = 7
 OPT_CELL_DIRS = 8
 OPT_TILE_ORDER = 9
+OPT_RANGE_EPOCH = 10
 
 
 class DtsdfError(RuntimeError):
@@ -355,7 +356,10 @@ class Renderer:
         _check(lib().dtsdf_reset_kernel_times(self._h))
 
     def set_option(self, option: int, value: int):
-        _check(lib().dtsdf_set_option(self._h, int(option), int(value)))
+        value = int(value)
+        if value > 0x7FFFFFFF:  # options read as uint32 (DTSDF_OPT_RANGE_EPOCH) pass their bits
+            value -= 1 << 32
+        _check(lib().dtsdf_set_option(self._h, int(option), value))
 
     def launch_count(self) -> int:
         return int(lib().dtsdf_launch_count(self._h))

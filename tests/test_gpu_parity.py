@@ -341,3 +341,21 @@ def test_random_and_axis_aligned_poses_inside_the_room(R, c1):
             o = ov.render(P, K)
             st = assert_parity(_sel(g, i), o, what=f"pose {i} {K.width}x{K.height}")
             print("inside-room pose", i, K.width, st["hits_gpu"], st["budget_used"], st["depth_max_err"])
+
+
+def test_range_epoch_wrap_is_result_invisible(R, c1):
+    """The range keys carry a per-pass epoch so the buffers are never cleared between calls; passes
+    just below and across the wrap (buffers cleared, epoch restarts at 1) render the same bits, and so
+    do passes whose tiles hold keys of many earlier epochs."""
+    from paper_2301_12796_b200.dtsdf import OPT_RANGE_EPOCH
+    R.upload_volume(c1.volume)
+    K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=320, height=240)
+    w3 = scenes.c3_batch(n_views=4, room=c1)
+    ref = [R.render(w3.poses[i:i + 1], K) for i in range(4)]
+    for start in (0xFFFFFFEC, 0xFFFFFFEE):  # passes run through 0xFFFFFFF0 and wrap
+        R.set_option(OPT_RANGE_EPOCH, start)
+        for rep in range(6):
+            i = rep % 4
+            g = R.render(w3.poses[i:i + 1], K)
+            for k in ref[i]:
+                assert torch.equal(ref[i][k], g[k]), (hex(start), rep, k)
