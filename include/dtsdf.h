@@ -63,7 +63,7 @@ extern "C" {
 
 typedef struct dtsdf_ctx dtsdf_ctx; /* opaque, one per device */
 
-/* Pinhole intrinsics and the march depth range.  fx, fy > 0; width, height > 0;
+/* Pinhole intrinsics and the march depth range.  fx, fy > 0; 0 < width, height <= 32768;
  * 0 < z_min < z_max (camera-frame z, metres; reading R24). */
 typedef struct {
   float fx, fy, cx, cy;

@@ -188,6 +188,8 @@ int check_intr(const dtsdf_intrinsics *K) {
   if (!K) return fail(DTSDF_ERR_INVALID_ARGUMENT, "intrinsics is NULL");
   if (!(K->fx > 0.f) || !(K->fy > 0.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "fx, fy must be > 0");
   if (K->width <= 0 || K->height <= 0) return fail(DTSDF_ERR_INVALID_ARGUMENT, "width, height must be > 0");
+  // the raycast packs a pixel as u | row << 16 (render.cu ray_pix)
+  if (K->width > 32768 || K->height > 32768) return fail(DTSDF_ERR_INVALID_ARGUMENT, "width, height must be <= 32768");
   if (!(K->z_min > 0.f) || !(K->z_min < K->z_max) || !std::isfinite(K->z_max))
     return fail(DTSDF_ERR_INVALID_ARGUMENT, "need 0 < z_min < z_max");
   if (!std::isfinite(K->cx) || !std::isfinite(K->cy)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "cx, cy not finite");

@@ -264,6 +264,9 @@ def test_errors(R, c0):
         fresh.render(c0.poses, bad)
     with pytest.raises(DtsdfError):
         fresh.render(c0.poses, c0.intrinsics, row0=30, row1=30)
+    bad = scenes.Intrinsics(fx=70.0, fy=70.0, cx=40, cy=0, width=40000, height=1)  # > 32768 columns
+    with pytest.raises(DtsdfError):
+        fresh.render(c0.poses, bad)
     fresh.close()
 
 
