@@ -365,6 +365,16 @@ def run_dtsdf(args):
         pk = sms * 4 * mhz * 1e6 / 1e12
         roof["issue"] = {"achieved": ach, "peak": pk, "unit": "Tinst/s (warp instructions)", "frac": ach / pk,
                          "insts_per_launch": ins, "source": ncu.get(w.name, {}).get("source")}
+    # the on-chip side: L1 load demand of one launch (sectors from the committed capture of this config)
+    # over this run's live kernel time, and the L1 wavefront utilisation ncu measured
+    ncu_c = ncu.get(w.name, {}) if args.mode == "direct" and args.views == 1 else {}
+    if ncu_c.get("raycast_l1_load_sectors_per_launch"):
+        dem = ncu_c["raycast_l1_load_sectors_per_launch"] * 32.0
+        roof["l1"] = {"demand_bytes_per_launch": dem, "demand_bytes_per_ray": dem / rays_per_step,
+                      "achieved_TBps": dem / (ray_ms / 1e3) / 1e12,
+                      "l2_bytes_per_launch": (ncu_c.get("raycast_l2_sectors_per_launch") or 0) * 32.0,
+                      "wavefront_pct_of_peak": ncu_c.get("raycast_l1_wavefronts_pct_of_peak"),
+                      "source": ncu_c.get("source")}
     if args.mode == "combined":
         roof["combine_ms_per_step"] = kt["combine_ms"] / args.steps
         roof["recombinations_per_step"] = combines / args.steps

@@ -65,6 +65,12 @@ def main():
         js[cfg] = {"raycast_dram_bytes_per_launch": (rd or 0) + (wr or 0), "source": f"profiles/{tag}_ncu_k_raycast.txt",
                    "duration_us": float(s.get("Duration [us]", "nan")),
                    "raycast_warp_insts_per_launch": float(ins.replace(",", "")) if ins else None}
+        for key, name in (("raycast_l1_load_sectors_per_launch", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"),
+                          ("raycast_l2_sectors_per_launch", "lts__t_sectors.sum"),
+                          ("raycast_l1_wavefronts_pct_of_peak", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed")):
+            k = [x for x in s if x.startswith(name + " ")]
+            if k:
+                js[cfg][key] = float(s[k[0]].replace(",", ""))
         json.dump(js, open(path, "w"), indent=1)
     lc = os.path.join(OUT, f"launches_{tag}.csv")
     if os.path.exists(lc):

@@ -25,7 +25,9 @@ def summary(rep):
     rr = list(csv.reader(raw.splitlines()))
     hh = rr[0]
     for name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
-                 "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active"):
+                 "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__warps_active.avg.pct_of_peak_sustained_active",
+                 "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "lts__t_sectors.sum",
+                 "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"):
         if name in hh:
             j = hh.index(name)
             res[f"{name} [{rr[1][j]}]"] = rr[2][j]
