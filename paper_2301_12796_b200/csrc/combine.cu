@@ -265,7 +265,7 @@ __device__ bool dir_cell(const CombineLaunch &p, int D, const double y[3], const
     if (x < 0 || yy < 0 || z < 0 || x >= V.dim_x || yy >= V.dim_y || z >= V.dim_z) return false;
     const int gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + yy) * V.dim_x + x]);
     if (gv < 0) return false;
-    e = gv & 0x3fffffff;
+    e = gv & kGridEntryMask;
   } else {
     const unsigned long long key = pack_key((int)b0, (int)b1, (int)b2);
     unsigned int h = hash_key(key) & V.table_mask;
@@ -450,7 +450,7 @@ __device__ __forceinline__ int comb_slot_of(const CombineLaunch &p, int bx, int 
     if (x >= (unsigned)V.dim_x || y >= (unsigned)V.dim_y || z >= (unsigned)V.dim_z) return -1;
     const int gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + y) * V.dim_x + x]);
     if (gv < 0) return -1;
-    e = gv & 0x3fffffff;
+    e = gv & kGridEntryMask;
   } else {
     const unsigned long long key = pack_key(bx, by, bz);
     unsigned int h = hash_key(key) & V.table_mask;

@@ -32,6 +32,10 @@ constexpr int kRgbApronStride = 736;                 // uchar4 records per brick
 constexpr int kRangeTile = 8;                        // range-pass tile (pixels)
 constexpr int kViewsPerLaunch = 256;
 constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
+// dense location grid value of an allocated location: hash entry | present directions << 24 |
+// surface bit << 30 (so a location resolves with one 4-B load); negative = empty-space distance
+constexpr int kGridEntryBits = 24;
+constexpr int kGridEntryMask = (1 << kGridEntryBits) - 1;
 
 // Hash-table entry: one per block location (x,y,z); the six direction slots are block ids
 // (rows of the pool / apron) or -1.  32 B = one sector: one probe returns all directions.
@@ -258,8 +262,8 @@ cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsig
                           CommitScratch sc, cudaStream_t s);
 cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
                           int dim_x, int dim_y, cudaStream_t s);
-cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, int *grid,
-                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
+cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, const HashEntry *table,
+                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
 cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,

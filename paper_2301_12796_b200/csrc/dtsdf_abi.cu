@@ -385,7 +385,7 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   end_timed(c, s, &tl);
   // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
   // raycast resolves locations through the bitmaps and the hash table
-  if (cells > 0 && cells <= (size_t(1) << 28)) {
+  if (cells > 0 && cells <= (size_t(1) << 28) && c->table_cap <= (size_t(1) << kGridEntryBits)) {
     if (ensure(c->loc_grid, c->cap_loc_grid, cells * 4) != cudaSuccess) {
       cudaGetLastError();
       c->loc_grid = nullptr;
@@ -393,8 +393,8 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
       c->index_bytes += cells * 4;
       CK(c, cudaMemsetAsync(c->loc_grid, 0xFF, cells * 4, s), "grid init");
       begin_timed(c, 2, s, &tl);
-      CK(c, launch_loc_grid(c->locations, c->n_loc, c->surface, c->loc_grid, lo[0], lo[1], lo[2], c->dim[0],
-                            c->dim[1], s),
+      CK(c, launch_loc_grid(c->locations, c->n_loc, c->surface, c->table, c->loc_grid, lo[0], lo[1], lo[2],
+                            c->dim[0], c->dim[1], s),
          "loc_grid");
       end_timed(c, s, &tl);
       if (ensure(c->dist_tmp, c->cap_dist, 2 * cells) == cudaSuccess) {

@@ -787,20 +787,19 @@ struct RayT {
           gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + y) * V.dim_x + x]);
         else
           gv = -0x7fffffff;
-        DTSDF_CHECK(gv < 0 || (long long)(gv & 0x3fffffff) < V.table_cap);
+        DTSDF_CHECK(gv < 0 || (long long)(gv & kGridEntryMask) < V.table_cap);
         cur.occ = gv >= 0;
         cur.dist = gv == -0x7fffffff ? 0 : (gv < 0 ? -gv : 0);
         cur.surf = (gv >> 30) & 1;
         if (cur.occ) {
-          cur.entry = gv & 0x3fffffff;
+          cur.entry = gv & kGridEntryMask;
+#if DTSDF_SLOTS_FROM_TABLE
+          cur.present = (gv >> kGridEntryBits) & 63;  // the slots themselves are read when evaluated
+#else
           const int4 *e = reinterpret_cast<const int4 *>(&V.table[cur.entry]);
           const int4 ea = __ldg(e), eb = __ldg(e + 1);
           DTSDF_CHECK(ea.z < V.n_blocks && ea.w < V.n_blocks && eb.x < V.n_blocks && eb.y < V.n_blocks &&
                       eb.z < V.n_blocks && eb.w < V.n_blocks);
-#if DTSDF_SLOTS_FROM_TABLE
-          cur.present = (ea.z >= 0) | (ea.w >= 0) << 1 | (eb.x >= 0) << 2 | (eb.y >= 0) << 3 | (eb.z >= 0) << 4 |
-                        (eb.w >= 0) << 5;
-#else
           cur.slots[0] = ea.z; cur.slots[1] = ea.w; cur.slots[2] = eb.x;
           cur.slots[3] = eb.y; cur.slots[4] = eb.z; cur.slots[5] = eb.w;
 #endif

@@ -172,16 +172,20 @@ __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const 
   if (u < n_loc && cell_dirs) cell_dirs[(size_t)loc[u].w * 512 + l] = (unsigned char)(live | (pos ? 128 : 0));
 }
 
-// Dense location grid: for each allocated location, its hash entry index and surface bit, so
-// the raycast resolves a location with one 4-B load instead of bitmap + surface + hash probe.
+// Dense location grid: for each allocated location, its hash entry index, present directions and
+// surface bit (kGridEntryBits layout), so the raycast resolves a location -- and knows which
+// directions it holds -- with one 4-B load instead of bitmap + surface + hash probe + entry.
 __global__ void k_loc_grid(const int4 *__restrict__ loc, long long n_loc, const unsigned int *__restrict__ surface,
-                           int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
+                           const HashEntry *__restrict__ table, int *grid, int lo_x, int lo_y, int lo_z, int dim_x,
+                           int dim_y) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_loc) return;
   const int4 b = loc[i];
   const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
   const int surf = (surface[cell >> 5] >> (cell & 31)) & 1;
-  grid[cell] = b.w | (surf << 30);
+  int present = 0;
+  for (int d = 0; d < 6; ++d) present |= (table[b.w].slot[d] >= 0) << d;
+  grid[cell] = b.w | (present << kGridEntryBits) | (surf << 30);
 }
 
 // Empty-space distance on the location grid (L-infinity, in blocks, capped): separable passes
@@ -256,10 +260,11 @@ cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *
   return cudaGetLastError();
 }
 
-cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, int *grid,
-                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
+cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, const HashEntry *table,
+                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
   if (n_loc == 0) return cudaSuccess;
-  k_loc_grid<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, surface, grid, lo_x, lo_y, lo_z, dim_x, dim_y);
+  k_loc_grid<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, surface, table, grid, lo_x, lo_y, lo_z, dim_x,
+                                                  dim_y);
   return cudaGetLastError();
 }
 
