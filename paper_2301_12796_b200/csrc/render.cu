@@ -1,17 +1,22 @@
-// render.cu -- the per-pixel DTSDF raycast (SURVEY.md §8 rows a2-a7; DESIGN.md §2, §5).
+// render.cu -- the per-pixel DTSDF raycast (SURVEY.md §8 rows a2-a7; DESIGN.md §2, §5, §6).
 //
 //   k_range_*  (a3) block-bounds range pass: every allocated block location's AABB, clipped
 //              to z >= z_min, is projected into each view; per 8x8 pixel tile the min/max
-//              camera z of the covering blocks is kept with order-independent atomics.
-//   k_raycast  (a2, a4-a7) one thread per pixel, 8x4-pixel warps: lattice march t_k = k*Delta
-//               inside the tile's [z_near, z_far], occupancy-bitmap skipping of
-//              unallocated block locations, one hash probe per block location, per-sample
-//              combination of the six directions (eq:combine_weight / eq:combine_tsdf_weight,
-//              PAPER.md:235-270) read from apron bricks, first +->- crossing, Illinois
-//              regula-falsi refinement, and the shading epilogue (normal, colour, dirmask).
+//              camera z of the covering blocks is kept with order-independent atomics on
+//              epoch-tagged keys, and the covering locations are counted.
+//   k_order    the raycast's CTA tiles of each view, longest predicted first (counting sort of
+//              the per-tile location counts), so slow tiles do not start last.
+//   k_raycast  (a2, a4-a7) one thread per pixel, 8x4-pixel warps, 16x8-pixel CTA tiles taken in
+//              k_order's order: lattice march t_k = k*Delta inside the tile's
+//              [z_near, z_far], empty-space and certainly-positive skipping, one 4-B location-grid
+//              load per block location, per-sample combination of the directions live at the
+//              sample's cell (eq:combine_weight / eq:combine_tsdf_weight) read
+//              from apron bricks, first +->- crossing, bisection + Illinois refinement, and the
+//              shading epilogue (normal, colour, dirmask) after the step loop.
 //
-// Skipping and the range pass are exact accelerations: a lattice point whose base voxel lies
-// in an unallocated block location has no present direction and is invalid (DESIGN.md §2 O2).
+// Every acceleration is exact: skipped lattice points cannot end or start a crossing, skipped
+// directions hold no data at the sample, and the tile order changes only when a tile runs
+// (DESIGN.md §2).
 #include <math_constants.h>
 
 #include <utility>
