@@ -38,3 +38,15 @@ for name in sys.argv[1:] or ["C1"]:
         t = tiles(cyc[..., i])
         print(f"  {nm:14s} share of warp cycles {t.max(1).sum() / tt.max(1).sum():.3f}  mean/ray {cyc[..., i].mean():.0f}")
     np.save(os.path.join(ROOT, "gpurun_out", f"stats_{name}.npy"), np.concatenate([cyc, cnt], -1))
+
+# per-warp step efficiency: a warp runs as many steps as its slowest lane needs
+for name in sys.argv[1:] or ["C1"]:
+    a = np.load(os.path.join(ROOT, "gpurun_out", f"stats_{name}.npy"))
+    H, W = a.shape[:2]
+    ev = a[..., 3] + a[..., 4]  # march + refinement evaluations per ray
+
+    def tiles(x):
+        return x[: H // 4 * 4, : W // 8 * 8].reshape(H // 4, 4, W // 8, 8).transpose(0, 2, 1, 3).reshape(-1, 32)
+    t = tiles(ev)
+    print(f"{name}: evaluations per ray mean {ev.mean():.2f}; per warp max {t.max(1).mean():.2f}; "
+          f"lane efficiency of the step loop {t.mean(1).sum() / t.max(1).sum():.3f}")
