@@ -275,7 +275,8 @@ DTSDF_API void dtsdf_default_icp_params(dtsdf_icp_params *params);
 /* Register a depth frame against a rendered view.  depth f32 [H][W] (camera z, 0 = missing),
  * ref_depth f32 [H][W] and ref_normal f32 [H][W][3] (world frame) as dtsdf_render outputs at
  * ref_pose; shared intrinsics; init_delta (NULL = identity).  Host or device buffers.  All
- * iterations are enqueued on cuda_stream; the call synchronizes once.  Errors: INVALID_ARGUMENT,
+ * iterations are enqueued on cuda_stream in chunks of 4, 8, 16, ...; after each chunk the call reads the
+ * device's convergence flag back (one synchronization per chunk).  Errors: INVALID_ARGUMENT,
  * SINGULAR (the result holds the last DeltaT), OUT_OF_MEMORY, CUDA. */
 DTSDF_API int dtsdf_icp(dtsdf_ctx *ctx, const float *depth, const float *ref_depth, const float *ref_normal,
                         const float ref_pose[16], const dtsdf_intrinsics *intr, const float init_delta[16],

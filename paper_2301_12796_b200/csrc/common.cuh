@@ -233,10 +233,13 @@ struct IcpLaunch {
   int width, height, max_iters;
   double *partials;                // [n_partials][29]
   IcpState *state;
+  double2 *pback;                  // [H][W] ((u - cx) / fx * z, (v - cy) / fy * z) of the frame (k_icp_backproject)
+  double *col_fac, *row_fac;       // [W] (u - cx) / fx, [H] (v - cy) / fy: the rendered pixels' back-projection
 };
 
 // host launchers (icp.cu)
 int icp_partials(int width, int height);
+cudaError_t launch_icp_backproject(const IcpLaunch &p, cudaStream_t s);  // once per call: pback, col/row factors
 cudaError_t launch_icp_reduce(const IcpLaunch &p, cudaStream_t s);
 cudaError_t launch_icp_solve(const IcpLaunch &p, cudaStream_t s);
 

@@ -51,6 +51,9 @@ struct dtsdf_ctx {
   void *fuse_stage = nullptr; // fusion / ICP: device staging of host frames
   double *icp_partials = nullptr;
   IcpState *icp_state = nullptr;
+  int *icp_done_host = nullptr;  // pinned: the done flag read back between chunks of iterations
+  unsigned char *icp_pback = nullptr;  // frame back-projections + column/row factors (icp_prepare)
+  size_t cap_icp_pback = 0;
   size_t cap_icp_partials = 0, cap_icp_state = 0;
   size_t fuse_stage_cap = 0;
   // index
@@ -266,6 +269,8 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   if (c->fuse_stage) cudaFree(c->fuse_stage);
   dfree(c->icp_partials);
   dfree(c->icp_state);
+  if (c->icp_done_host) cudaFreeHost(c->icp_done_host);
+  dfree(c->icp_pback);
   dfree(c->z_near);
   dfree(c->z_far);
   dfree(c->tile_count);
@@ -1088,8 +1093,22 @@ static int icp_prepare(dtsdf_ctx *c, const float *depth, const float *ref_depth,
   }
   L.partials = c->icp_partials;
   L.state = c->icp_state;
+  if (ensure(c->icp_pback, c->cap_icp_pback, px * sizeof(double2) + (K->width + K->height) * sizeof(double)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "ICP back-projections");
+  }
+  L.pback = reinterpret_cast<double2 *>(c->icp_pback);
+  L.col_fac = reinterpret_cast<double *>(c->icp_pback + px * sizeof(double2));
+  L.row_fac = L.col_fac + K->width;
+  TimedLaunch tl{};
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_icp_backproject(L, s), "ICP back-projection");
+  end_timed(c, s, &tl);
   return DTSDF_OK;
 }
+
+constexpr int kIcpChunk = 4;  // iterations enqueued before the first convergence poll (then 8, 16, ...)
 
 int dtsdf_icp(dtsdf_ctx *c, const float *depth, const float *ref_depth, const float *ref_normal,
               const float ref_pose[16], const dtsdf_intrinsics *K, const float init_delta[16],
@@ -1112,13 +1131,29 @@ int dtsdf_icp(dtsdf_ctx *c, const float *depth, const float *ref_depth, const fl
   std::memset(&init, 0, sizeof(init));
   for (int i = 0; i < 16; ++i) init.delta[i] = init_delta ? (double)init_delta[i] : ((i % 5) == 0 ? 1.0 : 0.0);
   CK(c, cudaMemcpyAsync(c->icp_state, &init, sizeof(init), cudaMemcpyHostToDevice, s), "ICP init");
-  TimedLaunch tl{};
-  begin_timed(c, 2, s, &tl, 2 * prm.max_iters);
-  for (int it = 0; it < prm.max_iters; ++it) {
-    CK(c, launch_icp_reduce(L, s), "ICP reduce");
-    CK(c, launch_icp_solve(L, s), "ICP solve");
+  if (!c->icp_done_host && cudaMallocHost((void **)&c->icp_done_host, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "ICP host flag");
   }
-  end_timed(c, s, &tl);
+  // Iterations are enqueued in chunks; between chunks the device's done flag (set by k_icp_solve
+  // on convergence or the cap) is read back, so a converged call does not pay for up to max_iters
+  // no-op launches (a launch after convergence returns at once but still costs a few us).
+  TimedLaunch tl{};
+  int launched = 0;
+  for (int chunk = kIcpChunk; launched < prm.max_iters; chunk *= 2) {
+    const int n = std::min(chunk, prm.max_iters - launched);
+    begin_timed(c, 2, s, &tl, 2 * n);
+    for (int it = 0; it < n; ++it) {
+      CK(c, launch_icp_reduce(L, s), "ICP reduce");
+      CK(c, launch_icp_solve(L, s), "ICP solve");
+    }
+    end_timed(c, s, &tl);
+    launched += n;
+    if (launched >= prm.max_iters) break;
+    CK(c, cudaMemcpyAsync(c->icp_done_host, &c->icp_state->done, sizeof(int), cudaMemcpyDeviceToHost, s), "ICP poll");
+    CK(c, cudaStreamSynchronize(s), "ICP poll sync");
+    if (*c->icp_done_host) break;
+  }
   IcpState fin;
   CK(c, cudaMemcpyAsync(&fin, c->icp_state, sizeof(fin), cudaMemcpyDeviceToHost, s), "ICP readback");
   CK(c, cudaStreamSynchronize(s), "ICP sync");

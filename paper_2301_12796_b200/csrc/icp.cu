@@ -11,7 +11,7 @@
 //                  DeltaT <- exp(xi) DeltaT, termination on |xi| < min_step or the iteration
 //                  cap; sets the done flag that turns the remaining launches into no-ops
 //
-// All iterations are enqueued at once (2 launches each); the host reads the state back once.
+// Iterations are enqueued in chunks (2 launches each); the host polls the done flag between chunks.
 #include "common.cuh"
 
 namespace dtsdf {
@@ -27,8 +27,9 @@ __device__ __forceinline__ void icp_pixel(const IcpLaunch &p, const double *D, i
   const float z = p.depth[pix];
   if (!icp_z_ok(p, z)) return;
   const double zd = (double)z;
-  const double p0 = __dmul_rn(__ddiv_rn(__dsub_rn((double)u, p.cx), p.fx), zd);
-  const double p1 = __dmul_rn(__ddiv_rn(__dsub_rn((double)v, p.cy), p.fy), zd);
+  // the frame point's back-projection, computed once per call (k_icp_backproject, same operations)
+  const double2 pb = p.pback[pix];
+  const double p0 = pb.x, p1 = pb.y;
   double x[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -45,8 +46,8 @@ __device__ __forceinline__ void icp_pixel(const IcpLaunch &p, const double *D, i
   const float nw0 = p.ref_normal[3 * j], nw1 = p.ref_normal[3 * j + 1], nw2 = p.ref_normal[3 * j + 2];
   if (!icp_z_ok(p, zr) || (nw0 == 0.f && nw1 == 0.f && nw2 == 0.f)) return;
   const double zrd = (double)zr;
-  const double q0 = __dmul_rn(__ddiv_rn(__dsub_rn((double)iu, p.cx), p.fx), zrd);
-  const double q1 = __dmul_rn(__ddiv_rn(__dsub_rn((double)iv, p.cy), p.fy), zrd);
+  const double q0 = __dmul_rn(p.col_fac[iu], zrd);  // (iu - cx) / fx * zr, the factor tabulated per column
+  const double q1 = __dmul_rn(p.row_fac[iv], zrd);
   double n[3];  // R_ref^T n_world
 #pragma unroll
   for (int a = 0; a < 3; ++a)
@@ -68,6 +69,20 @@ __device__ __forceinline__ void icp_pixel(const IcpLaunch &p, const double *D, i
   for (int a = 0; a < 6; ++a) acc[21 + a] += w2 * J[a] * r;
   acc[27] += 1.0;
   acc[28] += 0.5 * w2 * r * r;
+}
+
+// Per call: the frame's back-projected points (they do not change between iterations) and the
+// per-column / per-row factors of the rendered pixels' back-projection -- the divisions of
+// icp_pixel hoisted out of the iteration loop with the oracle's operations and roundings.
+__global__ void k_icp_backproject(const __grid_constant__ IcpLaunch p) {
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pix < p.width) p.col_fac[pix] = __ddiv_rn(__dsub_rn((double)pix, p.cx), p.fx);
+  if (pix < p.height) p.row_fac[pix] = __ddiv_rn(__dsub_rn((double)pix, p.cy), p.fy);
+  if (pix >= p.width * p.height) return;
+  const int u = pix % p.width, v = pix / p.width;
+  const double zd = (double)p.depth[pix];
+  p.pback[pix] = make_double2(__dmul_rn(__ddiv_rn(__dsub_rn((double)u, p.cx), p.fx), zd),
+                              __dmul_rn(__ddiv_rn(__dsub_rn((double)v, p.cy), p.fy), zd));
 }
 
 __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(const __grid_constant__ IcpLaunch p) {
@@ -212,6 +227,12 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_solve(const __grid_constant
 
 int icp_partials(int width, int height) {
   return (width * height + kIcpThreads * kIcpPix - 1) / (kIcpThreads * kIcpPix);
+}
+
+cudaError_t launch_icp_backproject(const IcpLaunch &p, cudaStream_t s) {
+  const int n = max(p.width * p.height, max(p.width, p.height));
+  k_icp_backproject<<<(n + 255) / 256, 256, 0, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_icp_reduce(const IcpLaunch &p, cudaStream_t s) {
