@@ -1,7 +1,7 @@
 // icp.cu -- weighted geometric point-to-plane ICP of a depth frame against a rendered view with a
 // deterministic reduction.
 //
-//   k_icp_reduce   fixed pixel -> thread mapping (4 pixels per thread, 1024 per CTA): projective
+//   k_icp_reduce   fixed pixel -> thread mapping (DTSDF_ICP_PIX = 5 pixels per thread, 1280 per CTA): projective
 //                  association of DeltaT p into the rendered view (fp64, the oracle's roundings,
 //                  so both sides associate the same pixels), r = <q - x, n>, J = (-n, -x x n),
 //                  w = w_ICP(z); the 21 + 6 + 2 sums (upper H, g, inliers, sum w r^2) in fp64, reduced
@@ -16,7 +16,10 @@
 
 namespace dtsdf {
 
-constexpr int kIcpThreads = 256, kIcpPix = 4, kIcpSums = 29;
+#ifndef DTSDF_ICP_PIX
+#define DTSDF_ICP_PIX 5  // 1280 pixels per CTA: a 640x480 frame is 240 CTAs, one wave of 2 per SM (4 gave 300: 4 CTAs in a 2nd wave)
+#endif
+constexpr int kIcpThreads = 256, kIcpPix = DTSDF_ICP_PIX, kIcpSums = 29;
 
 __device__ __forceinline__ bool icp_z_ok(const IcpLaunch &p, float z) {
   return z > 0.0f && (double)z >= p.z_min && (double)z <= p.z_max;
