@@ -26,7 +26,6 @@ __device__ __forceinline__ bool icp_z_ok(const IcpLaunch &p, float z) {
 }
 
 __device__ __forceinline__ void icp_pixel(const IcpLaunch &p, const double *D, int pix, double acc[kIcpSums]) {
-  const int u = pix % p.width, v = pix / p.width;
   const float z = p.depth[pix];
   if (!icp_z_ok(p, z)) return;
   const double zd = (double)z;

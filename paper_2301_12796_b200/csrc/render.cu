@@ -754,10 +754,10 @@ struct RayT {
     rsx = r[0] * V.inv_voxel; rsy = r[1] * V.inv_voxel; rsz = r[2] * V.inv_voxel;
     cur.bx = 0x7fffffff; cur.by = 0; cur.bz = 0; cur.occ = false; cur.surf = false; cur.present = 0; cur.entry = -1;
     cur.dist = 1;
-#pragma unroll
 #if DTSDF_SLOTS_FROM_TABLE
     cur.slot0 = -1;
 #else
+#pragma unroll
     for (int d = 0; d < 6; ++d) cur.slots[d] = -1;
 #endif
     mode = kMarch;
@@ -1248,6 +1248,7 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   int u0, v0;
   {
     const int ct = p.order ? __ldg(&p.order[(size_t)blockIdx.z * gridDim.x + blockIdx.x]) : blockIdx.x;
+    DTSDF_CHECK(ct >= 0 && ct < (int)gridDim.x);
     u0 = (ct % p.ct_x) * kTileW;
     v0 = (ct / p.ct_x) * kTileH;
     if (threadIdx.x == 0) { s_origin[0] = u0; s_origin[1] = v0; }
