@@ -78,60 +78,58 @@ __global__ void k_bitmap(const int4 *__restrict__ loc, long long n_loc, unsigned
 }
 
 // One thread per (brick, apron voxel).  Apron voxel a in [0,11)^3 is block-local voxel a-1.
-__global__ void k_apron(const int4 *__restrict__ keys, long long n, const HashEntry *__restrict__ table,
-                        unsigned int mask, const float *__restrict__ sdf, const float *__restrict__ weight,
-                        float2 *__restrict__ apron) {
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long b = gid / kApronStride;
-  int a = (int)(gid - b * kApronStride);
-  if (b >= n) return;
-  float2 out = make_float2(__int_as_float(0x7fc00000), 0.0f);  // NaN sdf = unallocated
-  if (a < kApronVox) {
-    int4 k = keys[b];
-    int ax = a % kApron, ay = (a / kApron) % kApron, az = a / (kApron * kApron);
-    int lx = ax - 1, ly = ay - 1, lz = az - 1;  // -1..9
-    int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
-    int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
-    int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
+// Apron bricks: one CTA per block.  The 27 neighbour slots (same direction) are resolved once into
+// shared memory -- a hash probe per neighbour instead of one per border record -- then the CTA
+// fills the block's 1331 {sdf, weight} records (NaN sdf where the neighbour is unallocated) and
+// its 729 colour records (voxels 0..8) with coalesced stores.
+constexpr int kApronThreads = 256;
+__global__ void __launch_bounds__(kApronThreads) k_apron(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
+                                                        unsigned int mask, const float *__restrict__ sdf,
+                                                        const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
+                                                        float2 *__restrict__ apron, uchar4 *__restrict__ rgb_apron) {
+  __shared__ int nb[27];  // slot of neighbour (ox, oy, oz) in -1..1, index (ox+1) + 3 (oy+1) + 9 (oz+1)
+  const long long b = blockIdx.x;
+  const int4 k = keys[b];
+  if (threadIdx.x < 27) {
+    const int ox = (int)threadIdx.x % 3 - 1, oy = ((int)threadIdx.x / 3) % 3 - 1, oz = (int)threadIdx.x / 9 - 1;
     int src = (int)b;
     if (ox | oy | oz) {
-      int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
+      const int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
       src = (e >= 0) ? table[e].slot[k.w] : -1;
     }
-    if (src >= 0) {
-      int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
-      long long r = (long long)src * kVoxPerBlock + l;
-      out = make_float2(sdf[r], weight[r]);
-    }
-  } else {
-    out = make_float2(__int_as_float(0x7fc00000), 0.0f);
+    nb[threadIdx.x] = src;
   }
-  apron[gid] = out;
-}
-
-__global__ void k_rgb_apron(const int4 *__restrict__ keys, long long n, const HashEntry *__restrict__ table,
-                            unsigned int mask, const unsigned char *__restrict__ rgb, uchar4 *__restrict__ rgb_apron) {
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long b = gid / kRgbApronStride;
-  int a = (int)(gid - b * kRgbApronStride);
-  if (b >= n) return;
-  uchar4 out = make_uchar4(0, 0, 0, 0);
-  if (a < kRgbApronVox && rgb != nullptr) {
-    int4 k = keys[b];
-    int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
-    int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
-    int src = (int)b;
-    if (ox | oy | oz) {
-      int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
-      src = (e >= 0) ? table[e].slot[k.w] : -1;
+  __syncthreads();
+  for (int a = threadIdx.x; a < kApronStride; a += kApronThreads) {
+    float2 out = make_float2(__int_as_float(0x7fc00000), 0.0f);  // NaN sdf = unallocated
+    if (a < kApronVox) {
+      const int lx = a % kApron - 1, ly = (a / kApron) % kApron - 1, lz = a / (kApron * kApron) - 1;  // -1..9
+      const int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
+      const int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
+      const int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
+      const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+      if (src >= 0) {
+        const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+        const long long r = (long long)src * kVoxPerBlock + l;
+        out = make_float2(sdf[r], weight[r]);
+      }
     }
-    if (src >= 0) {
-      int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
-      const unsigned char *c = rgb + 3 * ((long long)src * kVoxPerBlock + l);
-      out = make_uchar4(c[0], c[1], c[2], 0);
-    }
+    apron[b * kApronStride + a] = out;
   }
-  rgb_apron[gid] = out;
+  for (int a = threadIdx.x; a < kRgbApronStride; a += kApronThreads) {
+    uchar4 out = make_uchar4(0, 0, 0, 0);
+    if (a < kRgbApronVox && rgb != nullptr) {
+      const int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
+      const int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
+      const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+      if (src >= 0) {
+        const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+        const unsigned char *c = rgb + 3 * ((long long)src * kVoxPerBlock + l);
+        out = make_uchar4(c[0], c[1], c[2], 0);
+      }
+    }
+    rgb_apron[b * kRgbApronStride + a] = out;
+  }
 }
 
 // Certainly-positive base cells: bit l of location h is set iff, for every direction present
@@ -297,10 +295,7 @@ cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, 
                          const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
                          cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_apron<<<grid_for(n * kApronStride, 256), 256, 0, s>>>(keys, n, table, mask, sdf, weight, apron);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_rgb_apron<<<grid_for(n * kRgbApronStride, 256), 256, 0, s>>>(keys, n, table, mask, rgb, rgb_apron);
+  k_apron<<<(unsigned)n, kApronThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, apron, rgb_apron);
   return cudaGetLastError();
 }
 
