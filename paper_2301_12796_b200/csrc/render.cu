@@ -369,8 +369,15 @@ struct ShadeResult {
 
 __device__ __forceinline__ float lerpf(float a, float b, float t) { return fmaf(t, b - a, a); }
 // a + t (b - a) on a pair: two packed FFMA2 (a - t a, then + t b)
+#ifndef DTSDF_FFMA2
+#define DTSDF_FFMA2 1  // 0: the same two roundings per lane with scalar FFMAs
+#endif
 __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
+#if DTSDF_FFMA2
   return __ffma2_rn(t, b, __ffma2_rn(make_float2(-t.x, -t.y), a, a));
+#else
+  return make_float2(fmaf(t.x, b.x, fmaf(-t.x, a.x, a.x)), fmaf(t.y, b.y, fmaf(-t.y, a.y, a.y)));
+#endif
 }
 
 #define APRON_IDX(dx, dy, dz) (((dx) + 1) + kApron * ((dy) + 1) + kApron * kApron * ((dz) + 1))
