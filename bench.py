@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU code path (NCCL process group, volume broadcast into library buffers, "
                          "checksum all-gather, max over ranks) even at world size 1")
+    ap.add_argument("--shard", choices=["none", "views", "rows"], default="none",
+                    help="none: every rank renders its own --views views (weak scaling, the default); views: the "
+                         "--views views of one batch are split into contiguous ranges per rank (SURVEY §8(e), C3); "
+                         "rows: every view's rows are split per rank via row0/row1 (C4's large view) -- strong scaling")
     ap.add_argument("--combine-mode", type=int, default=0, choices=[0, 1],
                     help="combined mode: 0 eq:combine_weight (the paper's method), 1 Algorithm 1 (NEXT-4)")
     return ap.parse_args()
@@ -268,11 +272,25 @@ def run_dtsdf(args):
         R.upload_volume(w.volume)
     upload_ms = 1e3 * (time.perf_counter() - t_up)
     K = w.intrinsics
-    # this rank's views: round-robin over the config's poses (configs[1] has one)
-    idx = [(rank * args.views + i) % len(w.poses) for i in range(args.views)]
+    # this rank's views: round-robin over the config's poses (configs[1] has one).  Weak scaling:
+    # every rank renders its own --views views; --shard views / rows split one batch (strong scaling)
+    row0, row1 = 0, K.height
+    if args.shard == "views":
+        if args.views < world:
+            raise SystemExit("--shard views needs at least one view per rank")
+        lo, hi = pdist.shard_range(args.views, rank, world)
+        idx = [i % len(w.poses) for i in range(lo, hi)]
+        total_rays = K.width * K.height * args.views
+    elif args.shard == "rows":
+        idx = [i % len(w.poses) for i in range(args.views)]
+        row0, row1 = pdist.shard_range(K.height, rank, world)
+        total_rays = K.width * K.height * args.views
+    else:
+        idx = [(rank * args.views + i) % len(w.poses) for i in range(args.views)]
+        total_rays = world * K.width * K.height * args.views
     poses = np.ascontiguousarray(np.asarray(w.poses, np.float32)[idx])
-    rays_per_step = K.width * K.height * args.views
-    out = R.render(poses, K)
+    rays_per_step = K.width * (row1 - row0) * len(idx)  # this rank's
+    out = R.render(poses, K, row0=row0, row1=row1)
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     # combined mode (NEXT-1): every view is one frame of a sequence; before rendering it the
@@ -283,7 +301,7 @@ def run_dtsdf(args):
 
     def step(d, n, c, m, host=False):
         if args.mode == "direct":
-            R.render_into(poses, K, d, n, c, m, stream=stream)
+            R.render_into(poses, K, d, n, c, m, row0=row0, row1=row1, stream=stream)
             return
         for i in range(len(poses)):
             f = seq["frame"]
@@ -292,7 +310,7 @@ def run_dtsdf(args):
                 seq["last"], seq["last_pose"] = f, poses[i]
                 seq["combines"] += 1
             sl = slice(i, i + 1)
-            R.render_combined_into(poses[sl], K, d[sl], n[sl], c[sl], m[sl], stream=stream)
+            R.render_combined_into(poses[sl], K, d[sl], n[sl], c[sl], m[sl], row0=row0, row1=row1, stream=stream)
             seq["frame"] = f + 1
 
     clocks = ClockSampler(local)
@@ -327,8 +345,9 @@ def run_dtsdf(args):
     out_sum = pdist.checksum({"keys": out["depth"], "sdf": out["normal"], "weight": out["color"], "rgb": out["mask"]})
     if use_dist:
         sums = [None] * world
-        dist.all_gather_object(sums, (out_sum, [int(i) for i in idx]))
-        same = [s for s, v in sums if v == [int(i) for i in idx]]
+        mine = ([int(i) for i in idx], row0, row1)
+        dist.all_gather_object(sums, (out_sum, mine))
+        same = [s for s, v in sums if v == mine]
         replicas_equal = len(set(same)) == 1
     else:
         replicas_equal = None
@@ -337,7 +356,7 @@ def run_dtsdf(args):
     kt = R.kernel_times()
     total_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     max_ms = pdist.max_over_ranks(dist, total_ms, dev) if use_dist else total_ms
-    value = world * rays_per_step * args.steps / (max_ms / 1e3) / 1e6
+    value = total_rays * args.steps / (max_ms / 1e3) / 1e6
 
     # ---- roofline of the dominant kernel (raycast) ----
     ray_ms = kt["raycast_ms"] / max(kt["raycast_launches"], 1)
@@ -380,8 +399,8 @@ def run_dtsdf(args):
         roof["recombinations_per_step"] = combines / args.steps
 
     # ---- end to end through the C ABI with pinned HOST outputs (copies inside the timing) ----
-    H, W = K.height, K.width
-    V = args.views
+    H, W = row1 - row0, K.width  # this rank's share
+    V = len(idx)
     hd = torch.empty((V, H, W), dtype=torch.float32).pin_memory()
     hn = torch.empty((V, H, W, 3), dtype=torch.float32).pin_memory()
     hc = torch.empty((V, H, W, 3), dtype=torch.uint8).pin_memory()
@@ -409,12 +428,12 @@ def run_dtsdf(args):
     e2e_copy = e2e_run()
     R.set_option(OPT_HOST_WRITE, 1)  # default: the kernel writes the pinned outputs directly
     e2e_max = e2e_run()
-    e2e = {"value": world * rays_per_step * e2e_steps / e2e_max / 1e6, "unit": UNIT,
+    e2e = {"value": total_rays * e2e_steps / e2e_max / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(pose_host.numel() * 4 + 32),
            "d2h_bytes_per_step": int(hd.numel() * 4 + hn.numel() * 4 + hc.numel() + hm.numel()),
            "timing": "host wall clock per dtsdf_render_batch call into pinned host outputs, written by the "
                      "raycast across the host link (DTSDF_OPT_HOST_WRITE)",
-           "copy_path_value": world * rays_per_step * e2e_steps / e2e_copy / 1e6}
+           "copy_path_value": total_rays * e2e_steps / e2e_copy / 1e6}
 
     if rank != 0:
         dist.barrier() if use_dist else None
@@ -433,11 +452,15 @@ def run_dtsdf(args):
     st = R.stats()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.shard == "none" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scene, DESIGN.md §3)",
         "config": dict(describe(w, args.views), mode=args.mode,
-                       **({"combine_mode": args.combine_mode} if args.mode == "combined" else {})),
-        "frames_per_s": world * args.views * args.steps / (max_ms / 1e3),
+                       **({"combine_mode": args.combine_mode} if args.mode == "combined" else {}),
+                       **({"shard": args.shard, "views_per_step_total": args.views,
+                           "views_per_step_per_gpu": len(idx), "rows_per_gpu": row1 - row0}
+                          if args.shard != "none" else {})),
+        "frames_per_s": total_rays / (K.width * K.height) * args.steps / (max_ms / 1e3),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
         "extra": {"upload_and_index_ms": upload_ms, "broadcast_ms": bcast_ms, "n_locations": st["n_locations"],
