@@ -29,7 +29,10 @@ constexpr int kApronStride = 1344;                   // float2 records per brick
 constexpr int kRgbApron = 9;                         // colour apron: voxels 0..8 per axis (trilinear corners)
 constexpr int kRgbApronVox = kRgbApron * kRgbApron * kRgbApron;  // 729
 constexpr int kRgbApronStride = 736;                 // uchar4 records per brick (2944 B)
-constexpr int kRangeTile = 8;                        // range-pass tile (pixels)
+#ifndef DTSDF_RANGE_TILE
+#define DTSDF_RANGE_TILE 8
+#endif
+constexpr int kRangeTile = DTSDF_RANGE_TILE;         // range-pass tile (pixels)
 constexpr int kViewsPerLaunch = 256;
 constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
 // dense location grid value of an allocated location: hash entry | present directions << 24 |

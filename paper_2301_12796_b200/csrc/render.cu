@@ -739,7 +739,7 @@ struct RayT {
       ir[q] = 1.0f / r[q];
     }
     // O2 lattice bounds, narrowed to the tile's block range (a3)
-    const size_t tile = ((size_t)view * p.tiles_y + (vrel >> 3)) * p.tiles_x + (u >> 3);
+    const size_t tile = ((size_t)view * p.tiles_y + vrel / kRangeTile) * p.tiles_x + u / kRangeTile;
     const unsigned long long kn = __ldg(&p.z_near[tile]), kf = __ldg(&p.z_far[tile]);
     // a tile no block of this pass projected onto still holds keys of an earlier epoch: empty
     const bool covered = (kn >> 32) == (0xFFFFFFFFu - p.epoch) && (kf >> 32) == p.epoch;
