@@ -1,8 +1,9 @@
 """GPU-vs-oracle parity beyond the fixed config seeds: fresh seeded rooms (configs[1] recipe) and
-thin-plate clusters (configs[2] recipe, fewer plates), one full-frame view each, compared with the
+thin-plate clusters (configs[2] recipe, fewer plates) and dense spheres (configs[0] recipe, random
+radius and viewpoint), one full-frame view each, compared with the
 BASELINE.json tolerances (tests/parity.py).  Calls oracle/ and scenes/ only for the reference.
 
-    python tools/seed_sweep.py [--rooms 8] [--plates 4]   -> one JSON line per scene
+    python tools/seed_sweep.py [--rooms 8] [--plates 4] [--spheres 0]   -> one JSON line per scene
 """
 import argparse
 import json
@@ -51,26 +52,36 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rooms", type=int, default=8)
     ap.add_argument("--plates", type=int, default=4)
+    ap.add_argument("--spheres", type=int, default=0, help="dense spheres (configs[0] recipe), random radius and view")
     args = ap.parse_args()
     R = Renderer(0)
     K = scenes.Intrinsics(**ROOM_K)
-    cases = [("room", s) for s in range(args.rooms)] + [("plates", s) for s in range(args.plates)]
+    cases = ([("room", s) for s in range(args.rooms)] + [("plates", s) for s in range(args.plates)] +
+             [("sphere", s) for s in range(args.spheres)])
     worst = 0.0
     for kind, s in cases:
-        rng = np.random.default_rng([7, 100 + s] if kind == "room" else [8, 100 + s])
-        if kind == "room":
+        seed = {"room": 7, "plates": 8, "sphere": 9}[kind]
+        rng = np.random.default_rng([seed, 100 + s])
+        Kc = K
+        if kind == "sphere":
+            vol = scenes.sphere_volume(radius=rng.uniform(0.12, 0.28), voxel_size=0.01, truncation=0.04, theta=THETA)
+            d = rng.normal(size=3)
+            d /= np.linalg.norm(d)
+            pose = scenes.look_at(d * rng.uniform(0.45, 0.9), rng.uniform(-0.05, 0.05, size=3))
+            Kc = scenes.Intrinsics(fx=140.0, fy=140.0, cx=79.5, cy=59.5, width=160, height=120)
+        elif kind == "room":
             pat, pose = room_patches(rng, n_boxes=20), room_pose(rng)
             vol = scenes.patch_fill_c(pat, voxel_size=0.01, truncation=0.04, theta=THETA)
         else:
             pat, pose = plate_scene(rng)
             vol = scenes.patch_fill_c(pat, voxel_size=0.005, truncation=0.02, theta=THETA)
         R.upload_volume(vol)
-        g = R.render(pose[None], K)
-        o = oracle.OracleVolume(vol).render(pose, K)
+        g = R.render(pose[None], Kc)
+        o = oracle.OracleVolume(vol).render(pose, Kc)
         st = compare({k: v[0].cpu().numpy() for k, v in g.items()}, o)
         ok = st["budget_used"] <= 1e-3 and st["color_exact"] >= 0.999 and st["mask_equal"] >= 0.999
         worst = max(worst, st["budget_used"])
-        print(json.dumps({"scene": kind, "seed": [7 if kind == "room" else 8, 100 + s], "blocks": int(vol.n_blocks),
+        print(json.dumps({"scene": kind, "seed": [seed, 100 + s], "blocks": int(vol.n_blocks),
                           "hits": st["hits_gpu"], "hit_disagree": st["hit_disagree"],
                           "geom_out_of_tol": st["geom_out_of_tol"], "budget_used": st["budget_used"],
                           "color_exact": st["color_exact"], "mask_equal": st["mask_equal"],
