@@ -122,6 +122,28 @@ def c2_thin(n_clusters=10, plates_per_cluster=20) -> Workload:
     return Workload("C2", vol, Intrinsics(**ROOM_K), np.stack(poses), pat, {"plates": plates})
 
 
+def plate_cluster(rng, n_plates=40):
+    """One configs[2]-style cluster (plates 2-6 mm thick within 20 degrees of a random cluster normal,
+    front/back faces with their own colours) and a camera 0.8 m out on a random side of it."""
+    pat = Patches.empty()
+    cc = rng.uniform(-0.2, 0.2, size=3)
+    nc = _unit_sphere(rng)
+    for _ in range(n_plates):
+        while True:
+            n = _unit_sphere(rng)
+            if n @ nc >= np.cos(np.deg2rad(20.0)):
+                break
+        center = cc + rng.uniform(-0.25, 0.25, size=3)
+        hu, hv = 0.5 * rng.uniform(0.1, 0.3, size=2)
+        thick = rng.uniform(0.002, 0.006)
+        cf, cb = rng.integers(0, 256, 3), rng.integers(0, 256, 3)
+        u, v = _orthonormal(n, rng)
+        pat.extend(center + 0.5 * thick * n, n, u, v, hu, hv, cf)
+        pat.extend(center - 0.5 * thick * n, -n, u, v, hu, hv, cb)
+    side = 1.0 if rng.uniform() < 0.5 else -1.0
+    return pat, look_at(cc + side * 0.8 * nc, cc)
+
+
 def orbit_poses(rng, n_views=256, step_m=0.05, step_deg=2.0, height=1.5, target=(0, 0, 0)):
     """configs[3] trajectory: an orbit whose 2-degree steps are 0.05 m chords."""
     radius = step_m / np.deg2rad(step_deg)

@@ -22,32 +22,6 @@ from scenes.configs import ROOM_K, THETA, room_patches, room_pose  # noqa: E402
 from paper_2301_12796_b200 import Renderer  # noqa: E402
 
 
-def plate_scene(rng, n_plates=40):
-    pat = scenes.Patches.empty()
-    cc = rng.uniform(-0.2, 0.2, size=3)
-    nc = rng.normal(size=3)
-    nc /= np.linalg.norm(nc)
-    for _ in range(n_plates):
-        while True:
-            n = rng.normal(size=3)
-            n /= np.linalg.norm(n)
-            if n @ nc >= np.cos(np.deg2rad(20.0)):
-                break
-        center = cc + rng.uniform(-0.25, 0.25, size=3)
-        hu, hv = 0.5 * rng.uniform(0.1, 0.3, size=2)
-        thick = rng.uniform(0.002, 0.006)
-        cf, cb = rng.integers(0, 256, 3), rng.integers(0, 256, 3)
-        a = np.array([1.0, 0, 0]) if abs(n[0]) < 0.9 else np.array([0, 1.0, 0])
-        u = np.cross(n, a)
-        u /= np.linalg.norm(u)
-        v = np.cross(n, u)
-        pat.extend(center + 0.5 * thick * n, n, u, v, hu, hv, cf)
-        pat.extend(center - 0.5 * thick * n, -n, u, v, hu, hv, cb)
-    side = 1.0 if rng.uniform() < 0.5 else -1.0
-    pose = scenes.look_at(cc + side * 0.8 * nc, cc)
-    return pat, pose
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rooms", type=int, default=8)
@@ -73,7 +47,7 @@ def main():
             pat, pose = room_patches(rng, n_boxes=20), room_pose(rng)
             vol = scenes.patch_fill_c(pat, voxel_size=0.01, truncation=0.04, theta=THETA)
         else:
-            pat, pose = plate_scene(rng)
+            pat, pose = scenes.configs.plate_cluster(rng)
             vol = scenes.patch_fill_c(pat, voxel_size=0.005, truncation=0.02, theta=THETA)
         R.upload_volume(vol)
         g = R.render(pose[None], Kc)
