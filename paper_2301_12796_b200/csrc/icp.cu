@@ -20,6 +20,10 @@ namespace dtsdf {
 #define DTSDF_ICP_PIX 5  // 1280 pixels per CTA: a 640x480 frame is 240 CTAs, one wave of 2 per SM (4 gave 300: 4 CTAs in a 2nd wave)
 #endif
 constexpr int kIcpThreads = 256, kIcpPix = DTSDF_ICP_PIX, kIcpSums = 29;
+#ifndef DTSDF_ICP_UNROLL
+#define DTSDF_ICP_UNROLL 1
+#endif
+constexpr int kIcpUnroll = DTSDF_ICP_UNROLL;  // pixels of a thread in flight together
 
 __device__ __forceinline__ bool icp_z_ok(const IcpLaunch &p, float z) {
   return z > 0.0f && (double)z >= p.z_min && (double)z <= p.z_max;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(const __grid_constan
 #pragma unroll
   for (int k = 0; k < kIcpSums; ++k) acc[k] = 0.0;
   const int npix = p.width * p.height;
-#pragma unroll 1
+#pragma unroll kIcpUnroll
   for (int k = 0; k < kIcpPix; ++k) {
     const int pix = blockIdx.x * (kIcpThreads * kIcpPix) + k * kIcpThreads + tid;
     if (pix < npix) icp_pixel(p, s_d, pix, acc);
