@@ -309,7 +309,7 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *                         every direction present at the block location */
 #define DTSDF_OPT_CELL_DIRS 8
 /* Tuning (results unchanged):
- *   DTSDF_OPT_SCHEDULE    0 (default) one CTA per 16x16-pixel tile; 1 persistent warps pulling
+ *   DTSDF_OPT_SCHEDULE    0 (default) one CTA per 16x8-pixel tile (in the tile order); 1 persistent warps pulling
  *                         8x4-pixel tiles from an atomic counter
  *   DTSDF_OPT_LOCATION_GRID 1 (default) resolve block locations through the dense location grid
  *                         (built when the location AABB has <= 2^28 cells); 0 through the
