@@ -440,6 +440,25 @@ __device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, 
 #endif
 }
 
+#ifndef DTSDF_GRAD_DIFF
+#define DTSDF_GRAD_DIFF 1  // profiles/r1n_sweep_grad_sel.jsonl: C1 -0.9 %, C2 out-of-tolerance pixels 48 -> 27
+#endif
+#ifndef DTSDF_SEL_PTX
+#define DTSDF_SEL_PTX 1  // C1 -1.8 %, C2 -2.3 % (profiles/r1n_sweep_grad_sel.jsonl)
+#endif
+// (a, b, c)[axis] without a branch (the ternary chain compiles to a divergent branch region)
+__device__ __forceinline__ float sel3(int axis, float a, float b, float c) {
+#if DTSDF_SEL_PTX
+  float r;
+  asm("{\n\t.reg .pred p0, p1;\n\tsetp.eq.s32 p0, %1, 0;\n\tsetp.eq.s32 p1, %1, 1;\n\t"
+      "selp.f32 %0, %3, %4, p1;\n\tselp.f32 %0, %2, %0, p0;\n\t}"
+      : "=f"(r) : "r"(axis), "f"(a), "f"(b), "f"(c));
+  return r;
+#else
+  return axis == 0 ? a : (axis == 1 ? b : c);
+#endif
+}
+
 // F(x, r) of DESIGN.md §2 O3 for the sample at base voxel (block-local l, fractions f) of the
 // current cursor location; with shade = true also the shading sums of O7.  One instance of this
 // body is compiled (runtime direction loop) to keep the kernel inside the instruction cache.
@@ -500,6 +519,20 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     // bilinear interpolant of the stencil layer d along axis a
     const float R0 = R0w.x, R1 = R1w.x;
     // (P0, P1): bilinear over (y, z) of the corner columns x = 0, 1
+#if DTSDF_GRAD_DIFF
+    // the same central differences as bilinears of the layer differences (A1 - A-1, A2 - A0): the
+    // pairs are formed from fresh FADD results instead of register moves between loaded records
+    (void)R0; (void)R1;
+    const float2 Dx = lerp2(lerp2(make_float2(c100.x - xm00, xp00 - c000.x), make_float2(c110.x - xm10, xp10 - c010.x), fy2),
+                            lerp2(make_float2(c101.x - xm01, xp01 - c001.x), make_float2(c111.x - xm11, xp11 - c011.x), fy2), fz2);
+    const float2 Dy = lerp2(lerp2(make_float2(c010.x - ym00, yp00 - c000.x), make_float2(c110.x - ym10, yp10 - c100.x), fx2),
+                            lerp2(make_float2(c011.x - ym01, yp01 - c001.x), make_float2(c111.x - ym11, yp11 - c101.x), fx2), fz2);
+    const float2 Dz = lerp2(lerp2(make_float2(c001.x - zm00, zp00 - c000.x), make_float2(c101.x - zm10, zp10 - c100.x), fx2),
+                            lerp2(make_float2(c011.x - zm01, zp01 - c010.x), make_float2(c111.x - zm11, zp11 - c110.x), fx2), fy2);
+    const float gx = lerpf(Dx.x, Dx.y, fx) * half_inv_s;
+    const float gy = lerpf(Dy.x, Dy.y, fy) * half_inv_s;
+    const float gz = lerpf(Dz.x, Dz.y, fz) * half_inv_s;
+#else
     const float2 P01 = lerp2(lerp2(make_float2(c000.x, c100.x), make_float2(c010.x, c110.x), fy2),
                              lerp2(make_float2(c001.x, c101.x), make_float2(c011.x, c111.x), fy2), fz2);
     // (Q0, Q1) from the x-lerped rows
@@ -514,6 +547,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     const float gx = lerpf(P01.y - Pmp.x, Pmp.y - P01.x, fx) * half_inv_s;
     const float gy = lerpf(Q01.y - Qmp.x, Qmp.y - Q01.x, fy) * half_inv_s;
     const float gz = lerpf(R1 - Rmp.x, Rmp.y - R0, fz) * half_inv_s;
+#endif
 #if DTSDF_FAST_NORM
     const float gn2 = gx * gx + gy * gy + gz * gz;  // |g|^2: |g| > 1e-3 <=> |g|^2 > 1e-6 (up to rounding)
 #else
@@ -522,7 +556,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     // v^D = sign * e_axis
     const int axis = D >> 1;
     const float sign = (D & 1) ? -1.0f : 1.0f;
-    const float r_axis = axis == 0 ? rx : (axis == 1 ? ry : rz);
+    const float r_axis = sel3(axis, rx, ry, rz);
     // eq:combine_tsdf_weight: omega * max(0, <v^D, -r>)
     const float W2 = omega * fmaxf(-sign * r_axis, 0.0f);
     S2 += W2;
@@ -538,7 +572,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
       const float ig = 1.0f / gn;
 #endif
       nx = gx * ig; ny = gy * ig; nz = gz * ig;
-      const float n_axis = axis == 0 ? nx : (axis == 1 ? ny : nz);
+      const float n_axis = sel3(axis, nx, ny, nz);
       const float nr = -(nx * rx + ny * ry + nz * rz);
       // eq:combine_weight: w_dir(<n,v>) * max(0, <n,-r>) * omega
       W1 = w_dir(sign * n_axis, V) * fmaxf(nr, 0.0f) * omega;
@@ -796,7 +830,7 @@ struct RayT {
         const unsigned x = (unsigned)(bx - V.lo_x), y = (unsigned)(by - V.lo_y), z = (unsigned)(bz - V.lo_z);
         int gv = 0;  // outside the AABB: distance 0
         if (x < (unsigned)V.dim_x && y < (unsigned)V.dim_y && z < (unsigned)V.dim_z)
-          gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + y) * V.dim_x + x]);
+          gv = __ldg(&V.loc_grid[(z * (unsigned)V.dim_y + y) * (unsigned)V.dim_x + x]);  // < 2^28 cells: 32-bit index
         else
           gv = -0x7fffffff;
         DTSDF_CHECK(gv < 0 || (long long)(gv & kGridEntryMask) < V.table_cap);
