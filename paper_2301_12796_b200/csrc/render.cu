@@ -446,6 +446,20 @@ __device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, 
 #ifndef DTSDF_SEL_PTX
 #define DTSDF_SEL_PTX 1  // C1 -1.8 %, C2 -2.3 % (profiles/r1n_sweep_grad_sel.jsonl)
 #endif
+#ifndef DTSDF_RSQRT_FTZ
+#define DTSDF_RSQRT_FTZ 1
+#endif
+// 1/sqrt(x) for a normal x > 0 (the caller guarantees x > 1e-6): the MUFU approximation without
+// rsqrtf's subnormal rescaling (identical result for normal inputs, three instructions fewer)
+__device__ __forceinline__ float rsqrt_normal(float x) {
+#if DTSDF_RSQRT_FTZ
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+#else
+  return rsqrtf(x);
+#endif
+}
 // (a, b, c)[axis] without a branch (the ternary chain compiles to a divergent branch region)
 __device__ __forceinline__ float sel3(int axis, float a, float b, float c) {
 #if DTSDF_SEL_PTX
@@ -565,7 +579,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
 #if DTSDF_FAST_NORM
     if (gn2 > 1e-6f) {  // reading R8: gradient present (NaN stencil -> false)
       any_grad = true;
-      const float ig = rsqrtf(gn2);
+      const float ig = rsqrt_normal(gn2);
 #else
     if (gn > 1e-3f) {  // reading R8: gradient present (NaN stencil -> false)
       any_grad = true;
