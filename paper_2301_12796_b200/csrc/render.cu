@@ -446,6 +446,9 @@ __device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, 
 #ifndef DTSDF_SEL_PTX
 #define DTSDF_SEL_PTX 1  // C1 -1.8 %, C2 -2.3 % (profiles/r1n_sweep_grad_sel.jsonl)
 #endif
+#ifndef DTSDF_LA_IDX
+#define DTSDF_LA_IDX 1  // lookahead cells addressed by offsets from the block corner
+#endif
 #ifndef DTSDF_RSQRT_FTZ
 #define DTSDF_RSQRT_FTZ 1
 #endif
@@ -722,7 +725,7 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
 // ------------------------------------------------------------------------------------------
 enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
 #ifndef DTSDF_LOOKAHEAD
-#define DTSDF_LOOKAHEAD 8
+#define DTSDF_LOOKAHEAD 6  // with the block-offset addressing: C1 -1.9 %, C3 -0.9 %, C2 equal vs 8 (profiles/r1n_sweep_lookahead.jsonl)
 #endif
 constexpr int kLookahead = DTSDF_LOOKAHEAD;  // lattice points tested per certainly-positive scan
 
@@ -1042,13 +1045,24 @@ struct RayT {
           // look ahead over the next lattice points of this location at once (independent
           // loads): in a run of certainly-positive points only the last one needs evaluating
           unsigned run = 1u;
+#if DTSDF_LA_IDX
+          // voxel offsets from the cursor block's corner: in the block <=> all three in [0, 8)
+          const int ox = ibx - kBlock * cur.bx, oy = iby - kBlock * cur.by, oz = ibz - kBlock * cur.bz;
+#endif
 #pragma unroll
           for (int j = 1; j < kLookahead; ++j) {
             const float tj = (float)(k + j) * V.delta;
+#if DTSDF_LA_IDX
+            const int ux = ox + (int)floorf(fmaf(tj, rsx, g0x)), uy = oy + (int)floorf(fmaf(tj, rsy, g0y)),
+                      uz = oz + (int)floorf(fmaf(tj, rsz, g0z));
+            const int lj = ux + 8 * uy + 64 * uz;
+            bool ok = ((unsigned)ux < 8u) & ((unsigned)uy < 8u) & ((unsigned)uz < 8u);
+#else
             const int jx = ibx + (int)floorf(fmaf(tj, rsx, g0x)), jy = iby + (int)floorf(fmaf(tj, rsy, g0y)),
                       jz = ibz + (int)floorf(fmaf(tj, rsz, g0z));
             const int lj = (jx & 7) + 8 * (jy & 7) + 64 * (jz & 7);
             bool ok = (jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz;
+#endif
             if constexpr (kComb) ok = ok && cell_positive(p.comb.cell_pos, cur, lj);
             else ok = ok && (cell_byte(V, cur, lj) & 128);
             run |= (unsigned)ok << j;
