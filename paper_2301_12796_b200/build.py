@@ -44,7 +44,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     with open(os.path.join(HERE, "ptxas_report.txt"), "w") as fh:
-        fh.write(res.stdout + res.stderr)
+        # registers / spills per kernel; the per-function compile times are dropped so that a
+        # rebuild of unchanged sources leaves the tracked report unchanged
+        fh.write("".join(ln for ln in (res.stdout + res.stderr).splitlines(keepends=True)
+                         if "Compile time" not in ln))
     if verbose:
         sys.stdout.write(res.stdout + res.stderr)
     os.replace(tmp, LIB)
