@@ -84,8 +84,10 @@ typedef struct {
 
 /* Library-owned device buffers of the current volume (filled by dtsdf_alloc_volume).
  *   keys    int32 [N][4] = (bx, by, bz, D)
- *   sdf     f32   [N][512] normalised signed distance, positive in front (NaN is reserved)
- *   weight  f32   [N][512] distance weight w_d >= 0
+ *   sdf     f32   [N][512] normalised signed distance, positive in front; must be finite
+ *   weight  f32   [N][512] distance weight w_d, finite and >= 0
+ * dtsdf_commit_volume rejects a non-finite sdf or a negative / non-finite weight with
+ * DTSDF_ERR_INVALID_ARGUMENT (NaN is the apron bricks' "unallocated" sentinel).
  *   rgb     u8    [N][512][3] */
 typedef struct {
   int32_t *keys;
@@ -209,7 +211,7 @@ DTSDF_API int dtsdf_should_recombine(const dtsdf_combine_policy *policy, int64_t
  * <= voxel/2 (readings R39-R45). */
 typedef struct {
   float max_weight;     /* 128 */
-  float carve_weight;   /* 1 */
+  float carve_weight;   /* 1; 0 = no carving; negative -> DTSDF_ERR_INVALID_ARGUMENT */
   int32_t carve_radius; /* 2 pixels */
   int32_t reserved;     /* 0 */
 } dtsdf_fusion_params;
@@ -349,6 +351,12 @@ DTSDF_API int64_t dtsdf_launch_count(dtsdf_ctx *ctx);
 
 /* Thread-local message describing the last error on this thread ("" if none). */
 DTSDF_API const char *dtsdf_last_error(void);
+
+/* Thread-local warning left by the last call on this thread that checked volume parameters
+ * (dtsdf_alloc_volume / dtsdf_upload_volume / dtsdf_fusion_reserve): "" when none.  Set when
+ * theta < arccos(1/sqrt(3)) = 54.74 deg, which is accepted but breaks PAPER.md:84's "at least one
+ * direction" claim in 3D (reading R2). */
+DTSDF_API const char *dtsdf_last_warning(void);
 
 #ifdef __cplusplus
 }

@@ -113,10 +113,10 @@ __global__ void __launch_bounds__(256) k_comb_select(const __grid_constant__ Com
 __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ CombineLaunch p,
                                                  const unsigned char *__restrict__ cls_in) {
   const VolumeView &V = p.vol;
-  // the 4 CTAs of a slot are adjacent in launch order (x = quarter, y = slot): they share the
-  // slot's bricks in L2 while they run
-  const size_t slot = blockIdx.y;
-  const int l = blockIdx.x * 128 + threadIdx.x;
+  // the 4 CTAs of a slot are adjacent in launch order (blockIdx.x = 4 slot + quarter, so any
+  // number of slots fits the grid's x extent): they share the slot's bricks in L2 while they run
+  const size_t slot = blockIdx.x >> 2;
+  const int l = (blockIdx.x & 3) * 128 + threadIdx.x;
   const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
   const int4 b = p.comb_loc[slot];
   DTSDF_CHECK(b.w >= 0 && (long long)b.w < V.table_cap);
@@ -327,8 +327,8 @@ __device__ bool dir_normal(const CombineLaunch &p, int D, const double y[3], dou
 __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p,
                                                       const unsigned char *__restrict__ cls_in) {
   const VolumeView &V = p.vol;
-  const size_t slot = blockIdx.y;
-  const int l = blockIdx.x * 128 + threadIdx.x;
+  const size_t slot = blockIdx.x >> 2;  // as k_combine: 4 adjacent CTAs per slot on grid x
+  const int l = (blockIdx.x & 3) * 128 + threadIdx.x;
   const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
   const int4 b = p.comb_loc[slot];
   const int4 *ent = reinterpret_cast<const int4 *>(&V.table[b.w]);
@@ -594,10 +594,12 @@ cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s) {
 
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s) {
   if (n_sel == 0) return cudaSuccess;
+  // one grid row of 4 CTAs per slot would cap n_sel at gridDim.y's 65535: the slots go on x
+  const unsigned grid = (unsigned)(4 * n_sel);
   if (p.mode == 1)
-    k_combine_alg1<<<dim3(4, (unsigned)n_sel), 128, 0, s>>>(p, p.surf);
+    k_combine_alg1<<<grid, 128, 0, s>>>(p, p.surf);
   else
-    k_combine<<<dim3(4, (unsigned)n_sel), 128, 0, s>>>(p, p.surf);
+    k_combine<<<grid, 128, 0, s>>>(p, p.surf);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_comb_finish<<<(unsigned)n_sel, kFinishThreads, 0, s>>>(p);

@@ -259,11 +259,13 @@ cudaError_t launch_comb_remap(const HashEntry *table, unsigned int mask, int4 *c
 
 // host launchers (volume.cu); all run on stream s and return the first launch error
 struct CommitScratch {
-  int *flags;          // [0] bad key, [1] duplicate, [2] table full
+  int *flags;          // [0] bad key, [1] duplicate, [2] table full, [3] non-finite sdf / bad weight
   int *aabb;           // [6] min xyz, max xyz
   unsigned long long *n_loc;
 };
 cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s);
+cudaError_t launch_validate_values(const float *sdf, const float *weight, long long n, CommitScratch sc,
+                                   cudaStream_t s);
 cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsigned int mask, int4 *locations,
                           CommitScratch sc, cudaStream_t s);
 cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,

@@ -19,6 +19,7 @@ using namespace dtsdf;
 namespace {
 
 thread_local std::string g_err;
+thread_local std::string g_warn;  // dtsdf_last_warning: accepted-but-questionable arguments
 
 int fail(int code, const std::string &msg) {
   g_err = msg;
@@ -42,6 +43,7 @@ struct dtsdf_ctx {
   // current volume
   dtsdf_volume_params params{};
   bool allocated = false, committed = false;
+  bool values_trusted = false;  // set by dtsdf_fuse around its re-commit: its own kernels wrote the values
   int32_t *keys = nullptr;
   float *sdf = nullptr, *weight = nullptr;
   uint8_t *rgb = nullptr;
@@ -182,6 +184,12 @@ int check_params(const dtsdf_volume_params *p) {
   const double pi = 3.14159265358979323846;
   if (!(p->theta > pi / 4) || !(p->theta <= pi / 2 + 1e-6))
     return fail(DTSDF_ERR_INVALID_ARGUMENT, "theta must lie in (pi/4, pi/2]");
+  // reading R2: PAPER.md:84's "at least one and at most three directions" holds in 3D only for
+  // theta >= arccos(1/sqrt(3)) = 54.74 deg; below it some normals get no direction (accepted)
+  g_warn.clear();
+  if ((double)p->theta < std::acos(1.0 / std::sqrt(3.0)))
+    g_warn = "theta < 54.74 deg (arccos(1/sqrt(3))): surfaces whose normal is near a cube diagonal belong to no "
+             "direction (PAPER.md:84's 1-3 directions claim fails in 3D, reading R2)";
   if (!(p->step >= 0.f) || !std::isfinite(p->step)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "step must be >= 0");
   if (p->n_blocks < 0 || p->n_blocks > (int64_t)INT32_MAX) return fail(DTSDF_ERR_INVALID_ARGUMENT, "bad n_blocks");
   return DTSDF_OK;
@@ -238,6 +246,7 @@ void end_timed(dtsdf_ctx *c, cudaStream_t s, TimedLaunch *tl) {
 extern "C" {
 
 const char *dtsdf_last_error(void) { return g_err.c_str(); }
+const char *dtsdf_last_warning(void) { return g_warn.c_str(); }
 
 int dtsdf_create(int cuda_device, dtsdf_ctx **out) {
   if (!out) return fail(DTSDF_ERR_INVALID_ARGUMENT, "out is NULL");
@@ -331,10 +340,16 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   begin_timed(c, 2, s, &tl);
   CK(c, launch_validate_aabb(reinterpret_cast<const int4 *>(c->keys), n, sc, s), "validate");
   end_timed(c, s, &tl);
+  if (!c->values_trusted) {  // user-written values: sdf finite (NaN is the apron's sentinel), weight >= 0
+    begin_timed(c, 2, s, &tl);
+    CK(c, launch_validate_values(c->sdf, c->weight, n, sc, s), "validate values");
+    end_timed(c, s, &tl);
+  }
   int host[14];
   CK(c, cudaMemcpyAsync(host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, s), "commit readback");
   CK(c, cudaStreamSynchronize(s), "commit sync");
   if (host[0]) return fail(DTSDF_ERR_INVALID_ARGUMENT, "block key with D outside 0..5 or coordinate out of range");
+  if (host[3]) return fail(DTSDF_ERR_INVALID_ARGUMENT, "sdf must be finite and weight finite and >= 0");
   // hash table: capacity = next power of two >= 2N (load factor <= 1/2 over locations)
   unsigned int cap = 64;
   while ((long long)cap < 2 * std::max<long long>(n, c->cap)) cap <<= 1;  // room for fusion to grow into
@@ -1045,7 +1060,9 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   if (new_blocks) *new_blocks = n_new - c->n;
   c->n = n_new;
   c->params.n_blocks = n_new;
+  c->values_trusted = true;  // this library's fusion kernels wrote every value
   rc = dtsdf_commit_volume(c, stream);
+  c->values_trusted = false;
   if (rc) return rc;
   if (full) return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion capacity exhausted (blocks allocated so far are kept)");
   return DTSDF_OK;

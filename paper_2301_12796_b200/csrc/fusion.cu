@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     const size_t r = (size_t)b * kVoxPerBlock + l;
     if (ddd < -1.0) continue;  // behind the surface beyond the band: untouched
     if (ddd > 1.0) {
-      // R43: free space, unless a depth within the guard radius differs by more than tau
+      // R43: free space, unless a depth within the guard radius differs by more than tau;
+      // carve_weight 0 turns carving off (on a fresh voxel, W0 = 0, the update would be 0/0)
+      if (!(p.carve_weight > 0.f)) continue;
       bool edge = false;
       for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
         for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {

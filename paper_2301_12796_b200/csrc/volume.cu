@@ -33,6 +33,21 @@ __global__ void k_validate_aabb(const int4 *__restrict__ keys, long long n, int 
   atomicMax(&aabb[5], k.z);
 }
 
+// Voxel values: sdf must be finite (the apron bricks use NaN as their "unallocated" sentinel, so a
+// NaN in the input would silently read as an absent direction) and weights finite and >= 0
+// (eq:combine_weight and eq:combine_tsdf_weight are proportional to the weight).  flags[3] <- 1.
+__global__ void __launch_bounds__(256) k_validate_values(const float4 *__restrict__ sdf, const float4 *__restrict__ w,
+                                                         long long n4, int *flags) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(sdf + i), b = __ldg(w + i);
+    bad |= !isfinite(a.x) | !isfinite(a.y) | !isfinite(a.z) | !isfinite(a.w);
+    bad |= !(b.x >= 0.f) | !(b.y >= 0.f) | !(b.z >= 0.f) | !(b.w >= 0.f);
+    bad |= isinf(b.x) | isinf(b.y) | isinf(b.z) | isinf(b.w);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(&flags[3], 1);
+}
+
 __device__ __forceinline__ int find_entry(const HashEntry *__restrict__ table, unsigned int mask,
                                           unsigned long long key) {
   unsigned int h = hash_key(key) & mask;
@@ -241,6 +256,16 @@ static inline unsigned int grid_for(long long n, int threads) { return (unsigned
 cudaError_t launch_validate_aabb(const int4 *keys, long long n, CommitScratch sc, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   k_validate_aabb<<<grid_for(n, 256), 256, 0, s>>>(keys, n, sc.flags, sc.aabb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_values(const float *sdf, const float *weight, long long n, CommitScratch sc,
+                                   cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const long long n4 = n * (kVoxPerBlock / 4);
+  const long long blocks = std::min<long long>((n4 + 255) / 256, 148LL * 8);  // grid-stride, 8 CTAs per SM
+  k_validate_values<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(sdf),
+                                                     reinterpret_cast<const float4 *>(weight), n4, sc.flags);
   return cudaGetLastError();
 }
 

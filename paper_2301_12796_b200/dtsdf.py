@@ -22,7 +22,7 @@ VIEWS_PER_LAUNCH = 256
 EXPORTS = [
     "dtsdf_create", "dtsdf_destroy", "dtsdf_alloc_volume", "dtsdf_commit_volume", "dtsdf_upload_volume",
     "dtsdf_render", "dtsdf_render_batch", "dtsdf_volume_stats", "dtsdf_set_profiling", "dtsdf_kernel_times",
-    "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error",
+    "dtsdf_reset_kernel_times", "dtsdf_set_option", "dtsdf_launch_count", "dtsdf_last_error", "dtsdf_last_warning",
     "dtsdf_combine", "dtsdf_combine_mode", "dtsdf_render_combined", "dtsdf_combined_stats", "dtsdf_get_combined", "dtsdf_default_policy",
     "dtsdf_should_recombine", "dtsdf_default_fusion_params", "dtsdf_fusion_reserve", "dtsdf_depth_normals",
     "dtsdf_fuse", "dtsdf_get_volume", "dtsdf_default_icp_params", "dtsdf_icp", "dtsdf_icp_normal_equations",
@@ -121,8 +121,15 @@ def lib():
                                                  C.POINTER(I64), C.POINTER(C.c_double), P]
         L.dtsdf_last_error.argtypes = []
         L.dtsdf_last_error.restype = C.c_char_p
+        L.dtsdf_last_warning.argtypes = []
+        L.dtsdf_last_warning.restype = C.c_char_p
         _lib = L
     return _lib
+
+
+def last_warning() -> str:
+    """dtsdf_last_warning: the warning the last parameter check on this thread left ("" if none)."""
+    return lib().dtsdf_last_warning().decode()
 
 
 def _check(rc):
@@ -215,6 +222,14 @@ class Renderer:
         k = make_intrinsics(K)
         _check(lib().dtsdf_render_batch(self._h, poses.shape[0], poses.ctypes.data, C.byref(k), int(row0), int(row1),
                                         _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask), _stream_ptr(stream)))
+
+    def render_view(self, pose, K, depth, normal=None, color=None, mask=None, stream=None):
+        """dtsdf_render: one view (pose = world-from-camera 4x4) into caller-owned outputs (device
+        tensors -> async on the stream; host arrays / tensors, pinned or pageable -> synchronous)."""
+        pose = np.ascontiguousarray(np.asarray(pose, np.float32).reshape(16))
+        k = make_intrinsics(K)
+        _check(lib().dtsdf_render(self._h, pose.ctypes.data, C.byref(k), _ptr(depth), _ptr(normal), _ptr(color),
+                                  _ptr(mask), _stream_ptr(stream)))
 
     def render(self, poses, K, row0=0, row1=None, stream=None, outputs=("normal", "color", "mask"),
                combined=False):
