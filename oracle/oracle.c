@@ -572,10 +572,11 @@ static void combine_voxel(const ovol *v, const ocam *c, int64_t i, int64_t j, in
  *   R55 for D in F: q = first zero transition of Phi^D from p towards the camera (-r): samples
  *       p - k s r, k = 1 .. floor(|p - c| / s), the march ends without a transition (q = none) at
  *       the first sample where D is absent; bisection in the bracket (invalid midpoints positive)
- *   R56 D's free space stands iff q = none or no other direction D~ has Phi^D~(q) < -1e-6 ("lies
- *       within the occupied space": strictly inside -- a direction storing the same surface as D
- *       is ~0 at D's own root, and its sign there is rounding noise) with a gradient n^D~(q)
- *       (central differences, R7) and <n^D~(q), -r> > 0; freespace = OR over F
+ *   R56 D's free space stands iff q = none or no other direction D~ has Phi^D~(q) < 0 (as
+ *       printed) with a gradient n^D~(q) (central differences, R7) and <n^D~(q), -r> > 0;
+ *       freespace = OR over F.  (A direction storing the same surface as D is ~0 at D's own root,
+ *       so its sign there is decided by rounding: such voxels may differ between implementations
+ *       and count against the parity budget, reading R22.)
  *   R57 freespace -> the stored-weight average of the F directions; else of the O directions;
  *       else invalid ("all congruent directions are combined as weighted sum using the fused voxel
  *       weights")
@@ -664,7 +665,7 @@ static void combine_voxel_alg1(const ovol *v, const ocam *c, int64_t i, int64_t 
     for (int E = 0; E < 6 && !conflict; ++E) {
       if (E == D) continue;
       double fe, ne[3];
-      if (!dir_value(v, E, q, &fe) || !(fe < -1e-6)) continue;
+      if (!dir_value(v, E, q, &fe) || !(fe < 0.0)) continue; /* P:204 "Phi^D~(q) < 0" */
       if (!dir_normal(v, E, q, ne)) continue;
       if (-(ne[0] * r[0] + ne[1] * r[1] + ne[2] * r[2]) > 0.0) conflict = 1;
     }

@@ -407,3 +407,37 @@ def test_algorithm1_hidden_point_is_occupied_and_thin_plate_renders():
         nearer = np.abs(cpx - col).sum(1) < np.abs(cpx - other).sum(1)
         print("alg1 nearer", nearer.mean())
         assert nearer.mean() > 0.9  # blended, but the visible face dominates
+
+
+def _facing_walls(delta):
+    """X+ (D = 0) stores a wall at x = 0.6 facing +x (away from a camera at the origin looking
+    +x); X- (D = 1) stores a wall at x = 0.6 - delta facing the camera.  Input fields only."""
+    def field(D, X):
+        if D == 0:
+            return np.clip((X[:, 0] - 0.6) / 0.04, -1, 1), np.ones(len(X)), np.tile([10, 20, 30], (len(X), 1))
+        return np.clip(-(X[:, 0] - (0.6 - delta)) / 0.04, -1, 1), np.ones(len(X)), np.tile([200, 100, 50], (len(X), 1))
+    return field_volume(block_cube((6, -3, -3), (8, 2, 2), [0, 1]), field, 0.01, truncation=0.04)
+
+
+@pytest.mark.parametrize("delta,occupied", [(4e-3, True), (2e-8, True), (-2e-8, False), (-4e-3, False)])
+def test_algorithm1_conflict_test_is_strictly_negative(delta, occupied):
+    """P:203-204, Algorithm 1: D's free space fails iff another direction D~ has
+    "Phi^D~(q) < 0 and <n^D~(q), -r> > 0" at D's first zero transition q towards the camera.
+    Voxels p just behind x = 0.6 are free in X+ (phi > 0, its transition q at x = 0.6) and
+    occupied in X- (phi < 0, a camera-facing surface at 0.6 - delta).  q lies delta inside X-'s
+    occupied space: for every delta > 0 -- even 2e-8 m, Phi^X-(q) = -5e-7 -- the free space
+    conflicts and p takes the occupied direction's value; for delta < 0 (q in front of X-'s
+    surface, Phi^X-(q) > 0) it stays free.  The 2e-8 cases pin the strict "< 0" against any
+    threshold (a "< -1e-6" reading keeps them free)."""
+    vol = _facing_walls(delta)
+    ov = oracle.OracleVolume(vol)
+    K = pinhole(32, 24, 30.0)
+    pose = look_at([0, 0, 0], [1, 0, 0])
+    ijk = np.array([[i, j, k] for i in (61, 62, 63) for j in (-3, 0, 2) for k in (-2, 0, 3)], np.int64)
+    cv = oracle.combined_voxels(ov, pose, K, ijk, mode=1)
+    s0, _ = _stored(vol, 0, ijk)
+    s1, _ = _stored(vol, 1, ijk)
+    assert cv["valid"].all() and (s0 > 0).all() and (s1 < 0).all()
+    want, mask = (s1, 2) if occupied else (s0, 1)
+    assert np.abs(cv["sdf"] - want).max() < 1e-12, (delta, cv["sdf"], want)
+    assert (cv["mask"] == mask).all()
