@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ Co
     for (int E = 0; E < 6 && !conflict; ++E) {
       if (E == D) continue;
       const double fe = dir_value(p, E, q);
-      if (!(fe < -1e-6)) continue;  // strictly inside E's occupied space (R56)
+      if (!(fe < 0.0)) continue;  // "Phi^D~(q) < 0" (R56)
       double ne[3];
       if (!dir_normal(p, E, q, ne)) continue;
       if (-(ne[0] * r[0] + ne[1] * r[1] + ne[2] * r[2]) > 0.0) conflict = true;
