@@ -441,3 +441,50 @@ def test_algorithm1_conflict_test_is_strictly_negative(delta, occupied):
     want, mask = (s1, 2) if occupied else (s0, 1)
     assert np.abs(cv["sdf"] - want).max() < 1e-12, (delta, cv["sdf"], want)
     assert (cv["mask"] == mask).all()
+
+
+def _floor_with_tagged_layer():
+    """Z+ (D = 4) holds the floor phi = z / tau (weight 1).  Y+ (D = 2) holds phi = z / tau +
+    20 (y - 0.06) with weight 1 only on the voxel layer k = -1 (z = -s) for y in [0.02, 0.05),
+    weight 0 elsewhere: its 6-neighbour gradient (0, 20, 25) lies 51 deg from +y (membership > 0,
+    P:88-96), so combined voxels of that layer carry the mask {Z+, Y+}; layers k = 0, 1 carry
+    {Z+} and layer 0 is exactly 0 (the floor lies on the voxel plane z = 0)."""
+    s = 0.01
+
+    def field(D, X):
+        if D == 4:
+            return X[:, 2] / 0.04, np.ones(len(X)), np.tile([50, 60, 70], (len(X), 1))
+        k = np.round(X[:, 2] / s).astype(int)
+        j = np.round(X[:, 1] / s).astype(int)
+        w = ((k == -1) & (j >= 2) & (j <= 4)).astype(float)
+        return X[:, 2] / 0.04 + 20 * (X[:, 1] - 0.06), w, np.tile([200, 10, 10], (len(X), 1))
+    return field_volume(block_cube((-1, -1, -1), (0, 0, 0), [4, 2]), field, s, truncation=0.04)
+
+
+def test_combined_mask_on_a_voxel_plane_root():
+    """Reading R37: the combined render's mask is the OR of the masks of the corners with
+    trilinear weight >= 1/8.  The floor's root lies exactly on the voxel plane z = 0 (combined
+    sdf 0 there), so the shading point b (f <= 0) sits at the top of a cell of layers -1/0 with
+    fz -> 1: the layer -1 corners have weight ~0 and the mask is layer 0's {Z+}.  A plain OR over
+    all 8 corners would add layer -1's Y+ bit -- whereas b just above the plane would add layer 1's
+    mask: which side a root on a voxel plane is refined to must not decide the mask."""
+    vol = _floor_with_tagged_layer()
+    ov = oracle.OracleVolume(vol)
+    K = pinhole(16, 16, 100.0)
+    pose = look_at([0.003, 0.035, 0.3], [0.003, 0.035, 0.0], up=(0, 1, 0))
+    # the premise: layer -1 voxels of the window are {Z+, Y+}, layers 0 and 1 are {Z+}
+    ijk = np.array([[i, j, k] for i in (-1, 0, 1) for j in (2, 3) for k in (-1, 0, 1)], np.int64)
+    cv = oracle.combined_voxels(ov, pose, K, ijk)
+    assert cv["valid"].all()
+    assert (cv["mask"][ijk[:, 2] == -1] == (1 << 4) | (1 << 2)).all()
+    assert (cv["mask"][ijk[:, 2] >= 0] == 1 << 4).all()
+    assert (cv["sdf"][ijk[:, 2] == 0] == 0).all() and (cv["sdf"][ijk[:, 2] == -1] < 0).all()
+    out = oracle.render_combined(ov, pose, K, pose, K)
+    o, r, L = oracle.ray_dirs(pose, K)
+    y_hit = (o[1] - o[2] / r[:, 2] * r[:, 1]).reshape(16, 16)  # ray / plane z = 0
+    win = (y_hit > 0.0205) & (y_hit < 0.0395)
+    win[:, :2] = win[:, -2:] = False  # cells reaching beyond the widened frustum (R33) are invalid
+    assert win.sum() >= 20 and (out["depth"][win] > 0).all()
+    assert np.abs(out["depth"][win] - 0.3).max() < 1e-6  # camera height above the floor
+    assert (out["mask"][out["depth"] > 0] == 1 << 4).all()
+    assert (out["color"][win] == [50, 60, 70]).all()

@@ -473,3 +473,85 @@ def test_volume_errors():
     vol.keys = np.array([[0, 0, 0, 0], [0, 0, 0, 6]], np.int32)
     with pytest.raises(ValueError):
         oracle.OracleVolume(vol)
+
+
+# ---------------------------------------------------------------------------------------
+# O7 shading point (reading R32) and colour rounding (reading R13)
+# ---------------------------------------------------------------------------------------
+def _jump_volume():
+    """X- (D = 1) holds phi = +0.5, omega = 1, colour A over block locations x in [0.40, 0.80);
+    Y- (D = 3) holds phi = -1, omega = 3, colour B only over x in [0.56, 0.80).  Both fields are
+    constant (no gradient anywhere: eq:combine_tsdf_weight), so along a ray F is
+    +0.5 until Y- becomes present -- base cell i >= 56, x >= 0.56 -- and negative after: F jumps
+    from + to - at the root."""
+    A, B = (10, 20, 30), (201, 101, 61)
+
+    def field(D, X):
+        if D == 1:
+            return np.full(len(X), 0.5), np.ones(len(X)), np.tile(A, (len(X), 1))
+        return np.full(len(X), -1.0), np.full(len(X), 3.0), np.tile(B, (len(X), 1))
+    keys = block_cube((5, 5, -1), (9, 9, 0), [1]) + block_cube((7, 5, -1), (9, 9, 0), [3])
+    return field_volume(keys, field, 0.01), np.array(A, float), np.array(B, float)
+
+
+def test_shading_at_the_surface_side_of_a_jump():
+    """Reading R32: O7 shades at the final bracket end b (valid, f <= 0).  Where F jumps at the
+    root the two sides shade differently; hand-derived from eq:combine_tsdf_weight with
+    W_X- = omega_A <v^X-, -r> = r_x and W_Y- = 3 r_y: on the surface side the normal is
+    normalize(-r_x, -3 r_y, 0) and the colour (r_x A + 3 r_y B) / (r_x + 3 r_y); on the free side
+    (-1, 0, 0) and A.  The depth is the jump, x = 56 s.  For rays whose midpoint x* = (a+b)/2 of
+    the final fp64 bracket rounds onto the free side, shading "at x*" would give the free-side
+    values: at least one such ray is checked."""
+    vol, A, B = _jump_volume()
+    ov = oracle.OracleVolume(vol)
+    K = pinhole(41, 1, 200.0)  # one row: rays in the z = 0 plane, within 6 deg of (1, 1, 0)
+    pose = look_at([0, 0, 0], [1, 1, 0])
+    px = np.stack([np.arange(41), np.zeros(41, int)], 1).astype(np.int32)
+    out = ov.render(pose, K, pixels=px)
+    o, r, L = oracle.ray_dirs(pose, K, px)
+    assert np.abs(r[:, 2]).max() == 0.0 and (out["depth"] > 0).all()
+    t_jump = 56 * float(np.float32(0.01)) / r[:, 0]  # the voxel size reaches both paths as float32
+    assert np.abs(out["depth"] * L - t_jump).max() < 1e-12
+    n_surf = np.stack([-r[:, 0], -3 * r[:, 1], 0 * r[:, 0]], 1)
+    n_surf /= np.linalg.norm(n_surf, axis=1, keepdims=True)
+    assert np.abs(out["normal"] - n_surf).max() < 1e-12
+    c_surf = (r[:, :1] * A + 3 * r[:, 1:2] * B) / (r[:, :1] + 3 * r[:, 1:2])
+    clear = np.abs(c_surf - np.floor(c_surf) - 0.5) > 1e-9  # ties are pinned below (R13)
+    assert clear.mean() > 0.9 and (out["color"] == np.floor(c_surf + 0.5))[clear].all()
+    assert (out["mask"] == (1 << 1) | (1 << 3)).all()
+    # the free-side values differ, and for some rays x* lies on the free side
+    assert np.abs(out["normal"] - [-1, 0, 0]).max(1).min() > 0.5
+    free_side = [ov.eval(o + out["depth"][i] * L[i] * r[i], r[i]) for i in range(len(px))]
+    assert any(s["valid"] and s["f"] > 0 for s in free_side)
+
+
+def _colour_ramp(lo, hi):
+    """Z- (D = 5) plane z = 0.3 facing a camera at the origin looking +z, on a voxel grid of
+    s = 2^-7 m (exact binary positions); colour channel 0 = lo at even x voxels, hi at odd."""
+    s = 2.0 ** -7
+
+    def field(D, X):
+        i = np.round(X[:, 0] / s).astype(np.int64)
+        c = np.where(i % 2 == 0, lo, hi)
+        rgb = np.stack([c, np.full(len(X), 7), np.full(len(X), 255)], 1)
+        return np.clip(-(X[:, 2] - 0.3) / (4 * s), -1, 1), np.ones(len(X)), rgb
+    return field_volume(block_cube((-2, -2, 3), (1, 1, 6), [5]), field, s, truncation=4 * s)
+
+
+@pytest.mark.parametrize("lo,hi,want", [(10, 11, 11), (11, 12, 12), (254, 255, 255), (0, 1, 1), (255, 255, 255)])
+def test_colour_rounds_half_up_and_stays_in_range(lo, hi, want):
+    """Reading R13: colour = min(255, floor(c + 1/2)).  A camera at x = s/2 (exact in binary)
+    looks along +z at a camera-facing plane: at the hit the x fraction is exactly 1/2 between
+    voxels of channel-0 colours lo and hi, y/z fractions and the single direction's weight are
+    exact, so c = (lo + hi)/2 exactly: a tie that rounds up (10.5 -> 11, 11.5 -> 12; banker's
+    rounding would give 10 and 12, truncation 10 and 11).  The other channels are exact (7, 255)."""
+    s = 2.0 ** -7
+    ov = oracle.OracleVolume(_colour_ramp(lo, hi))
+    K = pinhole(9, 9, 10.0)
+    pose = look_at([s / 2, 0, 0], [s / 2, 0, 1], up=(0, 1, 0))
+    o, r, L = oracle.ray_dirs(pose, K, np.array([[4, 4]], np.int32))
+    assert np.array_equal(r[0], [0, 0, 1]) and o[0] == s / 2
+    out = ov.render(pose, K, pixels=np.array([[4, 4]], np.int32))
+    assert abs(out["depth"][0] - 0.3) < 1e-9  # float32 stored distances
+    assert np.allclose(out["normal"][0], [0, 0, -1], atol=1e-12)
+    assert list(out["color"][0]) == [want, 7, 255]
