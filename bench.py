@@ -4,6 +4,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dtsdf|reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
+With --gpus N > 1 and no torch.distributed environment (WORLD_SIZE unset) the script re-executes
+itself under torch.distributed.run with N processes; a world size other than --gpus is an error.
+
 One step = every rank renders one 640x480 depth+normal+colour+dirmask view of the configs[1]
 room volume (seeded synthetic) through dtsdf_render_batch; per-GPU work is fixed
 (weak scaling).  The volume is generated on rank 0, replicated by one NCCL broadcast per buffer
@@ -59,7 +62,48 @@ def parse():
                          "rows: every view's rows are split per rank via row0/row1 (C4's large view) -- strong scaling")
     ap.add_argument("--combine-mode", type=int, default=0, choices=[0, 1],
                     help="combined mode: 0 eq:combine_weight (the paper's method), 1 Algorithm 1 (NEXT-4)")
+    ap.add_argument("--batch-views", type=int, default=256,
+                    help="views of the strong-scaling C3 batch timed after the headline (SURVEY §8(e)); 0 = skip")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without kernels: every rank joins a gloo process group and reports; "
+                         "rank 0 prints the ranks it saw")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args) -> int:
+    """--gpus N > 1 without a torch.distributed environment: run this script under
+    torch.distributed.run with N processes on this node (one per GPU), same arguments."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dry_run(args) -> int:
+    """Launcher check (CPU, gloo): each rank reports (rank, world, pid); rank 0 prints them."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(free_port()))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seen = [None] * world
+    dist.all_gather_object(seen, {"rank": rank, "world": world, "pid": os.getpid(),
+                                  "local_rank": int(os.environ.get("LOCAL_RANK", "0"))})
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "impl": args.impl, "n_gpus": world, "ranks": seen,
+                          "comm": {"backend": dist.get_backend(), "world_size": dist.get_world_size()}}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
 
 
 def workload(name):
@@ -192,7 +236,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": describe(w, 1),
+            "config": dict(describe(w, args.views), mode=args.mode),  # the product arm's config keys
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"each step: {n} of {w.intrinsics.width * w.intrinsics.height} pixel rays "
                                        f"of the {w.name} view (seeded uniform subset)"},
@@ -435,6 +479,35 @@ def run_dtsdf(args):
                      "raycast across the host link (DTSDF_OPT_HOST_WRITE)",
            "copy_path_value": total_rays * e2e_steps / e2e_copy / 1e6}
 
+    # ---- SURVEY §8(e) strong scaling: the configs[3] batch (orbit views of this volume) split into
+    # contiguous per-rank view ranges, timed like the headline (events, flushed L2, max over ranks) ----
+    c3 = None
+    if args.batch_views > 0 and w.name == "C1" and args.mode == "direct" and args.shard == "none":
+        import scenes
+        allp = scenes.orbit_poses(np.random.default_rng([3, 0]), args.batch_views)  # c3_batch's poses
+        lo, hi = pdist.shard_range(args.batch_views, rank, world)
+        bp = np.ascontiguousarray(np.asarray(allp, np.float32)[lo:hi])
+        bo = R.render(bp, K) if hi > lo else None
+        c3_steps = 5
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(c3_steps)]
+        for i in range(2 + c3_steps):
+            if not args.no_flush:
+                flush.fill_(1.0)
+            if i >= 2:
+                ev[i - 2][0].record(stream)
+            if bo is not None:
+                R.render_into(bp, K, bo["depth"], bo["normal"], bo["color"], bo["mask"], stream=stream)
+            if i >= 2:
+                ev[i - 2][1].record(stream)
+        torch.cuda.synchronize()
+        c3_ms = sum(a.elapsed_time(b) for a, b in ev)
+        c3_max = pdist.max_over_ranks(dist, c3_ms, dev) if use_dist else c3_ms
+        c3 = {"workload": f"C3: the {args.batch_views} configs[3] orbit views of this volume, split into contiguous "
+                          f"per-rank view ranges (strong scaling)", "views": args.batch_views,
+              "views_this_rank": hi - lo, "value": K.width * K.height * args.batch_views * c3_steps / (c3_max / 1e3) / 1e6,
+              "unit": UNIT, "ms_per_batch": c3_max / c3_steps, "steps": c3_steps, "scaling": "strong"}
+        del bo
+
     if rank != 0:
         dist.barrier() if use_dist else None
         dist.destroy_process_group() if use_dist else None
@@ -463,7 +536,10 @@ def run_dtsdf(args):
         "frames_per_s": total_rays / (K.width * K.height) * args.steps / (max_ms / 1e3),
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk,
-        "extra": {"upload_and_index_ms": upload_ms, "broadcast_ms": bcast_ms, "n_locations": st["n_locations"],
+        "comm": ({"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                  "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())} if use_dist else
+                 {"backend": None, "world_size": 1, "note": "single process, no process group"}),
+        "extra": {"c3_strong_scaling": c3, "upload_and_index_ms": upload_ms, "broadcast_ms": bcast_ms, "n_locations": st["n_locations"],
                   "output_checksum": out_sum, "ranks_with_same_views_bit_identical": replicas_equal,
                   "device_bytes": st["bytes"], "parity_sample_vs_oracle": parity,
                   "device": torch.cuda.get_device_name(dev)},
@@ -477,6 +553,16 @@ def run_dtsdf(args):
 
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the process group has {world} ranks", file=sys.stderr, flush=True)
+        return 2
+    if args.dry_run:
+        return dry_run(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_dtsdf(args)

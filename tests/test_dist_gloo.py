@@ -81,3 +81,31 @@ def test_shard_range_partitions(n, world):
     sizes = [hi - lo for lo, hi in parts]
     assert max(sizes) - min(sizes) <= 1
     assert np.sum(sizes) == n
+
+
+def test_bench_launcher_spawns_the_requested_ranks():
+    """bench.py --gpus 2 without a torch.distributed environment re-executes itself under
+    torch.distributed.run with 2 processes (the form the driver uses for N > 1); --dry-run joins
+    a gloo group without kernels and rank 0 reports every rank it saw."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=240, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["comm"]["world_size"] == 2
+    assert sorted(r["rank"] for r in line["ranks"]) == [0, 1]
+    assert len({r["pid"] for r in line["ranks"]}) == 2
+
+
+def test_bench_rejects_a_world_size_other_than_gpus():
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=120, env=env)
+    assert out.returncode == 2 and "--gpus 2" in out.stderr
