@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
     d[2] = __dsub_rn(__dmul_rn((double)k, s), p.t[2]);
   }
   const int off = CAPRON(lx, ly, lz), coff = lx + kRgbApron * ly + kRgbApron * kRgbApron * lz;
+  const int roff = lx + kRec * ly + kRec * kRec * lz;  // the voxel's record in the directional bricks
   // r in fp32 from the fp64 offset (its rounding is far below the tolerance of the weights)
   const float dx = (float)d[0], dy = (float)d[1], dz = (float)d[2];
   const float dd = dx * dx + dy * dy + dz * dz;
@@ -153,50 +154,43 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
 #pragma unroll 1
   while (present) {
     int Dp[2];
-    float2 c[2];
-    float nb[2][6];
-    uchar4 q[2];
+    float4 ra[2];  // {sdf, weight, dsdf_x, dsdf_y}
+    float2 rb[2];  // {dsdf_z, rgb}
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       Dp[h] = present ? __ffs(present) - 1 : -1;
       present &= present - 1;
-      c[h] = make_float2(0.f, 0.f);
-      q[h] = make_uchar4(0, 0, 0, 0);
-#pragma unroll
-      for (int a = 0; a < 6; ++a) nb[h][a] = 0.f;
+      ra[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rb[h] = make_float2(0.f, 0.f);
       if (Dp[h] >= 0) {
         int slot_d = sl[0];
 #pragma unroll
         for (int D = 1; D < 6; ++D) slot_d = Dp[h] == D ? sl[D] : slot_d;  // register select
-        const float2 *br = V.apron + (size_t)slot_d * kApronStride + off;
-        c[h] = __ldg(br);
-        nb[h][0] = __ldg(&br[1].x);
-        nb[h][1] = __ldg(&br[-1].x);
-        nb[h][2] = __ldg(&br[kApron].x);
-        nb[h][3] = __ldg(&br[-kApron].x);
-        nb[h][4] = __ldg(&br[kApron * kApron].x);
-        nb[h][5] = __ldg(&br[-kApron * kApron].x);
-        q[h] = __ldg(V.rgb_apron + (size_t)slot_d * kRgbApronStride + coff);
+        ra[h] = __ldg(V.brick_a + (size_t)slot_d * kRecStride + roff);
+        rb[h] = __ldg(V.brick_b + (size_t)slot_d * kRecStride + roff);
       }
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int D = Dp[h];
-      if (D < 0 || !(c[h].y > 0.0f)) continue;  // D holds no data at the voxel (reading R8)
-      // the gradient from the 6 neighbouring voxels (NaN where unallocated)
-      const float gx = (nb[h][0] - nb[h][1]) * half_inv_s;
-      const float gy = (nb[h][2] - nb[h][3]) * half_inv_s;
-      const float gz = (nb[h][4] - nb[h][5]) * half_inv_s;
+      const float2 c = make_float2(ra[h].x, ra[h].y);
+      if (D < 0 || !(c.y > 0.0f)) continue;  // D holds no data at the voxel (reading R8)
+      // the gradient from the 6 neighbouring voxels (the record's central
+      // differences, NaN where a neighbour is unallocated)
+      const float gx = ra[h].z * half_inv_s;
+      const float gy = ra[h].w * half_inv_s;
+      const float gz = rb[h].x * half_inv_s;
       const float gn = sqrtf(gx * gx + gy * gy + gz * gz);
       const int axis = D >> 1;
       const float sign = (D & 1) ? -1.0f : 1.0f;
       const float r_axis = axis == 0 ? rx : (axis == 1 ? ry : rz);
-      const float cr = (float)q[h].x, cg = (float)q[h].y, cb = (float)q[h].z;
+      const unsigned int qq = rec_rgb(rb[h].y);
+      const float cr = (float)(qq & 255u), cg = (float)((qq >> 8) & 255u), cb = (float)(qq >> 16);
       // eq:combine_tsdf_weight: omega <v^D, -r>^+
-      const float W2 = c[h].y * fmaxf(-sign * r_axis, 0.0f);
+      const float W2 = c.y * fmaxf(-sign * r_axis, 0.0f);
       if (W2 > 0.0f) {
         S2 += W2;
-        F2 = fmaf(W2, c[h].x, F2);
+        F2 = fmaf(W2, c.x, F2);
         C2[0] = fmaf(W2, cr, C2[0]); C2[1] = fmaf(W2, cg, C2[1]); C2[2] = fmaf(W2, cb, C2[2]);
         m2 |= 1 << D;
       }
@@ -207,10 +201,10 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
         const float n_axis = axis == 0 ? nx : (axis == 1 ? ny : nz);
         const float nr = -(nx * rx + ny * ry + nz * rz);
         // eq:combine_weight: w_dir(<n,v>) <n,-r>^+ omega
-        const float W1 = w_dir_c(sign * n_axis, V) * fmaxf(nr, 0.0f) * c[h].y;
+        const float W1 = w_dir_c(sign * n_axis, V) * fmaxf(nr, 0.0f) * c.y;
         if (W1 > 0.0f) {
           S1 += W1;
-          F1 = fmaf(W1, c[h].x, F1);
+          F1 = fmaf(W1, c.x, F1);
           C1[0] = fmaf(W1, cr, C1[0]); C1[1] = fmaf(W1, cg, C1[1]); C1[2] = fmaf(W1, cb, C1[2]);
           m1 |= 1 << D;
         }
@@ -242,86 +236,126 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
 // direction's free space stands unless its first zero transition towards the camera lies in the
 // occupied space of another direction whose surface faces the camera; the result is the stored-
 // weight average of the free directions if any free space stands, else of the occupied ones.
-// Sample positions are fp64 (the oracle's formulas), interpolation fp32.
+//
+// Every quantity that feeds one of these discrete decisions -- participation, the first
+// transition q, "Phi^D~(q) < 0" (taken as printed), "<n^D~(q), -r> > 0" -- is evaluated in
+// fp64 with the oracle's operations in the oracle's order (explicit _rn intrinsics, so nvcc cannot
+// contract them into FMAs; the oracle is compiled with -ffp-contract=off) on the same float voxel
+// values.  A direction storing the same surface as D is ~0 at D's own root, so its sign there is
+// decided by the last bit: both sides take that decision on identical bits.  (The acos of the
+// membership test is the one libm call; a flip needs acos(c) within an ulp of theta.)
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ long long floordiv8_ll(long long i) { return i >= 0 ? i / 8 : -((-i + 7) / 8); }
+__device__ __forceinline__ double m64(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double a64(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double s64(double a, double b) { return __dsub_rn(a, b); }
 
-// direction D's apron brick for the base cell of world point y, and the cell's local offset and
-// fractions; false when D is not allocated at that location
-__device__ bool dir_cell(const CombineLaunch &p, int D, const double y[3], const float2 **br, double fr[3]) {
+// record brick (A) of direction D at block location (b0, b1, b2), or null if unallocated
+__device__ const float4 *dir_brick(const CombineLaunch &p, int D, long long b0, long long b1, long long b2) {
   const VolumeView &V = p.vol;
-  long long ci[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const double g = y[a] / (double)V.voxel_size;
-    const double fl = floor(g);
-    ci[a] = (long long)fl;
-    fr[a] = g - fl;
-  }
-  const long long b0 = floordiv8_ll(ci[0]), b1 = floordiv8_ll(ci[1]), b2 = floordiv8_ll(ci[2]);
   int e = -1;
   if (V.loc_grid) {
     const long long x = b0 - V.lo_x, yy = b1 - V.lo_y, z = b2 - V.lo_z;
-    if (x < 0 || yy < 0 || z < 0 || x >= V.dim_x || yy >= V.dim_y || z >= V.dim_z) return false;
+    if (x < 0 || yy < 0 || z < 0 || x >= V.dim_x || yy >= V.dim_y || z >= V.dim_z) return nullptr;
     const int gv = __ldg(&V.loc_grid[((size_t)z * V.dim_y + yy) * V.dim_x + x]);
-    if (gv < 0) return false;
+    if (gv < 0) return nullptr;
     e = gv & kGridEntryMask;
   } else {
+    if (b0 < -(1 << 20) || b0 >= (1 << 20) || b1 < -(1 << 20) || b1 >= (1 << 20) || b2 < -(1 << 20) || b2 >= (1 << 20))
+      return nullptr;
     const unsigned long long key = pack_key((int)b0, (int)b1, (int)b2);
     unsigned int h = hash_key(key) & V.table_mask;
     for (unsigned int probe = 0; probe <= V.table_mask; ++probe) {
       const unsigned long long k = V.table[h].key;
       if (k == key) { e = (int)h; break; }
-      if (k == kEmptyKey) return false;
+      if (k == kEmptyKey) return nullptr;
       h = (h + 1) & V.table_mask;
     }
-    if (e < 0) return false;
+    if (e < 0) return nullptr;
   }
   const int slot = V.table[e].slot[D];
-  if (slot < 0) return false;
+  if (slot < 0) return nullptr;
   DTSDF_CHECK(slot < V.n_blocks);
-  const int lx = (int)(ci[0] - 8 * b0), ly = (int)(ci[1] - 8 * b1), lz = (int)(ci[2] - 8 * b2);
-  *br = V.apron + (size_t)slot * kApronStride + lx + kApron * ly + kApron * kApron * lz;
+  return V.brick_a + (size_t)slot * kRecStride;
+}
+
+// oracle record_of: the stored sdf of voxel (i, j, k) in direction D; false if its block is
+// unallocated (the voxel's own record in its block's brick)
+__device__ bool vox_sdf(const CombineLaunch &p, int D, long long i, long long j, long long k, double *v) {
+  const long long b0 = floordiv8_ll(i), b1 = floordiv8_ll(j), b2 = floordiv8_ll(k);
+  const float4 *br = dir_brick(p, D, b0, b1, b2);
+  if (!br) return false;
+  *v = (double)__ldg(&br[(i - 8 * b0) + kRec * (j - 8 * b1) + kRec * kRec * (k - 8 * b2)].x);
   return true;
 }
 
-// Algorithm 1 takes discrete decisions from these values (free / occupied, first transition,
-// conflicting direction), so they are evaluated in fp64 like the oracle's (float voxel values,
-// fp64 fractions): a decision can only differ where the oracle's value itself is ~1e-16 from it.
-__device__ __forceinline__ double tri64(const float2 *c, const double f[3]) {
-  const double c000 = c[CAPRON(0, 0, 0)].x, c100 = c[CAPRON(1, 0, 0)].x, c010 = c[CAPRON(0, 1, 0)].x,
-               c110 = c[CAPRON(1, 1, 0)].x, c001 = c[CAPRON(0, 0, 1)].x, c101 = c[CAPRON(1, 0, 1)].x,
-               c011 = c[CAPRON(0, 1, 1)].x, c111 = c[CAPRON(1, 1, 1)].x;
-  const double e00 = c000 + f[0] * (c100 - c000), e10 = c010 + f[0] * (c110 - c010);
-  const double e01 = c001 + f[0] * (c101 - c001), e11 = c011 + f[0] * (c111 - c011);
-  const double r0 = e00 + f[1] * (e10 - e00), r1 = e01 + f[1] * (e11 - e01);
-  return r0 + f[2] * (r1 - r0);
+// oracle cell_interp (phi only): plain trilinear over the 8 corners of cell c with fractions fr,
+// corners in the oracle's order, wt = (x-factor * y-factor) * z-factor, p += wt * sdf; false
+// unless every corner's block is allocated.  The base block's brick holds voxels 0..8, i.e. all 8
+// corners, with NaN where a corner's block is unallocated.
+__device__ bool cell_interp64(const CombineLaunch &p, int D, const long long c[3], const double fr[3], double *phi) {
+  const long long b0 = floordiv8_ll(c[0]), b1 = floordiv8_ll(c[1]), b2 = floordiv8_ll(c[2]);
+  const float4 *br = dir_brick(p, D, b0, b1, b2);
+  if (!br) return false;
+  br += (c[0] - 8 * b0) + kRec * (c[1] - 8 * b1) + kRec * kRec * (c[2] - 8 * b2);
+  const double u0 = s64(1.0, fr[0]), u1 = s64(1.0, fr[1]), u2 = s64(1.0, fr[2]);
+  double acc = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
+    const float v = __ldg(&br[dx + kRec * dy + kRec * kRec * dz].x);
+    if (isnan(v)) return false;
+    const double wt = m64(m64(dx ? fr[0] : u0, dy ? fr[1] : u1), dz ? fr[2] : u2);
+    acc = a64(acc, m64(wt, (double)v));
+  }
+  *phi = acc;
+  return true;
 }
 
-// trilinear phi_D at y (NaN: absent -- a corner in an unallocated block)
-__device__ double dir_value(const CombineLaunch &p, int D, const double y[3]) {
-  const float2 *b;
-  double f[3];
-  if (!dir_cell(p, D, y, &b, f)) return CUDART_NAN;
-  return tri64(b, f);
-}
-
-// unit normal of phi_D at y: central differences of the trilinear field at +-s (R7); false if
-// the stencil is incomplete or |g| <= 1e-3
-__device__ bool dir_normal(const CombineLaunch &p, int D, const double y[3], double n[3]) {
-  const float2 *b;
-  double f[3];
-  if (!dir_cell(p, D, y, &b, f)) return false;
-  double g[3];
+// oracle locate: g = x / s, c = floor(g), fr = g - floor(g)
+__device__ __forceinline__ void locate64(double s, const double y[3], long long c[3], double fr[3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const int e = a == 0 ? 1 : (a == 1 ? kApron : kApron * kApron);
-    g[a] = (tri64(b + e, f) - tri64(b - e, f)) / (2.0 * (double)p.vol.voxel_size);
+    const double g = __ddiv_rn(y[a], s);
+    const double fl = floor(g);
+    c[a] = (long long)fl;
+    fr[a] = s64(g, fl);
   }
-  const double gn = sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]);
-  if (!(gn > 1e-3)) return false;  // NaN (incomplete stencil) -> false
-  n[0] = g[0] / gn; n[1] = g[1] / gn; n[2] = g[2] / gn;
+}
+
+// oracle dir_value: trilinear phi_D at y; false when D is absent there
+__device__ bool dir_value(const CombineLaunch &p, int D, double s, const double y[3], double *f) {
+  long long c[3];
+  double fr[3];
+  locate64(s, y, c, fr);
+  return cell_interp64(p, D, c, fr, f);
+}
+
+// oracle dir_normal: central differences of the trilinear field at +-s (cells shifted by one
+// voxel, same fractions, R7); false if the stencil is incomplete or |g| <= 1e-3
+__device__ bool dir_normal(const CombineLaunch &p, int D, double s, const double y[3], double n[3]) {
+  long long c[3];
+  double fr[3], g[3];
+  locate64(s, y, c, fr);
+  for (int a = 0; a < 3; ++a) {
+    long long cp[3] = {c[0], c[1], c[2]}, cm[3] = {c[0], c[1], c[2]};
+    cp[a] += 1;
+    cm[a] -= 1;
+    double pp, pm;
+    if (!cell_interp64(p, D, cp, fr, &pp) || !cell_interp64(p, D, cm, fr, &pm)) return false;
+    g[a] = __ddiv_rn(s64(pp, pm), m64(2.0, s));
+  }
+  const double gn = __dsqrt_rn(a64(a64(m64(g[0], g[0]), m64(g[1], g[1])), m64(g[2], g[2])));
+  if (!(gn > 1e-3)) return false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) n[a] = __ddiv_rn(g[a], gn);
   return true;
+}
+
+// y = x - t r per component (the oracle's back-march / bisection / q positions)
+__device__ __forceinline__ void back_point(const double x[3], double t, const double r[3], double y[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) y[a] = s64(x[a], m64(t, r[a]));
 }
 
 __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p,
@@ -335,110 +369,120 @@ __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ Co
   const int4 ea = __ldg(ent), eb = __ldg(ent + 1);
   const int sl[6] = {ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
   const int i = kBlock * b.x + lx, j = kBlock * b.y + ly, k = kBlock * b.z + lz;
+  const double s = (double)V.voxel_size;
   double d[3];
   bool in = true;
   if (cls_in[slot] == 2) {
-    in = in_frustum(p, (double)V.voxel_size, i, j, k, d);
+    in = in_frustum(p, s, i, j, k, d);
   } else {
-    const double s = (double)V.voxel_size;
-    d[0] = __dsub_rn(__dmul_rn((double)i, s), p.t[0]);
-    d[1] = __dsub_rn(__dmul_rn((double)j, s), p.t[1]);
-    d[2] = __dsub_rn(__dmul_rn((double)k, s), p.t[2]);
+    d[0] = s64(m64((double)i, s), p.t[0]);
+    d[1] = s64(m64((double)j, s), p.t[1]);
+    d[2] = s64(m64((double)k, s), p.t[2]);
   }
-  const double dist = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-  const double x[3] = {(double)i * (double)V.voxel_size, (double)j * (double)V.voxel_size,
-                       (double)k * (double)V.voxel_size};
-  const double r[3] = {d[0] / dist, d[1] / dist, d[2] / dist};
+  const double dist = __dsqrt_rn(a64(a64(m64(d[0], d[0]), m64(d[1], d[1])), m64(d[2], d[2])));
+  const double x[3] = {m64((double)i, s), m64((double)j, s), m64((double)k, s)};
+  const double r[3] = {__ddiv_rn(d[0], dist), __ddiv_rn(d[1], dist), __ddiv_rn(d[2], dist)};
   const int off = CAPRON(lx, ly, lz), coff = lx + kRgbApron * ly + kRgbApron * kRgbApron * lz;
+  const int roff = lx + kRec * ly + kRec * kRec * lz;
+  const long long vi[3] = {i, j, k};
   float phi[6], om[6];
   unsigned part = 0, free_m = 0;
   if (in && dist > 0.0) {
-#pragma unroll
     for (int D = 0; D < 6; ++D) {
       if (sl[D] < 0) continue;
-      const float2 *br = V.apron + (size_t)sl[D] * kApronStride + off;
-      const float2 c = __ldg(br);
+      const float4 c = __ldg(V.brick_a + (size_t)sl[D] * kRecStride + roff);
       phi[D] = c.x;
       om[D] = c.y;
-      if (!(c.y > p.w_floor)) continue;  // R53 (decided in fp64 like the oracle)
-      const double two_s = 2.0 * (double)V.voxel_size;
-      const double gx = ((double)__ldg(&br[1].x) - (double)__ldg(&br[-1].x)) / two_s;
-      const double gy = ((double)__ldg(&br[kApron].x) - (double)__ldg(&br[-kApron].x)) / two_s;
-      const double gz = ((double)__ldg(&br[kApron * kApron].x) - (double)__ldg(&br[-kApron * kApron].x)) / two_s;
-      const double gn = sqrt(gx * gx + gy * gy + gz * gz);
+      if (!(c.y > p.w_floor)) continue;  // R53
+      // the voxel's 6-neighbour gradient from the stored values, as the oracle
+      double g[3];
+      bool ok = true;
+      for (int a = 0; a < 3 && ok; ++a) {
+        long long pp[3] = {vi[0], vi[1], vi[2]}, mm[3] = {vi[0], vi[1], vi[2]};
+        pp[a] += 1;
+        mm[a] -= 1;
+        double vp, vm;
+        if (!vox_sdf(p, D, pp[0], pp[1], pp[2], &vp) || !vox_sdf(p, D, mm[0], mm[1], mm[2], &vm)) { ok = false; break; }
+        g[a] = __ddiv_rn(s64(vp, vm), m64(2.0, s));
+      }
+      if (!ok) continue;
+      const double gn = __dsqrt_rn(a64(a64(m64(g[0], g[0]), m64(g[1], g[1])), m64(g[2], g[2])));
       if (!(gn > 1e-3)) continue;
-      const double nax = (D >> 1) == 0 ? gx : ((D >> 1) == 1 ? gy : gz);
-      if (!(acos(fmin(fmax(((D & 1) ? -nax : nax) / gn, -1.0), 1.0)) < p.theta64)) continue;  // w_dir > 0
+      // <n, v^D> = +-g_axis / gn (the other products with v^D are exact zeros)
+      const double nv = __ddiv_rn((D & 1) ? -g[D >> 1] : g[D >> 1], gn);
+      const double cc = nv < -1.0 ? -1.0 : (nv > 1.0 ? 1.0 : nv);
+      const double w = __ddiv_rn(s64(p.theta64, acos(cc)), s64(m64(2.0, p.theta64), 1.5707963267948966));
+      if (!(w > 0.0)) continue;  // w_dir > 0 (eq:direction_weight, R1)
       part |= 1u << D;
       if (c.x > 0.0f) free_m |= 1u << D;
     }
   }
   // R55-R56: does any free direction's free space stand?
   bool freespace = false;
-  const long long K = (long long)floor(dist / (double)V.voxel_size);
+  const long long K = (long long)floor(__ddiv_rn(dist, s));
   for (int D = 0; D < 6 && !freespace; ++D) {
     if (!((free_m >> D) & 1u)) continue;
     double prev_t = 0.0, qt = -1.0;
     for (long long kk = 1; kk <= K; ++kk) {
-      const double t = (double)kk * (double)V.voxel_size;
-      const double y[3] = {x[0] - t * r[0], x[1] - t * r[1], x[2] - t * r[2]};
-      const double f = dir_value(p, D, y);
-      if (isnan(f)) break;  // D absent: no transition observed
+      const double t = m64((double)kk, s);
+      double y[3], f;
+      back_point(x, t, r, y);
+      if (!dir_value(p, D, s, y, &f)) break;  // D absent: no transition observed
       if (f <= 0.0) {
         double a = prev_t, bb = t;
         for (int it = 0; it < 50; ++it) {
-          const double m = 0.5 * (a + bb);
+          const double m = m64(0.5, a64(a, bb));
           if (!(m > a && m < bb)) break;
-          const double ym[3] = {x[0] - m * r[0], x[1] - m * r[1], x[2] - m * r[2]};
-          const double fm = dir_value(p, D, ym);
-          if (isnan(fm) || fm > 0.0) a = m; else bb = m;
+          double ym[3], fm;
+          back_point(x, m, r, ym);
+          if (!dir_value(p, D, s, ym, &fm) || fm > 0.0) a = m; else bb = m;
         }
-        qt = 0.5 * (a + bb);
+        qt = m64(0.5, a64(a, bb));
         break;
       }
       prev_t = t;
     }
     if (qt < 0.0) { freespace = true; break; }
-    const double q[3] = {x[0] - qt * r[0], x[1] - qt * r[1], x[2] - qt * r[2]};
+    double q[3];
+    back_point(x, qt, r, q);
     bool conflict = false;
     for (int E = 0; E < 6 && !conflict; ++E) {
       if (E == D) continue;
-      const double fe = dir_value(p, E, q);
-      if (!(fe < 0.0)) continue;  // "Phi^D~(q) < 0" (R56)
+      double fe;
+      if (!dir_value(p, E, s, q, &fe) || !(fe < 0.0)) continue;  // "Phi^D~(q) < 0" (R56)
       double ne[3];
-      if (!dir_normal(p, E, q, ne)) continue;
-      if (-(ne[0] * r[0] + ne[1] * r[1] + ne[2] * r[2]) > 0.0) conflict = true;
+      if (!dir_normal(p, E, s, q, ne)) continue;
+      if (-a64(a64(m64(ne[0], r[0]), m64(ne[1], r[1])), m64(ne[2], r[2])) > 0.0) conflict = true;
     }
     if (!conflict) freespace = true;
   }
-  // R57: stored-weight average of the chosen set.  The colour sums are fp64: stored weights are
-  // float32 and colours integers, so products and sums are exact and an average that is exactly
-  // k + 1/2 (equal weights, e.g. a plate's front and back directions) rounds as in the oracle.
+  // R57: stored-weight average of the chosen set in fp64, as the oracle: stored weights are float32
+  // and colours integers, so an average that is exactly k + 1/2 (equal weights, e.g. a plate's
+  // front and back directions) rounds as in the oracle.
   const unsigned use = freespace ? free_m : (part & ~free_m);
-  float S = 0.f, F = 0.f;
-  double Sd = 0.0, C[3] = {0.0, 0.0, 0.0};
-#pragma unroll
+  double S = 0.0, F = 0.0, C[3] = {0.0, 0.0, 0.0};
   for (int D = 0; D < 6; ++D) {
     if (!((use >> D) & 1u)) continue;
-    const uchar4 q = __ldg(V.rgb_apron + (size_t)sl[D] * kRgbApronStride + coff);
-    S += om[D];
-    F = fmaf(om[D], phi[D], F);
-    Sd += (double)om[D];
-    C[0] += (double)om[D] * q.x; C[1] += (double)om[D] * q.y; C[2] += (double)om[D] * q.z;
+    const unsigned int qc = rec_rgb(__ldg(&V.brick_b[(size_t)sl[D] * kRecStride + roff].y));
+    S = a64(S, (double)om[D]);
+    F = a64(F, m64((double)om[D], (double)phi[D]));
+    C[0] = a64(C[0], m64((double)om[D], (double)(qc & 255u)));
+    C[1] = a64(C[1], m64((double)om[D], (double)((qc >> 8) & 255u)));
+    C[2] = a64(C[2], m64((double)om[D], (double)(qc >> 16)));
   }
   float sdf = CUDART_NAN_F;
   uchar4 col = make_uchar4(0, 0, 0, 0);
-  const bool valid = use != 0 && S > 0.0f;
+  const bool valid = use != 0 && S > 0.0;
   if (valid) {
-    sdf = F / S;
+    sdf = (float)__ddiv_rn(F, S);
     unsigned char cc[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cc[a] = (unsigned char)fmin(fmax(floor(C[a] / Sd + 0.5), 0.0), 255.0);
+    for (int a = 0; a < 3; ++a) cc[a] = (unsigned char)fmin(fmax(floor(a64(__ddiv_rn(C[a], S), 0.5)), 0.0), 255.0);
     col = make_uchar4(cc[0], cc[1], cc[2], (unsigned char)use);
   }
   p.apron[slot * kApronStride + off] = sdf;
   p.rgb[slot * kRgbApronStride + coff] = col;
-  p.weight[slot * kVoxPerBlock + l] = valid ? S : 0.f;
+  p.weight[slot * kVoxPerBlock + l] = valid ? (float)S : 0.f;
 }
 
 // combined slot of block location (bx,by,bz), or -1

@@ -23,12 +23,24 @@ namespace dtsdf {
 
 constexpr int kBlock = 8;          // 8^3 voxel blocks
 constexpr int kVoxPerBlock = 512;
-constexpr int kApron = 11;         // apron brick: voxels -1..9 of the block per axis
+// Combined-TSDF bricks (combine.cu, NEXT-1): voxels -1..9 of the block per axis
+constexpr int kApron = 11;
 constexpr int kApronVox = kApron * kApron * kApron;  // 1331
-constexpr int kApronStride = 1344;                   // float2 records per brick (10752 B, 128-B aligned)
-constexpr int kRgbApron = 9;                         // colour apron: voxels 0..8 per axis (trilinear corners)
+constexpr int kApronStride = 1344;                   // records per combined brick (128-B aligned)
+constexpr int kRgbApron = 9;                         // combined colour bricks: voxels 0..8 per axis
 constexpr int kRgbApronVox = kRgbApron * kRgbApron * kRgbApron;  // 729
 constexpr int kRgbApronStride = 736;                 // uchar4 records per brick (2944 B)
+// Directional record bricks (volume.cu k_bricks): voxels 0..8 of the block per axis -- the 8
+// trilinear corners of every base cell of the block -- as two arrays of records:
+//   A float4 {sdf (NaN = the voxel's block is unallocated), weight, dsdf_x, dsdf_y}
+//   B float2 {dsdf_z, rgb (u8 x3 in the float's bits)}
+// with dsdf_a = sdf(voxel + e_a) - sdf(voxel - e_a) (NaN if either neighbour is unallocated), the
+// per-voxel central difference of reading R7: the gradient of trilinear phi at x +- s e_a is the
+// trilinear interpolant of these differences / 2s, so a sample reads 8 records per direction
+// (16-B + 4-B loads) instead of 8 corners + 24 stencil voxels.
+constexpr int kRec = 9;
+constexpr int kRecVox = kRec * kRec * kRec;          // 729
+constexpr int kRecStride = 732;                      // records per brick: A 11712 B, B 5856 B (32-B aligned)
 #ifndef DTSDF_RANGE_TILE
 #define DTSDF_RANGE_TILE 8
 #endif
@@ -81,8 +93,8 @@ struct VolumeView {
   int use_live;                    // 1: visit only the live directions of a cell (DTSDF_OPT_CELL_DIRS)
   int lo_x, lo_y, lo_z;        // AABB origin (block coords)
   int dim_x, dim_y, dim_z;     // AABB extent (blocks)
-  const float2 *apron;         // [N][kApronStride] {sdf (NaN = unallocated), weight}
-  const uchar4 *rgb_apron;     // [N][kRgbApronStride]
+  const float4 *brick_a;       // [N][kRecStride] {sdf (NaN = unallocated), weight, dsdf_x, dsdf_y}
+  const float2 *brick_b;       // [N][kRecStride] {dsdf_z, rgb bits}
   float voxel_size, inv_voxel;
   float theta, inv_blend;      // 1 / (2 theta - pi/2)
   float cos_theta, sin_theta;  // membership band edges: w_dir = 0 below cos(theta), 1 above sin(theta)
@@ -274,12 +286,22 @@ cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsign
                             int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
-cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
+cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float4 *brick_a,
                             unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s);
 cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
                            int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
-cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
-                         const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
-                         cudaStream_t s);
+cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
+                          const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
+                          cudaStream_t s);
+// rgb packed into a float's bits for the B records (r | g << 8 | b << 16)
+__host__ __device__ __forceinline__ unsigned int rec_rgb(float bits) {
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(bits);
+#else
+  unsigned int u;
+  __builtin_memcpy(&u, &bits, 4);
+  return u;
+#endif
+}
 
 }  // namespace dtsdf

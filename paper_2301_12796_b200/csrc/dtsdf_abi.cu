@@ -68,12 +68,12 @@ struct dtsdf_ctx {
   int lo[3] = {0, 0, 0}, dim[3] = {0, 0, 0};
   int4 *locations = nullptr;
   int64_t n_loc = 0;
-  float2 *apron = nullptr;
-  uchar4 *rgb_apron = nullptr;
+  float4 *brick_a = nullptr;  // record bricks (common.cuh kRec*): {sdf, weight, dsdf_x, dsdf_y}
+  float2 *brick_b = nullptr;  // {dsdf_z, rgb}
   size_t index_bytes = 0;
   // allocated sizes of the index buffers: a re-commit (e.g. after every fused frame) reuses them
-  size_t cap_table = 0, cap_locations = 0, cap_bitmap = 0, cap_surface = 0, cap_cell_pos = 0, cap_apron = 0,
-         cap_rgb_apron = 0, cap_loc_grid = 0, cap_dist = 0;
+  size_t cap_table = 0, cap_locations = 0, cap_bitmap = 0, cap_surface = 0, cap_cell_pos = 0, cap_brick_a = 0,
+         cap_brick_b = 0, cap_loc_grid = 0, cap_dist = 0;
   unsigned char *dist_tmp = nullptr;
   // commit scratch
   int *scratch = nullptr;  // flags[4] + aabb[6] + n_loc(u64)
@@ -156,11 +156,11 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->cell_dirs);
   dfree(c->loc_grid);
   dfree(c->locations);
-  dfree(c->apron);
-  dfree(c->rgb_apron);
+  dfree(c->brick_a);
+  dfree(c->brick_b);
   dfree(c->dist_tmp);
-  c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_apron =
-      c->cap_rgb_apron = c->cap_loc_grid = c->cap_dist = c->cap_cell_dirs = 0;
+  c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_brick_a =
+      c->cap_brick_b = c->cap_loc_grid = c->cap_dist = c->cap_cell_dirs = 0;
   c->allocated = c->committed = false;
   c->n = c->n_loc = c->cap = 0;
   c->index_bytes = 0;
@@ -368,13 +368,13 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
       ensure(c->surface, c->cap_surface, (bm_words + 1) * 4) != cudaSuccess ||
       ensure(c->cell_pos, c->cap_cell_pos, (size_t)cap * 64) != cudaSuccess ||
       ensure(c->cell_dirs, c->cap_cell_dirs, (size_t)cap * 512) != cudaSuccess ||
-      ensure(c->apron, c->cap_apron, nb * kApronStride * sizeof(float2)) != cudaSuccess ||
-      ensure(c->rgb_apron, c->cap_rgb_apron, nb * kRgbApronStride * sizeof(uchar4)) != cudaSuccess) {
+      ensure(c->brick_a, c->cap_brick_a, nb * kRecStride * sizeof(float4)) != cudaSuccess ||
+      ensure(c->brick_b, c->cap_brick_b, nb * kRecStride * sizeof(float2)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "index allocation");
   }
   c->index_bytes = (size_t)cap * (sizeof(HashEntry) + 64 + 512) + (size_t)n * sizeof(int4) + 2 * bm_words * 4 +
-                   (size_t)n * kApronStride * sizeof(float2) + (size_t)n * kRgbApronStride * sizeof(uchar4);
+                   (size_t)n * kRecStride * (sizeof(float4) + sizeof(float2));
   CK(c, cudaMemsetAsync(c->table, 0xFF, (size_t)cap * sizeof(HashEntry), s), "table init");
   CK(c, cudaMemsetAsync(c->bitmap, 0, (bm_words + 1) * 4, s), "bitmap init");
   CK(c, cudaMemsetAsync(c->surface, 0, (bm_words + 1) * 4, s), "surface init");
@@ -391,13 +391,13 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   begin_timed(c, 2, s, &tl);
   CK(c, launch_bitmap(c->locations, c->n_loc, c->bitmap, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s), "bitmap");
   end_timed(c, s, &tl);
-  begin_timed(c, 2, s, &tl, 2);  // launch_apron issues two kernels
-  CK(c, launch_apron(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
-                     c->apron, c->rgb_apron, s),
-     "apron");
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_bricks(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
+                      c->brick_a, c->brick_b, s),
+     "bricks");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
-  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->apron, c->cell_pos, c->cell_dirs, s), "cell_pos");
+  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->brick_a, c->cell_pos, c->cell_dirs, s), "cell_pos");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
   CK(c, launch_surface(c->locations, c->n_loc, c->cell_pos, c->surface, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s),
@@ -523,8 +523,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   V.loc_grid = c->use_grid ? c->loc_grid : nullptr;
   V.lo_x = c->lo[0]; V.lo_y = c->lo[1]; V.lo_z = c->lo[2];
   V.dim_x = c->dim[0]; V.dim_y = c->dim[1]; V.dim_z = c->dim[2];
-  V.apron = c->apron;
-  V.rgb_apron = c->rgb_apron;
+  V.brick_a = c->brick_a;
+  V.brick_b = c->brick_b;
   V.voxel_size = c->params.voxel_size;
   V.inv_voxel = 1.0f / c->params.voxel_size;
   V.theta = c->params.theta;
@@ -758,8 +758,8 @@ int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsic
   L.vol.loc_grid = c->use_grid ? c->loc_grid : nullptr;
   L.vol.lo_x = c->lo[0]; L.vol.lo_y = c->lo[1]; L.vol.lo_z = c->lo[2];
   L.vol.dim_x = c->dim[0]; L.vol.dim_y = c->dim[1]; L.vol.dim_z = c->dim[2];
-  L.vol.apron = c->apron;
-  L.vol.rgb_apron = c->rgb_apron;
+  L.vol.brick_a = c->brick_a;
+  L.vol.brick_b = c->brick_b;
   L.vol.voxel_size = c->params.voxel_size;
   L.vol.inv_voxel = 1.0f / c->params.voxel_size;
   L.vol.theta = c->params.theta;

@@ -382,6 +382,12 @@ __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) {
 
 #define APRON_IDX(dx, dy, dz) (((dx) + 1) + kApron * ((dy) + 1) + kApron * kApron * ((dz) + 1))
 #define RGB_IDX(dx, dy, dz) ((dx) + kRgbApron * (dy) + kRgbApron * kRgbApron * (dz))
+#define REC_IDX(dx, dy, dz) ((dx) + kRec * (dy) + kRec * kRec * (dz))
+// the colour of a B record (u8 r, g, b in the bits of its .y)
+__device__ __forceinline__ uchar4 rec_u8(float bits) {
+  const unsigned int u = __float_as_uint(bits);
+  return make_uchar4(u & 255u, (u >> 8) & 255u, (u >> 16) & 255u, 0);
+}
 
 // eq:direction_weight with reading R1: clamp((theta - acos c) / (2 theta - pi/2), 0, 1)
 // (outside the blend band the clamp decides: c <= cos(theta) -> 0, c >= sin(theta) -> 1)
@@ -440,9 +446,6 @@ __device__ __forceinline__ int dir_slot(const VolumeView &V, const Cursor &cur, 
 #endif
 }
 
-#ifndef DTSDF_GRAD_DIFF
-#define DTSDF_GRAD_DIFF 1  // profiles/r1n_sweep_grad_sel.jsonl: C1 -0.9 %, C2 out-of-tolerance pixels 48 -> 27
-#endif
 #ifndef DTSDF_SEL_PTX
 #define DTSDF_SEL_PTX 1  // C1 -1.8 %, C2 -2.3 % (profiles/r1n_sweep_grad_sel.jsonl)
 #endif
@@ -484,7 +487,7 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
                                                  float fx, float fy, float fz, float rx, float ry, float rz,
                                                  ShadeResult *sh, int live = -1) {
   SampleResult res;
-  const int off = lx + kApron * ly + kApron * kApron * lz;
+  const int off = lx + kRec * ly + kRec * kRec * lz;
   float S1 = 0.f, F1 = 0.f, S2 = 0.f, F2 = 0.f;
   bool any_grad = false;
   float N1x = 0.f, N1y = 0.f, N1z = 0.f, N2x = 0.f, N2y = 0.f, N2z = 0.f;
@@ -502,69 +505,42 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
     present &= present - 1;
     const int slot = dir_slot(V, cur, D);
     DTSDF_CHECK(slot >= 0 && slot < V.n_blocks && lx >= 0 && lx < 8 && ly >= 0 && ly < 8 && lz >= 0 && lz < 8);
-    const float2 *br = V.apron + (size_t)slot * kApronStride + off;
-    // all 32 stencil voxels are issued before any test (one load round per direction; the
-    // apron brick always holds them, NaN marking unallocated neighbours)
-    const float2 c000 = __ldg(br + APRON_IDX(0, 0, 0)), c100 = __ldg(br + APRON_IDX(1, 0, 0));
-    const float2 c010 = __ldg(br + APRON_IDX(0, 1, 0)), c110 = __ldg(br + APRON_IDX(1, 1, 0));
-    const float2 c001 = __ldg(br + APRON_IDX(0, 0, 1)), c101 = __ldg(br + APRON_IDX(1, 0, 1));
-    const float2 c011 = __ldg(br + APRON_IDX(0, 1, 1)), c111 = __ldg(br + APRON_IDX(1, 1, 1));
-    const float xm00 = __ldg(&br[APRON_IDX(-1, 0, 0)].x), xm10 = __ldg(&br[APRON_IDX(-1, 1, 0)].x);
-    const float xm01 = __ldg(&br[APRON_IDX(-1, 0, 1)].x), xm11 = __ldg(&br[APRON_IDX(-1, 1, 1)].x);
-    const float xp00 = __ldg(&br[APRON_IDX(2, 0, 0)].x), xp10 = __ldg(&br[APRON_IDX(2, 1, 0)].x);
-    const float xp01 = __ldg(&br[APRON_IDX(2, 0, 1)].x), xp11 = __ldg(&br[APRON_IDX(2, 1, 1)].x);
-    const float ym00 = __ldg(&br[APRON_IDX(0, -1, 0)].x), ym10 = __ldg(&br[APRON_IDX(1, -1, 0)].x);
-    const float ym01 = __ldg(&br[APRON_IDX(0, -1, 1)].x), ym11 = __ldg(&br[APRON_IDX(1, -1, 1)].x);
-    const float yp00 = __ldg(&br[APRON_IDX(0, 2, 0)].x), yp10 = __ldg(&br[APRON_IDX(1, 2, 0)].x);
-    const float yp01 = __ldg(&br[APRON_IDX(0, 2, 1)].x), yp11 = __ldg(&br[APRON_IDX(1, 2, 1)].x);
-    const float zm00 = __ldg(&br[APRON_IDX(0, 0, -1)].x), zm10 = __ldg(&br[APRON_IDX(1, 0, -1)].x);
-    const float zm01 = __ldg(&br[APRON_IDX(0, 1, -1)].x), zm11 = __ldg(&br[APRON_IDX(1, 1, -1)].x);
-    const float zp00 = __ldg(&br[APRON_IDX(0, 0, 2)].x), zp10 = __ldg(&br[APRON_IDX(1, 0, 2)].x);
-    const float zp01 = __ldg(&br[APRON_IDX(0, 1, 2)].x), zp11 = __ldg(&br[APRON_IDX(1, 1, 2)].x);
+    const float4 *ba = V.brick_a + (size_t)slot * kRecStride + off;
+    const float2 *bb = V.brick_b + (size_t)slot * kRecStride + off;
+    // the 8 corner records {sdf, weight, dsdf_x, dsdf_y} + dsdf_z are issued before any test (one
+    // load round per direction; the brick always holds them, NaN marking unallocated neighbours)
+    const float4 a000 = __ldg(ba + REC_IDX(0, 0, 0)), a100 = __ldg(ba + REC_IDX(1, 0, 0));
+    const float4 a010 = __ldg(ba + REC_IDX(0, 1, 0)), a110 = __ldg(ba + REC_IDX(1, 1, 0));
+    const float4 a001 = __ldg(ba + REC_IDX(0, 0, 1)), a101 = __ldg(ba + REC_IDX(1, 0, 1));
+    const float4 a011 = __ldg(ba + REC_IDX(0, 1, 1)), a111 = __ldg(ba + REC_IDX(1, 1, 1));
+    const float z000 = __ldg(&bb[REC_IDX(0, 0, 0)].x), z100 = __ldg(&bb[REC_IDX(1, 0, 0)].x);
+    const float z010 = __ldg(&bb[REC_IDX(0, 1, 0)].x), z110 = __ldg(&bb[REC_IDX(1, 1, 0)].x);
+    const float z001 = __ldg(&bb[REC_IDX(0, 0, 1)].x), z101 = __ldg(&bb[REC_IDX(1, 0, 1)].x);
+    const float z011 = __ldg(&bb[REC_IDX(0, 1, 1)].x), z111 = __ldg(&bb[REC_IDX(1, 1, 1)].x);
     // The lerps run pairwise on Blackwell's packed fp32x2 FMA (FFMA2): {sdf, weight} of the
-    // corners, and pairs of independent stencil layers.
+    // corners, and pairs of corner differences.
     // O3(a) trilinear phi_D, omega_D over the 8 cell corners (x: rows e_yz, y: slabs R(dz), z)
-    const float2 e00 = lerp2(c000, c100, fx2), e10 = lerp2(c010, c110, fx2);
-    const float2 e01 = lerp2(c001, c101, fx2), e11 = lerp2(c011, c111, fx2);
+    const float2 e00 = lerp2(make_float2(a000.x, a000.y), make_float2(a100.x, a100.y), fx2);
+    const float2 e10 = lerp2(make_float2(a010.x, a010.y), make_float2(a110.x, a110.y), fx2);
+    const float2 e01 = lerp2(make_float2(a001.x, a001.y), make_float2(a101.x, a101.y), fx2);
+    const float2 e11 = lerp2(make_float2(a011.x, a011.y), make_float2(a111.x, a111.y), fx2);
     const float2 R0w = lerp2(e00, e10, fy2), R1w = lerp2(e01, e11, fy2);
     const float2 pw = lerp2(R0w, R1w, fz2);
     const float phi = pw.x, omega = pw.y;
     if (isnan(phi)) continue;       // D absent: a corner lies in an unallocated block
     if (!(omega > 0.0f)) continue;  // D holds no data at x (reading R8)
-    // O3(c) central differences of trilinear phi at x +- s e_a (24 further stencil voxels):
-    // phi(x + s e_a) - phi(x - s e_a) = (1 - f_a)(A1 - A-1) + f_a (A2 - A0) with A(d) the
-    // bilinear interpolant of the stencil layer d along axis a
-    const float R0 = R0w.x, R1 = R1w.x;
-    // (P0, P1): bilinear over (y, z) of the corner columns x = 0, 1
-#if DTSDF_GRAD_DIFF
-    // the same central differences as bilinears of the layer differences (A1 - A-1, A2 - A0): the
-    // pairs are formed from fresh FADD results instead of register moves between loaded records
-    (void)R0; (void)R1;
-    const float2 Dx = lerp2(lerp2(make_float2(c100.x - xm00, xp00 - c000.x), make_float2(c110.x - xm10, xp10 - c010.x), fy2),
-                            lerp2(make_float2(c101.x - xm01, xp01 - c001.x), make_float2(c111.x - xm11, xp11 - c011.x), fy2), fz2);
-    const float2 Dy = lerp2(lerp2(make_float2(c010.x - ym00, yp00 - c000.x), make_float2(c110.x - ym10, yp10 - c100.x), fx2),
-                            lerp2(make_float2(c011.x - ym01, yp01 - c001.x), make_float2(c111.x - ym11, yp11 - c101.x), fx2), fz2);
-    const float2 Dz = lerp2(lerp2(make_float2(c001.x - zm00, zp00 - c000.x), make_float2(c101.x - zm10, zp10 - c100.x), fx2),
-                            lerp2(make_float2(c011.x - zm01, zp01 - c010.x), make_float2(c111.x - zm11, zp11 - c110.x), fx2), fy2);
+    // O3(c) central differences of trilinear phi at x +- s e_a: phi(x + s e_a) - phi(x - s e_a) is
+    // the trilinear interpolant of the corners' differences dsdf_a = sdf(+e_a) - sdf(-e_a) -- taken
+    // pairwise along a (corner 0, corner 1), bilinear over the other two axes, then along a
+    const float2 Dx = lerp2(lerp2(make_float2(a000.z, a100.z), make_float2(a010.z, a110.z), fy2),
+                            lerp2(make_float2(a001.z, a101.z), make_float2(a011.z, a111.z), fy2), fz2);
+    const float2 Dy = lerp2(lerp2(make_float2(a000.w, a010.w), make_float2(a100.w, a110.w), fx2),
+                            lerp2(make_float2(a001.w, a011.w), make_float2(a101.w, a111.w), fx2), fz2);
+    const float2 Dz = lerp2(lerp2(make_float2(z000, z001), make_float2(z100, z101), fx2),
+                            lerp2(make_float2(z010, z011), make_float2(z110, z111), fx2), fy2);
     const float gx = lerpf(Dx.x, Dx.y, fx) * half_inv_s;
     const float gy = lerpf(Dy.x, Dy.y, fy) * half_inv_s;
     const float gz = lerpf(Dz.x, Dz.y, fz) * half_inv_s;
-#else
-    const float2 P01 = lerp2(lerp2(make_float2(c000.x, c100.x), make_float2(c010.x, c110.x), fy2),
-                             lerp2(make_float2(c001.x, c101.x), make_float2(c011.x, c111.x), fy2), fz2);
-    // (Q0, Q1) from the x-lerped rows
-    const float2 Q01 = lerp2(make_float2(e00.x, e10.x), make_float2(e01.x, e11.x), fz2);
-    // (Pm, Pp), (Qm, Qp), (Rm, Rp): the outer stencil layers
-    const float2 Pmp = lerp2(lerp2(make_float2(xm00, xp00), make_float2(xm10, xp10), fy2),
-                             lerp2(make_float2(xm01, xp01), make_float2(xm11, xp11), fy2), fz2);
-    const float2 Qmp = lerp2(lerp2(make_float2(ym00, yp00), make_float2(ym10, yp10), fx2),
-                             lerp2(make_float2(ym01, yp01), make_float2(ym11, yp11), fx2), fz2);
-    const float2 Rmp = lerp2(lerp2(make_float2(zm00, zp00), make_float2(zm10, zp10), fx2),
-                             lerp2(make_float2(zm01, zp01), make_float2(zm11, zp11), fx2), fy2);
-    const float gx = lerpf(P01.y - Pmp.x, Pmp.y - P01.x, fx) * half_inv_s;
-    const float gy = lerpf(Q01.y - Qmp.x, Qmp.y - Q01.x, fy) * half_inv_s;
-    const float gz = lerpf(R1 - Rmp.x, Rmp.y - R0, fz) * half_inv_s;
-#endif
 #if DTSDF_FAST_NORM
     const float gn2 = gx * gx + gy * gy + gz * gz;  // |g|^2: |g| > 1e-3 <=> |g|^2 > 1e-6 (up to rounding)
 #else
@@ -597,10 +573,10 @@ __device__ __forceinline__ SampleResult eval_sample(const VolumeView &V, const C
       F1 = fmaf(W1, phi, F1);
     }
     if constexpr (shade) {
-      const uchar4 *cb = V.rgb_apron + (size_t)slot * kRgbApronStride + (lx + kRgbApron * ly + kRgbApron * kRgbApron * lz);
-      const uchar4 q000 = cb[RGB_IDX(0, 0, 0)], q100 = cb[RGB_IDX(1, 0, 0)], q010 = cb[RGB_IDX(0, 1, 0)],
-                   q110 = cb[RGB_IDX(1, 1, 0)], q001 = cb[RGB_IDX(0, 0, 1)], q101 = cb[RGB_IDX(1, 0, 1)],
-                   q011 = cb[RGB_IDX(0, 1, 1)], q111 = cb[RGB_IDX(1, 1, 1)];
+      const uchar4 q000 = rec_u8(bb[REC_IDX(0, 0, 0)].y), q100 = rec_u8(bb[REC_IDX(1, 0, 0)].y),
+                   q010 = rec_u8(bb[REC_IDX(0, 1, 0)].y), q110 = rec_u8(bb[REC_IDX(1, 1, 0)].y),
+                   q001 = rec_u8(bb[REC_IDX(0, 0, 1)].y), q101 = rec_u8(bb[REC_IDX(1, 0, 1)].y),
+                   q011 = rec_u8(bb[REC_IDX(0, 1, 1)].y), q111 = rec_u8(bb[REC_IDX(1, 1, 1)].y);
 #define TRI_CH(ch)                                                                                              \
   lerpf(lerpf(lerpf((float)q000.ch, (float)q100.ch, fx), lerpf((float)q010.ch, (float)q110.ch, fx), fy),        \
         lerpf(lerpf((float)q001.ch, (float)q101.ch, fx), lerpf((float)q011.ch, (float)q111.ch, fx), fy), fz)

@@ -5,11 +5,12 @@
 //                       (64-bit CAS, linear probing), then CAS of the direction slot; a slot
 //                       already taken means a duplicate (x,y,z,D) key
 //   bitmap              one thread per location: occupancy bit over the location AABB
-//   apron               one thread per apron voxel: each (location, D) brick gets the voxels
-//                       -1..9 of its block per axis gathered from up to 27 neighbouring blocks
-//                       of the same direction, NaN sdf where that neighbour is unallocated --
-//                       so one brick serves a whole sample (8 trilinear corners + 24 gradient
-//                       stencil voxels) with a single index lookup
+//   bricks              one CTA per block: each (location, D) brick gets the records of voxels
+//                       0..8 of its block per axis gathered from up to 27 neighbouring blocks of
+//                       the same direction -- sdf (NaN where that neighbour is unallocated),
+//                       weight, the three per-voxel central differences and the colour -- so one
+//                       brick serves a whole sample (8 trilinear corners carrying the gradient
+//                       stencil) with a single index lookup
 //
 // Slot placement in the table depends on insertion order; lookups do not.
 #include "common.cuh"
@@ -92,17 +93,20 @@ __global__ void k_bitmap(const int4 *__restrict__ loc, long long n_loc, unsigned
   atomicOr(&bitmap[cell >> 5], 1u << (cell & 31));
 }
 
-// One thread per (brick, apron voxel).  Apron voxel a in [0,11)^3 is block-local voxel a-1.
-// Apron bricks: one CTA per block.  The 27 neighbour slots (same direction) are resolved once into
-// shared memory -- a hash probe per neighbour instead of one per border record -- then the CTA
-// fills the block's 1331 {sdf, weight} records (NaN sdf where the neighbour is unallocated) and
-// its 729 colour records (voxels 0..8) with coalesced stores.
-constexpr int kApronThreads = 256;
-__global__ void __launch_bounds__(kApronThreads) k_apron(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
-                                                        unsigned int mask, const float *__restrict__ sdf,
-                                                        const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
-                                                        float2 *__restrict__ apron, uchar4 *__restrict__ rgb_apron) {
+// Record bricks (common.cuh kRec*): one CTA per block.  The 27 neighbour slots (same direction) are
+// resolved once into shared memory -- a hash probe per neighbour instead of one per record -- the
+// sdf of voxels -1..9 per axis is staged in shared memory (NaN where the neighbour block is
+// unallocated), then the CTA writes the 729 records of voxels 0..8: A {sdf, weight, dsdf_x,
+// dsdf_y}, B {dsdf_z, rgb} with dsdf_a = sdf(+e_a) - sdf(-e_a) (one fp32 subtraction, NaN if
+// either neighbour is absent), with coalesced stores.
+constexpr int kBrickThreads = 256;
+constexpr int kStage = 11;  // staged sdf: voxels -1..9 per axis
+__global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
+                                                         unsigned int mask, const float *__restrict__ sdf,
+                                                         const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
+                                                         float4 *__restrict__ brick_a, float2 *__restrict__ brick_b) {
   __shared__ int nb[27];  // slot of neighbour (ox, oy, oz) in -1..1, index (ox+1) + 3 (oy+1) + 9 (oz+1)
+  __shared__ float st[kStage * kStage * kStage];
   const long long b = blockIdx.x;
   const int4 k = keys[b];
   if (threadIdx.x < 27) {
@@ -115,35 +119,42 @@ __global__ void __launch_bounds__(kApronThreads) k_apron(const int4 *__restrict_
     nb[threadIdx.x] = src;
   }
   __syncthreads();
-  for (int a = threadIdx.x; a < kApronStride; a += kApronThreads) {
-    float2 out = make_float2(__int_as_float(0x7fc00000), 0.0f);  // NaN sdf = unallocated
-    if (a < kApronVox) {
-      const int lx = a % kApron - 1, ly = (a / kApron) % kApron - 1, lz = a / (kApron * kApron) - 1;  // -1..9
-      const int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
-      const int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
-      const int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
-      const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
-      if (src >= 0) {
-        const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
-        const long long r = (long long)src * kVoxPerBlock + l;
-        out = make_float2(sdf[r], weight[r]);
-      }
-    }
-    apron[b * kApronStride + a] = out;
+  // pool record of block-local voxel (lx, ly, lz) in -8..15, or -1 when its block is unallocated
+  auto rec_of = [&](int lx, int ly, int lz) -> long long {
+    const int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
+    const int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
+    const int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
+    const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
+    if (src < 0) return -1;
+    const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+    return (long long)src * kVoxPerBlock + l;
+  };
+  for (int a = threadIdx.x; a < kStage * kStage * kStage; a += kBrickThreads) {
+    const long long r = rec_of(a % kStage - 1, (a / kStage) % kStage - 1, a / (kStage * kStage) - 1);
+    st[a] = r >= 0 ? sdf[r] : __int_as_float(0x7fc00000);  // NaN sdf = unallocated
   }
-  for (int a = threadIdx.x; a < kRgbApronStride; a += kApronThreads) {
-    uchar4 out = make_uchar4(0, 0, 0, 0);
-    if (a < kRgbApronVox && rgb != nullptr) {
-      const int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);  // 0..8
-      const int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
-      const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
-      if (src >= 0) {
-        const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
-        const unsigned char *c = rgb + 3 * ((long long)src * kVoxPerBlock + l);
-        out = make_uchar4(c[0], c[1], c[2], 0);
+  __syncthreads();
+  for (int a = threadIdx.x; a < kRecStride; a += kBrickThreads) {
+    float4 ra = make_float4(__int_as_float(0x7fc00000), 0.0f, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+    float2 rb = make_float2(__int_as_float(0x7fc00000), 0.0f);
+    if (a < kRecVox) {
+      const int lx = a % kRec, ly = (a / kRec) % kRec, lz = a / (kRec * kRec);  // 0..8
+      const int c = (lx + 1) + kStage * (ly + 1) + kStage * kStage * (lz + 1);
+      const long long r = rec_of(lx, ly, lz);
+      ra.x = st[c];
+      ra.y = r >= 0 ? weight[r] : 0.0f;
+      ra.z = st[c + 1] - st[c - 1];
+      ra.w = st[c + kStage] - st[c - kStage];
+      rb.x = st[c + kStage * kStage] - st[c - kStage * kStage];
+      unsigned int col = 0;
+      if (r >= 0 && rgb != nullptr) {
+        const unsigned char *q = rgb + 3 * r;
+        col = (unsigned int)q[0] | ((unsigned int)q[1] << 8) | ((unsigned int)q[2] << 16);
       }
+      rb.y = __uint_as_float(col);
     }
-    rgb_apron[b * kRgbApronStride + a] = out;
+    brick_a[b * kRecStride + a] = ra;
+    brick_b[b * kRecStride + a] = rb;
   }
 }
 
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(kApronThreads) k_apron(const int4 *__restrict_
 // when the next lattice point is such a sample too -- start one (render.cu, exact).
 // One warp per 32 consecutive cells of a location; the ballot writes one mask word.
 __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const HashEntry *__restrict__ table,
-                           const float2 *__restrict__ apron, unsigned int *cell_pos, unsigned char *cell_dirs) {
+                           const float4 *__restrict__ brick_a, unsigned int *cell_pos, unsigned char *cell_dirs) {
   long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long u = gid >> 9;
   int l = (int)(gid & 511);
@@ -166,10 +177,10 @@ __global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const 
     for (int D = 0; D < 6; ++D) {
       const int slot = table[h].slot[D];
       if (slot < 0) continue;
-      const float2 *br = apron + (size_t)slot * kApronStride + (lx + 1) + kApron * (ly + 1) + kApron * kApron * (lz + 1);
+      const float4 *br = brick_a + (size_t)slot * kRecStride + lx + kRec * ly + kRec * kRec * lz;
       bool absent = false, allpos = true, weighted = false;
       for (int q = 0; q < 8; ++q) {
-        const float2 v = br[(q & 1) + kApron * ((q >> 1) & 1) + kApron * kApron * (q >> 2)];
+        const float4 v = br[(q & 1) + kRec * ((q >> 1) & 1) + kRec * kRec * (q >> 2)];
         absent |= isnan(v.x);
         allpos &= v.x > 0.0f;
         weighted |= v.y > 0.0f;
@@ -302,10 +313,10 @@ cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char 
   return cudaGetLastError();
 }
 
-cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float2 *apron,
+cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float4 *brick_a,
                             unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s) {
   if (n_loc == 0) return cudaSuccess;
-  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, apron, cell_pos, cell_dirs);
+  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, brick_a, cell_pos, cell_dirs);
   return cudaGetLastError();
 }
 
@@ -316,11 +327,11 @@ cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigne
   return cudaGetLastError();
 }
 
-cudaError_t launch_apron(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
-                         const float *weight, const unsigned char *rgb, float2 *apron, uchar4 *rgb_apron,
-                         cudaStream_t s) {
+cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
+                          const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
+                          cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_apron<<<(unsigned)n, kApronThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, apron, rgb_apron);
+  k_bricks<<<(unsigned)n, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b);
   return cudaGetLastError();
 }
 

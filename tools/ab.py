@@ -54,7 +54,12 @@ def run_one(args):
         if not args.no_parity:
             ora = oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
             st = compare({k: v[0].cpu().numpy() for k, v in out.items()}, ora)
+        import hashlib
+        h = hashlib.sha1()
+        for k in ("depth", "normal", "color", "mask"):
+            h.update(out[k].cpu().numpy().tobytes())
         print(json.dumps({"variant": args.name, "config": name, "l2": "warm" if args.no_flush else "flushed",
+                          "out_sha1": h.hexdigest()[:16],
                           "options": args.set,
                           "raycast_ms": round(ms, 4), "range_order_ms": round(pre_ms, 4),
                           "budget_used": st.get("budget_used"), "color_exact": st.get("color_exact"),
