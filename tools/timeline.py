@@ -45,3 +45,4 @@ for name in sys.argv[1:] or ["C1"]:
     act = [int(((wst <= b) & (wen > b)).sum()) for b in bins[:-1]]
     print("  active warps over time (20 bins):", act)
     print(f"  total warp-time / (span * max active) = {wd.sum() / (span * max(act)):.3f}")
+    np.save(os.path.join(ROOT, "gpurun_out", f"timeline_{name}.npy"), np.stack([st, en, sm.astype(np.float64)], -1))
