@@ -57,6 +57,10 @@ def lib():
         L.oracle_combined_voxels_mode.restype = None
         L.oracle_render_combined_mode.argtypes = [P, P, P, D, I32, D, P, P, I64, P, I32, I32, P, P, P, P]
         L.oracle_render_combined_mode.restype = None
+        L.oracle_combined_voxels_update.argtypes = [P, P, P, P, D, I32, D, I64, P, P, P, P, P, P]
+        L.oracle_combined_voxels_update.restype = None
+        L.oracle_render_combined_update.argtypes = [P, P, P, P, D, I32, D, P, P, I64, P, I32, I32, P, P, P, P]
+        L.oracle_render_combined_update.restype = None
         L.oracle_should_recombine.argtypes = [I64, I64, P, P, I64, I64, D, D]
         L.oracle_should_recombine.restype = I32
         L.oracle_fuse_create.argtypes = [D, D, D, I64, I64, P, P, P, P, C.POINTER(P)]
@@ -190,26 +194,32 @@ def _intr32(K):
                      np.float32(K.z_min), np.float32(K.z_max)], np.float64)
 
 
-def combined_voxels(ov: "OracleVolume", pose, K, ijk, margin: float = MARGIN, mode: int = 0, w_floor: float = 0.0):
+def combined_voxels(ov: "OracleVolume", pose, K, ijk, margin: float = MARGIN, mode: int = 0, w_floor: float = 0.0,
+                    before: "OracleVolume" = None):
     """Combined TSDF voxels (oracle.c combine_voxel, readings R33-R35; mode 1: Algorithm 1,
-    R53-R57) at integer positions ijk [n, 3] for the source camera (pose, K).
-    Returns dict(valid, sdf, weight, rgb, mask)."""
+    R53-R57) at integer positions ijk [n, 3] for the source camera (pose, K).  before: the volume
+    the combined TSDF was computed from when fusion has since changed it to ov (reading R58:
+    first-time voxels from ov, the others from before).  Returns dict(valid, sdf, weight, rgb, mask)."""
     ijk = np.ascontiguousarray(ijk, np.int64).reshape(-1, 3)
     n = len(ijk)
     valid = np.zeros(n, np.int32)
     sdf, S = np.zeros(n), np.zeros(n)
     rgb = np.zeros((n, 3), np.uint8)
     mask = np.zeros(n, np.uint8)
-    lib().oracle_combined_voxels_mode(ov.h, _ptr(_pose32(pose)), _ptr(_intr32(K)), float(np.float32(margin)),
-                                      int(mode), float(np.float32(w_floor)), n, _ptr(ijk), _ptr(valid), _ptr(sdf),
-                                      _ptr(S), _ptr(rgb), _ptr(mask))
+    args = (_ptr(_pose32(pose)), _ptr(_intr32(K)), float(np.float32(margin)), int(mode), float(np.float32(w_floor)),
+            n, _ptr(ijk), _ptr(valid), _ptr(sdf), _ptr(S), _ptr(rgb), _ptr(mask))
+    if before is None:
+        lib().oracle_combined_voxels_mode(ov.h, *args)
+    else:
+        lib().oracle_combined_voxels_update(before.h, ov.h, *args)
     return dict(valid=valid.astype(bool), sdf=sdf, weight=S, rgb=rgb, mask=mask)
 
 
 def render_combined(ov: "OracleVolume", src_pose, src_K, pose, K, pixels=None, row0=0, row1=None, threads=None,
-                    margin: float = MARGIN, mode: int = 0, w_floor: float = 0.0):
+                    margin: float = MARGIN, mode: int = 0, w_floor: float = 0.0, before: "OracleVolume" = None):
     """Raycast (pose, K) through the combined TSDF of the source camera (src_pose, src_K)
-    (oracle.c render_pixel_combined, readings R36-R37).  Output layout as OracleVolume.render."""
+    (oracle.c render_pixel_combined, readings R36-R37; before: as combined_voxels, R58).
+    Output layout as OracleVolume.render."""
     if pixels is None:
         row1 = K.height if row1 is None else row1
         npix = (row1 - row0) * K.width
@@ -224,9 +234,13 @@ def render_combined(ov: "OracleVolume", src_pose, src_K, pose, K, pixels=None, r
     color = np.zeros((npix, 3), np.uint8)
     mask = np.zeros(npix, np.uint8)
     threads = threads or os.cpu_count() or 1
-    lib().oracle_render_combined_mode(ov.h, _ptr(_pose32(src_pose)), _ptr(_intr32(src_K)), float(np.float32(margin)),
-                                      int(mode), float(np.float32(w_floor)), _ptr(_pose32(pose)), _ptr(_intr32(K)),
-                                      npix, _ptr(uv), row0, threads, _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask))
+    args = (_ptr(_pose32(src_pose)), _ptr(_intr32(src_K)), float(np.float32(margin)), int(mode),
+            float(np.float32(w_floor)), _ptr(_pose32(pose)), _ptr(_intr32(K)), npix, _ptr(uv), row0, threads,
+            _ptr(depth), _ptr(normal), _ptr(color), _ptr(mask))
+    if before is None:
+        lib().oracle_render_combined_mode(ov.h, *args)
+    else:
+        lib().oracle_render_combined_update(before.h, ov.h, *args)
     return dict(depth=depth.reshape(shape), normal=normal.reshape(shape + (3,)), color=color.reshape(shape + (3,)),
                 mask=mask.reshape(shape))
 

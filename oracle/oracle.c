@@ -447,6 +447,8 @@ typedef struct {
   double margin; /* fraction of the image size added on every side (1/8) */
   int mode;      /* 0: eq:combine_weight / eq:combine_tsdf_weight (R34); 1: Algorithm 1 (R53-R57) */
   double w_floor;/* Algorithm 1: directions need a stored weight above this (R53) */
+  const ovol *vprev; /* R58: the volume the combined TSDF was computed from, when fusion has changed the
+                      * volume since (NULL: combined from the current volume) */
 } ocam;
 
 static void cam_from(ocam *c, const double pose[16], const double intr[8], double margin) {
@@ -459,6 +461,7 @@ static void cam_from(ocam *c, const double pose[16], const double intr[8], doubl
   c->margin = margin;
   c->mode = 0;
   c->w_floor = 0.0;
+  c->vprev = NULL;
 }
 
 /* R33: voxel (i,j,k) lies in the source view frustum widened by margin*W / margin*H pixels on
@@ -692,6 +695,29 @@ static void combine_voxel_alg1(const ovol *v, const ocam *c, int64_t i, int64_t 
   o->mask = m;
 }
 
+/* a voxel "has data" iff some direction's block holding it is allocated with stored weight > 0 */
+static int has_data(const ovol *v, int64_t i, int64_t j, int64_t k) {
+  for (int D = 0; D < 6; ++D) {
+    int64_t r = record_of(v, D, i, j, k);
+    if (r >= 0 && v->weight[r] > 0.0f) return 1;
+  }
+  return 0;
+}
+
+/* R58: "Voxels that receive data for the first time are always directly added to the combined
+ * TSDF".  After fusion changed the volume from c->vprev (the volume the combined TSDF
+ * was computed from) to v, a voxel that had no data in vprev and has data in v takes its combined
+ * value from v; every other voxel keeps the value combined from vprev (stale until the next
+ * recombination, eqs. condition_1-4).  Without vprev: the combined value from v. */
+static void combined_at(const ovol *v, const ocam *c, int64_t i, int64_t j, int64_t k, ocvox *o) {
+  if (c->vprev) {
+    const int first = !has_data(c->vprev, i, j, k) && has_data(v, i, j, k);
+    combine_voxel(first ? v : c->vprev, c, i, j, k, o);
+    return;
+  }
+  combine_voxel(v, c, i, j, k, o);
+}
+
 /* R35: the stored colour of a combined voxel is the u8 value min(255, floor(c + 1/2)) */
 static uint8_t u8_round(double c) {
   double q = floor(c + 0.5);
@@ -700,23 +726,37 @@ static uint8_t u8_round(double c) {
 
 /* Combined voxels of a list of integer positions (element-wise parity / pins).
  * ijk [n][3]; outputs valid[n], sdf[n], S[n], rgb[n][3] (u8 after R35), mask[n]. */
-void oracle_combined_voxels_mode(void *p, const double pose[16], const double intr[8], double margin, int mode,
-                                 double w_floor, int64_t n, const int64_t *ijk, int32_t *valid, double *sdf, double *S,
-                                 uint8_t *rgb, uint8_t *mask) {
-  const ovol *v = (const ovol *)p;
+static void combined_voxels(const ovol *v, const ovol *vprev, const double pose[16], const double intr[8],
+                            double margin, int mode, double w_floor, int64_t n, const int64_t *ijk, int32_t *valid,
+                            double *sdf, double *S, uint8_t *rgb, uint8_t *mask) {
   ocam c;
   cam_from(&c, pose, intr, margin);
   c.mode = mode;
   c.w_floor = w_floor;
+  c.vprev = vprev;
   for (int64_t q = 0; q < n; ++q) {
     ocvox o;
-    combine_voxel(v, &c, ijk[3 * q], ijk[3 * q + 1], ijk[3 * q + 2], &o);
+    combined_at(v, &c, ijk[3 * q], ijk[3 * q + 1], ijk[3 * q + 2], &o);
     valid[q] = o.valid;
     sdf[q] = o.valid ? o.sdf : 0.0;
     S[q] = o.S;
     for (int a = 0; a < 3; ++a) rgb[3 * q + a] = o.valid ? u8_round(o.rgb[a]) : 0;
     mask[q] = (uint8_t)o.mask;
   }
+}
+
+void oracle_combined_voxels_mode(void *p, const double pose[16], const double intr[8], double margin, int mode,
+                                 double w_floor, int64_t n, const int64_t *ijk, int32_t *valid, double *sdf, double *S,
+                                 uint8_t *rgb, uint8_t *mask) {
+  combined_voxels((const ovol *)p, NULL, pose, intr, margin, mode, w_floor, n, ijk, valid, sdf, S, rgb, mask);
+}
+
+/* R58: combined voxels after fusion changed the volume `before` (the one combined) to `after` */
+void oracle_combined_voxels_update(void *before, void *after, const double pose[16], const double intr[8],
+                                   double margin, int mode, double w_floor, int64_t n, const int64_t *ijk,
+                                   int32_t *valid, double *sdf, double *S, uint8_t *rgb, uint8_t *mask) {
+  combined_voxels((const ovol *)after, (const ovol *)before, pose, intr, margin, mode, w_floor, n, ijk, valid, sdf,
+                  S, rgb, mask);
 }
 
 /* R36: the combined field is a regular TSDF ("can then be used like a regular
@@ -727,7 +767,7 @@ static int ccell(const ovol *v, const ocam *c, const int64_t cc[3], const double
   for (int q = 0; q < 8; ++q) {
     int dx = q & 1, dy = (q >> 1) & 1, dz = (q >> 2) & 1;
     ocvox o;
-    combine_voxel(v, c, cc[0] + dx, cc[1] + dy, cc[2] + dz, &o);
+    combined_at(v, c, cc[0] + dx, cc[1] + dy, cc[2] + dz, &o);
     if (!o.valid) return 0;
     double wt = (dx ? fr[0] : 1.0 - fr[0]) * (dy ? fr[1] : 1.0 - fr[1]) * (dz ? fr[2] : 1.0 - fr[2]);
     ph += wt * o.sdf;
@@ -870,16 +910,17 @@ static void *worker_combined(void *arg) {
 
 /* Render npix pixels of the view (pose, intr) from the combined TSDF of the source camera
  * (src_pose, src_intr, margin).  Argument conventions as oracle_render. */
-void oracle_render_combined_mode(void *p, const double src_pose[16], const double src_intr[8], double margin,
-                                 int mode, double w_floor, const double pose[16], const double intr[8], int64_t npix,
-                                 const int32_t *uv, int row0, int nthreads, double *depth, double *normal,
-                                 uint8_t *color, uint8_t *mask) {
+static void render_combined(const ovol *v, const ovol *vprev, const double src_pose[16], const double src_intr[8],
+                            double margin, int mode, double w_floor, const double pose[16], const double intr[8],
+                            int64_t npix, const int32_t *uv, int row0, int nthreads, double *depth, double *normal,
+                            uint8_t *color, uint8_t *mask) {
   ocjob C;
   memset(&C, 0, sizeof(C));
-  C.v = (const ovol *)p;
+  C.v = v;
   cam_from(&C.src, src_pose, src_intr, margin);
   C.src.mode = mode;
   C.src.w_floor = w_floor;
+  C.src.vprev = vprev;
   ojob *J = &C.J;
   J->v = C.v;
   for (int a = 0; a < 3; ++a) {
@@ -895,6 +936,23 @@ void oracle_render_combined_mode(void *p, const double src_pose[16], const doubl
   for (int i = 0; i < nthreads; ++i) pthread_create(&th[i], NULL, worker_combined, &C);
   for (int i = 0; i < nthreads; ++i) pthread_join(th[i], NULL);
   free(th);
+}
+
+void oracle_render_combined_mode(void *p, const double src_pose[16], const double src_intr[8], double margin,
+                                 int mode, double w_floor, const double pose[16], const double intr[8], int64_t npix,
+                                 const int32_t *uv, int row0, int nthreads, double *depth, double *normal,
+                                 uint8_t *color, uint8_t *mask) {
+  render_combined((const ovol *)p, NULL, src_pose, src_intr, margin, mode, w_floor, pose, intr, npix, uv, row0,
+                  nthreads, depth, normal, color, mask);
+}
+
+/* R58: render the combined TSDF after fusion changed the volume `before` (the one combined) to `after` */
+void oracle_render_combined_update(void *before, void *after, const double src_pose[16], const double src_intr[8],
+                                   double margin, int mode, double w_floor, const double pose[16], const double intr[8],
+                                   int64_t npix, const int32_t *uv, int row0, int nthreads, double *depth,
+                                   double *normal, uint8_t *color, uint8_t *mask) {
+  render_combined((const ovol *)after, (const ovol *)before, src_pose, src_intr, margin, mode, w_floor, pose, intr,
+                  npix, uv, row0, nthreads, depth, normal, color, mask);
 }
 
 /* Conditional combination (eqs. condition_1-4): recombine iff

@@ -488,3 +488,69 @@ def test_combined_mask_on_a_voxel_plane_root():
     assert np.abs(out["depth"][win] - 0.3).max() < 1e-6  # camera height above the floor
     assert (out["mask"][out["depth"] > 0] == 1 << 4).all()
     assert (out["color"][win] == [50, 60, 70]).all()
+
+
+# ---------------------------------------------------------------------------------------
+# R58: voxels receiving data for the first time are added to the combined TSDF
+# ---------------------------------------------------------------------------------------
+def _wall_volume(x_old, x_new, by_hi, w_zero_above=None):
+    """X- (D = 1) walls facing a camera at the origin: blocks by in [-3, by_hi], bx 6..8, bz -3..2.
+    Voxels with y < 0 hold the wall at x_old, y >= 0 at x_new; with w_zero_above, voxels with
+    z > w_zero_above store weight 0 (allocated, no data).  Input fields only."""
+    def field(D, X):
+        x0 = np.where(X[:, 1] < 0, x_old, x_new)
+        w = np.ones(len(X)) if w_zero_above is None else (X[:, 2] <= w_zero_above).astype(float)
+        return np.clip(-(X[:, 0] - x0) / 0.04, -1, 1), w, np.tile([30, 60, 90], (len(X), 1))
+    return field_volume(block_cube((6, -3, -3), (8, by_hi, 2), [1]), field, 0.01, truncation=0.04)
+
+
+def test_first_time_voxels_are_added_and_stale_voxels_kept():
+    """R58 ("Voxels that receive data for the first time are always directly added to the
+    combined TSDF"; P:254-256 conditional combination).  The combined TSDF was computed from
+    `before`: a wall at x = 0.60 over y < 0, weight 0 above z = 0.05.  Fusion produced `after`:
+    the wall at 0.62 everywhere, new blocks over y >= 0, weights 1.  Voxels that had data before
+    keep the value combined from `before` (the wall at 0.60, stale); voxels of the new blocks and
+    the zero-weight voxels above z = 0.05 take the value combined from `after` (0.62).  Rendered
+    from the source camera: depth 0.60 where the old data lies, 0.62 elsewhere (closed forms)."""
+    before = _wall_volume(0.60, 0.60, -1, w_zero_above=0.05)
+    after = _wall_volume(0.62, 0.62, 2)
+    ob, oa = oracle.OracleVolume(before), oracle.OracleVolume(after)
+    K = pinhole(48, 36, 40.0)
+    pose = look_at([0, 0, 0], [1, 0, 0])
+    ijk = _vox_grid(after)
+    cv = oracle.combined_voxels(oa, pose, K, ijk, before=ob)
+    s_old, w_old = _stored(before, 1, ijk)
+    s_new, _ = _stored(after, 1, ijk)
+    had = w_old > 0  # NaN (unallocated before) compares False
+    inner = (np.abs(s_new) < 0.74) & (np.abs(ijk[:, 1:] + 0.5) < 20).all(1)
+    inner &= ~had | (np.abs(s_old) < 0.74)
+    assert (inner & had).sum() > 200 and (inner & ~had).sum() > 200
+    assert cv["valid"][inner].all()
+    assert np.abs(cv["sdf"][inner & had] - s_old[inner & had]).max() < 1e-12   # stale
+    assert np.abs(cv["sdf"][inner & ~had] - s_new[inner & ~had]).max() < 1e-12  # added
+    # without `before` the same call is the fresh combination of `after`
+    fresh = oracle.combined_voxels(oa, pose, K, ijk)
+    assert np.abs(fresh["sdf"][inner] - s_new[inner]).max() < 1e-12
+    # render from the source camera
+    out = oracle.render_combined(oa, pose, K, pose, K, before=ob)
+    o, r, L = oracle.ray_dirs(pose, K)
+    hit = out["depth"].ravel() > 0
+    X = (o + (out["depth"].ravel() * L)[:, None] * r)
+    old = hit & (X[:, 1] < -0.03) & (X[:, 2] < 0.02) & (X[:, 2] > -0.02)
+    new = hit & ((X[:, 1] > 0.03) | (X[:, 2] > 0.08)) & (np.abs(X[:, 1]) < 0.18) & (np.abs(X[:, 2]) < 0.18)
+    assert old.sum() > 20 and new.sum() > 20
+    assert np.abs(out["depth"].ravel()[old] - 0.60).max() < 1e-6
+    assert np.abs(out["depth"].ravel()[new] - 0.62).max() < 1e-6
+
+
+def test_first_time_voxels_outside_the_frustum_stay_invalid():
+    """R58 with R33: a first-time voxel outside the source camera's widened frustum is not added
+    (such pixels stay invalid until the next recombination)."""
+    before = _wall_volume(0.60, 0.60, -1)
+    after = _wall_volume(0.60, 0.60, 2)
+    ob, oa = oracle.OracleVolume(before), oracle.OracleVolume(after)
+    K = pinhole(8, 8, 40.0, z_max=15.0)  # narrow view: the new blocks (y >= 0.16) lie outside it
+    pose = look_at([0, -0.1, 0], [1, -0.1, 0])
+    ijk = np.array([[61, j, 0] for j in range(16, 24)], np.int64)
+    cv = oracle.combined_voxels(oa, pose, K, ijk, before=ob)
+    assert not cv["valid"].any()
