@@ -92,12 +92,14 @@ __device__ int classify_block(const CombineLaunch &p, int bx, int by, int bz, in
 
 // One warp per allocated block location: a location with any voxel in the widened frustum gets a
 // combined slot (atomic counter); .w of comb_loc keeps the hash entry, cls (1 inside, 2
-// straddling) rides in bit 30 of slot_of_entry's companion array comb_cls.
+// straddling) goes to p.cls.  Locations that already hold a slot are skipped (an R58 update
+// selects only the locations a fused frame added).
 __global__ void __launch_bounds__(256) k_comb_select(const __grid_constant__ CombineLaunch p, unsigned char *cls_out) {
   const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (u >= p.n_loc) return;
   const int4 b = p.locations[u];
+  if (p.slot_of_entry[b.w] >= 0) return;  // warp-uniform
   const int cls = classify_block(p, b.x, b.y, b.z, lane);
   if (cls == 0 || lane != 0) return;
   const int slot = (int)atomicAdd(p.n_sel, 1u);
@@ -106,12 +108,25 @@ __global__ void __launch_bounds__(256) k_comb_select(const __grid_constant__ Com
   cls_out[slot] = (unsigned char)cls;
 }
 
+// R58: in a full combination every voxel is computed; in an update after a fused frame, a voxel of
+// a slot that existed before the frame is recomputed only if it had no data before (had bit
+// clear) and has data now (some direction's record with weight > 0); new slots are computed whole.
+__device__ __forceinline__ bool first_time(const CombineLaunch &p, size_t slot, int l, const int sl[6]) {
+  if (!p.had || (long long)slot >= p.n_old) return true;
+  if ((__ldg(&p.had[slot * 16 + (l >> 5)]) >> (l & 31)) & 1u) return false;
+  const int roff = (l & 7) + kRec * ((l >> 3) & 7) + kRec * kRec * (l >> 6);
+  bool now = false;
+#pragma unroll
+  for (int D = 0; D < 6; ++D)
+    if (sl[D] >= 0) now |= __ldg(&p.vol.brick_a[(size_t)sl[D] * kRecStride + roff].y) > 0.0f;
+  return now;
+}
+
 // R34: one thread per voxel of a combined slot (4 CTAs of 128 per slot).  All loads of the
 // present directions -- centre {sdf, weight}, the 6 neighbouring sdf values ("the
 // gradient can be computed with just looking up the SDF values stored in the 6 neighboring
 // voxels"; NaN where unallocated) and the colour -- are issued before any is used.
-__global__ void __launch_bounds__(128) k_combine(const __grid_constant__ CombineLaunch p,
-                                                 const unsigned char *__restrict__ cls_in) {
+__global__ void __launch_bounds__(128) k_combine(const __grid_constant__ CombineLaunch p) {
   const VolumeView &V = p.vol;
   // the 4 CTAs of a slot are adjacent in launch order (blockIdx.x = 4 slot + quarter, so any
   // number of slots fits the grid's x extent): they share the slot's bricks in L2 while they run
@@ -123,10 +138,11 @@ __global__ void __launch_bounds__(128) k_combine(const __grid_constant__ Combine
   const int4 *e = reinterpret_cast<const int4 *>(&V.table[b.w]);
   const int4 ea = __ldg(e), eb = __ldg(e + 1);
   const int sl[6] = {ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
+  if (!first_time(p, slot, l, sl)) return;  // R58 update: this voxel keeps its value
   const int i = kBlock * b.x + lx, j = kBlock * b.y + ly, k = kBlock * b.z + lz;
   double d[3];
   bool in = true;
-  if (cls_in[slot] == 2) {
+  if (p.cls[slot] == 2) {
     in = in_frustum(p, (double)V.voxel_size, i, j, k, d);
   } else {
     const double s = (double)V.voxel_size;
@@ -358,8 +374,7 @@ __device__ __forceinline__ void back_point(const double x[3], double t, const do
   for (int a = 0; a < 3; ++a) y[a] = s64(x[a], m64(t, r[a]));
 }
 
-__global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p,
-                                                      const unsigned char *__restrict__ cls_in) {
+__global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ CombineLaunch p) {
   const VolumeView &V = p.vol;
   const size_t slot = blockIdx.x >> 2;  // as k_combine: 4 adjacent CTAs per slot on grid x
   const int l = (blockIdx.x & 3) * 128 + threadIdx.x;
@@ -368,11 +383,12 @@ __global__ void __launch_bounds__(128) k_combine_alg1(const __grid_constant__ Co
   const int4 *ent = reinterpret_cast<const int4 *>(&V.table[b.w]);
   const int4 ea = __ldg(ent), eb = __ldg(ent + 1);
   const int sl[6] = {ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
+  if (!first_time(p, slot, l, sl)) return;  // R58 update: this voxel keeps its value
   const int i = kBlock * b.x + lx, j = kBlock * b.y + ly, k = kBlock * b.z + lz;
   const double s = (double)V.voxel_size;
   double d[3];
   bool in = true;
-  if (cls_in[slot] == 2) {
+  if (p.cls[slot] == 2) {
     in = in_frustum(p, s, i, j, k, d);
   } else {
     d[0] = s64(m64((double)i, s), p.t[0]);
@@ -630,9 +646,39 @@ cudaError_t launch_comb_remap(const HashEntry *table, unsigned int mask, int4 *c
   return cudaGetLastError();
 }
 
+// R58: one thread per voxel of a combined slot: did any direction hold data there (pool weight > 0)?
+__global__ void k_comb_had(const HashEntry *__restrict__ table, const int4 *__restrict__ comb_loc, long long n,
+                           const float *__restrict__ w, unsigned int *had) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long slot = g >> 9;
+  const int l = (int)(g & 511);
+  bool h = false;
+  if (slot < n) {
+    const int e = comb_loc[slot].w;
+    if (e < 0) {
+      h = true;  // the location left the volume: nothing to add
+    } else {
+#pragma unroll
+      for (int D = 0; D < 6; ++D) {
+        const int b = table[e].slot[D];
+        if (b >= 0) h |= w[(size_t)b * kVoxPerBlock + l] > 0.0f;
+      }
+    }
+  }
+  const unsigned int word = __ballot_sync(0xffffffffu, h);
+  if (slot < n && (l & 31) == 0) had[slot * 16 + (l >> 5)] = word;
+}
+
+cudaError_t launch_comb_had(const HashEntry *table, const int4 *comb_loc, long long n, const float *pool_weight,
+                            unsigned int *had, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_comb_had<<<(unsigned)((n * 512 + 255) / 256), 256, 0, s>>>(table, comb_loc, n, pool_weight, had);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s) {
   if (p.n_loc == 0) return cudaSuccess;
-  k_comb_select<<<(unsigned)((p.n_loc * 32 + 255) / 256), 256, 0, s>>>(p, p.surf);
+  k_comb_select<<<(unsigned)((p.n_loc * 32 + 255) / 256), 256, 0, s>>>(p, p.cls);
   return cudaGetLastError();
 }
 
@@ -641,9 +687,9 @@ cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaS
   // one grid row of 4 CTAs per slot would cap n_sel at gridDim.y's 65535: the slots go on x
   const unsigned grid = (unsigned)(4 * n_sel);
   if (p.mode == 1)
-    k_combine_alg1<<<grid, 128, 0, s>>>(p, p.surf);
+    k_combine_alg1<<<grid, 128, 0, s>>>(p);
   else
-    k_combine<<<grid, 128, 0, s>>>(p, p.surf);
+    k_combine<<<grid, 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_comb_finish<<<(unsigned)n_sel, kFinishThreads, 0, s>>>(p);

@@ -165,6 +165,11 @@ struct CombineLaunch {
   float *weight;                   // [cap][512] S = sum_D W_D of each interior voxel
   unsigned int *cell_pos;          // [cap][16]
   unsigned char *surf;             // [cap]
+  unsigned char *cls;              // [cap] frustum class of each slot's block: 1 inside, 2 straddling
+  // R58 update after a fused frame (null had: a full combination): slots < n_old keep their
+  // voxels except those without data before the frame (had bit clear) that have data now
+  const unsigned int *had;         // [n_old][16] bit l: voxel l of the slot had data before the frame
+  long long n_old;
   int mode;                        // 0 eq:combine_weight / eq:combine_tsdf_weight, 1 Algorithm 1
   float w_floor;                   // Algorithm 1: stored-weight floor of a taking-part direction
   double theta64;                  // Algorithm 1: theta (fp64) for the w_dir > 0 decision
@@ -268,6 +273,10 @@ cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s);             
 cudaError_t launch_combine_finish(const CombineLaunch &p, long long n_sel, cudaStream_t s);  // aprons, masks
 cudaError_t launch_comb_remap(const HashEntry *table, unsigned int mask, int4 *comb_loc, long long n,
                               int *slot_of_entry, cudaStream_t s);
+// R58: bit l of had[s] = voxel l of combined slot s has data (a direction's block with weight > 0)
+// in the pool as it stands (before a fused frame); comb_loc[s].w are current hash entries
+cudaError_t launch_comb_had(const HashEntry *table, const int4 *comb_loc, long long n, const float *pool_weight,
+                            unsigned int *had, cudaStream_t s);
 
 // host launchers (volume.cu); all run on stream s and return the first launch error
 struct CommitScratch {

@@ -100,7 +100,14 @@ struct dtsdf_ctx {
   float *comb_apron = nullptr, *comb_weight = nullptr;
   uchar4 *comb_rgb = nullptr;
   unsigned int *comb_cell_pos = nullptr, *comb_count = nullptr;
-  unsigned char *comb_surf = nullptr;
+  unsigned char *comb_surf = nullptr, *comb_cls = nullptr;
+  unsigned int *comb_had = nullptr;  // R58: per-slot "had data" masks captured before a fused frame
+  size_t cap_comb_had = 0;
+  // the camera and rule of the current combined TSDF (R58 updates after fused frames reuse them)
+  float comb_pose[16] = {0};
+  dtsdf_intrinsics comb_K{};
+  float comb_margin = 0.f, comb_wfloor = 0.f;
+  int comb_mode = 0;
   // tracing
   bool profiling = false;
   std::vector<TimedLaunch> timed;
@@ -136,6 +143,9 @@ void free_combined(dtsdf_ctx *c) {
   dfree(c->comb_rgb);
   dfree(c->comb_cell_pos);
   dfree(c->comb_surf);
+  dfree(c->comb_cls);
+  dfree(c->comb_had);
+  c->cap_comb_had = 0;
   dfree(c->comb_count);
   c->combined = false;
   c->n_comb = c->comb_cap = 0;
@@ -717,42 +727,64 @@ int dtsdf_combine(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K,
   return dtsdf_combine_mode(c, pose, K, margin, DTSDF_COMBINE_WEIGHTED, 0.0f, stream);
 }
 
-int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float margin, int32_t mode,
-                       float w_floor, void *stream) {
-  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
-  if (mode != DTSDF_COMBINE_WEIGHTED && mode != DTSDF_COMBINE_ALGORITHM1)
-    return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown combination mode");
-  if (!(w_floor >= 0.f) || !std::isfinite(w_floor)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "w_floor must be >= 0");
-  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
-  int rc = check_intr(K);
-  if (rc) return rc;
-  if (!pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is NULL");
-  for (int i = 0; i < 16; ++i)
-    if (!std::isfinite(pose[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
-  if (!(margin >= 0.f) || !(margin <= 16.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "margin must lie in [0, 16]");
-  if (!c->committed) return fail(DTSDF_ERR_NO_VOLUME, "no committed volume");
-  cudaSetDevice(c->device);
-  cudaStream_t s = (cudaStream_t)stream;
-  c->combined = false;
-  // capacity: every allocated location (kept across combines of the same volume)
-  const int64_t cap = std::max<int64_t>(c->n_loc, 1);
-  if (c->comb_cap < cap || c->comb_entries != c->table_cap) {
+}  // extern "C"
+
+namespace {
+
+// combined-TSDF buffers for `cap` slots (slot_of_entry sized by the hash table)
+int comb_alloc(dtsdf_ctx *c, int64_t cap) {
+  if (dalloc(c->comb_slot, (size_t)c->table_cap * 4) != cudaSuccess ||
+      dalloc(c->comb_loc, (size_t)cap * sizeof(int4)) != cudaSuccess ||
+      dalloc(c->comb_apron, (size_t)cap * kApronStride * 4) != cudaSuccess ||
+      dalloc(c->comb_weight, (size_t)cap * kVoxPerBlock * 4) != cudaSuccess ||
+      dalloc(c->comb_rgb, (size_t)cap * kRgbApronStride * sizeof(uchar4)) != cudaSuccess ||
+      dalloc(c->comb_cell_pos, (size_t)cap * 64) != cudaSuccess || dalloc(c->comb_surf, (size_t)cap) != cudaSuccess ||
+      dalloc(c->comb_cls, (size_t)cap) != cudaSuccess || dalloc(c->comb_count, 16) != cudaSuccess) {
+    cudaGetLastError();
     free_combined(c);
-    if (dalloc(c->comb_slot, (size_t)c->table_cap * 4) != cudaSuccess ||
-        dalloc(c->comb_loc, (size_t)cap * sizeof(int4)) != cudaSuccess ||
-        dalloc(c->comb_apron, (size_t)cap * kApronStride * 4) != cudaSuccess ||
-        dalloc(c->comb_weight, (size_t)cap * kVoxPerBlock * 4) != cudaSuccess ||
-        dalloc(c->comb_rgb, (size_t)cap * kRgbApronStride * sizeof(uchar4)) != cudaSuccess ||
-        dalloc(c->comb_cell_pos, (size_t)cap * 64) != cudaSuccess || dalloc(c->comb_surf, (size_t)cap) != cudaSuccess ||
-        dalloc(c->comb_count, 16) != cudaSuccess) {
-      cudaGetLastError();
-      free_combined(c);
-      return fail(DTSDF_ERR_OUT_OF_MEMORY, "combined TSDF buffers");
-    }
-    c->comb_cap = cap;
-    c->comb_entries = c->table_cap;
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "combined TSDF buffers");
   }
-  CombineLaunch L;
+  c->comb_cap = cap;
+  c->comb_entries = c->table_cap;
+  return DTSDF_OK;
+}
+
+// grow the combined buffers to `cap` slots keeping the first n_comb slots (R58 updates add slots)
+template <typename T>
+cudaError_t grow_copy(T *&p, size_t old_bytes, size_t new_bytes, cudaStream_t s) {
+  T *q = nullptr;
+  cudaError_t e = cudaMalloc((void **)&q, std::max<size_t>(new_bytes, 16));
+  if (e != cudaSuccess) return e;
+  if (old_bytes) e = cudaMemcpyAsync(q, p, old_bytes, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) { cudaFree(q); return e; }
+  cudaStreamSynchronize(s);
+  cudaFree(p);
+  p = q;
+  return cudaSuccess;
+}
+
+int comb_grow(dtsdf_ctx *c, int64_t cap, cudaStream_t s) {
+  const size_t n = (size_t)c->n_comb, m = (size_t)cap;
+  if (grow_copy(c->comb_loc, n * sizeof(int4), m * sizeof(int4), s) != cudaSuccess ||
+      grow_copy(c->comb_apron, n * kApronStride * 4, m * kApronStride * 4, s) != cudaSuccess ||
+      grow_copy(c->comb_weight, n * kVoxPerBlock * 4, m * kVoxPerBlock * 4, s) != cudaSuccess ||
+      grow_copy(c->comb_rgb, n * kRgbApronStride * sizeof(uchar4), m * kRgbApronStride * sizeof(uchar4), s) != cudaSuccess ||
+      grow_copy(c->comb_cell_pos, n * 64, m * 64, s) != cudaSuccess || grow_copy(c->comb_surf, n, m, s) != cudaSuccess ||
+      grow_copy(c->comb_cls, n, m, s) != cudaSuccess) {
+    cudaGetLastError();
+    free_combined(c);
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "combined TSDF buffers (growth after fusion)");
+  }
+  c->comb_cap = cap;
+  return DTSDF_OK;
+}
+
+// the combine launch of the current volume and the stored camera / rule of the combined TSDF
+void comb_launch(dtsdf_ctx *c, CombineLaunch &L) {
+  const float *pose = c->comb_pose;
+  const dtsdf_intrinsics *K = &c->comb_K;
+  const float margin = c->comb_margin;
+  L = CombineLaunch{};
   L.vol.table = c->table;
   L.vol.table_mask = c->table_cap - 1;
   L.vol.loc_grid = c->use_grid ? c->loc_grid : nullptr;
@@ -787,9 +819,79 @@ int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsic
   L.weight = c->comb_weight;
   L.cell_pos = c->comb_cell_pos;
   L.surf = c->comb_surf;
-  L.mode = mode;
-  L.w_floor = w_floor;
+  L.cls = c->comb_cls;
+  L.had = nullptr;
+  L.n_old = 0;
+  L.mode = c->comb_mode;
+  L.w_floor = c->comb_wfloor;
   L.theta64 = (double)c->params.theta;
+}
+
+// R58: after a fused frame -- the volume re-committed, the kept slots re-pointed --
+// combine the voxels that received data for the first time with the stored camera: the frame's
+// new locations inside the widened frustum get slots (computed whole), the old slots only at
+// voxels whose had bit (captured before the frame) is clear and that hold data now; then the
+// aprons and skip masks of every slot are rebuilt.
+int comb_update(dtsdf_ctx *c, cudaStream_t s) {
+  const int64_t n_old = c->n_comb;
+  if (c->n_loc > c->comb_cap) {
+    int rc = comb_grow(c, c->n_loc, s);
+    if (rc) return rc;
+  }
+  CombineLaunch L;
+  comb_launch(c, L);
+  L.had = c->comb_had;
+  L.n_old = n_old;
+  const unsigned int n0 = (unsigned int)n_old;
+  CK(c, cudaMemcpyAsync(c->comb_count, &n0, 4, cudaMemcpyHostToDevice, s), "combine update init");
+  TimedLaunch tl{};
+  begin_timed(c, 3, s, &tl, c->n_loc > 0 ? 1 : 0);
+  CK(c, launch_combine(L, s), "combine update select");
+  end_timed(c, s, &tl);
+  unsigned int nsel = 0;
+  CK(c, cudaMemcpyAsync(&nsel, c->comb_count, 4, cudaMemcpyDeviceToHost, s), "combine update readback");
+  CK(c, cudaStreamSynchronize(s), "combine update sync");
+  begin_timed(c, 3, s, &tl, nsel > 0 ? 2 : 0);
+  CK(c, launch_combine_finish(L, (long long)nsel, s), "combine update");
+  end_timed(c, s, &tl);
+  c->n_comb = nsel;
+  return DTSDF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtsdf_combine_mode(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, float margin, int32_t mode,
+                       float w_floor, void *stream) {
+  if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (mode != DTSDF_COMBINE_WEIGHTED && mode != DTSDF_COMBINE_ALGORITHM1)
+    return fail(DTSDF_ERR_INVALID_ARGUMENT, "unknown combination mode");
+  if (!(w_floor >= 0.f) || !std::isfinite(w_floor)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "w_floor must be >= 0");
+  if (c->sticky) return fail(DTSDF_ERR_CUDA, "context has a sticky CUDA error");
+  int rc = check_intr(K);
+  if (rc) return rc;
+  if (!pose) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is NULL");
+  for (int i = 0; i < 16; ++i)
+    if (!std::isfinite(pose[i])) return fail(DTSDF_ERR_INVALID_ARGUMENT, "pose is not finite");
+  if (!(margin >= 0.f) || !(margin <= 16.f)) return fail(DTSDF_ERR_INVALID_ARGUMENT, "margin must lie in [0, 16]");
+  if (!c->committed) return fail(DTSDF_ERR_NO_VOLUME, "no committed volume");
+  cudaSetDevice(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  c->combined = false;
+  // capacity: every allocated location (kept across combines of the same volume)
+  const int64_t cap = std::max<int64_t>(c->n_loc, 1);
+  if (c->comb_cap < cap || c->comb_entries != c->table_cap) {
+    free_combined(c);
+    if ((rc = comb_alloc(c, cap))) return rc;
+  }
+  std::memcpy(c->comb_pose, pose, sizeof(c->comb_pose));
+  c->comb_K = *K;
+  c->comb_margin = margin;
+  c->comb_mode = mode;
+  c->comb_wfloor = w_floor;
+  CombineLaunch L;
+  comb_launch(c, L);
   TimedLaunch tl{};
   CK(c, cudaMemsetAsync(c->comb_slot, 0xFF, (size_t)c->table_cap * 4, s), "combine init");
   CK(c, cudaMemsetAsync(c->comb_count, 0, 16, s), "combine init");
@@ -1036,6 +1138,18 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   L.max_weight = prm.max_weight;
   L.carve_weight = prm.carve_weight;
   L.carve_radius = prm.carve_radius;
+  // R58: which voxels of the combined TSDF's slots hold data before this frame
+  const bool comb = c->combined;
+  if (comb && c->n_comb > 0) {
+    if (ensure(c->comb_had, c->cap_comb_had, (size_t)c->n_comb * 64) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "combined TSDF update masks");
+    }
+    TimedLaunch tlh{};
+    begin_timed(c, 3, s, &tlh);
+    CK(c, launch_comb_had(c->table, c->comb_loc, c->n_comb, c->weight, c->comb_had, s), "combine had");
+    end_timed(c, s, &tlh);
+  }
   // scratch: flags (int) + pool counter (u64)
   L.flags = c->scratch;
   L.n_blocks = reinterpret_cast<unsigned long long *>(c->scratch + 12);
@@ -1064,6 +1178,7 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   rc = dtsdf_commit_volume(c, stream);
   c->values_trusted = false;
   if (rc) return rc;
+  if (comb && c->combined && (rc = comb_update(c, s))) return rc;
   if (full) return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion capacity exhausted (blocks allocated so far are kept)");
   return DTSDF_OK;
 }

@@ -41,15 +41,18 @@ def _voxels(locs):
     return (locs.astype(np.int64)[:, None, :] * 8 + off[None]).reshape(-1, 3)
 
 
-def _compare_voxels(R, w, pose, budget=1e-3, mode=0):
+def _compare_voxels(R, w, pose, budget=1e-3, mode=0, vol=None, before=None):
     """Every exported combined voxel against the oracle's combine_voxel at the same position, and
-    sampled non-exported locations hold no valid oracle voxel."""
+    sampled non-exported locations hold no valid oracle voxel.  vol: the volume (default
+    w.volume); before: the OracleVolume the combined TSDF was computed from when fusion has since
+    changed it (reading R58)."""
+    vol = w.volume if vol is None else vol
     ex = R.get_combined()
     n = len(ex["locs"])
     assert n > 0
-    ov = oracle.OracleVolume(w.volume)
+    ov = oracle.OracleVolume(vol)
     ijk = _voxels(ex["locs"])
-    o = oracle.combined_voxels(ov, pose, w.intrinsics, ijk, mode=mode)
+    o = oracle.combined_voxels(ov, pose, w.intrinsics, ijk, mode=mode, before=before)
     g_valid = ~np.isnan(ex["sdf"].reshape(-1))
     assert np.array_equal(g_valid, ex["weight"].reshape(-1) > 0)
     disagree = (g_valid != o["valid"]).sum()
@@ -66,13 +69,13 @@ def _compare_voxels(R, w, pose, budget=1e-3, mode=0):
     assert (w_rel > WEIGHT_RTOL).sum() <= budget * both.sum(), st
     assert rgb_eq >= 0.999 and mask_eq >= 0.999, st
     # completeness: allocated locations the GPU did not combine have no valid oracle voxel
-    locs_all = np.unique(w.volume.keys[:, :3], axis=0)
+    locs_all = np.unique(vol.keys[:, :3], axis=0)
     got = {tuple(l) for l in ex["locs"]}
     rest = np.array([l for l in locs_all if tuple(l) not in got])
     if len(rest):
         rng = np.random.default_rng(0)
         pick = rest[rng.choice(len(rest), min(len(rest), 400), replace=False)]
-        assert oracle.combined_voxels(ov, pose, w.intrinsics, _voxels(pick), mode=mode)["valid"].sum() <= \
+        assert oracle.combined_voxels(ov, pose, w.intrinsics, _voxels(pick), mode=mode, before=before)["valid"].sum() <= \
             budget * both.sum()
     return st
 
@@ -223,3 +226,40 @@ def test_combined_host_outputs_equal_device_outputs(R, c1):
         for k, h in (("depth", hd), ("normal", hn), ("color", hc), ("mask", hm)):
             assert torch.equal(g[k].cpu(), h), (k, host_write)
     R.set_option(OPT_HOST_WRITE, 1)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fused_frame_adds_first_time_voxels(R, c1, mode):
+    """Reading R58: the combined TSDF of the bench pose is computed from the room
+    without its last 8 boxes; a frame of the whole room (ideal depth camera) is then fused.  Every
+    combined voxel equals the oracle's: voxels that received data for the first time (the missing
+    boxes' new blocks, zero-weight voxels that gained weight) combined from the fused volume, all
+    others kept from the combination before the frame; the render through it likewise.  The fused
+    volume on the oracle side is the oracle's own fusion (oracle/fusion.c) of the same frame."""
+    import dataclasses
+    S, TAU = 0.01, 0.04
+    pat = c1.patches
+    keep = 1 + 5 * 12  # floor + 12 of the 20 boxes (5 patches each)
+    sub = dataclasses.replace(pat, **{f: getattr(pat, f)[:keep] for f in ("q", "n", "u", "v", "hu", "hv", "color", "kind")})
+    before = scenes.patch_fill(sub, voxel_size=S, truncation=TAU, theta=scenes.THETA)
+    pose, K = c1.poses[0], c1.intrinsics
+    K_half = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=320, height=240)
+    fr = scenes.analytic_frame(pat, pose, K_half)
+    cap = before.n_blocks + 30000
+    R.upload_volume(before)
+    R.fusion_reserve(cap)
+    R.combine(pose, K, mode=mode)
+    n_before = R.combined_stats()["n_locations"]
+    new_blocks = R.fuse(fr.depth, fr.normal, fr.color, pose, K_half)
+    F = oracle.OracleFusion(S, TAU, scenes.THETA, cap, vol=before)
+    assert F.fuse(fr.depth, fr.normal, fr.color, pose, K_half) == new_blocks > 500
+    after = F.volume()
+    n_after = R.combined_stats()["n_locations"]
+    assert n_after > n_before
+    ob = oracle.OracleVolume(before)
+    st = _compare_voxels(R, c1, pose, mode=mode, vol=after, before=ob)
+    g = R.render(c1.poses, K, combined=True)
+    o = oracle.render_combined(oracle.OracleVolume(after), pose, K, pose, K, mode=mode, before=ob)
+    rs = assert_parity(_sel(g, 0), o, what=f"C1 combined after a fused frame (mode {mode})")
+    # the added boxes are visible: more hits than the combination before the frame rendered
+    print("R58", mode, n_before, n_after, st, rs)
