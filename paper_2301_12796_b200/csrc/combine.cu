@@ -126,7 +126,10 @@ __device__ __forceinline__ bool first_time(const CombineLaunch &p, size_t slot, 
 // present directions -- centre {sdf, weight}, the 6 neighbouring sdf values ("the
 // gradient can be computed with just looking up the SDF values stored in the 6 neighboring
 // voxels"; NaN where unallocated) and the colour -- are issued before any is used.
-__global__ void __launch_bounds__(128) k_combine(const __grid_constant__ CombineLaunch p) {
+#ifndef DTSDF_COMB_MINB
+#define DTSDF_COMB_MINB 16  // 32 registers, full occupancy: C1 combine 0.195 -> 0.165 ms (profiles/r2j_ab_combine.txt)
+#endif
+__global__ void __launch_bounds__(128, DTSDF_COMB_MINB) k_combine(const __grid_constant__ CombineLaunch p) {
   const VolumeView &V = p.vol;
   // the 4 CTAs of a slot are adjacent in launch order (blockIdx.x = 4 slot + quarter, so any
   // number of slots fits the grid's x extent): they share the slot's bricks in L2 while they run
