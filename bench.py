@@ -62,6 +62,8 @@ def parse():
                          "rows: every view's rows are split per rank via row0/row1 (C4's large view) -- strong scaling")
     ap.add_argument("--combine-mode", type=int, default=0, choices=[0, 1],
                     help="combined mode: 0 eq:combine_weight (the paper's method), 1 Algorithm 1 (NEXT-4)")
+    ap.add_argument("--boxes", type=int, default=20,
+                    help="C1 only: boxes in the room (20 = configs[1]; more approach configs[1]'s ~40k blocks, R30)")
     ap.add_argument("--batch-views", type=int, default=256,
                     help="views of the strong-scaling C3 batch timed after the headline (SURVEY §8(e)); 0 = skip")
     ap.add_argument("--dry-run", action="store_true",
@@ -106,8 +108,10 @@ def dry_run(args) -> int:
     return 0
 
 
-def workload(name):
+def workload(name, boxes=20):
     import scenes
+    if name == "C1" and boxes != 20:  # sensitivity to the block count (reading R30: configs[1] says ~40k)
+        return scenes.c1_room(n_boxes=boxes)
     if name == "C0":
         return scenes.c0_sphere()
     if name == "C2":
@@ -119,10 +123,10 @@ def workload(name):
     return scenes.c1_room()
 
 
-def describe(w, views):
+def describe(w, views, boxes=20):
     K = w.intrinsics
     return {"workload": f"{w.name}: " + {
-        "C1": "room scale, 20 seeded boxes on a 4x4 m floor, 1 cm voxels, tau 4 cm, one 640x480 view at the "
+        "C1": f"room scale, {boxes} seeded boxes on a 4x4 m floor, 1 cm voxels, tau 4 cm, one 640x480 view at the "
               "seeded pose (fx=fy=525, cx=319.5, cy=239.5)",
         "C0": "dense sphere r=0.2 m, 64^3 voxels at 1 cm, 80x60 view",
         "C2": "200 thin plates, 5 mm voxels, 640x480 views",
@@ -220,7 +224,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    w = workload(args.config)
+    w = workload(args.config, args.boxes)
     threads = os.cpu_count() or 1
     n0, dt0, _, _ = oracle_sample_rate(w, 1024, seed=1, threads=threads)
     rate = n0 / max(dt0, 1e-3)
@@ -236,7 +240,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(describe(w, args.views), mode=args.mode),  # the product arm's config keys
+            "config": dict(describe(w, args.views, args.boxes), mode=args.mode),  # the product arm's config keys
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"each step: {n} of {w.intrinsics.width * w.intrinsics.height} pixel rays "
                                        f"of the {w.name} view (seeded uniform subset)"},
@@ -276,7 +280,7 @@ def run_dtsdf(args):
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=dev)
-    w = workload(args.config) if rank == 0 else None
+    w = workload(args.config, args.boxes) if rank == 0 else None
     R = Renderer(local)
     stream = torch.cuda.current_stream()
 
@@ -528,7 +532,7 @@ def run_dtsdf(args):
         "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
         "scaling": "weak" if args.shard == "none" else "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scene, DESIGN.md §3)",
-        "config": dict(describe(w, args.views), mode=args.mode,
+        "config": dict(describe(w, args.views, args.boxes), mode=args.mode,
                        **({"combine_mode": args.combine_mode} if args.mode == "combined" else {}),
                        **({"shard": args.shard, "views_per_step_total": args.views,
                            "views_per_step_per_gpu": len(idx), "rows_per_gpu": row1 - row0}
