@@ -339,6 +339,13 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *                         drain; longer batches stay row-major.  2 always, 0 never.  Changes only when a
  *                         tile runs, never what it computes. */
 #define DTSDF_OPT_TILE_ORDER 9
+/*   DTSDF_OPT_INCREMENTAL  1 (default) dtsdf_fuse updates the index incrementally: the allocation
+ *                          extends the hash table in place, and only the locations within one block
+ *                          of a block the frame changed get their record bricks, cell masks and
+ *                          location-grid values rebuilt (a full re-commit when a new location falls
+ *                          outside the location AABB or the pool fills); 0 re-commits the whole
+ *                          volume after every frame.  Same results either way. */
+#define DTSDF_OPT_INCREMENTAL 11
 /* Testing only:
  *   DTSDF_OPT_RANGE_EPOCH  n != 0 (read as uint32): the next range pass uses epoch n + 1 (the range keys carry a per-pass
  *                          epoch; passes at or above 0xFFFFFFF0 clear the buffers and restart at 1), to

@@ -232,6 +232,13 @@ struct FuseLaunch {
   float theta_f, cos_theta_f, sin_theta_f, inv_blend;
   float max_weight, carve_weight;
   int carve_radius;
+  // incremental index update (dtsdf_fuse): new locations are appended to `locations` (counter
+  // n_loc) and checked against the location AABB (flags[1] <- 1 when one lies outside it); blocks
+  // whose voxels changed, and new blocks, get dirty[b] = 1 (null: not tracked)
+  int4 *locations;
+  unsigned long long *n_loc;
+  int lo[3], dim[3];
+  unsigned char *dirty;
 };
 
 // ICP state in device memory (icp.cu): written by k_icp_solve, read back once per call
@@ -295,13 +302,28 @@ cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsign
                             int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
-cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float4 *brick_a,
-                            unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s);
-cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
-                           int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
+// record bricks of n blocks (list: their pool indices, or null for blocks 0..n-1), each adding its
+// direction's bits to the location's live-direction bytes (cell_dirs, which start at 0x80)
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
-                          cudaStream_t s);
+                          unsigned char *cell_dirs, const int *list, cudaStream_t s);
+cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s);
+// incremental commit after a fused frame: the locations whose record bricks must be rebuilt (the
+// 27-neighbourhoods, in the dirty block's direction, of every dirty block) -> loc_list (deduplicated
+// by loc_mark[entry]), then all blocks of those locations -> blk_list; counters ctr[0], ctr[1]
+cudaError_t launch_inc_mark(const int4 *keys, long long n, const unsigned char *dirty, const HashEntry *table,
+                            unsigned int mask, int *loc_mark, int4 *loc_list, unsigned long long *ctr, cudaStream_t s);
+cudaError_t launch_inc_blocks(const int4 *loc_list, long long n, const HashEntry *table, int *blk_list,
+                              unsigned long long *ctr, cudaStream_t s);
+cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s);
+// k_bricks over a device-counted list: grid = an upper bound, CTAs at or beyond *count return
+cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsigned long long *count,
+                                  const HashEntry *table, unsigned int mask, const float *sdf, const float *weight,
+                                  const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
+                                  const int *list, cudaStream_t s);
+cudaError_t launch_cell_masks(const int4 *locations, long long n, const unsigned char *cell_dirs, unsigned int *cell_pos,
+                              unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y,
+                              cudaStream_t s);
 // rgb packed into a float's bits for the B records (r | g << 8 | b << 16)
 __host__ __device__ __forceinline__ unsigned int rec_rgb(float bits) {
 #ifdef __CUDA_ARCH__

@@ -44,6 +44,14 @@ struct dtsdf_ctx {
   dtsdf_volume_params params{};
   bool allocated = false, committed = false;
   bool values_trusted = false;  // set by dtsdf_fuse around its re-commit: its own kernels wrote the values
+  // incremental index update after a fused frame (DTSDF_OPT_INCREMENTAL)
+  int incremental = 1;
+  unsigned char *blk_dirty = nullptr;  // [cap] blocks whose voxels the frame changed (or new)
+  int *blk_list = nullptr;             // [cap] blocks whose record bricks are rebuilt
+  int *loc_mark = nullptr;             // [table cap] 1 while the location is in loc_list (zero between frames)
+  int4 *loc_list = nullptr;            // [table cap] locations whose bricks / cell bytes / grid values are rebuilt
+  unsigned long long *inc_ctr = nullptr;
+  size_t cap_blk_dirty = 0, cap_blk_list = 0, cap_loc_mark = 0, cap_loc_list = 0, cap_inc_ctr = 0;
   int32_t *keys = nullptr;
   float *sdf = nullptr, *weight = nullptr;
   uint8_t *rgb = nullptr;
@@ -168,6 +176,12 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->locations);
   dfree(c->brick_a);
   dfree(c->brick_b);
+  dfree(c->blk_dirty);
+  dfree(c->blk_list);
+  dfree(c->loc_mark);
+  dfree(c->loc_list);
+  dfree(c->inc_ctr);
+  c->cap_blk_dirty = c->cap_blk_list = c->cap_loc_mark = c->cap_loc_list = c->cap_inc_ctr = 0;
   dfree(c->dist_tmp);
   c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_brick_a =
       c->cap_brick_b = c->cap_loc_grid = c->cap_dist = c->cap_cell_dirs = 0;
@@ -401,17 +415,16 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   begin_timed(c, 2, s, &tl);
   CK(c, launch_bitmap(c->locations, c->n_loc, c->bitmap, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s), "bitmap");
   end_timed(c, s, &tl);
+  CK(c, cudaMemsetAsync(c->cell_dirs, 0x80, (size_t)cap * 512, s), "cell bytes init");
   begin_timed(c, 2, s, &tl);
   CK(c, launch_bricks(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
-                      c->brick_a, c->brick_b, s),
+                      c->brick_a, c->brick_b, c->cell_dirs, nullptr, s),
      "bricks");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
-  CK(c, launch_cell_pos(c->locations, c->n_loc, c->table, c->brick_a, c->cell_pos, c->cell_dirs, s), "cell_pos");
-  end_timed(c, s, &tl);
-  begin_timed(c, 2, s, &tl);
-  CK(c, launch_surface(c->locations, c->n_loc, c->cell_pos, c->surface, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s),
-     "surface");
+  CK(c, launch_cell_masks(c->locations, c->n_loc, c->cell_dirs, c->cell_pos, c->surface, lo[0], lo[1], lo[2], c->dim[0],
+                          c->dim[1], s),
+     "cell masks");
   end_timed(c, s, &tl);
   // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
   // raycast resolves locations through the bitmaps and the hash table
@@ -1032,6 +1045,61 @@ int dtsdf_fusion_reserve(dtsdf_ctx *c, const dtsdf_volume_params *p, int64_t cap
   return dtsdf_commit_volume(c, nullptr);
 }
 
+// Incremental index update after a fused frame (the hash table was extended in place by the
+// allocation, new locations appended, dirty blocks flagged): the 27-neighbourhoods of the dirty
+// blocks get their locations' record bricks, live-direction bytes, certainly-positive masks,
+// surface bits and location-grid values rebuilt; new locations set their occupancy bits and, if
+// any, the empty-space distances are recomputed.  Equals a full re-commit (tests: DTSDF_OPT_
+// INCREMENTAL 0 vs 1 render bit-identical).
+static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_loc_old, int64_t n_loc_new) {
+  const unsigned int mask = c->table_cap - 1;
+  const int4 *keys = reinterpret_cast<const int4 *>(c->keys);
+  TimedLaunch tl{};
+  CK(c, cudaMemsetAsync(c->inc_ctr, 0, 16, s), "incremental init");
+  begin_timed(c, 2, s, &tl);
+  CK(c, launch_inc_mark(keys, c->n, c->blk_dirty, c->table, mask, c->loc_mark, c->loc_list, c->inc_ctr, s),
+     "incremental mark");
+  end_timed(c, s, &tl);
+  unsigned long long nl = 0;
+  CK(c, cudaMemcpyAsync(&nl, c->inc_ctr, 8, cudaMemcpyDeviceToHost, s), "incremental readback");
+  CK(c, cudaStreamSynchronize(s), "incremental sync");
+  const long long n_list = (long long)nl;
+  begin_timed(c, 2, s, &tl, n_list > 0 ? 5 : 0);
+  CK(c, launch_cell_init(c->loc_list, n_list, c->cell_dirs, s), "incremental cell init");
+  CK(c, launch_inc_blocks(c->loc_list, n_list, c->table, c->blk_list, c->inc_ctr, s), "incremental blocks");
+  CK(c, launch_bricks_counted(keys, 6 * n_list, c->inc_ctr + 1, c->table, mask, c->sdf, c->weight, c->rgb, c->brick_a,
+                              c->brick_b, c->cell_dirs, c->blk_list, s),
+     "incremental bricks");
+  CK(c, launch_cell_masks(c->loc_list, n_list, c->cell_dirs, c->cell_pos, c->surface, c->lo[0], c->lo[1], c->lo[2],
+                          c->dim[0], c->dim[1], s),
+     "incremental cell masks");
+  CK(c, launch_loc_grid(c->loc_list, n_list, c->surface, c->table, c->loc_grid, c->lo[0], c->lo[1], c->lo[2],
+                        c->dim[0], c->dim[1], s),
+     "incremental grid");
+  end_timed(c, s, &tl);
+  if (n_loc_new > n_loc_old) {
+    begin_timed(c, 2, s, &tl, 1);
+    CK(c, launch_bitmap(c->locations + n_loc_old, n_loc_new - n_loc_old, c->bitmap, c->lo[0], c->lo[1], c->lo[2],
+                        c->dim[0], c->dim[1], s),
+       "incremental bitmap");
+    end_timed(c, s, &tl);
+    const size_t cells = (size_t)c->dim[0] * c->dim[1] * c->dim[2];
+    if (c->dist_tmp && c->cap_dist >= 2 * cells) {
+      begin_timed(c, 2, s, &tl, 4);
+      CK(c, launch_empty_distance(c->loc_grid, c->dist_tmp, c->dist_tmp + cells, c->dim[0], c->dim[1], c->dim[2], s),
+         "incremental distance");
+      end_timed(c, s, &tl);
+    }
+  }
+  begin_timed(c, 2, s, &tl, n_list > 0 ? 1 : 0);
+  CK(c, launch_inc_unmark(c->loc_list, n_list, c->loc_mark, s), "incremental unmark");
+  end_timed(c, s, &tl);
+  CK(c, cudaStreamSynchronize(s), "incremental sync");
+  c->n_loc = n_loc_new;
+  c->committed = true;
+  return DTSDF_OK;
+}
+
 static void fuse_launch_common(dtsdf_ctx *c, const float pose[16], const dtsdf_intrinsics *K, FuseLaunch &L) {
   std::memset(&L, 0, sizeof(L));
   for (int a = 0; a < 3; ++a) {
@@ -1150,12 +1218,34 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
     CK(c, launch_comb_had(c->table, c->comb_loc, c->n_comb, c->weight, c->comb_had, s), "combine had");
     end_timed(c, s, &tlh);
   }
-  // scratch: flags (int) + pool counter (u64)
+  // incremental index update: dirty blocks, appended locations (the full re-commit rebuilds both)
+  const bool inc = c->incremental && c->loc_grid != nullptr;
+  if (inc) {
+    const size_t capb = (size_t)std::max<int64_t>(c->cap, 1), cape = (size_t)c->table_cap;
+    const bool fresh_mark = c->cap_loc_mark < cape * 4;
+    if (ensure(c->blk_dirty, c->cap_blk_dirty, capb) != cudaSuccess ||
+        ensure(c->blk_list, c->cap_blk_list, capb * 4) != cudaSuccess ||
+        ensure(c->loc_mark, c->cap_loc_mark, cape * 4) != cudaSuccess ||
+        ensure(c->loc_list, c->cap_loc_list, cape * sizeof(int4)) != cudaSuccess ||
+        ensure(c->inc_ctr, c->cap_inc_ctr, 16) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DTSDF_ERR_OUT_OF_MEMORY, "incremental fusion buffers");
+    }
+    if (fresh_mark) CK(c, cudaMemsetAsync(c->loc_mark, 0, cape * 4, s), "loc mark init");
+    CK(c, cudaMemsetAsync(c->blk_dirty, 0, capb, s), "dirty init");
+    L.dirty = c->blk_dirty;
+    L.locations = c->locations;
+    L.n_loc = reinterpret_cast<unsigned long long *>(c->scratch + 4);
+    for (int a = 0; a < 3; ++a) { L.lo[a] = c->lo[a]; L.dim[a] = c->dim[a]; }
+  }
+  // scratch: flags [0] pool / table full, [1] a new location outside the AABB; u64 location
+  // counter at int 4, u64 pool counter at int 12
   L.flags = c->scratch;
   L.n_blocks = reinterpret_cast<unsigned long long *>(c->scratch + 12);
   int init[14] = {0};
-  const unsigned long long n0 = (unsigned long long)c->n;
+  const unsigned long long n0 = (unsigned long long)c->n, nl0 = (unsigned long long)c->n_loc;
   std::memcpy(&init[12], &n0, 8);
+  std::memcpy(&init[4], &nl0, 8);
   CK(c, cudaMemcpyAsync(c->scratch, init, sizeof(init), cudaMemcpyHostToDevice, s), "fuse init");
   TimedLaunch tl{};
   begin_timed(c, 2, s, &tl);
@@ -1174,9 +1264,15 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   if (new_blocks) *new_blocks = n_new - c->n;
   c->n = n_new;
   c->params.n_blocks = n_new;
-  c->values_trusted = true;  // this library's fusion kernels wrote every value
-  rc = dtsdf_commit_volume(c, stream);
-  c->values_trusted = false;
+  unsigned long long nl1;
+  std::memcpy(&nl1, &host[4], 8);
+  if (inc && !full && host[1] == 0) {
+    rc = recommit_incremental(c, s, c->n_loc, (int64_t)nl1);
+  } else {
+    c->values_trusted = true;  // this library's fusion kernels wrote every value
+    rc = dtsdf_commit_volume(c, stream);
+    c->values_trusted = false;
+  }
   if (rc) return rc;
   if (comb && c->combined && (rc = comb_update(c, s))) return rc;
   if (full) return fail(DTSDF_ERR_OUT_OF_MEMORY, "fusion capacity exhausted (blocks allocated so far are kept)");
@@ -1414,6 +1510,7 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   else if (option == DTSDF_OPT_HOST_WRITE) c->host_write = value ? 1 : 0;
   else if (option == DTSDF_OPT_CELL_DIRS) c->use_live = value ? 1 : 0;
   else if (option == DTSDF_OPT_TILE_ORDER && value >= 0 && value <= 2) c->use_order = value;
+  else if (option == DTSDF_OPT_INCREMENTAL) c->incremental = value ? 1 : 0;
   else if (option == DTSDF_OPT_RANGE_EPOCH && value != 0) {  // value: the epoch's 32 bits
     if (c->range_epoch != 0) c->range_epoch = (unsigned int)value;  // testing: next pass uses value + 1
   }

@@ -87,6 +87,13 @@ __device__ int alloc_key(const FuseLaunch &p, int bx, int by, int bz, int D) {
       if (k != kEmptyKey) { h = (h + 1) & p.table_mask; continue; }
       k = atomicCAS(&p.table[h].key, kEmptyKey, key);
       if (k != kEmptyKey && k != key) { h = (h + 1) & p.table_mask; continue; }
+      if (k == kEmptyKey && p.locations) {  // this thread added the location: append it
+        const unsigned long long li = atomicAdd(p.n_loc, 1ull);
+        p.locations[li] = make_int4(bx, by, bz, (int)h);
+        if ((unsigned)(bx - p.lo[0]) >= (unsigned)p.dim[0] || (unsigned)(by - p.lo[1]) >= (unsigned)p.dim[1] ||
+            (unsigned)(bz - p.lo[2]) >= (unsigned)p.dim[2])
+          atomicExch(&p.flags[1], 1);  // outside the location AABB: the index needs a full rebuild
+      }
     }
     int *slot = &p.table[h].slot[D];
     if (*((volatile int *)slot) != -1) return 0;
@@ -140,6 +147,7 @@ __global__ void __launch_bounds__(256) k_fuse_init(FuseLaunch p, long long n0, l
   const long long b = n0 + (g >> 9);
   if (b >= n1) return;
   const size_t r = (size_t)b * kVoxPerBlock + (g & 511);
+  if (p.dirty && (g & 511) == 0) p.dirty[b] = 1;
   p.sdf[r] = 1.0f;
   p.weight[r] = 0.0f;
   p.cweight[r] = 0.0f;
@@ -160,6 +168,7 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
   const int axis = D >> 1;
   const float sgnD = (D & 1) ? -1.0f : 1.0f;
   const float tau = (float)p.tau;
+  bool wrote = false;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int l = threadIdx.x + 256 * h;
@@ -214,6 +223,7 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
       const float W0 = p.weight[r];
       p.sdf[r] = (W0 * p.sdf[r] + p.carve_weight) / (W0 + p.carve_weight);
       p.weight[r] = fminf(W0 + p.carve_weight, p.max_weight);
+      wrote = true;
       continue;
     }
     const float wdir = w_dir_f(sgnD * (axis == 0 ? nx : (axis == 1 ? ny : nz)), p);
@@ -226,6 +236,7 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     const float W0 = p.weight[r];
     p.sdf[r] = (W0 * p.sdf[r] + wn * dd) / (W0 + wn);
     p.weight[r] = fminf(W0 + wn, p.max_weight);
+    wrote = true;
     if (p.color) {
       const float dist = (float)sqrt(ex * ex + ey * ey + ez * ez);
       const float wc = wn * (1.0f - fminf(1.0f, dist / tau));  // eq:color_weight
@@ -240,6 +251,7 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
       }
     }
   }
+  if (p.dirty && __syncthreads_or(wrote) && threadIdx.x == 0) p.dirty[b] = 1;
 }
 
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s) {

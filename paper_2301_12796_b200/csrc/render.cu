@@ -412,7 +412,7 @@ struct Cursor {
 #endif
 };
 
-// cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (k_cell_pos)
+// cell l (= lx + 8 ly + 64 lz) of the cursor's location is certainly positive (combined bricks, k_comb_finish)
 __device__ __forceinline__ bool cell_positive(const unsigned int *cell_pos, const Cursor &cur, int l) {
   DTSDF_CHECK(cur.entry >= 0 && l >= 0 && l < 512);
   return (__ldg(&cell_pos[(size_t)cur.entry * 16 + (l >> 5)]) >> (l & 31)) & 1u;

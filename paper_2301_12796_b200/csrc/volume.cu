@@ -104,10 +104,16 @@ constexpr int kStage = 11;  // staged sdf: voxels -1..9 per axis
 __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
                                                          unsigned int mask, const float *__restrict__ sdf,
                                                          const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
-                                                         float4 *__restrict__ brick_a, float2 *__restrict__ brick_b) {
+                                                         float4 *__restrict__ brick_a, float2 *__restrict__ brick_b,
+                                                         unsigned int *__restrict__ cell_dirs32,
+                                                         const int *__restrict__ list,
+                                                         const unsigned long long *__restrict__ count) {
   __shared__ int nb[27];  // slot of neighbour (ox, oy, oz) in -1..1, index (ox+1) + 3 (oy+1) + 9 (oz+1)
+  __shared__ int self_entry;
   __shared__ float st[kStage * kStage * kStage];
-  const long long b = blockIdx.x;
+  __shared__ float sw[kRecVox];
+  if (count && blockIdx.x >= *count) return;  // CTA-uniform
+  const long long b = list ? (long long)list[blockIdx.x] : (long long)blockIdx.x;
   const int4 k = keys[b];
   if (threadIdx.x < 27) {
     const int ox = (int)threadIdx.x % 3 - 1, oy = ((int)threadIdx.x / 3) % 3 - 1, oz = (int)threadIdx.x / 9 - 1;
@@ -115,6 +121,8 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     if (ox | oy | oz) {
       const int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
       src = (e >= 0) ? table[e].slot[k.w] : -1;
+    } else {
+      self_entry = find_entry(table, mask, pack_key(k.x, k.y, k.z));
     }
     nb[threadIdx.x] = src;
   }
@@ -133,6 +141,10 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     const long long r = rec_of(a % kStage - 1, (a / kStage) % kStage - 1, a / (kStage * kStage) - 1);
     st[a] = r >= 0 ? sdf[r] : __int_as_float(0x7fc00000);  // NaN sdf = unallocated
   }
+  for (int a = threadIdx.x; a < kRecVox; a += kBrickThreads) {
+    const long long r = rec_of(a % kRec, (a / kRec) % kRec, a / (kRec * kRec));
+    sw[a] = r >= 0 ? weight[r] : 0.0f;
+  }
   __syncthreads();
   for (int a = threadIdx.x; a < kRecStride; a += kBrickThreads) {
     float4 ra = make_float4(__int_as_float(0x7fc00000), 0.0f, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
@@ -142,7 +154,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
       const int c = (lx + 1) + kStage * (ly + 1) + kStage * kStage * (lz + 1);
       const long long r = rec_of(lx, ly, lz);
       ra.x = st[c];
-      ra.y = r >= 0 ? weight[r] : 0.0f;
+      ra.y = sw[a];
       ra.z = st[c + 1] - st[c - 1];
       ra.w = st[c + kStage] - st[c - kStage];
       rb.x = st[c + kStage * kStage] - st[c - kStage * kStage];
@@ -156,44 +168,64 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     brick_a[b * kRecStride + a] = ra;
     brick_b[b * kRecStride + a] = rb;
   }
+  // This direction's share of the location's live-direction byte per base cell (render.cu
+  // cell_byte): bit D when no corner is unallocated and some corner weight is > 0 (the evaluation
+  // drops D otherwise); bit 7, "certainly positive", cleared when all corners are allocated and
+  // one has sdf <= 0.  The location's bytes start at 0x80 (k_cell_init / the commit's memset).
+  if (cell_dirs32 == nullptr || self_entry < 0) return;
+  for (int l = threadIdx.x; l < kVoxPerBlock; l += kBrickThreads) {
+    const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
+    bool absent = false, allpos = true, weighted = false;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int dx = q & 1, dy = (q >> 1) & 1, dz = q >> 2;
+      const float v = st[(lx + dx + 1) + kStage * (ly + dy + 1) + kStage * kStage * (lz + dz + 1)];
+      absent |= isnan(v);
+      allpos &= v > 0.0f;
+      weighted |= sw[(lx + dx) + kRec * (ly + dy) + kRec * kRec * (lz + dz)] > 0.0f;
+    }
+    unsigned int *w = cell_dirs32 + ((size_t)self_entry * kVoxPerBlock + l) / 4;
+    const int sh = (l & 3) * 8;
+    if (!absent && weighted) atomicOr(w, (1u << k.w) << sh);
+    if (!absent && !allpos) atomicAnd(w, ~(0x80u << sh));
+  }
 }
 
-// Certainly-positive base cells: bit l of location h is set iff, for every direction present
-// at the cell (all 8 corners allocated), all 8 corner sdf values are > 0.  A sample in such a cell
-// has F > 0 or is invalid (convex combination, O3(e)), so it can neither end a crossing nor --
-// when the next lattice point is such a sample too -- start one (render.cu, exact).
-// One warp per 32 consecutive cells of a location; the ballot writes one mask word.
-__global__ void k_cell_pos(const int4 *__restrict__ loc, long long n_loc, const HashEntry *__restrict__ table,
-                           const float4 *__restrict__ brick_a, unsigned int *cell_pos, unsigned char *cell_dirs) {
-  long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long u = gid >> 9;
-  int l = (int)(gid & 511);
-  bool pos = false;
-  int live = 0;
-  if (u < n_loc) {
-    const int h = loc[u].w;
-    const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
-    pos = true;
-    for (int D = 0; D < 6; ++D) {
-      const int slot = table[h].slot[D];
-      if (slot < 0) continue;
-      const float4 *br = brick_a + (size_t)slot * kRecStride + lx + kRec * ly + kRec * kRec * lz;
-      bool absent = false, allpos = true, weighted = false;
-      for (int q = 0; q < 8; ++q) {
-        const float4 v = br[(q & 1) + kRec * ((q >> 1) & 1) + kRec * kRec * (q >> 2)];
-        absent |= isnan(v.x);
-        allpos &= v.x > 0.0f;
-        weighted |= v.y > 0.0f;
-      }
-      if (!absent && !allpos) pos = false;
-      // a NaN corner makes the trilinear phi NaN, corner weights all <= 0 make omega <= 0: either
-      // way the evaluation drops D here (O3(a), reading R8), so it need not visit it
-      if (!absent && weighted) live |= 1 << D;
-    }
+// The live-direction bytes of the listed locations' entries set to 0x80 (no direction live,
+// certainly positive) before their bricks are rebuilt (incremental commit).
+__global__ void k_cell_init(const int4 *__restrict__ loc, long long n, unsigned int *cell_dirs32) {
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long i = g >> 7;
+  if (i >= n) return;
+  cell_dirs32[(size_t)loc[i].w * (kVoxPerBlock / 4) + (g & 127)] = 0x80808080u;
+}
+
+// One warp per location: the certainly-positive masks (bit l of cell_pos[entry][l / 32]) from bit 7
+// of the live-direction bytes, and the location's surface bit -- set unless every base cell is
+// certainly positive (then every sample whose base voxel lies in the location has F > 0 or is
+// invalid, and the march may jump to the location's last lattice points, exact).  The surface bit
+// is cleared first (a re-built location may have lost its surface).
+__global__ void k_cell_masks(const int4 *__restrict__ loc, long long n, const unsigned char *__restrict__ cell_dirs,
+                             unsigned int *cell_pos, unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x,
+                             int dim_y) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;  // warp-uniform
+  const int4 b = loc[i];
+  bool all_pos = true;
+#pragma unroll
+  for (int h = 0; h < 16; ++h) {
+    const int l = h * 32 + lane;
+    const bool cp = (cell_dirs[(size_t)b.w * kVoxPerBlock + l] & 0x80) != 0;
+    const unsigned int word = __ballot_sync(0xffffffffu, cp);
+    if (lane == 0) cell_pos[(size_t)b.w * 16 + h] = word;
+    all_pos &= word == 0xffffffffu;
   }
-  const unsigned int word = __ballot_sync(0xffffffffu, pos);
-  if (u < n_loc && (l & 31) == 0) cell_pos[(size_t)loc[u].w * 16 + (l >> 5)] = word;
-  if (u < n_loc && cell_dirs) cell_dirs[(size_t)loc[u].w * 512 + l] = (unsigned char)(live | (pos ? 128 : 0));
+  if (lane == 0) {
+    const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
+    if (all_pos) atomicAnd(&surface[cell >> 5], ~(1u << (cell & 31)));
+    else atomicOr(&surface[cell >> 5], 1u << (cell & 31));
+  }
 }
 
 // Dense location grid: for each allocated location, its hash entry index, present directions and
@@ -246,21 +278,6 @@ __global__ void k_dist_store(int *grid, const unsigned char *__restrict__ dist, 
   if (grid[c] < 0) grid[c] = -(dist[c] > 1 ? (int)dist[c] : 1);
 }
 
-// Surface bit of a block location: set unless every base cell of the location is certainly
-// positive (k_cell_pos).  Where it is clear, every sample whose base voxel lies in the location
-// has F > 0 or is invalid, so the march may jump to the location's last lattice points (exact).
-__global__ void k_surface(const int4 *__restrict__ loc, long long n_loc, const unsigned int *__restrict__ cell_pos,
-                          unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_loc) return;
-  const int4 b = loc[i];
-  bool all_pos = true;
-  for (int w = 0; w < 16; ++w) all_pos &= cell_pos[(size_t)b.w * 16 + w] == 0xffffffffu;
-  if (!all_pos) {
-    const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
-    atomicOr(&surface[cell >> 5], 1u << (cell & 31));
-  }
-}
 
 static inline unsigned int grid_for(long long n, int threads) { return (unsigned int)((n + threads - 1) / threads); }
 
@@ -313,25 +330,96 @@ cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char 
   return cudaGetLastError();
 }
 
-cudaError_t launch_cell_pos(const int4 *locations, long long n_loc, const HashEntry *table, const float4 *brick_a,
-                            unsigned int *cell_pos, unsigned char *cell_dirs, cudaStream_t s) {
-  if (n_loc == 0) return cudaSuccess;
-  k_cell_pos<<<grid_for(n_loc * 512, 256), 256, 0, s>>>(locations, n_loc, table, brick_a, cell_pos, cell_dirs);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_surface(const int4 *locations, long long n_loc, const unsigned int *cell_pos, unsigned int *surface,
-                           int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
-  if (n_loc == 0) return cudaSuccess;
-  k_surface<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, cell_pos, surface, lo_x, lo_y, lo_z, dim_x, dim_y);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
-                          cudaStream_t s) {
+                          unsigned char *cell_dirs, const int *list, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_bricks<<<(unsigned)n, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b);
+  k_bricks<<<(unsigned)n, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
+                                                reinterpret_cast<unsigned int *>(cell_dirs), list, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsigned long long *count,
+                                  const HashEntry *table, unsigned int mask, const float *sdf, const float *weight,
+                                  const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
+                                  const int *list, cudaStream_t s) {
+  if (grid == 0) return cudaSuccess;
+  k_bricks<<<(unsigned)grid, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
+                                                   reinterpret_cast<unsigned int *>(cell_dirs), list, count);
+  return cudaGetLastError();
+}
+
+// ---- incremental commit after a fused frame ----------------------------------------------
+// A block's record brick reads voxels -1..9 of its block, i.e. all 26 neighbours in its
+// direction; a location's live-direction bytes combine all its directions.  So a dirty block
+// (changed voxels, or new) invalidates the bricks of its 27-neighbourhood in its direction, and
+// every location holding one of those is rebuilt whole (all its directions' bricks).
+__global__ void k_inc_mark(const int4 *__restrict__ keys, long long n, const unsigned char *__restrict__ dirty,
+                           const HashEntry *__restrict__ table, unsigned int mask, int *loc_mark, int4 *loc_list,
+                           unsigned long long *ctr) {
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n || !dirty[b]) return;
+  const int4 k = keys[b];
+  for (int q = 0; q < 27; ++q) {
+    const int ox = q % 3 - 1, oy = (q / 3) % 3 - 1, oz = q / 9 - 1;
+    const int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
+    if (e < 0 || table[e].slot[k.w] < 0) continue;
+    if (atomicCAS(&loc_mark[e], 0, 1) != 0) continue;
+    const unsigned long long i = atomicAdd(&ctr[0], 1ull);
+    loc_list[i] = make_int4(k.x + ox, k.y + oy, k.z + oz, e);
+  }
+}
+
+__global__ void k_inc_blocks(const int4 *__restrict__ loc_list, long long n, const HashEntry *__restrict__ table,
+                             int *blk_list, unsigned long long *ctr) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int e = loc_list[i].w;
+#pragma unroll
+  for (int D = 0; D < 6; ++D) {
+    const int b = table[e].slot[D];
+    if (b >= 0) blk_list[atomicAdd(&ctr[1], 1ull)] = b;
+  }
+}
+
+__global__ void k_inc_unmark(const int4 *__restrict__ loc_list, long long n, int *loc_mark) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) loc_mark[loc_list[i].w] = 0;
+}
+
+cudaError_t launch_inc_mark(const int4 *keys, long long n, const unsigned char *dirty, const HashEntry *table,
+                            unsigned int mask, int *loc_mark, int4 *loc_list, unsigned long long *ctr, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_inc_mark<<<grid_for(n, 256), 256, 0, s>>>(keys, n, dirty, table, mask, loc_mark, loc_list, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_inc_blocks(const int4 *loc_list, long long n, const HashEntry *table, int *blk_list,
+                              unsigned long long *ctr, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_inc_blocks<<<grid_for(n, 256), 256, 0, s>>>(loc_list, n, table, blk_list, ctr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_inc_unmark<<<grid_for(n, 256), 256, 0, s>>>(loc_list, n, loc_mark);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_cell_init<<<grid_for(n * 128, 256), 256, 0, s>>>(locations, n, reinterpret_cast<unsigned int *>(cell_dirs));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_masks(const int4 *locations, long long n, const unsigned char *cell_dirs, unsigned int *cell_pos,
+                              unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y,
+                              cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_cell_masks<<<grid_for(n * 32, 256), 256, 0, s>>>(locations, n, cell_dirs, cell_pos, surface, lo_x, lo_y, lo_z,
+                                                     dim_x, dim_y);
   return cudaGetLastError();
 }
 

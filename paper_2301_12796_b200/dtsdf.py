@@ -33,6 +33,7 @@ OPT_HOST_WRITE = 7
 OPT_CELL_DIRS = 8
 OPT_TILE_ORDER = 9
 OPT_RANGE_EPOCH = 10
+OPT_INCREMENTAL = 11
 
 
 class DtsdfError(RuntimeError):

@@ -113,3 +113,39 @@ def test_fusion_capacity_exhaustion(R):
         R.fuse(fr.depth, fr.normal, fr.color, pose, K)
     assert e.value.code == OUT_OF_MEMORY
     assert R.stats()["n_blocks"] == 3
+
+
+@pytest.mark.parametrize("start", ["c1", "empty"])
+def test_incremental_index_equals_full_recommit(c1, start):
+    """DTSDF_OPT_INCREMENTAL: after every fused frame the incrementally updated index (bricks, cell
+    masks, surface bits, location grid, empty-space distances of the locations within one block of a
+    changed block) renders exactly what a full re-commit of the same pool renders, and the pools
+    hold the same blocks -- into the uploaded configs[1] volume and from an empty volume (whose
+    growing AABB takes the full path)."""
+    from paper_2301_12796_b200 import Renderer
+    from paper_2301_12796_b200.dtsdf import OPT_INCREMENTAL
+    poses = scenes.room_scan_poses(np.random.default_rng([7, 0]), 6)
+    outs = {}
+    for inc in (1, 0):
+        Q = Renderer(0)
+        Q.set_option(OPT_INCREMENTAL, inc)
+        if start == "c1":
+            Q.upload_volume(c1.volume)
+            Q.fusion_reserve(c1.volume.n_blocks + 30000)
+        else:
+            Q.upload(S, TAU, scenes.THETA, np.zeros((0, 4), np.int32), np.zeros((0, 512), np.float32),
+                     np.zeros((0, 512), np.float32))
+            Q.fusion_reserve(60000)
+        renders = []
+        for P in poses:
+            fr = scenes.analytic_frame(c1.patches, P, K_HALF)
+            Q.fuse(fr.depth, fr.normal, fr.color, P, K_HALF)
+            renders.append({k: v.cpu() for k, v in Q.render(poses[:2], K_HALF).items()})
+        outs[inc] = (renders, _sorted(*Q.get_volume()), Q.stats())
+        Q.close()
+    assert outs[1][2]["n_blocks"] == outs[0][2]["n_blocks"] and outs[1][2]["n_locations"] == outs[0][2]["n_locations"]
+    for a, b in zip(outs[1][1], outs[0][1]):
+        assert np.array_equal(a, b)
+    for i, (a, b) in enumerate(zip(outs[1][0], outs[0][0])):
+        for k in a:
+            assert torch.equal(a[k], b[k]), (i, k)

@@ -15,6 +15,9 @@ from paper_2301_12796_b200 import Renderer  # noqa
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=30)
 ap.add_argument("--warmup", type=int, default=5)
+ap.add_argument("--start", choices=["c1", "empty"], default="c1",
+                help="c1: fuse into the uploaded configs[1] volume; empty: scan the room from nothing")
+ap.add_argument("--incremental", type=int, default=1, help="DTSDF_OPT_INCREMENTAL")
 args = ap.parse_args()
 w = scenes.c1_room()
 K = w.intrinsics
@@ -22,9 +25,15 @@ poses = scenes.room_scan_poses(np.random.default_rng([9, 0]), args.frames + args
 frames = [scenes.analytic_frame(w.patches, P, K) for P in poses]
 dev = [{k: torch.from_numpy(getattr(f, k)).cuda() for k in ("depth", "normal", "color")} for f in frames]
 R = Renderer(0)
-R.upload(0.01, 0.04, scenes.THETA, np.zeros((0, 4), np.int32), np.zeros((0, 512), np.float32),
-         np.zeros((0, 512), np.float32))
-R.fusion_reserve(80000)
+from paper_2301_12796_b200.dtsdf import OPT_INCREMENTAL  # noqa: E402
+R.set_option(OPT_INCREMENTAL, args.incremental)
+if args.start == "c1":
+    R.upload_volume(w.volume)
+    R.fusion_reserve(w.volume.n_blocks + 60000)
+else:
+    R.upload(0.01, 0.04, scenes.THETA, np.zeros((0, 4), np.int32), np.zeros((0, 512), np.float32),
+             np.zeros((0, 512), np.float32))
+    R.fusion_reserve(80000)
 for i in range(args.warmup):
     R.fuse(dev[i]["depth"], dev[i]["normal"], dev[i]["color"], poses[i], K)
 torch.cuda.synchronize()
@@ -44,6 +53,7 @@ for i in range(args.warmup, args.warmup + args.frames):
 R.set_profiling(False)
 kt = R.kernel_times()
 print(json.dumps({"what": "fusion", "config": "C1 room, 640x480 ideal depth frames, 1 cm voxels, tau 4 cm",
+                  "start": args.start, "incremental": args.incremental,
                   "frames": args.frames, "ms_per_frame_median": 1e3 * float(np.median(t)),
                   "frames_per_s": 1.0 / float(np.median(t)), "kernel_ms_per_frame": kt["other_ms"] / args.frames,
                   "kernel_launches_per_frame": kt["other_launches"] / args.frames, "new_blocks": new,
