@@ -239,6 +239,15 @@ struct FuseLaunch {
   unsigned long long *n_loc;
   int lo[3], dim[3];
   unsigned char *dirty;
+  // per-pixel world-rotated back-projection R P and world normal R n of the frame (k_frame_points,
+  // once per frame instead of once per associated voxel; null: k_fuse computes them)
+  double4 *pix_x, *pix_n;
+  // incremental index update: a block k_fuse changed marks the locations of its 27-neighbourhood
+  // that hold a block in its direction (loc_mark dedup, appended to loc_list, counter loc_ctr);
+  // null: not tracked
+  int *loc_mark;
+  int4 *loc_list;
+  unsigned long long *loc_ctr;
 };
 
 // ICP state in device memory (icp.cu): written by k_icp_solve, read back once per call
@@ -273,7 +282,11 @@ cudaError_t launch_icp_solve(const IcpLaunch &p, cudaStream_t s);
 // host launchers (fusion.cu)
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s);
 cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s);
-cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, cudaStream_t s);
+cudaError_t launch_frame_points(const FuseLaunch &p, cudaStream_t s);  // fills p.pix_x, p.pix_n
+// new blocks initialised; then (fuse) the frame fused into the blocks -- with list / count (count
+// zeroed beforehand) only those k_fuse_select finds in the frame's view
+cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, int *list,
+                        unsigned long long *count, cudaStream_t s);
 
 // host launchers (combine.cu)
 cudaError_t launch_combine(const CombineLaunch &p, cudaStream_t s);                  // interiors + slots
@@ -311,8 +324,10 @@ cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *
 // incremental commit after a fused frame: the locations whose record bricks must be rebuilt (the
 // 27-neighbourhoods, in the dirty block's direction, of every dirty block) -> loc_list (deduplicated
 // by loc_mark[entry]), then all blocks of those locations -> blk_list; counters ctr[0], ctr[1]
-cudaError_t launch_inc_mark(const int4 *keys, long long n, const unsigned char *dirty, const HashEntry *table,
-                            unsigned int mask, int *loc_mark, int4 *loc_list, unsigned long long *ctr, cudaStream_t s);
+cudaError_t launch_inc_mark(const int4 *keys, long long b0, long long n, const unsigned char *dirty,
+                            const HashEntry *table,
+                            unsigned int mask, const int *grid, const int lo[3], const int dim[3], int *loc_mark,
+                            int4 *loc_list, unsigned long long *ctr, cudaStream_t s);
 cudaError_t launch_inc_blocks(const int4 *loc_list, long long n, const HashEntry *table, int *blk_list,
                               unsigned long long *ctr, cudaStream_t s);
 cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s);

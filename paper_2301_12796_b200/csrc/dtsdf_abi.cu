@@ -59,6 +59,8 @@ struct dtsdf_ctx {
   int64_t cap = 0;            // pool capacity in blocks (>= n; fusion grows n up to it)
   float *cweight = nullptr;   // fusion: colour weights [cap][512] (eq:color_weight accumulator)
   void *fuse_stage = nullptr; // fusion / ICP: device staging of host frames
+  double4 *pix_buf = nullptr;  // fusion: per-pixel world points + normals of the frame (k_frame_points)
+  size_t cap_pix_buf = 0;
   double *icp_partials = nullptr;
   IcpState *icp_state = nullptr;
   int *icp_done_host = nullptr;  // pinned: the done flag read back between chunks of iterations
@@ -300,6 +302,7 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   dfree(c->scratch);
   dfree(c->tile_counter);
   if (c->fuse_stage) cudaFree(c->fuse_stage);
+  dfree(c->pix_buf);
   dfree(c->icp_partials);
   dfree(c->icp_state);
   if (c->icp_done_host) cudaFreeHost(c->icp_done_host);
@@ -1051,13 +1054,23 @@ int dtsdf_fusion_reserve(dtsdf_ctx *c, const dtsdf_volume_params *p, int64_t cap
 // surface bits and location-grid values rebuilt; new locations set their occupancy bits and, if
 // any, the empty-space distances are recomputed.  Equals a full re-commit (tests: DTSDF_OPT_
 // INCREMENTAL 0 vs 1 render bit-identical).
-static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_loc_old, int64_t n_loc_new) {
+static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_blk_old, int64_t n_loc_old,
+                                int64_t n_loc_new) {
   const unsigned int mask = c->table_cap - 1;
   const int4 *keys = reinterpret_cast<const int4 *>(c->keys);
   TimedLaunch tl{};
-  CK(c, cudaMemsetAsync(c->inc_ctr, 0, 16, s), "incremental init");
+  // (inc_ctr[0] already counts the locations k_fuse marked; [1] is zero)
+  if (n_loc_new > n_loc_old) {  // the new locations enter the grid first (their final values follow below)
+    begin_timed(c, 2, s, &tl);
+    CK(c, launch_loc_grid(c->locations + n_loc_old, n_loc_new - n_loc_old, c->surface, c->table, c->loc_grid, c->lo[0],
+                          c->lo[1], c->lo[2], c->dim[0], c->dim[1], s),
+       "incremental grid (new locations)");
+    end_timed(c, s, &tl);
+  }
   begin_timed(c, 2, s, &tl);
-  CK(c, launch_inc_mark(keys, c->n, c->blk_dirty, c->table, mask, c->loc_mark, c->loc_list, c->inc_ctr, s),
+  // the frame's new blocks (k_fuse marked the neighbourhoods of the blocks it changed)
+  CK(c, launch_inc_mark(keys, n_blk_old, c->n, c->blk_dirty, c->table, mask, c->loc_grid, c->lo, c->dim, c->loc_mark,
+                        c->loc_list, c->inc_ctr, s),
      "incremental mark");
   end_timed(c, s, &tl);
   unsigned long long nl = 0;
@@ -1227,13 +1240,16 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
         ensure(c->blk_list, c->cap_blk_list, capb * 4) != cudaSuccess ||
         ensure(c->loc_mark, c->cap_loc_mark, cape * 4) != cudaSuccess ||
         ensure(c->loc_list, c->cap_loc_list, cape * sizeof(int4)) != cudaSuccess ||
-        ensure(c->inc_ctr, c->cap_inc_ctr, 16) != cudaSuccess) {
+        ensure(c->inc_ctr, c->cap_inc_ctr, 32) != cudaSuccess) {
       cudaGetLastError();
       return fail(DTSDF_ERR_OUT_OF_MEMORY, "incremental fusion buffers");
     }
     if (fresh_mark) CK(c, cudaMemsetAsync(c->loc_mark, 0, cape * 4, s), "loc mark init");
     CK(c, cudaMemsetAsync(c->blk_dirty, 0, capb, s), "dirty init");
     L.dirty = c->blk_dirty;
+    L.loc_mark = c->loc_mark;
+    L.loc_list = c->loc_list;
+    L.loc_ctr = c->inc_ctr;
     L.locations = c->locations;
     L.n_loc = reinterpret_cast<unsigned long long *>(c->scratch + 4);
     for (int a = 0; a < 3; ++a) { L.lo[a] = c->lo[a]; L.dim[a] = c->dim[a]; }
@@ -1247,8 +1263,15 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   std::memcpy(&init[12], &n0, 8);
   std::memcpy(&init[4], &nl0, 8);
   CK(c, cudaMemcpyAsync(c->scratch, init, sizeof(init), cudaMemcpyHostToDevice, s), "fuse init");
+  if (ensure(c->pix_buf, c->cap_pix_buf, px * 2 * sizeof(double4)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DTSDF_ERR_OUT_OF_MEMORY, "frame points");
+  }
+  L.pix_x = c->pix_buf;
+  L.pix_n = c->pix_buf + px;
   TimedLaunch tl{};
-  begin_timed(c, 2, s, &tl);
+  begin_timed(c, 2, s, &tl, 2);
+  CK(c, launch_frame_points(L, s), "frame points");
   CK(c, launch_fuse_alloc(L, s), "fuse alloc");
   end_timed(c, s, &tl);
   int host[14];
@@ -1258,8 +1281,13 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   std::memcpy(&n1, &host[12], 8);
   const int64_t n_new = std::min<int64_t>((int64_t)n1, c->cap);
   const bool full = host[0] != 0;
-  begin_timed(c, 2, s, &tl, full ? (n_new > c->n ? 1 : 0) : 2);
-  CK(c, launch_fuse(L, c->n, n_new, !full, s), "fuse");  // when full: new blocks initialised, not fused
+  // counters: [0] marked locations (k_fuse), [1] rebuilt blocks, [2] k_fuse's frustum selection
+  // (into blk_list, free until the incremental update)
+  int *fuse_list = inc ? c->blk_list : nullptr;
+  if (fuse_list) CK(c, cudaMemsetAsync(c->inc_ctr, 0, 32, s), "fuse counters init");
+  const int64_t n_blk_old = c->n;
+  begin_timed(c, 2, s, &tl, full ? (n_new > c->n ? 1 : 0) : (fuse_list ? 3 : 2));
+  CK(c, launch_fuse(L, c->n, n_new, !full, fuse_list, fuse_list ? c->inc_ctr + 2 : nullptr, s), "fuse");  // when full: new blocks initialised, not fused
   end_timed(c, s, &tl);
   if (new_blocks) *new_blocks = n_new - c->n;
   c->n = n_new;
@@ -1267,8 +1295,9 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   unsigned long long nl1;
   std::memcpy(&nl1, &host[4], 8);
   if (inc && !full && host[1] == 0) {
-    rc = recommit_incremental(c, s, c->n_loc, (int64_t)nl1);
+    rc = recommit_incremental(c, s, n_blk_old, c->n_loc, (int64_t)nl1);
   } else {
+    if (inc) CK(c, cudaMemsetAsync(c->loc_mark, 0, (size_t)c->table_cap * 4, s), "loc mark reset");
     c->values_trusted = true;  // this library's fusion kernels wrote every value
     rc = dtsdf_commit_volume(c, stream);
     c->values_trusted = false;

@@ -142,6 +142,33 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(const __grid_constant__ Fuse
   }
 }
 
+// Per pixel of the frame: R P (the back-projected depth point rotated into the world, relative to
+// the camera centre) and R n (the world normal), with the operations k_fuse would apply per voxel.
+__global__ void __launch_bounds__(256) k_frame_points(const __grid_constant__ FuseLaunch p) {
+  const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
+  if (u >= p.width || v >= p.height) return;
+  const size_t i = (size_t)v * p.width + u;
+  const float z = p.depth[i];
+  double P[3], X[3] = {0, 0, 0}, nc[3] = {p.normal[3 * i], p.normal[3 * i + 1], p.normal[3 * i + 2]}, n[3] = {0, 0, 0};
+  bool edge = false;
+  if (depth_ok(p, z)) {
+    backproject(p, u, v, (double)z, P);
+    rotate(p, P, X);
+    rotate(p, nc, n);
+    // R43's carving guard of this pixel: a valid depth within carve_radius differing by more than tau
+    for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
+      for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
+        const int qu = u + du, qv = v + dv;
+        if (qu < 0 || qv < 0 || qu >= p.width || qv >= p.height) continue;
+        const float zq = p.depth[(size_t)qv * p.width + qu];
+        if (!depth_ok(p, zq)) continue;
+        if (fabs((double)zq - (double)z) > p.tau) { edge = true; break; }
+      }
+  }
+  p.pix_x[i] = make_double4(X[0], X[1], X[2], edge ? 1.0 : 0.0);
+  p.pix_n[i] = make_double4(n[0], n[1], n[2], 0.0);
+}
+
 __global__ void __launch_bounds__(256) k_fuse_init(FuseLaunch p, long long n0, long long n1) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long b = n0 + (g >> 9);
@@ -161,8 +188,43 @@ __device__ __forceinline__ float w_dir_f(float c, const FuseLaunch &p) {
   return fminf(fmaxf((p.theta_f - a) * p.inv_blend, 0.0f), 1.0f);
 }
 
-__global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch p) {
-  const long long b = blockIdx.x;
+// One warp per block: does any voxel of the block project into the frame?  A voxel is associated
+// iff its camera z > 0 and its nearest pixel floor(u + 1/2), floor(v + 1/2) lies in the image, i.e.
+// u in [-1/2, W - 1/2), v likewise -- for z > 0 linear constraints in camera coordinates
+// (fx x + (cx + 1/2) z >= 0, ...).  The block's voxels are convex combinations of its 8 corner
+// voxels, so when all 8 corners violate one constraint (by a margin far above fp64 rounding) no
+// voxel is associated and the block is left out (exact).  Selected blocks go to list / *count.
+__global__ void __launch_bounds__(256) k_fuse_select(const __grid_constant__ FuseLaunch p, long long n, int *list,
+                                                     unsigned long long *count) {
+  const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (b >= n) return;  // warp-uniform
+  const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
+  const int q = lane & 7;
+  const int i = kBlock * key.x + ((q & 1) ? kBlock - 1 : 0), j = kBlock * key.y + ((q & 2) ? kBlock - 1 : 0),
+            k = kBlock * key.z + ((q & 4) ? kBlock - 1 : 0);
+  const double d0 = (double)i * p.s - p.t[0], d1 = (double)j * p.s - p.t[1], d2 = (double)k * p.s - p.t[2];
+  const double xc = p.R[0] * d0 + p.R[3] * d1 + p.R[6] * d2;
+  const double yc = p.R[1] * d0 + p.R[4] * d1 + p.R[7] * d2;
+  const double zc = p.R[2] * d0 + p.R[5] * d1 + p.R[8] * d2;
+  const double tol = 1e-6;
+  double g[5];
+  g[0] = zc;                                                   // z > 0
+  g[1] = p.fx * xc + (p.cx + 0.5) * zc;                         // u >= -1/2
+  g[2] = ((double)p.width - 0.5 - p.cx) * zc - p.fx * xc;       // u < W - 1/2
+  g[3] = p.fy * yc + (p.cy + 0.5) * zc;                         // v >= -1/2
+  g[4] = ((double)p.height - 0.5 - p.cy) * zc - p.fy * yc;      // v < H - 1/2
+  bool out = false;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out |= (__ballot_sync(0xffffffffu, g[c] < -tol) & 0xffu) == 0xffu;
+  if (out || lane != 0) return;
+  list[atomicAdd(count, 1ull)] = (int)b;
+}
+
+__global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch p, const int *list,
+                                              const unsigned long long *count) {
+  if (list && blockIdx.x >= *count) return;  // CTA-uniform
+  const long long b = list ? (long long)list[blockIdx.x] : (long long)blockIdx.x;
   const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
   const int D = key.w;
   const int axis = D >> 1;
@@ -194,10 +256,17 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     // the band decisions (|d| <= 1, d > 1) sit exactly on lattice planes for axis-aligned
     // surfaces (a voxel tau from a floor at z = 0), so d is formed in fp64 with the oracle's
     // operation order -- both sides take the same decision
-    double P[3], X[3], ncd[3] = {nc0, nc1, nc2}, nd[3];
-    backproject(p, iu, iv, (double)z, P);
-    rotate(p, P, X);
-    rotate(p, ncd, nd);
+    double X[3], nd[3];
+    if (p.pix_x) {  // the frame's per-pixel values, computed once by k_frame_points (same operations)
+      const double4 xx = p.pix_x[pi], nn = p.pix_n[pi];
+      X[0] = xx.x; X[1] = xx.y; X[2] = xx.z;
+      nd[0] = nn.x; nd[1] = nn.y; nd[2] = nn.z;
+    } else {
+      double P[3], ncd[3] = {nc0, nc1, nc2};
+      backproject(p, iu, iv, (double)z, P);
+      rotate(p, P, X);
+      rotate(p, ncd, nd);
+    }
     const double ex = __dsub_rn(x0, __dadd_rn(X[0], p.t[0])), ey = __dsub_rn(x1, __dadd_rn(X[1], p.t[1])),
                  ez = __dsub_rn(x2, __dadd_rn(X[2], p.t[2]));
     const double ddd =
@@ -211,6 +280,8 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
       // carve_weight 0 turns carving off (on a fresh voxel, W0 = 0, the update would be 0/0)
       if (!(p.carve_weight > 0.f)) continue;
       bool edge = false;
+      if (p.pix_x) edge = p.pix_x[pi].w != 0.0;  // the pixel's guard, once per frame (k_frame_points)
+      else
       for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
         for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
           const int qu = iu + du, qv = iv + dv;
@@ -251,12 +322,36 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
       }
     }
   }
-  if (p.dirty && __syncthreads_or(wrote) && threadIdx.x == 0) p.dirty[b] = 1;
+  if (!p.dirty && !p.loc_mark) return;  // uniform
+  if (!__syncthreads_or(wrote)) return;
+  if (threadIdx.x == 0 && p.dirty) p.dirty[b] = 1;
+  if (p.loc_mark && threadIdx.x < 27) {
+    // the record bricks of this block's 27-neighbourhood (its direction) read its voxels: their
+    // locations are rebuilt by the incremental index update (hash table: new locations included)
+    const int ox = (int)threadIdx.x % 3 - 1, oy = ((int)threadIdx.x / 3) % 3 - 1, oz = (int)threadIdx.x / 9 - 1;
+    const unsigned long long nkey = pack_key(key.x + ox, key.y + oy, key.z + oz);
+    unsigned int h = hash_key(nkey) & p.table_mask;
+    int e = -1;
+    for (unsigned int probe = 0; probe <= p.table_mask; ++probe) {
+      const unsigned long long kk = p.table[h].key;
+      if (kk == nkey) { e = (int)h; break; }
+      if (kk == kEmptyKey) break;
+      h = (h + 1) & p.table_mask;
+    }
+    if (e >= 0 && p.table[e].slot[D] >= 0 && atomicCAS(&p.loc_mark[e], 0, 1) == 0)
+      p.loc_list[atomicAdd(p.loc_ctr, 1ull)] = make_int4(key.x + ox, key.y + oy, key.z + oz, e);
+  }
 }
 
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s) {
   dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
   k_depth_normals<<<grid, 256, 0, s>>>(depth, p, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_frame_points(const FuseLaunch &p, cudaStream_t s) {
+  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
+  k_frame_points<<<grid, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -266,14 +361,20 @@ cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, cudaStream_t s) {
+cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, int *list,
+                        unsigned long long *count, cudaStream_t s) {
   if (n_new > n_old) {
     k_fuse_init<<<(unsigned)(((n_new - n_old) * kVoxPerBlock + 255) / 256), 256, 0, s>>>(p, n_old, n_new);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (n_new == 0 || !fuse) return cudaSuccess;
-  k_fuse<<<(unsigned)n_new, 256, 0, s>>>(p);
+  if (list) {  // only the blocks with a voxel in the frame's view (count zeroed by the caller)
+    k_fuse_select<<<(unsigned)((n_new * 32 + 255) / 256), 256, 0, s>>>(p, n_new, list, count);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  k_fuse<<<(unsigned)n_new, 256, 0, s>>>(p, list, count);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,31 @@ __global__ void k_bitmap(const int4 *__restrict__ loc, long long n_loc, unsigned
 // either neighbour is absent), with coalesced stores.
 constexpr int kBrickThreads = 256;
 constexpr int kStage = 11;  // staged sdf: voxels -1..9 per axis
+
+// Source of a staged voxel: (neighbour index (ox+1) + 3 (oy+1) + 9 (oz+1)) << 9 | that block's
+// local index l, for the 11^3 staged voxels -1..9 (kStageSrc) and the 9^3 record voxels 0..8
+// (kRecSrc); built at compile time, so the staging loops do no index arithmetic.
+struct SrcTable {
+  unsigned short stage[kStage * kStage * kStage];
+  unsigned short rec[kRecVox];
+  unsigned short rec_c[kRecVox];  // staged index of record voxel a
+  static constexpr unsigned short src(int lx, int ly, int lz) {
+    const int ox = lx < 0 ? -1 : (lx >= kBlock ? 1 : 0), oy = ly < 0 ? -1 : (ly >= kBlock ? 1 : 0),
+              oz = lz < 0 ? -1 : (lz >= kBlock ? 1 : 0);
+    const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
+    return (unsigned short)((((ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)) << 9) | l);
+  }
+  constexpr SrcTable() : stage(), rec(), rec_c() {
+    for (int a = 0; a < kStage * kStage * kStage; ++a)
+      stage[a] = src(a % kStage - 1, (a / kStage) % kStage - 1, a / (kStage * kStage) - 1);
+    for (int a = 0; a < kRecVox; ++a) {
+      const int lx = a % kRec, ly = (a / kRec) % kRec, lz = a / (kRec * kRec);
+      rec[a] = src(lx, ly, lz);
+      rec_c[a] = (unsigned short)((lx + 1) + kStage * (ly + 1) + kStage * kStage * (lz + 1));
+    }
+  }
+};
+__device__ const SrcTable kSrc = SrcTable();
 __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
                                                          unsigned int mask, const float *__restrict__ sdf,
                                                          const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
@@ -127,22 +152,17 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     nb[threadIdx.x] = src;
   }
   __syncthreads();
-  // pool record of block-local voxel (lx, ly, lz) in -8..15, or -1 when its block is unallocated
-  auto rec_of = [&](int lx, int ly, int lz) -> long long {
-    const int ox = (lx < 0) ? -1 : (lx >= kBlock ? 1 : 0);
-    const int oy = (ly < 0) ? -1 : (ly >= kBlock ? 1 : 0);
-    const int oz = (lz < 0) ? -1 : (lz >= kBlock ? 1 : 0);
-    const int src = nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
-    if (src < 0) return -1;
-    const int l = (lx - ox * kBlock) + kBlock * (ly - oy * kBlock) + kBlock * kBlock * (lz - oz * kBlock);
-    return (long long)src * kVoxPerBlock + l;
+  // pool record of a table entry (neighbour << 9 | local index), or -1 when that block is unallocated
+  auto rec_of = [&](unsigned int e) -> long long {
+    const int src = nb[e >> 9];
+    return src < 0 ? -1 : (long long)src * kVoxPerBlock + (e & 511);
   };
   for (int a = threadIdx.x; a < kStage * kStage * kStage; a += kBrickThreads) {
-    const long long r = rec_of(a % kStage - 1, (a / kStage) % kStage - 1, a / (kStage * kStage) - 1);
+    const long long r = rec_of(kSrc.stage[a]);
     st[a] = r >= 0 ? sdf[r] : __int_as_float(0x7fc00000);  // NaN sdf = unallocated
   }
   for (int a = threadIdx.x; a < kRecVox; a += kBrickThreads) {
-    const long long r = rec_of(a % kRec, (a / kRec) % kRec, a / (kRec * kRec));
+    const long long r = rec_of(kSrc.rec[a]);
     sw[a] = r >= 0 ? weight[r] : 0.0f;
   }
   __syncthreads();
@@ -150,9 +170,8 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     float4 ra = make_float4(__int_as_float(0x7fc00000), 0.0f, __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
     float2 rb = make_float2(__int_as_float(0x7fc00000), 0.0f);
     if (a < kRecVox) {
-      const int lx = a % kRec, ly = (a / kRec) % kRec, lz = a / (kRec * kRec);  // 0..8
-      const int c = (lx + 1) + kStage * (ly + 1) + kStage * kStage * (lz + 1);
-      const long long r = rec_of(lx, ly, lz);
+      const int c = kSrc.rec_c[a];  // voxels 0..8: staged index
+      const long long r = rec_of(kSrc.rec[a]);
       ra.x = st[c];
       ra.y = sw[a];
       ra.z = st[c + 1] - st[c - 1];
@@ -355,20 +374,32 @@ cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsign
 // direction; a location's live-direction bytes combine all its directions.  So a dirty block
 // (changed voxels, or new) invalidates the bricks of its 27-neighbourhood in its direction, and
 // every location holding one of those is rebuilt whole (all its directions' bricks).
-__global__ void k_inc_mark(const int4 *__restrict__ keys, long long n, const unsigned char *__restrict__ dirty,
-                           const HashEntry *__restrict__ table, unsigned int mask, int *loc_mark, int4 *loc_list,
-                           unsigned long long *ctr) {
-  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_inc_mark(const int4 *__restrict__ keys, long long b0, long long n,
+                           const unsigned char *__restrict__ dirty, const HashEntry *__restrict__ table,
+                           unsigned int mask, const int *__restrict__ grid, int lo_x, int lo_y, int lo_z, int dim_x,
+                           int dim_y, int dim_z, int *loc_mark, int4 *loc_list, unsigned long long *ctr) {
+  // one thread per (block, neighbour q): the 27 lookups of a block run in parallel
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long b = b0 + g / 27;
+  const int q = (int)(g % 27);
   if (b >= n || !dirty[b]) return;
   const int4 k = keys[b];
-  for (int q = 0; q < 27; ++q) {
-    const int ox = q % 3 - 1, oy = (q / 3) % 3 - 1, oz = q / 9 - 1;
-    const int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
-    if (e < 0 || table[e].slot[k.w] < 0) continue;
-    if (atomicCAS(&loc_mark[e], 0, 1) != 0) continue;
-    const unsigned long long i = atomicAdd(&ctr[0], 1ull);
-    loc_list[i] = make_int4(k.x + ox, k.y + oy, k.z + oz, e);
+  const int ox = q % 3 - 1, oy = (q / 3) % 3 - 1, oz = q / 9 - 1;
+  int e = -1;
+  if (grid) {  // the dense location grid: one load instead of a hash probe
+    const unsigned x = (unsigned)(k.x + ox - lo_x), y = (unsigned)(k.y + oy - lo_y), z = (unsigned)(k.z + oz - lo_z);
+    if (x < (unsigned)dim_x && y < (unsigned)dim_y && z < (unsigned)dim_z) {
+      const int gv = grid[((size_t)z * dim_y + y) * dim_x + x];
+      e = gv >= 0 ? (gv & kGridEntryMask) : -1;
+    }
+    // (the locations this frame added were entered into the grid before this kernel)
+  } else {
+    e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
   }
+  if (e < 0 || table[e].slot[k.w] < 0) return;
+  if (atomicCAS(&loc_mark[e], 0, 1) != 0) return;
+  const unsigned long long i = atomicAdd(&ctr[0], 1ull);
+  loc_list[i] = make_int4(k.x + ox, k.y + oy, k.z + oz, e);
 }
 
 __global__ void k_inc_blocks(const int4 *__restrict__ loc_list, long long n, const HashEntry *__restrict__ table,
@@ -388,10 +419,12 @@ __global__ void k_inc_unmark(const int4 *__restrict__ loc_list, long long n, int
   if (i < n) loc_mark[loc_list[i].w] = 0;
 }
 
-cudaError_t launch_inc_mark(const int4 *keys, long long n, const unsigned char *dirty, const HashEntry *table,
-                            unsigned int mask, int *loc_mark, int4 *loc_list, unsigned long long *ctr, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  k_inc_mark<<<grid_for(n, 256), 256, 0, s>>>(keys, n, dirty, table, mask, loc_mark, loc_list, ctr);
+cudaError_t launch_inc_mark(const int4 *keys, long long b0, long long n, const unsigned char *dirty,
+                            const HashEntry *table, unsigned int mask, const int *grid, const int lo[3], const int dim[3],
+                            int *loc_mark, int4 *loc_list, unsigned long long *ctr, cudaStream_t s) {
+  if (n <= b0) return cudaSuccess;
+  k_inc_mark<<<grid_for((n - b0) * 27, 256), 256, 0, s>>>(keys, b0, n, dirty, table, mask, grid, lo[0], lo[1], lo[2],
+                                                          dim[0], dim[1], dim[2], loc_mark, loc_list, ctr);
   return cudaGetLastError();
 }
 
