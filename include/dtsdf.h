@@ -311,15 +311,13 @@ DTSDF_API int dtsdf_reset_kernel_times(dtsdf_ctx *ctx);
  *                         every direction present at the block location */
 #define DTSDF_OPT_CELL_DIRS 8
 /* Tuning (results unchanged):
- *   DTSDF_OPT_SCHEDULE    0 (default) one CTA per 16x8-pixel tile (in the tile order); 1 persistent warps pulling
- *                         8x4-pixel tiles from an atomic counter
+ *   (option 3, a persistent warp schedule, was measured slower and removed in round 2)
  *   DTSDF_OPT_LOCATION_GRID 1 (default) resolve block locations through the dense location grid
  *                         (built when the location AABB has <= 2^28 cells); 0 through the
  *                         occupancy bitmaps and the hash table
  * Testing only (changes which root a multi-root lattice interval yields):
  *   DTSDF_OPT_BISECT_STEPS  -1 (default) enough bisection steps to narrow the bracket to
  *                           <= 5e-5 m before regula falsi; n >= 0 forces n steps */
-#define DTSDF_OPT_SCHEDULE 3
 #define DTSDF_OPT_BISECT_STEPS 4
 #define DTSDF_OPT_LOCATION_GRID 5
 /*   DTSDF_OPT_REFINE_TOL_NM  0 (default) regula falsi stops when f(b) is within 1e-7 of the root or after

@@ -129,8 +129,6 @@ struct RenderLaunch {
   int use_range, use_skip;         // exact accelerations (DTSDF_OPT_*)
   int n_bisect;                    // bisection steps: bracket Delta -> <= 5e-5 m
   float refine_tol;                // regula falsi also stops once the bracket is narrower (m)
-  int schedule;                    // 0 grid of 16x8-pixel CTA tiles, 1 persistent warps + tile counter
-  int *tile_counter;               // persistent schedule work counter (reset per launch)
   const unsigned long long *z_near;  // [n_views][tiles_y][tiles_x] range keys of k_range (epoch-tagged
   const unsigned long long *z_far;   // float bits, range_key_*)
   unsigned int epoch;                // range-pass epoch of this launch

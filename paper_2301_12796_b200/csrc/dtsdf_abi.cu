@@ -97,10 +97,9 @@ struct dtsdf_ctx {
   size_t range_cap = 0;  // tiles
   void *host_stage = nullptr;  // device scratch for host-output renders
   size_t host_stage_cap = 0;
-  int use_range = 1, use_skip = 1, schedule = 0, bisect_steps = -1, use_grid = 1, refine_tol_nm = 0;
+  int use_range = 1, use_skip = 1, bisect_steps = -1, use_grid = 1, refine_tol_nm = 0;
   int host_write = 1;
   int use_live = 1;            // DTSDF_OPT_CELL_DIRS          // DTSDF_OPT_HOST_WRITE: the raycast writes mapped pinned host outputs directly
-  int *tile_counter = nullptr;
   // view-dependent combined TSDF (NEXT-1, combine.cu)
   bool combined = false;
   int64_t n_comb = 0, comb_cap = 0;
@@ -286,7 +285,7 @@ int dtsdf_create(int cuda_device, dtsdf_ctx **out) {
   dtsdf_ctx *c = new (std::nothrow) dtsdf_ctx();
   if (!c) return fail(DTSDF_ERR_OUT_OF_MEMORY, "host allocation");
   c->device = cuda_device;
-  if (dalloc(c->scratch, 64) != cudaSuccess || dalloc(c->tile_counter, 16) != cudaSuccess) {
+  if (dalloc(c->scratch, 64) != cudaSuccess) {
     delete c;
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "scratch allocation");
   }
@@ -300,7 +299,6 @@ int dtsdf_destroy(dtsdf_ctx *c) {
   cudaDeviceSynchronize();
   free_volume(c);
   dfree(c->scratch);
-  dfree(c->tile_counter);
   if (c->fuse_stage) cudaFree(c->fuse_stage);
   dfree(c->pix_buf);
   dfree(c->icp_partials);
@@ -536,7 +534,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
   }
   // the order pays most when the launch is a few waves of CTAs (one view: C1 -12 %); by 256-view
   // batches the drain is amortised and it is neutral (profiles/r1f_sweep_tile_order.jsonl)
-  const bool order = c->schedule == 0 && tile_order_fits(W, rows) &&
+  const bool order = tile_order_fits(W, rows) &&
                      (c->use_order == 2 || (c->use_order == 1 && cts <= (size_t)kOrderAutoMaxCtas));
   VolumeView V;
   V.table = c->table;
@@ -604,9 +602,7 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.n_bisect = 0;
     while (V.delta / (float)(1 << pl.n_bisect) > 5e-5f && pl.n_bisect < 20) ++pl.n_bisect;
     if (c->bisect_steps >= 0) pl.n_bisect = c->bisect_steps;
-    pl.schedule = c->schedule;
     pl.refine_tol = 1e-9f * (float)c->refine_tol_nm;
-    pl.tile_counter = c->tile_counter;
     pl.z_near = c->z_near; pl.z_far = c->z_far;
     pl.epoch = rl.epoch;
     pl.order = order ? c->tile_order : nullptr;
@@ -1532,7 +1528,6 @@ int dtsdf_set_option(dtsdf_ctx *c, int option, int value) {
   if (!c) return fail(DTSDF_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (option == DTSDF_OPT_RANGE_PASS) c->use_range = value ? 1 : 0;
   else if (option == DTSDF_OPT_BLOCK_SKIP) c->use_skip = value ? 1 : 0;
-  else if (option == DTSDF_OPT_SCHEDULE && (value == 0 || value == 1)) c->schedule = value;
   else if (option == DTSDF_OPT_LOCATION_GRID) c->use_grid = value ? 1 : 0;
   else if (option == DTSDF_OPT_BISECT_STEPS && value >= -1 && value <= 30) c->bisect_steps = value;
   else if (option == DTSDF_OPT_REFINE_TOL_NM && value >= 0 && value <= 100000) c->refine_tol_nm = value;

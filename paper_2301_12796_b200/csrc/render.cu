@@ -1180,7 +1180,7 @@ struct RayT {
 #endif
   }
 
-  // per-pixel scalar stores (persistent schedule)
+  // per-pixel scalar stores (device outputs)
   __device__ __forceinline__ void store(const RenderLaunch &p) const {
     float depth, nrm[3];
     int col[3], mask;
@@ -1359,51 +1359,8 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   }
 }
 
-// persistent schedule: resident warps pull 8x4-pixel warp tiles (view-major, row-major) from an
-// atomic counter until the batch is done -- no CTA-granularity tail, uneven tiles balance out
-template <bool kComb>
-__global__ void __launch_bounds__(256, 2) k_raycast_persistent(const __grid_constant__ RenderLaunch p) {
-  const int lane = threadIdx.x & 31;
-  const int wx = (p.width + 7) >> 3, wy = (p.row1 - p.row0 + 3) >> 2;
-  const int per_view = wx * wy, total = per_view * p.n_views;
-  for (;;) {
-    int tile = 0;
-    if (lane == 0) tile = atomicAdd(p.tile_counter, 1);
-    tile = __shfl_sync(0xffffffffu, tile, 0);
-    if (tile >= total) return;
-    const int view = tile / per_view, rr = tile - view * per_view;
-    const int ty = rr / wx, tx = rr - ty * wx;
-    const int u = tx * 8 + (lane & 7), vrel = ty * 4 + (lane >> 3);
-    if (u < p.width && p.row0 + vrel < p.row1) {
-      RayT<kComb> ray;
-      ray.init(p, view, u, vrel);
-      while (!ray.step(p)) {
-      }
-      if (ray.hit) ray.shade(p);
-      ray.store(p);
-    }
-  }
-}
-
 template <bool kComb>
 static cudaError_t launch_raycast_t(const RenderLaunch &p, cudaStream_t s) {
-  if (p.schedule == 1) {
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_raycast_persistent<kComb>, 256, 0);
-      if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
-    cudaError_t e = cudaMemsetAsync(p.tile_counter, 0, sizeof(int), s);
-    if (e != cudaSuccess) return e;
-    const long long tiles = (long long)((p.width + 7) >> 3) * ((p.row1 - p.row0 + 3) >> 2) * p.n_views;
-    long long grid = (long long)blocks_per_sm * sms;
-    grid = grid < (tiles + 7) / 8 ? grid : (tiles + 7) / 8;
-    k_raycast_persistent<kComb><<<(unsigned)grid, 256, 0, s>>>(p);
-    return cudaGetLastError();
-  }
   const int ct_y = (p.row1 - p.row0 + kTileH - 1) / kTileH;
   dim3 grid((unsigned)(p.ct_x * ct_y), 1u, (unsigned)p.n_views);
   return launch_pdl(k_raycast<kComb>, grid, dim3(DTSDF_CTA), s, p);

@@ -28,7 +28,7 @@ EXPORTS = [
     "dtsdf_fuse", "dtsdf_get_volume", "dtsdf_default_icp_params", "dtsdf_icp", "dtsdf_icp_normal_equations",
 ]
 MARGIN = 0.125  # PAPER.md:262 "(±1/8 image size)"
-OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_SCHEDULE, OPT_BISECT_STEPS, OPT_LOCATION_GRID, OPT_REFINE_TOL_NM = 1, 2, 3, 4, 5, 6
+OPT_RANGE_PASS, OPT_BLOCK_SKIP, OPT_BISECT_STEPS, OPT_LOCATION_GRID, OPT_REFINE_TOL_NM = 1, 2, 4, 5, 6
 OPT_HOST_WRITE = 7
 OPT_CELL_DIRS = 8
 OPT_TILE_ORDER = 9

@@ -227,3 +227,24 @@ def test_combine_more_than_65535_locations(R):
     st = compare(_sel(g, 0, px), oc)
     assert st["budget_used"] <= 1e-3 and st["hits_gpu"] > 0.5 * len(px), st
     print("combine > 65535", n, st)
+
+
+def test_out_of_device_memory_is_reported_and_the_context_stays_usable(R, c0):
+    """a volume whose record bricks do not fit in device memory fails with
+    DTSDF_ERR_OUT_OF_MEMORY (not the sticky CUDA error), and the context renders the next volume.
+    Device memory is first filled with a torch tensor, leaving 4 GiB free."""
+    from paper_2301_12796_b200.dtsdf import OUT_OF_MEMORY, DtsdfError
+    vol = _slab_volume(96, 96, 24)  # 221k blocks: 1.2 GB pool + 3.9 GB record bricks + index
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    hog = torch.empty(max(free - (4 << 30), 0), dtype=torch.uint8, device="cuda")
+    try:
+        with pytest.raises(DtsdfError) as e:
+            R.upload_volume(vol)
+        assert e.value.code == OUT_OF_MEMORY, str(e.value)
+    finally:
+        del hog
+        torch.cuda.empty_cache()
+    R.upload_volume(c0.volume)
+    g = R.render(c0.poses, c0.intrinsics)
+    assert_parity(_sel(g), oracle.OracleVolume(c0.volume).render(c0.poses[0], c0.intrinsics), what="C0 after OOM")

@@ -167,21 +167,6 @@ def test_location_grid_and_hash_paths_agree(R, c1):
         assert torch.equal(ref[k], g[k]), k
 
 
-def test_schedules_give_identical_bits(R, c1):
-    """Grid and persistent (lane-level work fetching) schedules run the same per-ray code."""
-    from paper_2301_12796_b200.dtsdf import OPT_SCHEDULE
-    w = scenes.c3_batch(n_views=3, room=c1)
-    R.upload_volume(w.volume)
-    K = scenes.Intrinsics(fx=262.5, fy=262.5, cx=159.5, cy=119.5, width=321, height=243)
-    R.set_option(OPT_SCHEDULE, 0)
-    ref = R.render(w.poses, K, row0=5, row1=240)
-    R.set_option(OPT_SCHEDULE, 1)
-    g = R.render(w.poses, K, row0=5, row1=240)
-    R.set_option(OPT_SCHEDULE, 0)
-    for k in ref:
-        assert torch.equal(ref[k], g[k]), k
-
-
 def test_host_outputs_equal_device_outputs(R, c1):
     """Pinned host outputs written by the kernel (DTSDF_OPT_HOST_WRITE), pinned via the copy path,
     and pageable host outputs all equal the device render bit for bit -- full frame, and a ragged

@@ -1,7 +1,6 @@
 """Small workload touching every kernel of libdtsdf.so, for compute-sanitizer (SURVEY.md §4
-memory-safety gate): index build, range pass + raycast (grid and persistent schedules, row
-shards, host outputs), combined TSDF (both modes) + its raycast, fusion (normals, allocation,
-fusion, re-commit), ICP."""
+memory-safety gate): index build, range pass + raycast (row shards, host outputs), combined TSDF (both modes) + its raycast, fusion (normals, allocation,
+fusion, incremental and full re-commit), ICP."""
 import os
 import sys
 
@@ -13,16 +12,14 @@ import torch  # noqa: E402
 
 import scenes  # noqa: E402
 from paper_2301_12796_b200 import Renderer  # noqa: E402
-from paper_2301_12796_b200.dtsdf import OPT_LOCATION_GRID, OPT_SCHEDULE  # noqa: E402
+from paper_2301_12796_b200.dtsdf import OPT_LOCATION_GRID  # noqa: E402
 
 w = scenes.c0_sphere()
 R = Renderer(0)
 R.upload_volume(w.volume)
 K = w.intrinsics
 out = R.render(w.poses, K)
-R.set_option(OPT_SCHEDULE, 1)
 R.render(w.poses, K, row0=3, row1=41)
-R.set_option(OPT_SCHEDULE, 0)
 R.set_option(OPT_LOCATION_GRID, 0)
 R.render(w.poses, K)
 R.set_option(OPT_LOCATION_GRID, 1)

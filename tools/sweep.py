@@ -18,12 +18,12 @@ import oracle  # noqa: E402
 import scenes  # noqa: E402
 from parity import compare  # noqa: E402
 from paper_2301_12796_b200 import Renderer  # noqa: E402
-from paper_2301_12796_b200.dtsdf import OPT_BISECT_STEPS, OPT_REFINE_TOL_NM, OPT_SCHEDULE  # noqa: E402
+from paper_2301_12796_b200.dtsdf import OPT_BISECT_STEPS, OPT_REFINE_TOL_NM  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C1,C2")
 ap.add_argument("--reps", type=int, default=200)
-ap.add_argument("--schedules", default="0,1")
+ap.add_argument("--schedules", default="0", help="(the persistent schedule 1 was removed in round 2)")
 ap.add_argument("--bisect", default="-1,6,5,4,3")
 ap.add_argument("--views", type=int, default=1)
 ap.add_argument("--tol", default="0")
@@ -40,7 +40,6 @@ for name in args.configs.split(","):
     for sch, nb, tol in itertools.product([int(x) for x in args.schedules.split(",")],
                                           [int(x) for x in args.bisect.split(",")],
                                           [int(x) for x in args.tol.split(",")]):
-        R.set_option(OPT_SCHEDULE, sch)
         R.set_option(OPT_REFINE_TOL_NM, tol)
         R.set_option(OPT_BISECT_STEPS, nb)
         out = R.render(poses, w.intrinsics)
@@ -63,6 +62,5 @@ for name in args.configs.split(","):
                           "Mrays_s_kernel": round(rays / ms / 1e3, 1), "budget_used": st["budget_used"],
                           "color_exact": st["color_exact"], "depth_max": st["depth_max_err"],
                           "hit_disagree": st["hit_disagree"], "geom_bad": st["geom_out_of_tol"]}), flush=True)
-R.set_option(OPT_SCHEDULE, 0)
 R.set_option(OPT_BISECT_STEPS, -1)
 R.set_option(OPT_REFINE_TOL_NM, 0)
