@@ -232,12 +232,14 @@ def test_combine_more_than_65535_locations(R):
 def test_out_of_device_memory_is_reported_and_the_context_stays_usable(R, c0):
     """a volume whose record bricks do not fit in device memory fails with
     DTSDF_ERR_OUT_OF_MEMORY (not the sticky CUDA error), and the context renders the next volume.
-    Device memory is first filled with a torch tensor, leaving 4 GiB free."""
+    The context first holds a tiny volume (an upload frees the previous one), then device memory is
+    filled with a torch tensor, leaving 2 GiB free."""
     from paper_2301_12796_b200.dtsdf import OUT_OF_MEMORY, DtsdfError
     vol = _slab_volume(96, 96, 24)  # 221k blocks: 1.2 GB pool + 3.9 GB record bricks + index
+    R.upload_volume(c0.volume)
     torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
-    hog = torch.empty(max(free - (4 << 30), 0), dtype=torch.uint8, device="cuda")
+    hog = torch.empty(max(free - (2 << 30), 0), dtype=torch.uint8, device="cuda")
     try:
         with pytest.raises(DtsdfError) as e:
             R.upload_volume(vol)
