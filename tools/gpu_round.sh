@@ -14,7 +14,7 @@ timeout 600 python bench.py > $OUT/bench_$TAG.log 2>&1; echo "bench_rc=$?"
 cat $OUT/bench_$TAG.log | tail -2
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > $OUT/bench_ref_$TAG.log 2>&1; echo "ref_rc=$?"
 tail -1 $OUT/bench_ref_$TAG.log
-CMD="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 5"
+CMD="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 5 --batch-views 0"
 $CMD > $OUT/plain_$TAG.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launch_$TAG.log 2>&1 && \
