@@ -591,18 +591,14 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
     const int a = tid + k * kFinishThreads;
     if (a < kApronStride) {
       s_c[a] = v[k];
-      // the interior (voxels 0..7) is the slot's own k_combine output, already in place
-      const unsigned ix = (unsigned)(a % kApron - 1), iy = (unsigned)((a / kApron) % kApron - 1),
-                     iz = (unsigned)(a / (kApron * kApron) - 1);
-      if (a >= kApronVox || ix >= (unsigned)kBlock || iy >= (unsigned)kBlock || iz >= (unsigned)kBlock) ap[a] = v[k];
+      ap[a] = v[k];
     }
   }
   uchar4 *cp = p.rgb + slot * kRgbApronStride;
 #pragma unroll
   for (int k = 0; k < kRgbPer; ++k) {
     const int a = tid + k * kFinishThreads;
-    const int ix = a % kRgbApron, iy = (a / kRgbApron) % kRgbApron, iz = a / (kRgbApron * kRgbApron);
-    if (a < kRgbApronStride && (a >= kRgbApronVox || ix >= kBlock || iy >= kBlock || iz >= kBlock)) cp[a] = cv[k];
+    if (a < kRgbApronStride) cp[a] = cv[k];
   }
   __syncthreads();
   int any_neg = 0;
