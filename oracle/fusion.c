@@ -278,7 +278,9 @@ int64_t oracle_fuse_frame(void *p, const float *depth, const float *normal, cons
       if (dd < -1.0) continue; /* behind the surface beyond the band: untouched */
       if (dd > 1.0) {
         /* R43: free space -> towards 1 with a constant weight, unless a depth within `rad`
-         * pixels differs by more than tau (depth edge) */
+         * pixels differs by more than tau (depth edge); a carving weight of 0 means no carving
+         * (on a fresh voxel, W0 = 0, the running average would be 0/0) */
+        if (!(carve_w > 0.0)) continue;
         int edge = 0;
         for (int dv = -rad; dv <= rad && !edge; ++dv)
           for (int du = -rad; du <= rad; ++du) {

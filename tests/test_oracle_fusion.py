@@ -265,3 +265,23 @@ def test_capacity_exhaustion_raises():
     F = oracle.OracleFusion(S, TAU, TH, 3)
     with pytest.raises(MemoryError):
         F.fuse(fr.depth, fr.normal, fr.color, pose, K)
+
+
+def test_carve_weight_zero_means_no_carving():
+    """R43 with carve_weight 0 (include/dtsdf.h: 0 = no carving): voxels in front of the surface
+    keep their values -- a fresh block's free-space voxels stay at sdf 1, weight 0 (the running
+    average would otherwise be 0/0) -- and everything else equals the fusion with carving on."""
+    K = pinhole(40, 30, 30.0)
+    pose = look_at([0, 0, 0], [1, 0, 0])
+    fr = scenes.analytic_frame(_wall_patches(0.8), pose, K)
+    F0 = oracle.OracleFusion(S, TAU, TH, 40000)
+    F1 = oracle.OracleFusion(S, TAU, TH, 40000)
+    F0.fuse(fr.depth, fr.normal, fr.color, pose, K, carve_weight=0.0)
+    F1.fuse(fr.depth, fr.normal, fr.color, pose, K)
+    v0, v1 = F0.volume(), F1.volume()
+    assert np.array_equal(v0.keys, v1.keys)
+    assert np.isfinite(v0.sdf).all() and np.isfinite(v0.weight).all()
+    carved = v1.weight != v0.weight
+    free = (v0.weight == 0) & (v0.sdf == 1.0)
+    assert carved.any() and (carved <= free).all()  # carving touched only free-space voxels
+    assert np.array_equal(v0.sdf[~carved], v1.sdf[~carved])
