@@ -240,6 +240,11 @@ struct FuseLaunch {
   // per-pixel world-rotated back-projection R P and world normal R n of the frame (k_frame_points,
   // once per frame instead of once per associated voxel; null: k_fuse computes them)
   double4 *pix_x, *pix_n;
+  // the same in fp32 for k_fuse's pre-test: pix_a (R P, z or -1 when the pixel holds no usable
+  // depth / normal), pix_b (R n, carving guard 1 / 0)
+  float4 *pix_a, *pix_b;
+  // fp32 copies for the pre-test of k_fuse (DTSDF_FUSE_PRETEST): rotation, intrinsics, 1 / tau
+  float Rf[9], fxf, fyf, cxf, cyf, inv_tau_f;
   // incremental index update: a block k_fuse changed marks the locations of its 27-neighbourhood
   // that hold a block in its direction (loc_mark dedup, appended to loc_list, counter loc_ctr);
   // null: not tracked

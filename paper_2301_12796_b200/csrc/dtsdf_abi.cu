@@ -1118,6 +1118,8 @@ static void fuse_launch_common(dtsdf_ctx *c, const float pose[16], const dtsdf_i
   L.fx = K->fx; L.fy = K->fy; L.cx = K->cx; L.cy = K->cy; L.z_min = K->z_min; L.z_max = K->z_max;
   L.width = K->width;
   L.height = K->height;
+  for (int a = 0; a < 9; ++a) L.Rf[a] = (float)L.R[a];
+  L.fxf = K->fx; L.fyf = K->fy; L.cxf = K->cx; L.cyf = K->cy;
 }
 
 static const void *to_device(dtsdf_ctx *c, const void *src, size_t bytes, size_t offset, cudaStream_t s, bool *ok) {
@@ -1205,6 +1207,7 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   L.capacity = c->cap;
   L.s = (double)c->params.voxel_size;
   L.tau = (double)c->params.truncation;
+  L.inv_tau_f = (float)(1.0 / L.tau);
   L.M = (int)std::ceil(4.0 * L.tau / L.s);
   L.step = 2.0 * L.tau / (double)L.M;
   L.cos_theta = std::cos((double)c->params.theta);
@@ -1259,12 +1262,14 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   std::memcpy(&init[12], &n0, 8);
   std::memcpy(&init[4], &nl0, 8);
   CK(c, cudaMemcpyAsync(c->scratch, init, sizeof(init), cudaMemcpyHostToDevice, s), "fuse init");
-  if (ensure(c->pix_buf, c->cap_pix_buf, px * 2 * sizeof(double4)) != cudaSuccess) {
+  if (ensure(c->pix_buf, c->cap_pix_buf, px * 3 * sizeof(double4)) != cudaSuccess) {
     cudaGetLastError();
     return fail(DTSDF_ERR_OUT_OF_MEMORY, "frame points");
   }
   L.pix_x = c->pix_buf;
   L.pix_n = c->pix_buf + px;
+  L.pix_a = reinterpret_cast<float4 *>(c->pix_buf + 2 * px);
+  L.pix_b = L.pix_a + px;
   TimedLaunch tl{};
   begin_timed(c, 2, s, &tl, 2);
   CK(c, launch_frame_points(L, s), "frame points");

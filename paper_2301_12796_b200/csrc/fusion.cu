@@ -24,6 +24,10 @@
 
 #include "common.cuh"
 
+#ifndef DTSDF_FUSE_PRETEST
+#define DTSDF_FUSE_PRETEST 1  // fp32 pre-test of the association and band decisions in k_fuse (exact)
+#endif
+
 namespace dtsdf {
 
 __device__ __forceinline__ bool depth_ok(const FuseLaunch &p, float z) {
@@ -167,6 +171,9 @@ __global__ void __launch_bounds__(256) k_frame_points(const __grid_constant__ Fu
   }
   p.pix_x[i] = make_double4(X[0], X[1], X[2], edge ? 1.0 : 0.0);
   p.pix_n[i] = make_double4(n[0], n[1], n[2], 0.0);
+  const bool usable = depth_ok(p, z) && !(nc[0] == 0.0 && nc[1] == 0.0 && nc[2] == 0.0);
+  p.pix_a[i] = make_float4((float)X[0], (float)X[1], (float)X[2], usable ? z : -1.0f);
+  p.pix_b[i] = make_float4((float)n[0], (float)n[1], (float)n[2], edge ? 1.0f : 0.0f);
 }
 
 __global__ void __launch_bounds__(256) k_fuse_init(FuseLaunch p, long long n0, long long n1) {
@@ -238,18 +245,76 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     // association (R41): projection and nearest pixel in fp64 with the oracle's roundings
     const double x0 = __dmul_rn((double)i, p.s), x1 = __dmul_rn((double)j, p.s), x2 = __dmul_rn((double)k, p.s);
     const double d0 = __dsub_rn(x0, p.t[0]), d1 = __dsub_rn(x1, p.t[1]), d2 = __dsub_rn(x2, p.t[2]);
-    double xc[3];
+    int iu, iv;
+    bool exact64 = true;
+#if DTSDF_FUSE_PRETEST
+    {
+      // fp32 pre-test: the projection in fp32 from the fp64 offset; where u + 1/2 and v + 1/2 are
+      // clear of an integer (and z of 0) by more than a bound on the fp32 error, the nearest
+      // pixel -- or "outside the image" -- is the fp64 decision; else the fp64 path decides
+      const float e0 = (float)d0, e1 = (float)d1, e2 = (float)d2;
+      const float zc = p.Rf[2] * e0 + p.Rf[5] * e1 + p.Rf[8] * e2;
+      if (zc > 0.05f) {
+        const float xcf = p.Rf[0] * e0 + p.Rf[3] * e1 + p.Rf[6] * e2;
+        const float ycf = p.Rf[1] * e0 + p.Rf[4] * e1 + p.Rf[7] * e2;
+        const float dn = fabsf(e0) + fabsf(e1) + fabsf(e2);
+        const float iz = 1.0f / zc;
+        const float uf = p.fxf * xcf * iz + p.cxf + 0.5f, vf = p.fyf * ycf * iz + p.cyf + 0.5f;
+        // |error| of u, v: relative 2.5e-7 of |d| in xc and zc (fp32 rotation of a rounded offset),
+        // amplified by f (z + |x|) / z^2, plus the roundings of the division and additions
+        const float eu = 2.5e-7f * p.fxf * dn * (zc + fabsf(xcf)) * iz * iz + 1e-5f * (1.0f + fabsf(uf));
+        const float ev = 2.5e-7f * p.fyf * dn * (zc + fabsf(ycf)) * iz * iz + 1e-5f * (1.0f + fabsf(vf));
+        const float fu = floorf(uf), fv = floorf(vf);
+        if (uf - fu > eu && fu + 1.0f - uf > eu && vf - fv > ev && fv + 1.0f - vf > ev) {
+          exact64 = false;
+          if (!(fu >= 0.0f && fu <= (float)(p.width - 1) && fv >= 0.0f && fv <= (float)(p.height - 1))) continue;
+          iu = (int)fu;
+          iv = (int)fv;
+        }
+      } else if (zc < -0.05f) {
+        continue;  // behind the camera (z < 0 with an fp32 error far below 0.05 m)
+      }
+    }
+#endif
+    if (exact64) {
+      double xc[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-      xc[a] = __dadd_rn(__dadd_rn(__dmul_rn(p.R[a], d0), __dmul_rn(p.R[3 + a], d1)), __dmul_rn(p.R[6 + a], d2));
-    if (!(xc[2] > 0.0)) continue;
-    const double uu = __dadd_rn(__ddiv_rn(__dmul_rn(p.fx, xc[0]), xc[2]), p.cx);
-    const double vv = __dadd_rn(__ddiv_rn(__dmul_rn(p.fy, xc[1]), xc[2]), p.cy);
-    const double fu = floor(__dadd_rn(uu, 0.5)), fv = floor(__dadd_rn(vv, 0.5));
-    if (!(fu >= 0.0 && fu <= (double)(p.width - 1) && fv >= 0.0 && fv <= (double)(p.height - 1))) continue;
-    const int iu = (int)fu, iv = (int)fv;
+      for (int a = 0; a < 3; ++a)
+        xc[a] = __dadd_rn(__dadd_rn(__dmul_rn(p.R[a], d0), __dmul_rn(p.R[3 + a], d1)), __dmul_rn(p.R[6 + a], d2));
+      if (!(xc[2] > 0.0)) continue;
+      const double uu = __dadd_rn(__ddiv_rn(__dmul_rn(p.fx, xc[0]), xc[2]), p.cx);
+      const double vv = __dadd_rn(__ddiv_rn(__dmul_rn(p.fy, xc[1]), xc[2]), p.cy);
+      const double fu = floor(__dadd_rn(uu, 0.5)), fv = floor(__dadd_rn(vv, 0.5));
+      if (!(fu >= 0.0 && fu <= (double)(p.width - 1) && fv >= 0.0 && fv <= (double)(p.height - 1))) continue;
+      iu = (int)fu;
+      iv = (int)fv;
+    }
     const size_t pi = (size_t)iv * p.width + iu;
     DTSDF_CHECK(iu >= 0 && iu < p.width && iv >= 0 && iv < p.height);
+#if DTSDF_FUSE_PRETEST
+    // the pixel's fp32 record: no usable depth -> untouched; a band decision clear of -1 and 1 by
+    // more than its fp32 error is taken here (behind: untouched; free space: carving)
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;
+    if (p.pix_a) {
+      pa = p.pix_a[pi];
+      if (!(pa.w > 0.0f)) continue;
+      pb = p.pix_b[pi];
+      const float fex = (float)d0 - pa.x, fey = (float)d1 - pa.y, fez = (float)d2 - pa.z;
+      const float df = (fex * pb.x + fey * pb.y + fez * pb.z) * p.inv_tau_f;
+      const float m = 1e-5f + 5e-7f * (fabsf((float)d0) + fabsf((float)d1) + fabsf((float)d2) + fabsf(pa.x) +
+                                        fabsf(pa.y) + fabsf(pa.z)) * p.inv_tau_f;
+      if (df < -1.0f - m) continue;  // behind the surface beyond the band: untouched
+      if (df > 1.0f + m) {           // R43 free space
+        if (!(p.carve_weight > 0.f) || pb.w != 0.0f) continue;
+        const size_t r = (size_t)b * kVoxPerBlock + l;
+        const float W0 = p.weight[r];
+        p.sdf[r] = (W0 * p.sdf[r] + p.carve_weight) / (W0 + p.carve_weight);
+        p.weight[r] = fminf(W0 + p.carve_weight, p.max_weight);
+        wrote = true;
+        continue;
+      }
+    }
+#endif
     const float z = p.depth[pi];
     const float nc0 = p.normal[3 * pi], nc1 = p.normal[3 * pi + 1], nc2 = p.normal[3 * pi + 2];
     if (!depth_ok(p, z) || (nc0 == 0.f && nc1 == 0.f && nc2 == 0.f)) continue;
@@ -269,13 +334,18 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     }
     const double ex = __dsub_rn(x0, __dadd_rn(X[0], p.t[0])), ey = __dsub_rn(x1, __dadd_rn(X[1], p.t[1])),
                  ez = __dsub_rn(x2, __dadd_rn(X[2], p.t[2]));
-    const double ddd =
-        __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(ex, nd[0]), __dmul_rn(ey, nd[1])), __dmul_rn(ez, nd[2])), p.tau);
+    // the band decision: -1 behind the band (untouched), 1 free space (carving), 0 in the band
+    int cls = 2;  // 2: decide from d in fp64
+    double ddd = 0.0;
+    if (cls == 2) {
+      ddd = __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(ex, nd[0]), __dmul_rn(ey, nd[1])), __dmul_rn(ez, nd[2])), p.tau);
+      cls = ddd < -1.0 ? -1 : (ddd > 1.0 ? 1 : 0);
+    }
     const float dd = (float)ddd;  // eq:point-to-plane, sign of reading R6
     const float nx = (float)nd[0], ny = (float)nd[1], nz = (float)nd[2];
     const size_t r = (size_t)b * kVoxPerBlock + l;
-    if (ddd < -1.0) continue;  // behind the surface beyond the band: untouched
-    if (ddd > 1.0) {
+    if (cls < 0) continue;  // behind the surface beyond the band: untouched
+    if (cls == 1) {
       // R43: free space, unless a depth within the guard radius differs by more than tau;
       // carve_weight 0 turns carving off (on a fresh voxel, W0 = 0, the update would be 0/0)
       if (!(p.carve_weight > 0.f)) continue;
