@@ -236,6 +236,8 @@ struct FuseLaunch {
   int4 *locations;
   unsigned long long *n_loc;
   int lo[3], dim[3];
+  const int *grid;                 // the committed location grid (null: none): existing (location, D)
+                                   // keys are recognised with one load, without a hash probe
   unsigned char *dirty;
   // per-pixel world-rotated back-projection R P and world normal R n of the frame (k_frame_points,
   // once per frame instead of once per associated voxel; null: k_fuse computes them)
@@ -244,7 +246,7 @@ struct FuseLaunch {
   // depth / normal), pix_b (R n, carving guard 1 / 0)
   float4 *pix_a, *pix_b;
   // fp32 copies for the pre-test of k_fuse (DTSDF_FUSE_PRETEST): rotation, intrinsics, 1 / tau
-  float Rf[9], fxf, fyf, cxf, cyf, inv_tau_f;
+  float Rf[9], fxf, fyf, cxf, cyf, inv_tau_f, inv_s_f;
   // incremental index update: a block k_fuse changed marks the locations of its 27-neighbourhood
   // that hold a block in its direction (loc_mark dedup, appended to loc_list, counter loc_ctr);
   // null: not tracked
@@ -318,11 +320,24 @@ cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsign
                             int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
+// The dense location grid as a lookup for index-build kernels: hash entry of a block location, or
+// -1 (unallocated / outside the AABB); grid null: unavailable (use the hash table).
+struct GridRef {
+  const int *grid;
+  int lo[3], dim[3];
+  __device__ __forceinline__ int entry(int bx, int by, int bz) const {
+    const unsigned x = (unsigned)(bx - lo[0]), y = (unsigned)(by - lo[1]), z = (unsigned)(bz - lo[2]);
+    if (x >= (unsigned)dim[0] || y >= (unsigned)dim[1] || z >= (unsigned)dim[2]) return -1;
+    const int gv = __ldg(&grid[((size_t)z * dim[1] + y) * dim[0] + x]);
+    return gv >= 0 ? (gv & ((1 << 24) - 1)) : -1;
+  }
+};
+
 // record bricks of n blocks (list: their pool indices, or null for blocks 0..n-1), each adding its
 // direction's bits to the location's live-direction bytes (cell_dirs, which start at 0x80)
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
-                          unsigned char *cell_dirs, const int *list, cudaStream_t s);
+                          unsigned char *cell_dirs, const int *list, const GridRef &gr, cudaStream_t s);
 cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s);
 // incremental commit after a fused frame: the locations whose record bricks must be rebuilt (the
 // 27-neighbourhoods, in the dirty block's direction, of every dirty block) -> loc_list (deduplicated
@@ -338,7 +353,7 @@ cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, 
 cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsigned long long *count,
                                   const HashEntry *table, unsigned int mask, const float *sdf, const float *weight,
                                   const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
-                                  const int *list, cudaStream_t s);
+                                  const int *list, const GridRef &gr, cudaStream_t s);
 cudaError_t launch_cell_masks(const int4 *locations, long long n, const unsigned char *cell_dirs, unsigned int *cell_pos,
                               unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y,
                               cudaStream_t s);

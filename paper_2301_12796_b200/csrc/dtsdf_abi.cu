@@ -416,10 +416,35 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
   begin_timed(c, 2, s, &tl);
   CK(c, launch_bitmap(c->locations, c->n_loc, c->bitmap, lo[0], lo[1], lo[2], c->dim[0], c->dim[1], s), "bitmap");
   end_timed(c, s, &tl);
+  // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
+  // raycast resolves locations through the bitmaps and the hash table.  Its entries go in first
+  // (k_bricks resolves neighbours through it); the final values, with the surface bits, follow
+  // the cell masks.
+  const bool grid_ok = cells > 0 && cells <= (size_t(1) << 28) && c->table_cap <= (size_t(1) << kGridEntryBits);
+  if (grid_ok) {
+    if (ensure(c->loc_grid, c->cap_loc_grid, cells * 4) != cudaSuccess) {
+      cudaGetLastError();
+      c->loc_grid = nullptr;
+    } else {
+      c->index_bytes += cells * 4;
+      CK(c, cudaMemsetAsync(c->loc_grid, 0xFF, cells * 4, s), "grid init");
+      begin_timed(c, 2, s, &tl);
+      CK(c, launch_loc_grid(c->locations, c->n_loc, c->surface, c->table, c->loc_grid, lo[0], lo[1], lo[2],
+                            c->dim[0], c->dim[1], s),
+         "loc_grid entries");
+      end_timed(c, s, &tl);
+    }
+  } else {
+    dfree(c->loc_grid);  // AABB too large for the dense grid: the hash-probe path
+    c->cap_loc_grid = 0;
+  }
+  GridRef gr{};
+  gr.grid = c->loc_grid;
+  for (int a = 0; a < 3; ++a) { gr.lo[a] = lo[a]; gr.dim[a] = c->dim[a]; }
   CK(c, cudaMemsetAsync(c->cell_dirs, 0x80, (size_t)cap * 512, s), "cell bytes init");
   begin_timed(c, 2, s, &tl);
   CK(c, launch_bricks(reinterpret_cast<const int4 *>(c->keys), n, c->table, cap - 1, c->sdf, c->weight, c->rgb,
-                      c->brick_a, c->brick_b, c->cell_dirs, nullptr, s),
+                      c->brick_a, c->brick_b, c->cell_dirs, nullptr, gr, s),
      "bricks");
   end_timed(c, s, &tl);
   begin_timed(c, 2, s, &tl);
@@ -427,15 +452,8 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
                           c->dim[1], s),
      "cell masks");
   end_timed(c, s, &tl);
-  // dense location grid when the AABB is small enough (<= 2^28 locations, 1 GiB); else the
-  // raycast resolves locations through the bitmaps and the hash table
-  if (cells > 0 && cells <= (size_t(1) << 28) && c->table_cap <= (size_t(1) << kGridEntryBits)) {
-    if (ensure(c->loc_grid, c->cap_loc_grid, cells * 4) != cudaSuccess) {
-      cudaGetLastError();
-      c->loc_grid = nullptr;
-    } else {
-      c->index_bytes += cells * 4;
-      CK(c, cudaMemsetAsync(c->loc_grid, 0xFF, cells * 4, s), "grid init");
+  if (c->loc_grid) {
+    {
       begin_timed(c, 2, s, &tl);
       CK(c, launch_loc_grid(c->locations, c->n_loc, c->surface, c->table, c->loc_grid, lo[0], lo[1], lo[2],
                             c->dim[0], c->dim[1], s),
@@ -450,9 +468,6 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
         cudaGetLastError();
       }
     }
-  } else {
-    dfree(c->loc_grid);  // AABB too large for the dense grid: the hash-probe path
-    c->cap_loc_grid = 0;
   }
   if (c->combined) {
     if (c->comb_entries != c->table_cap) {
@@ -1076,8 +1091,11 @@ static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_blk_old,
   begin_timed(c, 2, s, &tl, n_list > 0 ? 5 : 0);
   CK(c, launch_cell_init(c->loc_list, n_list, c->cell_dirs, s), "incremental cell init");
   CK(c, launch_inc_blocks(c->loc_list, n_list, c->table, c->blk_list, c->inc_ctr, s), "incremental blocks");
+  GridRef gr{};
+  gr.grid = c->loc_grid;
+  for (int a = 0; a < 3; ++a) { gr.lo[a] = c->lo[a]; gr.dim[a] = c->dim[a]; }
   CK(c, launch_bricks_counted(keys, 6 * n_list, c->inc_ctr + 1, c->table, mask, c->sdf, c->weight, c->rgb, c->brick_a,
-                              c->brick_b, c->cell_dirs, c->blk_list, s),
+                              c->brick_b, c->cell_dirs, c->blk_list, gr, s),
      "incremental bricks");
   CK(c, launch_cell_masks(c->loc_list, n_list, c->cell_dirs, c->cell_pos, c->surface, c->lo[0], c->lo[1], c->lo[2],
                           c->dim[0], c->dim[1], s),
@@ -1208,6 +1226,7 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   L.s = (double)c->params.voxel_size;
   L.tau = (double)c->params.truncation;
   L.inv_tau_f = (float)(1.0 / L.tau);
+  L.inv_s_f = (float)(1.0 / L.s);
   L.M = (int)std::ceil(4.0 * L.tau / L.s);
   L.step = 2.0 * L.tau / (double)L.M;
   L.cos_theta = std::cos((double)c->params.theta);
@@ -1250,6 +1269,7 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
     L.loc_list = c->loc_list;
     L.loc_ctr = c->inc_ctr;
     L.locations = c->locations;
+    L.grid = c->loc_grid;
     L.n_loc = reinterpret_cast<unsigned long long *>(c->scratch + 4);
     for (int a = 0; a < 3; ++a) { L.lo[a] = c->lo[a]; L.dim[a] = c->dim[a]; }
   }

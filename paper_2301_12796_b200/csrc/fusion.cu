@@ -137,10 +137,29 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(const __grid_constant__ Fuse
       const double tj = __dadd_rn(-p.tau, __dmul_rn((double)j, p.step));
       long long b[3];
 #pragma unroll
-      for (int a = 0; a < 3; ++a)
+      for (int a = 0; a < 3; ++a) {
+#if DTSDF_FUSE_PRETEST
+        // the voxel index floor((X + t n) / s) in fp32 where the fraction clears 0 and 1 by more
+        // than its fp32 error (relative 2^-24 per operand and operation, in voxel units); else fp64
+        const float g = ((float)X[a] + (float)tj * (float)n[a]) * p.inv_s_f;
+        const float fl = floorf(g), fr = g - fl;
+        const float m = 1e-4f + 5e-7f * (fabsf((float)X[a]) + (float)p.tau) * p.inv_s_f;
+        if (fr > m && fr < 1.0f - m) {
+          b[a] = floordiv8((long long)fl);
+          continue;
+        }
+#endif
         b[a] = floordiv8((long long)floor(__ddiv_rn(__dadd_rn(X[a], __dmul_rn(tj, n[a])), p.s)));
+      }
       if (b[0] == pb[0] && b[1] == pb[1] && b[2] == pb[2]) continue;
       pb[0] = b[0]; pb[1] = b[1]; pb[2] = b[2];
+      if (p.grid) {  // already allocated at the last commit: nothing to insert
+        const unsigned gx = (unsigned)(b[0] - p.lo[0]), gy = (unsigned)(b[1] - p.lo[1]), gz = (unsigned)(b[2] - p.lo[2]);
+        if (gx < (unsigned)p.dim[0] && gy < (unsigned)p.dim[1] && gz < (unsigned)p.dim[2]) {
+          const int gv = __ldg(&p.grid[((size_t)gz * p.dim[1] + gy) * p.dim[0] + gx]);
+          if (gv >= 0 && ((gv >> kGridEntryBits) >> D) & 1) continue;
+        }
+      }
       if (alloc_key(p, (int)b[0], (int)b[1], (int)b[2], D)) return;
     }
   }

@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
                                                          float4 *__restrict__ brick_a, float2 *__restrict__ brick_b,
                                                          unsigned int *__restrict__ cell_dirs32,
                                                          const int *__restrict__ list,
-                                                         const unsigned long long *__restrict__ count) {
+                                                         const unsigned long long *__restrict__ count,
+                                                         const GridRef gr) {
   __shared__ int nb[27];  // slot of neighbour (ox, oy, oz) in -1..1, index (ox+1) + 3 (oy+1) + 9 (oz+1)
   __shared__ int self_entry;
   __shared__ float st[kStage * kStage * kStage];
@@ -143,12 +144,9 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
   if (threadIdx.x < 27) {
     const int ox = (int)threadIdx.x % 3 - 1, oy = ((int)threadIdx.x / 3) % 3 - 1, oz = (int)threadIdx.x / 9 - 1;
     int src = (int)b;
-    if (ox | oy | oz) {
-      const int e = find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
-      src = (e >= 0) ? table[e].slot[k.w] : -1;
-    } else {
-      self_entry = find_entry(table, mask, pack_key(k.x, k.y, k.z));
-    }
+    const int e = gr.grid ? gr.entry(k.x + ox, k.y + oy, k.z + oz) : find_entry(table, mask, pack_key(k.x + ox, k.y + oy, k.z + oz));
+    if (ox | oy | oz) src = (e >= 0) ? table[e].slot[k.w] : -1;
+    else self_entry = e;
     nb[threadIdx.x] = src;
   }
   __syncthreads();
@@ -352,20 +350,20 @@ cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char 
 
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
-                          unsigned char *cell_dirs, const int *list, cudaStream_t s) {
+                          unsigned char *cell_dirs, const int *list, const GridRef &gr, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   k_bricks<<<(unsigned)n, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
-                                                reinterpret_cast<unsigned int *>(cell_dirs), list, nullptr);
+                                                reinterpret_cast<unsigned int *>(cell_dirs), list, nullptr, gr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsigned long long *count,
                                   const HashEntry *table, unsigned int mask, const float *sdf, const float *weight,
                                   const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
-                                  const int *list, cudaStream_t s) {
+                                  const int *list, const GridRef &gr, cudaStream_t s) {
   if (grid == 0) return cudaSuccess;
   k_bricks<<<(unsigned)grid, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
-                                                   reinterpret_cast<unsigned int *>(cell_dirs), list, count);
+                                                   reinterpret_cast<unsigned int *>(cell_dirs), list, count, gr);
   return cudaGetLastError();
 }
 
