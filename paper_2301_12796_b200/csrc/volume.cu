@@ -138,9 +138,13 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
   __shared__ int self_entry;
   __shared__ float st[kStage * kStage * kStage];
   __shared__ float sw[kRecVox];
-  if (count && blockIdx.x >= *count) return;  // CTA-uniform
-  const long long b = list ? (long long)list[blockIdx.x] : (long long)blockIdx.x;
+  __shared__ unsigned int sc[kRecVox];
+  // blocks: one per CTA (list null or uncounted), or a grid-stride loop over a device-counted list
+  const long long n_items = count ? (long long)*count : (long long)gridDim.x;
+  for (long long item = blockIdx.x; item < n_items; item += count ? gridDim.x : n_items) {
+  const long long b = list ? (long long)list[item] : item;
   const int4 k = keys[b];
+  __syncthreads();  // the previous item's readers of nb / st / sw / sc are done
   if (threadIdx.x < 27) {
     const int ox = (int)threadIdx.x % 3 - 1, oy = ((int)threadIdx.x / 3) % 3 - 1, oz = (int)threadIdx.x / 9 - 1;
     int src = (int)b;
@@ -155,13 +159,28 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     const int src = nb[e >> 9];
     return src < 0 ? -1 : (long long)src * kVoxPerBlock + (e & 511);
   };
-  for (int a = threadIdx.x; a < kStage * kStage * kStage; a += kBrickThreads) {
-    const long long r = rec_of(kSrc.stage[a]);
-    st[a] = r >= 0 ? sdf[r] : __int_as_float(0x7fc00000);  // NaN sdf = unallocated
+  // staging, unrolled so that each thread's loads are in flight together
+#pragma unroll
+  for (int kk = 0; kk < (kStage * kStage * kStage + kBrickThreads - 1) / kBrickThreads; ++kk) {
+    const int a = threadIdx.x + kk * kBrickThreads;
+    if (a < kStage * kStage * kStage) {
+      const long long r = rec_of(kSrc.stage[a]);
+      st[a] = r >= 0 ? __ldg(sdf + r) : __int_as_float(0x7fc00000);  // NaN sdf = unallocated
+    }
   }
-  for (int a = threadIdx.x; a < kRecVox; a += kBrickThreads) {
-    const long long r = rec_of(kSrc.rec[a]);
-    sw[a] = r >= 0 ? weight[r] : 0.0f;
+#pragma unroll
+  for (int kk = 0; kk < (kRecVox + kBrickThreads - 1) / kBrickThreads; ++kk) {
+    const int a = threadIdx.x + kk * kBrickThreads;
+    if (a < kRecVox) {
+      const long long r = rec_of(kSrc.rec[a]);
+      sw[a] = r >= 0 ? __ldg(weight + r) : 0.0f;
+      unsigned int col = 0;
+      if (r >= 0 && rgb != nullptr) {
+        const unsigned char *q = rgb + 3 * r;
+        col = (unsigned int)__ldg(q) | ((unsigned int)__ldg(q + 1) << 8) | ((unsigned int)__ldg(q + 2) << 16);
+      }
+      sc[a] = col;
+    }
   }
   __syncthreads();
   for (int a = threadIdx.x; a < kRecStride; a += kBrickThreads) {
@@ -169,18 +188,12 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
     float2 rb = make_float2(__int_as_float(0x7fc00000), 0.0f);
     if (a < kRecVox) {
       const int c = kSrc.rec_c[a];  // voxels 0..8: staged index
-      const long long r = rec_of(kSrc.rec[a]);
       ra.x = st[c];
       ra.y = sw[a];
       ra.z = st[c + 1] - st[c - 1];
       ra.w = st[c + kStage] - st[c - kStage];
       rb.x = st[c + kStage * kStage] - st[c - kStage * kStage];
-      unsigned int col = 0;
-      if (r >= 0 && rgb != nullptr) {
-        const unsigned char *q = rgb + 3 * r;
-        col = (unsigned int)q[0] | ((unsigned int)q[1] << 8) | ((unsigned int)q[2] << 16);
-      }
-      rb.y = __uint_as_float(col);
+      rb.y = __uint_as_float(sc[a]);
     }
     brick_a[b * kRecStride + a] = ra;
     brick_b[b * kRecStride + a] = rb;
@@ -189,7 +202,7 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
   // cell_byte): bit D when no corner is unallocated and some corner weight is > 0 (the evaluation
   // drops D otherwise); bit 7, "certainly positive", cleared when all corners are allocated and
   // one has sdf <= 0.  The location's bytes start at 0x80 (k_cell_init / the commit's memset).
-  if (cell_dirs32 == nullptr || self_entry < 0) return;
+  if (cell_dirs32 == nullptr || self_entry < 0) continue;  // CTA-uniform
   for (int l = threadIdx.x; l < kVoxPerBlock; l += kBrickThreads) {
     const int lx = l & 7, ly = (l >> 3) & 7, lz = l >> 6;
     bool absent = false, allpos = true, weighted = false;
@@ -201,10 +214,21 @@ __global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict
       allpos &= v > 0.0f;
       weighted |= sw[(lx + dx) + kRec * (ly + dy) + kRec * kRec * (lz + dz)] > 0.0f;
     }
-    unsigned int *w = cell_dirs32 + ((size_t)self_entry * kVoxPerBlock + l) / 4;
+    // the 4 cells of one 32-bit word sit in 4 consecutive lanes: combine their bits first, one
+    // atomic per word and only when it changes something
     const int sh = (l & 3) * 8;
-    if (!absent && weighted) atomicOr(w, (1u << k.w) << sh);
-    if (!absent && !allpos) atomicAnd(w, ~(0x80u << sh));
+    unsigned int orb = (!absent && weighted) ? (1u << k.w) << sh : 0u;
+    unsigned int andb = (!absent && !allpos) ? ~(0x80u << sh) : 0xffffffffu;
+    orb |= __shfl_xor_sync(0xffffffffu, orb, 1);
+    andb &= __shfl_xor_sync(0xffffffffu, andb, 1);
+    orb |= __shfl_xor_sync(0xffffffffu, orb, 2);
+    andb &= __shfl_xor_sync(0xffffffffu, andb, 2);
+    if ((l & 3) == 0) {
+      unsigned int *w = cell_dirs32 + ((size_t)self_entry * kVoxPerBlock + l) / 4;
+      if (orb) atomicOr(w, orb);
+      if (andb != 0xffffffffu) atomicAnd(w, andb);
+    }
+  }
   }
 }
 
@@ -362,7 +386,9 @@ cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsign
                                   const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
                                   const int *list, const GridRef &gr, cudaStream_t s) {
   if (grid == 0) return cudaSuccess;
-  k_bricks<<<(unsigned)grid, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
+  // a grid-stride loop over the counted list: the CTAs resident at once (6 of 256 per SM, 148 SMs)
+  const long long ctas = grid < 148LL * 6 ? grid : 148LL * 6;
+  k_bricks<<<(unsigned)ctas, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
                                                    reinterpret_cast<unsigned int *>(cell_dirs), list, count, gr);
   return cudaGetLastError();
 }
