@@ -329,7 +329,7 @@ struct GridRef {
     const unsigned x = (unsigned)(bx - lo[0]), y = (unsigned)(by - lo[1]), z = (unsigned)(bz - lo[2]);
     if (x >= (unsigned)dim[0] || y >= (unsigned)dim[1] || z >= (unsigned)dim[2]) return -1;
     const int gv = __ldg(&grid[((size_t)z * dim[1] + y) * dim[0] + x]);
-    return gv >= 0 ? (gv & ((1 << 24) - 1)) : -1;
+    return gv >= 0 ? (gv & kGridEntryMask) : -1;
   }
 };
 
