@@ -139,6 +139,8 @@ struct RenderLaunch {
   unsigned char *out_color;        // [n_views][rows][W][3] or null
   unsigned char *out_mask;         // [n_views][rows][W] or null
   unsigned long long *dbg_timeline;  // DTSDF_STATS builds only: per-pixel start/end/smid
+  long long *dbg_trace;              // DTSDF_STATS builds only: per-step trace of one ray (8 x int64 per step)
+  int dbg_trace_pix;                 // its pixel u | vrel << 16 in view 0, or -1
   int staged;                      // grid schedule: outputs leave via shared memory in whole tile rows
                                    // (mapped host outputs); 0: per-pixel stores
   int combined;                    // 1: march the combined TSDF (comb) instead of the six directions

@@ -35,6 +35,8 @@ struct TimedLaunch {
 
 #ifdef DTSDF_STATS
 extern "C" __attribute__((visibility("default"))) unsigned long long *dtsdf_debug_timeline = nullptr;
+extern "C" __attribute__((visibility("default"))) long long *dtsdf_debug_trace = nullptr;  // [32 lanes][128 steps][8]
+extern "C" __attribute__((visibility("default"))) int dtsdf_debug_trace_pix = -1;
 #endif
 
 struct dtsdf_ctx {
@@ -628,6 +630,8 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
     pl.out_color = color ? color + 3 * px : nullptr;
     pl.out_mask = mask ? mask + px : nullptr;
     pl.dbg_timeline = nullptr;
+    pl.dbg_trace = nullptr;
+    pl.dbg_trace_pix = -1;
 #ifdef DTSDF_ALWAYS_STAGED
     staged = true;
 #endif
@@ -651,6 +655,12 @@ static int render_impl(dtsdf_ctx *c, int32_t n_views, const float *poses, const 
       }
       pl.dbg_timeline = tl_buf;
       dtsdf_debug_timeline = tl_buf;
+      if (!dtsdf_debug_trace) {
+        cudaMalloc(&dtsdf_debug_trace, 32 * 128 * 8 * 8);
+        cudaMemset(dtsdf_debug_trace, 0, 32 * 128 * 8 * 8);
+      }
+      pl.dbg_trace = dtsdf_debug_trace;
+      pl.dbg_trace_pix = dtsdf_debug_trace_pix;
     }
 #endif
 

@@ -700,6 +700,12 @@ __device__ __forceinline__ SampleResult eval_comb(const VolumeView &V, const Com
 // bisecting, regula-falsi or shading -- all run the same sample-evaluation code together
 // ------------------------------------------------------------------------------------------
 enum : int { kMarch = 0, kBisect = 1, kIllinois = 2, kShade = 3 };
+#ifndef DTSDF_PF_TABLE
+#define DTSDF_PF_TABLE 0
+#endif
+#ifndef DTSDF_EMPTY_NEXT
+#define DTSDF_EMPTY_NEXT 1  // C1 -4.2 %, C2 -2.2 %, bit-identical (profiles/r3_sweep_empty_next.jsonl)
+#endif
 #ifndef DTSDF_LOOKAHEAD
 #define DTSDF_LOOKAHEAD 6  // with the block-offset addressing: C1 -1.9 %, C3 -0.9 %, C2 equal vs 8 (profiles/r1n_sweep_lookahead.jsonl)
 #endif
@@ -742,7 +748,7 @@ struct RayT {
   int ix, iy, iz;
   float frx, fry, frz;
 #ifdef DTSDF_STATS
-  int st_march, st_refine, st_skip, st_empty, st_jump, st_cpi;
+  int st_march, st_refine, st_skip, st_empty, st_jump, st_cpi, st_newblk, st_scan, st_loc;
   long long cy_adv, cy_march, cy_refine;
   unsigned long long g_start, g_end;
   unsigned smid;
@@ -804,18 +810,24 @@ struct RayT {
     it = side = 0;
     hit = false;
 #ifdef DTSDF_STATS
-    st_march = st_refine = st_skip = st_empty = st_jump = st_cpi = 0;
+    st_march = st_refine = st_skip = st_empty = st_jump = st_cpi = st_newblk = st_scan = st_loc = 0;
     cy_adv = cy_march = cy_refine = 0;
 #endif
   }
 
   __device__ __forceinline__ void locate(const VolumeView &V, const CombinedView &C, float tt) {
+#ifdef DTSDF_STATS
+    ++st_loc;
+#endif
     const float gx = fmaf(tt, rsx, g0x), gy = fmaf(tt, rsy, g0y), gz = fmaf(tt, rsz, g0z);
     const float flx = floorf(gx), fly = floorf(gy), flz = floorf(gz);
     frx = gx - flx; fry = gy - fly; frz = gz - flz;
     ix = ibx + (int)flx; iy = iby + (int)fly; iz = ibz + (int)flz;
     const int bx = ix >> 3, by = iy >> 3, bz = iz >> 3;
     if (bx != cur.bx || by != cur.by || bz != cur.bz) {
+#ifdef DTSDF_STATS
+      ++st_newblk;
+#endif
       cur.bx = bx; cur.by = by; cur.bz = bz;
       cur.present = 0;
       cur.entry = -1;
@@ -832,6 +844,11 @@ struct RayT {
         cur.surf = (gv >> 30) & 1;
         if (cur.occ) {
           cur.entry = gv & kGridEntryMask;
+#if DTSDF_PF_TABLE
+          // the entry's direction slots are read when a sample of this location is evaluated:
+          // start their trip to L1 now
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(&V.table[cur.entry]));
+#endif
 #if DTSDF_SLOTS_FROM_TABLE
           cur.present = (gv >> kGridEntryBits) & 63;  // the slots themselves are read when evaluated
 #else
@@ -987,6 +1004,16 @@ struct RayT {
             }
             const float kn = floorf(texit * V.inv_delta);
             k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);
+#if DTSDF_EMPTY_NEXT
+            // the landing point still in this empty block: the next iteration would only step on
+            // to k + 1 (locate's block test, here without the loop round)
+            if (cur.dist != 0 && k <= k1) {
+              const float tk = (float)k * V.delta;
+              const int jx = ibx + (int)floorf(fmaf(tk, rsx, g0x)), jy = iby + (int)floorf(fmaf(tk, rsy, g0y)),
+                        jz = ibz + (int)floorf(fmaf(tk, rsz, g0z));
+              if ((jx >> 3) == cur.bx && (jy >> 3) == cur.by && (jz >> 3) == cur.bz) ++k;
+            }
+#endif
           } else {
             ++k;
           }
@@ -1021,6 +1048,10 @@ struct RayT {
           // look ahead over the next lattice points of this location at once (independent
           // loads): in a run of certainly-positive points only the last one needs evaluating
           unsigned run = 1u;
+#ifdef DTSDF_STATS
+          ++st_scan;
+#endif
+
 #if DTSDF_LA_IDX
           // voxel offsets from the cursor block's corner: in the block <=> all three in [0, 8)
           const int ox = ibx - kBlock * cur.bx, oy = iby - kBlock * cur.by, oz = ibz - kBlock * cur.bz;
@@ -1310,8 +1341,30 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
 #ifdef DTSDF_STATS
     const long long c0 = clock64();
 #endif
+#ifdef DTSDF_STATS
+    // per-step trace of one ray: clock at step start, cycles of the step, of its advance, mode
+    // before | after << 8, k before, k after, new blocks located, lookahead scans
+    // (all 32 lanes of the warp tile whose origin is dbg_trace_pix, 128 steps each)
+    const int tu = p.dbg_trace_pix & 0xffff, tv = p.dbg_trace_pix >> 16;
+    const bool tr = p.dbg_trace && blockIdx.z == 0 && u - tu >= 0 && u - tu < 8 && vrel - tv >= 0 && vrel - tv < 4;
+    long long *tb = p.dbg_trace + (tr ? 8 * 128 * ((u - tu) + 8 * (vrel - tv)) : 0);
+    int n_tr = 0;
+    for (;;) {
+      const long long s0 = clock64(), a0 = ray.cy_adv;
+      const int m0 = ray.mode, k0 = ray.k, nb0 = ray.st_newblk, ns0 = ray.st_scan, nl0 = ray.st_loc;
+      const bool done = ray.step(p);
+      if (tr && n_tr < 127) {
+        long long *e = tb + 8 * n_tr++;
+        e[0] = s0; e[1] = clock64() - s0; e[2] = ray.cy_adv - a0; e[3] = m0 | (ray.mode << 8) | (ray.hit << 16);
+        e[4] = k0; e[5] = ray.k; e[6] = (ray.st_newblk - nb0) | ((long long)(ray.st_loc - nl0) << 16); e[7] = ray.st_scan - ns0;
+      }
+      if (done) break;
+    }
+    if (tr) tb[8 * n_tr] = -1;
+#else
     while (!ray.step(p)) {
     }
+#endif
     if (ray.hit) ray.shade(p);
 #ifdef DTSDF_STATS
     ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations

@@ -17,6 +17,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+# row strips holding the slowest warp tiles of a view (tools/isolate.py): launched alone, their
+# k_raycast time is the uncontended critical path
+STRIPS = {"C1": "64:72,224:232", "C2": "344:352,472:480"}
+
+
 def run_one(args):
     import numpy as np
     import torch
@@ -50,6 +55,25 @@ def run_one(args):
         kt = R.kernel_times()
         ms = kt["raycast_ms"] / kt["raycast_launches"]
         pre_ms = kt["range_ms"] / max(kt["range_launches"], 1)  # range pass + tile order
+        strips = {}
+        for sp in (STRIPS.get(name, "") if args.strips else "").split(","):
+            if not sp:
+                continue
+            r0, r1 = map(int, sp.split(":"))
+            so = R.render(poses, w.intrinsics, row0=r0, row1=r1)
+            for _ in range(3):
+                R.render_into(poses, w.intrinsics, so["depth"], so["normal"], so["color"], so["mask"], row0=r0, row1=r1)
+            torch.cuda.synchronize()
+            R.reset_kernel_times()
+            R.set_profiling(True)
+            for _ in range(20):
+                if not args.no_flush:
+                    flush.fill_(1.0)
+                R.render_into(poses, w.intrinsics, so["depth"], so["normal"], so["color"], so["mask"], row0=r0, row1=r1)
+            torch.cuda.synchronize()
+            R.set_profiling(False)
+            kt2 = R.kernel_times()
+            strips[sp] = round(kt2["raycast_ms"] / kt2["raycast_launches"], 4)
         st = {}
         if not args.no_parity:
             ora = oracle.OracleVolume(w.volume).render(w.poses[0], w.intrinsics)
@@ -62,6 +86,7 @@ def run_one(args):
                           "out_sha1": h.hexdigest()[:16],
                           "options": args.set,
                           "raycast_ms": round(ms, 4), "range_order_ms": round(pre_ms, 4),
+                          **({"strips_alone_ms": strips} if strips else {}),
                           "budget_used": st.get("budget_used"), "color_exact": st.get("color_exact"),
                           "depth_max": st.get("depth_max_err"), "hit_disagree": st.get("hit_disagree"),
                           "geom_bad": st.get("geom_out_of_tol")}), flush=True)
@@ -76,6 +101,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="keep L2 warm between launches (an upper bound)")
     ap.add_argument("--run", action="store_true")
+    ap.add_argument("--strips", action="store_true", help="also time the slow-tile row strips alone")
     ap.add_argument("--set", action="append", default=[], help="dtsdf_set_option for the --run process: opt=value")
     ap.add_argument("--name", default="")
     args = ap.parse_args()
@@ -107,7 +133,7 @@ def main():
             env = dict(os.environ, DTSDF_LIB=lib)
             cmd = [sys.executable, os.path.abspath(__file__), "--run", "--name", name, "--configs", args.configs,
                    "--reps", str(args.reps)] + (["--no-parity"] if args.no_parity or r > 0 else []) + \
-                  (["--no-flush"] if args.no_flush else []) + sum((["--set", o] for o in name_opts.get(name, [])), [])
+                  (["--no-flush"] if args.no_flush else []) + (["--strips"] if args.strips else []) + sum((["--set", o] for o in name_opts.get(name, [])), [])
             subprocess.run(cmd, env=env, check=True)
 
 
