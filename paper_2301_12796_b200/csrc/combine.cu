@@ -528,23 +528,52 @@ __device__ __forceinline__ int comb_slot_of(const CombineLaunch &p, int bx, int 
   return p.slot_of_entry[e];
 }
 
-// apron cell a (< kApronVox) -> (neighbour index 0..26, that neighbour's apron index)
-__device__ __forceinline__ void apron_src(int a, int *nbi, int *src) {
-  const int lx = a % kApron - 1, ly = (a / kApron) % kApron - 1, lz = a / (kApron * kApron) - 1;
-  const int ox = lx < 0 ? -1 : (lx >= kBlock ? 1 : 0), oy = ly < 0 ? -1 : (ly >= kBlock ? 1 : 0),
-            oz = lz < 0 ? -1 : (lz >= kBlock ? 1 : 0);
-  *nbi = (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1);
-  *src = CAPRON(lx - ox * kBlock, ly - oy * kBlock, lz - oz * kBlock);
-}
-
 constexpr int kFinishThreads = 256;
-constexpr int kApronPer = (kApronStride + kFinishThreads - 1) / kFinishThreads;      // 6
-constexpr int kRgbPer = (kRgbApronStride + kFinishThreads - 1) / kFinishThreads;     // 3
+constexpr int kApronBorder = kApronVox - kVoxPerBlock;                          // 819: voxels -1, 8, 9
+constexpr int kRgbFar = kRgbApronVox - kVoxPerBlock;                            // 217: voxels 8
+constexpr int kBorderPer = (kApronBorder + kFinishThreads - 1) / kFinishThreads;  // 4
+
+// The border of a combined brick, built at compile time (no index arithmetic in the kernel): for
+// each border voxel of the sdf apron its apron index, and the neighbour (0..26) and that
+// neighbour's apron index it is copied from; likewise for the colour brick's far faces.
+struct FinishTable {
+  unsigned short dst[kApronBorder];
+  unsigned int src[kApronBorder];   // nbi << 16 | source apron index
+  unsigned short rgb_dst[kRgbFar];
+  unsigned int rgb_src[kRgbFar];    // nbi << 16 | source colour index
+  constexpr FinishTable() : dst(), src(), rgb_dst(), rgb_src() {
+    int n = 0;
+    for (int a = 0; a < kApronVox; ++a) {
+      const int lx = a % kApron - 1, ly = (a / kApron) % kApron - 1, lz = a / (kApron * kApron) - 1;
+      const int ox = lx < 0 ? -1 : (lx >= kBlock ? 1 : 0), oy = ly < 0 ? -1 : (ly >= kBlock ? 1 : 0),
+                oz = lz < 0 ? -1 : (lz >= kBlock ? 1 : 0);
+      if (!(ox | oy | oz)) continue;
+      dst[n] = (unsigned short)a;
+      src[n] = ((unsigned)((ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)) << 16) |
+               (unsigned)(((lx - ox * kBlock) + 1) + kApron * ((ly - oy * kBlock) + 1) +
+                          kApron * kApron * ((lz - oz * kBlock) + 1));
+      ++n;
+    }
+    n = 0;
+    for (int a = 0; a < kRgbApronVox; ++a) {
+      const int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);
+      const int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
+      if (!(ox | oy | oz)) continue;
+      rgb_dst[n] = (unsigned short)a;
+      rgb_src[n] = ((unsigned)((ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)) << 16) |
+                   (unsigned)((lx - ox * kBlock) + kRgbApron * (ly - oy * kBlock) + kRgbApron * kRgbApron * (lz - oz * kBlock));
+      ++n;
+    }
+  }
+};
+__device__ const FinishTable kFin = FinishTable();
 
 // One CTA per combined slot: resolve the 26 neighbouring combined slots once, gather the apron
-// border (voxels -1, 8, 9 per axis) and the colour brick's far faces from them with all loads in
-// flight together, assemble the brick in shared memory, then write the exact skip masks of the
-// 512 base cells (bit set: no valid corner with sdf <= 0, R36) and the brick's surface flag.
+// border (voxels -1, 8, 9 per axis) and the colour brick's far faces from the neighbours'
+// interiors (k_combine wrote them) with all loads in flight together and write them -- only
+// border positions are written and only interiors read, so the slots' CTAs never race -- then the
+// exact skip masks of the 512 base cells from the brick assembled in shared memory (bit set: no
+// valid corner with sdf <= 0, R36) and the brick's surface flag.
 __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_constant__ CombineLaunch p) {
   __shared__ float s_c[kApronStride];
   __shared__ int s_nb[27];
@@ -557,49 +586,49 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
   }
   __syncthreads();
   const float *__restrict__ apin = p.apron;
-  float v[kApronPer];
-#pragma unroll
-  for (int k = 0; k < kApronPer; ++k) {
-    const int a = tid + k * kFinishThreads;
-    v[k] = CUDART_NAN_F;
-    if (a < kApronVox) {
-      int nbi, src;
-      apron_src(a, &nbi, &src);
-      const int ns = s_nb[nbi];
-      DTSDF_CHECK(ns < (int)gridDim.x && src >= 0 && src < kApronVox);
-      if (ns >= 0) v[k] = __ldg(apin + (size_t)ns * kApronStride + src);
-    }
-  }
-  uchar4 cv[kRgbPer];
-#pragma unroll
-  for (int k = 0; k < kRgbPer; ++k) {
-    const int a = tid + k * kFinishThreads;
-    cv[k] = make_uchar4(0, 0, 0, 0);
-    if (a < kRgbApronVox) {
-      const int lx = a % kRgbApron, ly = (a / kRgbApron) % kRgbApron, lz = a / (kRgbApron * kRgbApron);
-      const int ox = lx >= kBlock, oy = ly >= kBlock, oz = lz >= kBlock;
-      const int ns = s_nb[(ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)];
-      if (ns >= 0)
-        cv[k] = __ldg(p.rgb + (size_t)ns * kRgbApronStride + (lx - ox * kBlock) + kRgbApron * (ly - oy * kBlock) +
-                      kRgbApron * kRgbApron * (lz - oz * kBlock));
-    }
-  }
-  __syncthreads();  // every read of this slot's interior (by this CTA) is done before any write
   float *ap = p.apron + slot * kApronStride;
+  float vi[2];  // own interior
 #pragma unroll
-  for (int k = 0; k < kApronPer; ++k) {
-    const int a = tid + k * kFinishThreads;
-    if (a < kApronStride) {
-      s_c[a] = v[k];
-      ap[a] = v[k];
+  for (int h = 0; h < 2; ++h) {
+    const int l = tid + h * kFinishThreads;
+    vi[h] = __ldg(apin + slot * kApronStride + CAPRON(l & 7, (l >> 3) & 7, l >> 6));
+  }
+  float v[kBorderPer];
+  int dst[kBorderPer];
+#pragma unroll
+  for (int k = 0; k < kBorderPer; ++k) {
+    const int e = tid + k * kFinishThreads;
+    v[k] = CUDART_NAN_F;
+    dst[k] = -1;
+    if (e < kApronBorder) {
+      const unsigned int sr = __ldg(&kFin.src[e]);
+      dst[k] = __ldg(&kFin.dst[e]);
+      const int ns = s_nb[sr >> 16];
+      DTSDF_CHECK(ns < (int)gridDim.x);
+      if (ns >= 0) v[k] = __ldg(apin + (size_t)ns * kApronStride + (sr & 0xffffu));
     }
   }
-  uchar4 *cp = p.rgb + slot * kRgbApronStride;
-#pragma unroll
-  for (int k = 0; k < kRgbPer; ++k) {
-    const int a = tid + k * kFinishThreads;
-    if (a < kRgbApronStride) cp[a] = cv[k];
+  uchar4 cv = make_uchar4(0, 0, 0, 0);
+  int rdst = -1;
+  if (tid < kRgbFar) {
+    const unsigned int sr = __ldg(&kFin.rgb_src[tid]);
+    rdst = __ldg(&kFin.rgb_dst[tid]);
+    const int ns = s_nb[sr >> 16];
+    if (ns >= 0) cv = __ldg(p.rgb + (size_t)ns * kRgbApronStride + (sr & 0xffffu));
   }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int l = tid + h * kFinishThreads;
+    s_c[CAPRON(l & 7, (l >> 3) & 7, l >> 6)] = vi[h];
+  }
+#pragma unroll
+  for (int k = 0; k < kBorderPer; ++k) {
+    if (dst[k] >= 0) {
+      s_c[dst[k]] = v[k];
+      ap[dst[k]] = v[k];
+    }
+  }
+  if (rdst >= 0) p.rgb[slot * kRgbApronStride + rdst] = cv;
   __syncthreads();
   int any_neg = 0;
 #pragma unroll

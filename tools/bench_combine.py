@@ -35,5 +35,13 @@ for _ in range(a.reps):
 torch.cuda.synchronize()
 R.set_profiling(False)
 kt = R.kernel_times()
-print(json.dumps({"config": a.config, "mode": a.mode, "combine_ms": kt["combine_ms"] / a.reps,
+# checksum of the combined TSDF in location order (the slot order depends on an atomic counter)
+import hashlib  # noqa: E402
+g = R.get_combined()
+locs = np.asarray(g["locs"]).reshape(-1, 3)
+order = np.lexsort((locs[:, 2], locs[:, 1], locs[:, 0]))
+h = hashlib.sha1(locs[order].tobytes())
+for k in ("sdf", "weight", "rgb", "mask"):
+    h.update(np.ascontiguousarray(np.asarray(g[k])[order]).tobytes())
+print(json.dumps({"config": a.config, "mode": a.mode, "combine_ms": kt["combine_ms"] / a.reps, "sha1": h.hexdigest()[:16],
                   "locations": R.combined_stats()["n_locations"], "l2": "flushed (256 MiB write) before each combine"}))
