@@ -247,10 +247,10 @@ __global__ void __launch_bounds__(256) k_fuse_select(const __grid_constant__ Fus
   list[atomicAdd(count, 1ull)] = (int)b;
 }
 
-__global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch p, const int *list,
-                                              const unsigned long long *count) {
-  if (list && blockIdx.x >= *count) return;  // CTA-uniform
-  const long long b = list ? (long long)list[blockIdx.x] : (long long)blockIdx.x;
+#ifndef DTSDF_FUSE_MINB
+#define DTSDF_FUSE_MINB 8  // 32 registers, full occupancy: fused frame kernels 0.348 -> 0.285 ms (profiles/r3_ab_fusion.txt)
+#endif
+__device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
   const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
   const int D = key.w;
   const int axis = D >> 1;
@@ -430,6 +430,13 @@ __global__ void __launch_bounds__(256) k_fuse(const __grid_constant__ FuseLaunch
     if (e >= 0 && p.table[e].slot[D] >= 0 && atomicCAS(&p.loc_mark[e], 0, 1) == 0)
       p.loc_list[atomicAdd(p.loc_ctr, 1ull)] = make_int4(key.x + ox, key.y + oy, key.z + oz, e);
   }
+}
+
+// One CTA per selected block
+__global__ void __launch_bounds__(256, DTSDF_FUSE_MINB) k_fuse(const __grid_constant__ FuseLaunch p, const int *list,
+                                                               const unsigned long long *count) {
+  if (list && blockIdx.x >= *count) return;  // CTA-uniform
+  fuse_block(p, list ? (long long)list[blockIdx.x] : (long long)blockIdx.x);
 }
 
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s) {

@@ -126,7 +126,13 @@ struct SrcTable {
   }
 };
 __device__ const SrcTable kSrc = SrcTable();
-__global__ void __launch_bounds__(kBrickThreads) k_bricks(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
+#ifndef DTSDF_BRICK_MINB
+#define DTSDF_BRICK_MINB 8  // 32 registers, 8 CTAs per SM: fused frame kernels -17 % (profiles/r3_ab_fusion.txt)
+#endif
+#ifndef DTSDF_BRICK_RES
+#define DTSDF_BRICK_RES 8
+#endif
+__global__ void __launch_bounds__(kBrickThreads, DTSDF_BRICK_MINB) k_bricks(const int4 *__restrict__ keys, const HashEntry *__restrict__ table,
                                                          unsigned int mask, const float *__restrict__ sdf,
                                                          const float *__restrict__ weight, const unsigned char *__restrict__ rgb,
                                                          float4 *__restrict__ brick_a, float2 *__restrict__ brick_b,
@@ -386,8 +392,8 @@ cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsign
                                   const unsigned char *rgb, float4 *brick_a, float2 *brick_b, unsigned char *cell_dirs,
                                   const int *list, const GridRef &gr, cudaStream_t s) {
   if (grid == 0) return cudaSuccess;
-  // a grid-stride loop over the counted list: the CTAs resident at once (6 of 256 per SM, 148 SMs)
-  const long long ctas = grid < 148LL * 6 ? grid : 148LL * 6;
+  // a grid-stride loop over the counted list: the CTAs resident at once (8 of 256 per SM, 148 SMs)
+  const long long ctas = grid < 148LL * DTSDF_BRICK_RES ? grid : 148LL * DTSDF_BRICK_RES;
   k_bricks<<<(unsigned)ctas, kBrickThreads, 0, s>>>(keys, table, mask, sdf, weight, rgb, brick_a, brick_b,
                                                    reinterpret_cast<unsigned int *>(cell_dirs), list, count, gr);
   return cudaGetLastError();
