@@ -241,7 +241,7 @@ struct FuseLaunch {
   const int *grid;                 // the committed location grid (null: none): existing (location, D)
                                    // keys are recognised with one load, without a hash probe
   unsigned char *dirty;
-  // per-pixel world-rotated back-projection R P and world normal R n of the frame (k_frame_points,
+  // per-pixel world-rotated back-projection R P and world normal R n of the frame (k_fuse_alloc,
   // once per frame instead of once per associated voxel; null: k_fuse computes them)
   double4 *pix_x, *pix_n;
   // the same in fp32 for k_fuse's pre-test: pix_a (R P, z or -1 when the pixel holds no usable
@@ -289,7 +289,6 @@ cudaError_t launch_icp_solve(const IcpLaunch &p, cudaStream_t s);
 // host launchers (fusion.cu)
 cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float *out, cudaStream_t s);
 cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s);
-cudaError_t launch_frame_points(const FuseLaunch &p, cudaStream_t s);  // fills p.pix_x, p.pix_n
 // new blocks initialised; then (fuse) the frame fused into the blocks -- with list / count (count
 // zeroed beforehand) only those k_fuse_select finds in the frame's view
 cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, bool fuse, int *list,

@@ -61,7 +61,7 @@ struct dtsdf_ctx {
   int64_t cap = 0;            // pool capacity in blocks (>= n; fusion grows n up to it)
   float *cweight = nullptr;   // fusion: colour weights [cap][512] (eq:color_weight accumulator)
   void *fuse_stage = nullptr; // fusion / ICP: device staging of host frames
-  double4 *pix_buf = nullptr;  // fusion: per-pixel world points + normals of the frame (k_frame_points)
+  double4 *pix_buf = nullptr;  // fusion: per-pixel world points + normals of the frame (k_fuse_alloc)
   size_t cap_pix_buf = 0;
   double *icp_partials = nullptr;
   IcpState *icp_state = nullptr;
@@ -1301,9 +1301,8 @@ int dtsdf_fuse(dtsdf_ctx *c, const float *depth, const float *normal, const uint
   L.pix_a = reinterpret_cast<float4 *>(c->pix_buf + 2 * px);
   L.pix_b = L.pix_a + px;
   TimedLaunch tl{};
-  begin_timed(c, 2, s, &tl, 2);
-  CK(c, launch_frame_points(L, s), "frame points");
-  CK(c, launch_fuse_alloc(L, s), "fuse alloc");
+  begin_timed(c, 2, s, &tl, 1);
+  CK(c, launch_fuse_alloc(L, s), "fuse alloc");  // (with the frame points)
   end_timed(c, s, &tl);
   int host[14];
   CK(c, cudaMemcpyAsync(host, c->scratch, sizeof(host), cudaMemcpyDeviceToHost, s), "fuse readback");

@@ -116,19 +116,45 @@ __device__ int alloc_key(const FuseLaunch &p, int bx, int by, int bz, int D) {
   return 1;
 }
 
+// Per pixel of the frame: first its frame point (when p.pix_x is set) -- R P (the back-projected
+// depth point rotated into the world, relative to the camera centre), R n (the world normal) and
+// the carving guard, with the operations k_fuse would apply per voxel, once per frame -- then the
+// allocation of the blocks around the depth point in every admitted direction (R40).
 __global__ void __launch_bounds__(256) k_fuse_alloc(const __grid_constant__ FuseLaunch p) {
   const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
   if (u >= p.width || v >= p.height) return;
   const size_t i = (size_t)v * p.width + u;
   const float z = p.depth[i];
   const float n0 = p.normal[3 * i], n1 = p.normal[3 * i + 1], n2 = p.normal[3 * i + 2];
-  if (!depth_ok(p, z) || (n0 == 0.f && n1 == 0.f && n2 == 0.f)) return;
-  double P[3], X[3], nc[3] = {n0, n1, n2}, n[3];
-  backproject(p, u, v, (double)z, P);
-  rotate(p, P, X);
+  double P[3], X[3] = {0, 0, 0}, nc[3] = {n0, n1, n2}, n[3] = {0, 0, 0};
+  const bool zok = depth_ok(p, z);
+  if (zok) {
+    backproject(p, u, v, (double)z, P);
+    rotate(p, P, X);
+    rotate(p, nc, n);
+  }
+  if (p.pix_x) {
+    bool edge = false;
+    if (zok) {
+      // R43's carving guard of this pixel: a valid depth within carve_radius differing by more than tau
+      for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
+        for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
+          const int qu = u + du, qv = v + dv;
+          if (qu < 0 || qv < 0 || qu >= p.width || qv >= p.height) continue;
+          const float zq = p.depth[(size_t)qv * p.width + qu];
+          if (!depth_ok(p, zq)) continue;
+          if (fabs((double)zq - (double)z) > p.tau) { edge = true; break; }
+        }
+    }
+    p.pix_x[i] = make_double4(X[0], X[1], X[2], edge ? 1.0 : 0.0);
+    p.pix_n[i] = make_double4(n[0], n[1], n[2], 0.0);
+    const bool usable = zok && !(nc[0] == 0.0 && nc[1] == 0.0 && nc[2] == 0.0);
+    p.pix_a[i] = make_float4((float)X[0], (float)X[1], (float)X[2], usable ? z : -1.0f);
+    p.pix_b[i] = make_float4((float)n[0], (float)n[1], (float)n[2], edge ? 1.0f : 0.0f);
+  }
+  if (!zok || (n0 == 0.f && n1 == 0.f && n2 == 0.f)) return;
 #pragma unroll
   for (int a = 0; a < 3; ++a) X[a] = __dadd_rn(X[a], p.t[a]);
-  rotate(p, nc, n);
   for (int D = 0; D < 6; ++D) {
     const double dot = (D & 1) ? -n[D >> 1] : n[D >> 1];
     if (!(dot > p.cos_theta)) continue;
@@ -165,36 +191,6 @@ __global__ void __launch_bounds__(256) k_fuse_alloc(const __grid_constant__ Fuse
   }
 }
 
-// Per pixel of the frame: R P (the back-projected depth point rotated into the world, relative to
-// the camera centre) and R n (the world normal), with the operations k_fuse would apply per voxel.
-__global__ void __launch_bounds__(256) k_frame_points(const __grid_constant__ FuseLaunch p) {
-  const int u = blockIdx.x * 16 + (threadIdx.x & 15), v = blockIdx.y * 16 + (threadIdx.x >> 4);
-  if (u >= p.width || v >= p.height) return;
-  const size_t i = (size_t)v * p.width + u;
-  const float z = p.depth[i];
-  double P[3], X[3] = {0, 0, 0}, nc[3] = {p.normal[3 * i], p.normal[3 * i + 1], p.normal[3 * i + 2]}, n[3] = {0, 0, 0};
-  bool edge = false;
-  if (depth_ok(p, z)) {
-    backproject(p, u, v, (double)z, P);
-    rotate(p, P, X);
-    rotate(p, nc, n);
-    // R43's carving guard of this pixel: a valid depth within carve_radius differing by more than tau
-    for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
-      for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
-        const int qu = u + du, qv = v + dv;
-        if (qu < 0 || qv < 0 || qu >= p.width || qv >= p.height) continue;
-        const float zq = p.depth[(size_t)qv * p.width + qu];
-        if (!depth_ok(p, zq)) continue;
-        if (fabs((double)zq - (double)z) > p.tau) { edge = true; break; }
-      }
-  }
-  p.pix_x[i] = make_double4(X[0], X[1], X[2], edge ? 1.0 : 0.0);
-  p.pix_n[i] = make_double4(n[0], n[1], n[2], 0.0);
-  const bool usable = depth_ok(p, z) && !(nc[0] == 0.0 && nc[1] == 0.0 && nc[2] == 0.0);
-  p.pix_a[i] = make_float4((float)X[0], (float)X[1], (float)X[2], usable ? z : -1.0f);
-  p.pix_b[i] = make_float4((float)n[0], (float)n[1], (float)n[2], edge ? 1.0f : 0.0f);
-}
-
 __global__ void __launch_bounds__(256) k_fuse_init(FuseLaunch p, long long n0, long long n1) {
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long b = n0 + (g >> 9);
@@ -222,10 +218,10 @@ __device__ __forceinline__ float w_dir_f(float c, const FuseLaunch &p) {
 // voxel is associated and the block is left out (exact).  Selected blocks go to list / *count.
 __global__ void __launch_bounds__(256) k_fuse_select(const __grid_constant__ FuseLaunch p, long long n, int *list,
                                                      unsigned long long *count) {
-  const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (b >= n) return;  // warp-uniform
-  const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
+  // four blocks per warp, eight lanes (the corners) each
+  const long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 3;
+  const int lane = threadIdx.x & 31, grp = lane & ~7;
+  const int4 key = reinterpret_cast<const int4 *>(p.keys)[b < n ? b : n - 1];
   const int q = lane & 7;
   const int i = kBlock * key.x + ((q & 1) ? kBlock - 1 : 0), j = kBlock * key.y + ((q & 2) ? kBlock - 1 : 0),
             k = kBlock * key.z + ((q & 4) ? kBlock - 1 : 0);
@@ -242,14 +238,22 @@ __global__ void __launch_bounds__(256) k_fuse_select(const __grid_constant__ Fus
   g[4] = ((double)p.height - 0.5 - p.cy) * zc - p.fy * yc;      // v < H - 1/2
   bool out = false;
 #pragma unroll
-  for (int c = 0; c < 5; ++c) out |= (__ballot_sync(0xffffffffu, g[c] < -tol) & 0xffu) == 0xffu;
-  if (out || lane != 0) return;
+  for (int c = 0; c < 5; ++c) out |= ((__ballot_sync(0xffffffffu, g[c] < -tol) >> grp) & 0xffu) == 0xffu;
+  if (out || b >= n || lane != grp) return;
   list[atomicAdd(count, 1ull)] = (int)b;
 }
 
 #ifndef DTSDF_FUSE_MINB
 #define DTSDF_FUSE_MINB 8  // 32 registers, full occupancy: fused frame kernels 0.348 -> 0.285 ms (profiles/r3_ab_fusion.txt)
 #endif
+// store v over old only if its bits differ; true when stored.  A block whose stored values did not
+// change keeps its record bricks (and its neighbours'): the incremental index update skips it.
+__device__ __forceinline__ bool store_changed(float *a, float old, float v) {
+  if (__float_as_uint(old) == __float_as_uint(v)) return false;
+  *a = v;
+  return true;
+}
+
 __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
   const int4 key = reinterpret_cast<const int4 *>(p.keys)[b];
   const int D = key.w;
@@ -326,10 +330,9 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
       if (df > 1.0f + m) {           // R43 free space
         if (!(p.carve_weight > 0.f) || pb.w != 0.0f) continue;
         const size_t r = (size_t)b * kVoxPerBlock + l;
-        const float W0 = p.weight[r];
-        p.sdf[r] = (W0 * p.sdf[r] + p.carve_weight) / (W0 + p.carve_weight);
-        p.weight[r] = fminf(W0 + p.carve_weight, p.max_weight);
-        wrote = true;
+        const float W0 = p.weight[r], S0 = p.sdf[r];
+        wrote |= store_changed(p.sdf + r, S0, (W0 * S0 + p.carve_weight) / (W0 + p.carve_weight));
+        wrote |= store_changed(p.weight + r, W0, fminf(W0 + p.carve_weight, p.max_weight));
         continue;
       }
     }
@@ -341,7 +344,7 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
     // surfaces (a voxel tau from a floor at z = 0), so d is formed in fp64 with the oracle's
     // operation order -- both sides take the same decision
     double X[3], nd[3];
-    if (p.pix_x) {  // the frame's per-pixel values, computed once by k_frame_points (same operations)
+    if (p.pix_x) {  // the frame's per-pixel values, computed once by k_fuse_alloc (same operations)
       const double4 xx = p.pix_x[pi], nn = p.pix_n[pi];
       X[0] = xx.x; X[1] = xx.y; X[2] = xx.z;
       nd[0] = nn.x; nd[1] = nn.y; nd[2] = nn.z;
@@ -369,7 +372,7 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
       // carve_weight 0 turns carving off (on a fresh voxel, W0 = 0, the update would be 0/0)
       if (!(p.carve_weight > 0.f)) continue;
       bool edge = false;
-      if (p.pix_x) edge = p.pix_x[pi].w != 0.0;  // the pixel's guard, once per frame (k_frame_points)
+      if (p.pix_x) edge = p.pix_x[pi].w != 0.0;  // the pixel's guard, once per frame (k_fuse_alloc)
       else
       for (int dv = -p.carve_radius; dv <= p.carve_radius && !edge; ++dv)
         for (int du = -p.carve_radius; du <= p.carve_radius; ++du) {
@@ -380,10 +383,9 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
           if (fabs((double)zq - (double)z) > p.tau) { edge = true; break; }
         }
       if (edge) continue;
-      const float W0 = p.weight[r];
-      p.sdf[r] = (W0 * p.sdf[r] + p.carve_weight) / (W0 + p.carve_weight);
-      p.weight[r] = fminf(W0 + p.carve_weight, p.max_weight);
-      wrote = true;
+      const float W0 = p.weight[r], S0 = p.sdf[r];
+      wrote |= store_changed(p.sdf + r, S0, (W0 * S0 + p.carve_weight) / (W0 + p.carve_weight));
+      wrote |= store_changed(p.weight + r, W0, fminf(W0 + p.carve_weight, p.max_weight));
       continue;
     }
     const float wdir = w_dir_f(sgnD * (axis == 0 ? nx : (axis == 1 ? ny : nz)), p);
@@ -393,10 +395,9 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
     const float zz = z + (1.0f - (float)p.z_min);
     const float wn = (1.0f / (zz * zz)) * fmaxf(ca, 0.0f) * wdir;  // w_ICP(z) w_angle w_dir
     if (!(wn > 0.0f)) continue;
-    const float W0 = p.weight[r];
-    p.sdf[r] = (W0 * p.sdf[r] + wn * dd) / (W0 + wn);
-    p.weight[r] = fminf(W0 + wn, p.max_weight);
-    wrote = true;
+    const float W0 = p.weight[r], S0 = p.sdf[r];
+    wrote |= store_changed(p.sdf + r, S0, (W0 * S0 + wn * dd) / (W0 + wn));
+    wrote |= store_changed(p.weight + r, W0, fminf(W0 + wn, p.max_weight));
     if (p.color) {
       const float dist = (float)sqrt(ex * ex + ey * ey + ez * ez);
       const float wc = wn * (1.0f - fminf(1.0f, dist / tau));  // eq:color_weight
@@ -404,10 +405,16 @@ __device__ __forceinline__ void fuse_block(const FuseLaunch &p, long long b) {
         const float C0 = p.cweight[r];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          const float c = (C0 * (float)p.rgb[3 * r + a] + wc * (float)p.color[3 * pi + a]) / (C0 + wc);
-          p.rgb[3 * r + a] = (unsigned char)fminf(fmaxf(floorf(c + 0.5f), 0.f), 255.f);
+          const unsigned char q0 = p.rgb[3 * r + a];
+          const float c = (C0 * (float)q0 + wc * (float)p.color[3 * pi + a]) / (C0 + wc);
+          const unsigned char q1 = (unsigned char)fminf(fmaxf(floorf(c + 0.5f), 0.f), 255.f);
+          if (q1 != q0) {
+            p.rgb[3 * r + a] = q1;
+            wrote = true;
+          }
         }
-        p.cweight[r] = fminf(C0 + wc, p.max_weight);
+        // (the colour weight is not read by the index: no rebuild for it alone)
+        store_changed(p.cweight + r, C0, fminf(C0 + wc, p.max_weight));
       }
     }
   }
@@ -445,12 +452,6 @@ cudaError_t launch_depth_normals(const float *depth, const FuseLaunch &p, float 
   return cudaGetLastError();
 }
 
-cudaError_t launch_frame_points(const FuseLaunch &p, cudaStream_t s) {
-  dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
-  k_frame_points<<<grid, 256, 0, s>>>(p);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_fuse_alloc(const FuseLaunch &p, cudaStream_t s) {
   dim3 grid((unsigned)((p.width + 15) / 16), (unsigned)((p.height + 15) / 16));
   k_fuse_alloc<<<grid, 256, 0, s>>>(p);
@@ -466,7 +467,7 @@ cudaError_t launch_fuse(const FuseLaunch &p, long long n_old, long long n_new, b
   }
   if (n_new == 0 || !fuse) return cudaSuccess;
   if (list) {  // only the blocks with a voxel in the frame's view (count zeroed by the caller)
-    k_fuse_select<<<(unsigned)((n_new * 32 + 255) / 256), 256, 0, s>>>(p, n_new, list, count);
+    k_fuse_select<<<(unsigned)((n_new * 8 + 255) / 256), 256, 0, s>>>(p, n_new, list, count);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
