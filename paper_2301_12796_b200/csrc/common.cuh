@@ -318,7 +318,8 @@ cudaError_t launch_insert(const int4 *keys, long long n, HashEntry *table, unsig
 cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *bitmap, int lo_x, int lo_y, int lo_z,
                           int dim_x, int dim_y, cudaStream_t s);
 cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, const HashEntry *table,
-                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s);
+                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s,
+                            const unsigned long long *count = nullptr);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
 // The dense location grid as a lookup for index-build kernels: hash entry of a block location, or
@@ -339,7 +340,9 @@ struct GridRef {
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
                           unsigned char *cell_dirs, const int *list, const GridRef &gr, cudaStream_t s);
-cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s);
+// (count non-null, here and below: the item count is *count, read on the device, n an upper bound)
+cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s,
+                             const unsigned long long *count = nullptr);
 // incremental commit after a fused frame: the locations whose record bricks must be rebuilt (the
 // 27-neighbourhoods, in the dirty block's direction, of every dirty block) -> loc_list (deduplicated
 // by loc_mark[entry]), then all blocks of those locations -> blk_list; counters ctr[0], ctr[1]
@@ -347,9 +350,11 @@ cudaError_t launch_inc_mark(const int4 *keys, long long b0, long long n, const u
                             const HashEntry *table,
                             unsigned int mask, const int *grid, const int lo[3], const int dim[3], int *loc_mark,
                             int4 *loc_list, unsigned long long *ctr, cudaStream_t s);
+// (the location count is read from ctr[0] on the device; n an upper bound)
 cudaError_t launch_inc_blocks(const int4 *loc_list, long long n, const HashEntry *table, int *blk_list,
                               unsigned long long *ctr, cudaStream_t s);
-cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s);
+cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s,
+                              const unsigned long long *count = nullptr);
 // k_bricks over a device-counted list: grid = an upper bound, CTAs at or beyond *count return
 cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsigned long long *count,
                                   const HashEntry *table, unsigned int mask, const float *sdf, const float *weight,
@@ -357,7 +362,7 @@ cudaError_t launch_bricks_counted(const int4 *keys, long long grid, const unsign
                                   const int *list, const GridRef &gr, cudaStream_t s);
 cudaError_t launch_cell_masks(const int4 *locations, long long n, const unsigned char *cell_dirs, unsigned int *cell_pos,
                               unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y,
-                              cudaStream_t s);
+                              cudaStream_t s, const unsigned long long *count = nullptr);
 // rgb packed into a float's bits for the B records (r | g << 8 | b << 16)
 __host__ __device__ __forceinline__ unsigned int rec_rgb(float bits) {
 #ifdef __CUDA_ARCH__

@@ -1094,12 +1094,12 @@ static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_blk_old,
                         c->loc_list, c->inc_ctr, s),
      "incremental mark");
   end_timed(c, s, &tl);
-  unsigned long long nl = 0;
-  CK(c, cudaMemcpyAsync(&nl, c->inc_ctr, 8, cudaMemcpyDeviceToHost, s), "incremental readback");
-  CK(c, cudaStreamSynchronize(s), "incremental sync");
-  const long long n_list = (long long)nl;
-  begin_timed(c, 2, s, &tl, n_list > 0 ? 5 : 0);
-  CK(c, launch_cell_init(c->loc_list, n_list, c->cell_dirs, s), "incremental cell init");
+  // the listed locations are counted on the device (inc_ctr[0]); the kernels below read the count
+  // themselves (n_list: its upper bound, every location of the table), so the host does not wait
+  const unsigned long long *cnt = c->inc_ctr;
+  const long long n_list = (long long)c->table_cap;
+  begin_timed(c, 2, s, &tl, 5);
+  CK(c, launch_cell_init(c->loc_list, n_list, c->cell_dirs, s, cnt), "incremental cell init");
   CK(c, launch_inc_blocks(c->loc_list, n_list, c->table, c->blk_list, c->inc_ctr, s), "incremental blocks");
   GridRef gr{};
   gr.grid = c->loc_grid;
@@ -1108,10 +1108,10 @@ static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_blk_old,
                               c->brick_b, c->cell_dirs, c->blk_list, gr, s),
      "incremental bricks");
   CK(c, launch_cell_masks(c->loc_list, n_list, c->cell_dirs, c->cell_pos, c->surface, c->lo[0], c->lo[1], c->lo[2],
-                          c->dim[0], c->dim[1], s),
+                          c->dim[0], c->dim[1], s, cnt),
      "incremental cell masks");
   CK(c, launch_loc_grid(c->loc_list, n_list, c->surface, c->table, c->loc_grid, c->lo[0], c->lo[1], c->lo[2],
-                        c->dim[0], c->dim[1], s),
+                        c->dim[0], c->dim[1], s, cnt),
      "incremental grid");
   end_timed(c, s, &tl);
   if (n_loc_new > n_loc_old) {
@@ -1128,8 +1128,8 @@ static int recommit_incremental(dtsdf_ctx *c, cudaStream_t s, int64_t n_blk_old,
       end_timed(c, s, &tl);
     }
   }
-  begin_timed(c, 2, s, &tl, n_list > 0 ? 1 : 0);
-  CK(c, launch_inc_unmark(c->loc_list, n_list, c->loc_mark, s), "incremental unmark");
+  begin_timed(c, 2, s, &tl, 1);
+  CK(c, launch_inc_unmark(c->loc_list, n_list, c->loc_mark, s, cnt), "incremental unmark");
   end_timed(c, s, &tl);
   CK(c, cudaStreamSynchronize(s), "incremental sync");
   c->n_loc = n_loc_new;

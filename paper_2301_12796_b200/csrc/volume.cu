@@ -240,11 +240,12 @@ __global__ void __launch_bounds__(kBrickThreads, DTSDF_BRICK_MINB) k_bricks(cons
 
 // The live-direction bytes of the listed locations' entries set to 0x80 (no direction live,
 // certainly positive) before their bricks are rebuilt (incremental commit).
-__global__ void k_cell_init(const int4 *__restrict__ loc, long long n, unsigned int *cell_dirs32) {
-  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long i = g >> 7;
-  if (i >= n) return;
-  cell_dirs32[(size_t)loc[i].w * (kVoxPerBlock / 4) + (g & 127)] = 0x80808080u;
+// (count non-null: the number of listed locations is *count, read on the device; grid-stride)
+__global__ void k_cell_init(const int4 *__restrict__ loc, long long n, unsigned int *cell_dirs32,
+                            const unsigned long long *count) {
+  if (count) n = (long long)*count;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < n * 128; g += (long long)gridDim.x * blockDim.x)
+    cell_dirs32[(size_t)loc[g >> 7].w * (kVoxPerBlock / 4) + (g & 127)] = 0x80808080u;
 }
 
 // One warp per location: the certainly-positive masks (bit l of cell_pos[entry][l / 32]) from bit 7
@@ -254,10 +255,11 @@ __global__ void k_cell_init(const int4 *__restrict__ loc, long long n, unsigned 
 // is cleared first (a re-built location may have lost its surface).
 __global__ void k_cell_masks(const int4 *__restrict__ loc, long long n, const unsigned char *__restrict__ cell_dirs,
                              unsigned int *cell_pos, unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x,
-                             int dim_y) {
-  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                             int dim_y, const unsigned long long *count) {
+  if (count) n = (long long)*count;
   const int lane = threadIdx.x & 31;
-  if (i >= n) return;  // warp-uniform
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += ((long long)gridDim.x * blockDim.x) >> 5) {  // warp-uniform
   const int4 b = loc[i];
   bool all_pos = true;
 #pragma unroll
@@ -273,6 +275,7 @@ __global__ void k_cell_masks(const int4 *__restrict__ loc, long long n, const un
     if (all_pos) atomicAnd(&surface[cell >> 5], ~(1u << (cell & 31)));
     else atomicOr(&surface[cell >> 5], 1u << (cell & 31));
   }
+  }
 }
 
 // Dense location grid: for each allocated location, its hash entry index, present directions and
@@ -280,15 +283,16 @@ __global__ void k_cell_masks(const int4 *__restrict__ loc, long long n, const un
 // directions it holds -- with one 4-B load instead of bitmap + surface + hash probe + entry.
 __global__ void k_loc_grid(const int4 *__restrict__ loc, long long n_loc, const unsigned int *__restrict__ surface,
                            const HashEntry *__restrict__ table, int *grid, int lo_x, int lo_y, int lo_z, int dim_x,
-                           int dim_y) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_loc) return;
-  const int4 b = loc[i];
-  const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
-  const int surf = (surface[cell >> 5] >> (cell & 31)) & 1;
-  int present = 0;
-  for (int d = 0; d < 6; ++d) present |= (table[b.w].slot[d] >= 0) << d;
-  grid[cell] = b.w | (present << kGridEntryBits) | (surf << 30);
+                           int dim_y, const unsigned long long *count) {
+  if (count) n_loc = (long long)*count;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_loc; i += (long long)gridDim.x * blockDim.x) {
+    const int4 b = loc[i];
+    const long long cell = ((long long)(b.z - lo_z) * dim_y + (b.y - lo_y)) * dim_x + (b.x - lo_x);
+    const int surf = (surface[cell >> 5] >> (cell & 31)) & 1;
+    int present = 0;
+    for (int d = 0; d < 6; ++d) present |= (table[b.w].slot[d] >= 0) << d;
+    grid[cell] = b.w | (present << kGridEntryBits) | (surf << 30);
+  }
 }
 
 // Empty-space distance on the location grid (L-infinity, in blocks, capped): separable passes
@@ -358,11 +362,19 @@ cudaError_t launch_bitmap(const int4 *locations, long long n_loc, unsigned int *
   return cudaGetLastError();
 }
 
+// Launch grid for n items of `per` threads each, at most `cap` CTAs of 256 when the item count is
+// read on the device (count non-null, n an upper bound): a grid-stride loop covers the rest.
+static unsigned grid_counted(long long n, long long per, const unsigned long long *count, unsigned cap) {
+  const unsigned g = grid_for(n * per, 256);
+  return count && g > cap ? cap : g;
+}
+
 cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsigned int *surface, const HashEntry *table,
-                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s) {
+                            int *grid, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y, cudaStream_t s,
+                            const unsigned long long *count) {
   if (n_loc == 0) return cudaSuccess;
-  k_loc_grid<<<grid_for(n_loc, 256), 256, 0, s>>>(locations, n_loc, surface, table, grid, lo_x, lo_y, lo_z, dim_x,
-                                                  dim_y);
+  k_loc_grid<<<grid_counted(n_loc, 1, count, 148 * 2), 256, 0, s>>>(locations, n_loc, surface, table, grid, lo_x, lo_y,
+                                                                  lo_z, dim_x, dim_y, count);
   return cudaGetLastError();
 }
 
@@ -434,19 +446,22 @@ __global__ void k_inc_mark(const int4 *__restrict__ keys, long long b0, long lon
 
 __global__ void k_inc_blocks(const int4 *__restrict__ loc_list, long long n, const HashEntry *__restrict__ table,
                              int *blk_list, unsigned long long *ctr) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int e = loc_list[i].w;
+  n = (long long)ctr[0];  // the listed locations (k_fuse / k_inc_mark counted them)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int e = loc_list[i].w;
 #pragma unroll
-  for (int D = 0; D < 6; ++D) {
-    const int b = table[e].slot[D];
-    if (b >= 0) blk_list[atomicAdd(&ctr[1], 1ull)] = b;
+    for (int D = 0; D < 6; ++D) {
+      const int b = table[e].slot[D];
+      if (b >= 0) blk_list[atomicAdd(&ctr[1], 1ull)] = b;
+    }
   }
 }
 
-__global__ void k_inc_unmark(const int4 *__restrict__ loc_list, long long n, int *loc_mark) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) loc_mark[loc_list[i].w] = 0;
+__global__ void k_inc_unmark(const int4 *__restrict__ loc_list, long long n, int *loc_mark,
+                             const unsigned long long *count) {
+  if (count) n = (long long)*count;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    loc_mark[loc_list[i].w] = 0;
 }
 
 cudaError_t launch_inc_mark(const int4 *keys, long long b0, long long n, const unsigned char *dirty,
@@ -461,28 +476,31 @@ cudaError_t launch_inc_mark(const int4 *keys, long long b0, long long n, const u
 cudaError_t launch_inc_blocks(const int4 *loc_list, long long n, const HashEntry *table, int *blk_list,
                               unsigned long long *ctr, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_inc_blocks<<<grid_for(n, 256), 256, 0, s>>>(loc_list, n, table, blk_list, ctr);
+  k_inc_blocks<<<grid_counted(n, 1, ctr, 148 * 2), 256, 0, s>>>(loc_list, n, table, blk_list, ctr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s) {
+cudaError_t launch_inc_unmark(const int4 *loc_list, long long n, int *loc_mark, cudaStream_t s,
+                              const unsigned long long *count) {
   if (n == 0) return cudaSuccess;
-  k_inc_unmark<<<grid_for(n, 256), 256, 0, s>>>(loc_list, n, loc_mark);
+  k_inc_unmark<<<grid_counted(n, 1, count, 148 * 2), 256, 0, s>>>(loc_list, n, loc_mark, count);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s) {
+cudaError_t launch_cell_init(const int4 *locations, long long n, unsigned char *cell_dirs, cudaStream_t s,
+                             const unsigned long long *count) {
   if (n == 0) return cudaSuccess;
-  k_cell_init<<<grid_for(n * 128, 256), 256, 0, s>>>(locations, n, reinterpret_cast<unsigned int *>(cell_dirs));
+  k_cell_init<<<grid_counted(n, 128, count, 148 * 8), 256, 0, s>>>(locations, n,
+                                                                   reinterpret_cast<unsigned int *>(cell_dirs), count);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cell_masks(const int4 *locations, long long n, const unsigned char *cell_dirs, unsigned int *cell_pos,
                               unsigned int *surface, int lo_x, int lo_y, int lo_z, int dim_x, int dim_y,
-                              cudaStream_t s) {
+                              cudaStream_t s, const unsigned long long *count) {
   if (n == 0) return cudaSuccess;
-  k_cell_masks<<<grid_for(n * 32, 256), 256, 0, s>>>(locations, n, cell_dirs, cell_pos, surface, lo_x, lo_y, lo_z,
-                                                     dim_x, dim_y);
+  k_cell_masks<<<grid_counted(n, 32, count, 148 * 8), 256, 0, s>>>(locations, n, cell_dirs, cell_pos, surface, lo_x,
+                                                                   lo_y, lo_z, dim_x, dim_y, count);
   return cudaGetLastError();
 }
 
