@@ -51,6 +51,17 @@ constexpr unsigned long long kEmptyKey = 0xFFFFFFFFFFFFFFFFull;
 // surface bit << 30 (so a location resolves with one 4-B load); negative = empty-space distance
 constexpr int kGridEntryBits = 24;
 constexpr int kGridEntryMask = (1 << kGridEntryBits) - 1;
+// An empty location's grid value: -(1 + box), box = six 5-bit extents (blocks, 0..31) of an
+// all-empty axis-aligned box of locations around it, faces -x, +x, -y, +y, -z, +z (bits 5 f); a
+// ray may skip to the box's exit (render.cu).  The distance transform alone gives the cube of
+// radius d - 1 (d = L-inf distance to the nearest allocated location); k_empty_box grows it.
+#ifndef DTSDF_EMPTY_BOX
+#define DTSDF_EMPTY_BOX 1
+#endif
+constexpr int kBoxBits = 5, kBoxMax = 31;
+__host__ __device__ __forceinline__ int box_cube(int r) {  // all six extents r
+  return r | (r << 5) | (r << 10) | (r << 15) | (r << 20) | (r << 25);
+}
 
 // Hash-table entry: one per block location (x,y,z); the six direction slots are block ids
 // (rows of the pool / apron) or -1.  32 B = one sector: one probe returns all directions.
@@ -322,6 +333,9 @@ cudaError_t launch_loc_grid(const int4 *locations, long long n_loc, const unsign
                             const unsigned long long *count = nullptr);
 cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char *tmp1, int dim_x, int dim_y, int dim_z,
                                   cudaStream_t s);
+// grows every empty location's box (after launch_empty_distance) with a summed-volume table of
+// occupancy; sat: (dim_x + 1) (dim_y + 1) (dim_z + 1) ints of scratch
+cudaError_t launch_empty_box(int *grid, int *sat, int dim_x, int dim_y, int dim_z, cudaStream_t s);
 // The dense location grid as a lookup for index-build kernels: hash entry of a block location, or
 // -1 (unallocated / outside the AABB); grid null: unavailable (use the hash table).
 struct GridRef {

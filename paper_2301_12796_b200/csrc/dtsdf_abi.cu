@@ -87,6 +87,8 @@ struct dtsdf_ctx {
   size_t cap_table = 0, cap_locations = 0, cap_bitmap = 0, cap_surface = 0, cap_cell_pos = 0, cap_brick_a = 0,
          cap_brick_b = 0, cap_loc_grid = 0, cap_dist = 0;
   unsigned char *dist_tmp = nullptr;
+  int *box_sat = nullptr;  // summed-volume table of the location grid's occupancy (k_empty_box)
+  size_t cap_box_sat = 0;
   // commit scratch
   int *scratch = nullptr;  // flags[4] + aabb[6] + n_loc(u64)
   // render scratch
@@ -186,6 +188,8 @@ void free_volume(dtsdf_ctx *c) {
   dfree(c->inc_ctr);
   c->cap_blk_dirty = c->cap_blk_list = c->cap_loc_mark = c->cap_loc_list = c->cap_inc_ctr = 0;
   dfree(c->dist_tmp);
+  dfree(c->box_sat);
+  c->cap_box_sat = 0;
   c->cap_table = c->cap_locations = c->cap_bitmap = c->cap_surface = c->cap_cell_pos = c->cap_brick_a =
       c->cap_brick_b = c->cap_loc_grid = c->cap_dist = c->cap_cell_dirs = 0;
   c->allocated = c->committed = false;
@@ -466,6 +470,18 @@ int dtsdf_commit_volume(dtsdf_ctx *c, void *stream) {
         CK(c, launch_empty_distance(c->loc_grid, c->dist_tmp, c->dist_tmp + cells, c->dim[0], c->dim[1], c->dim[2], s),
            "distance");
         end_timed(c, s, &tl);
+#if DTSDF_EMPTY_BOX
+        // the cubes grown into boxes (the incremental update after a fused frame keeps the grown
+        // boxes while no location is added, and falls back to the cubes when one is)
+        const size_t sat_n = (size_t)(c->dim[0] + 1) * (c->dim[1] + 1) * (c->dim[2] + 1);
+        if (ensure(c->box_sat, c->cap_box_sat, sat_n * 4) == cudaSuccess) {
+          begin_timed(c, 2, s, &tl, 5);
+          CK(c, launch_empty_box(c->loc_grid, c->box_sat, c->dim[0], c->dim[1], c->dim[2], s), "empty boxes");
+          end_timed(c, s, &tl);
+        } else {
+          cudaGetLastError();
+        }
+#endif
       } else {
         cudaGetLastError();
       }

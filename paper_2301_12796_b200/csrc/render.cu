@@ -917,6 +917,18 @@ struct RayT {
     return texit;
   }
   __device__ __forceinline__ float block_exit(const VolumeView &V) const { return box_exit(V, 0); }
+  // ray parameter where it leaves an empty location's box (common.cuh: six 5-bit extents)
+  __device__ __forceinline__ float packed_box_exit(const VolumeView &V, int packed) const {
+    const float bsz = kBlock * V.voxel_size;
+    float texit = 3.0e38f;
+    const int bb[3] = {cur.bx, cur.by, cur.bz};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (r[q] > 0.f) texit = fminf(texit, ((bb[q] + 1 + ((packed >> (kBoxBits * (2 * q + 1))) & kBoxMax)) * bsz - o[q]) * ir[q]);
+      else if (r[q] < 0.f) texit = fminf(texit, ((bb[q] - ((packed >> (kBoxBits * 2 * q)) & kBoxMax)) * bsz - o[q]) * ir[q]);
+    }
+    return texit;
+  }
 
   // a6: bracket [t_{k-1}, t_k] with F(t_{k-1}) = f_prev > 0 and F(t_k) = f_k <= 0
   __device__ __forceinline__ void begin_bracket(const RenderLaunch &p, float f_prev, float f_k) {
@@ -1000,7 +1012,11 @@ struct RayT {
               texit = (t0 <= t1 && t1 > t) ? fmaxf(t0, t) : 3.0e38f;
               if (texit >= 3.0e38f) { k = k1 + 1; continue; }
             } else {
+#if DTSDF_EMPTY_BOX
+              texit = packed_box_exit(V, cur.dist - 1);
+#else
               texit = box_exit(V, cur.dist - 1);
+#endif
             }
             const float kn = floorf(texit * V.inv_delta);
             k = (kn > (float)k1) ? k1 + 1 : max(k + 1, (int)kn);

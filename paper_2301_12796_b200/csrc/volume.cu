@@ -326,7 +326,86 @@ __global__ void k_dist_pass(const int *__restrict__ grid, const unsigned char *_
 __global__ void k_dist_store(int *grid, const unsigned char *__restrict__ dist, long long cells) {
   long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cells) return;
-  if (grid[c] < 0) grid[c] = -(dist[c] > 1 ? (int)dist[c] : 1);
+  const int d = dist[c] > 1 ? (int)dist[c] : 1;
+#if DTSDF_EMPTY_BOX
+  if (grid[c] < 0) grid[c] = -(1 + box_cube(d - 1));  // the cube of radius d - 1 (kDistCap = kBoxMax)
+#else
+  if (grid[c] < 0) grid[c] = -d;
+#endif
+}
+
+// Summed-volume table of occupancy: sat[k][j][i] = allocated locations with x < i, y < j, z < k.
+__global__ void k_sat_fill(const int *__restrict__ grid, int *sat, int dx, int dy, int dz) {
+  const long long n = (long long)(dx + 1) * (dy + 1) * (dz + 1);
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int i = (int)(c % (dx + 1)), j = (int)((c / (dx + 1)) % (dy + 1)), k = (int)(c / ((long long)(dx + 1) * (dy + 1)));
+  sat[c] = (i > 0 && j > 0 && k > 0) ? (grid[((long long)(k - 1) * dy + (j - 1)) * dx + (i - 1)] >= 0) : 0;
+}
+// inclusive prefix sums along one axis, one thread per line
+__global__ void k_sat_scan(int *sat, int axis, int dx, int dy, int dz) {
+  const int nx = dx + 1, ny = dy + 1, nz = dz + 1;
+  const long long lines = axis == 0 ? (long long)ny * nz : (axis == 1 ? (long long)nx * nz : (long long)nx * ny);
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= lines) return;
+  long long base, stride;
+  int len;
+  if (axis == 0) { base = t * nx; stride = 1; len = nx; }
+  else if (axis == 1) { base = (t / nx) * (long long)nx * ny + (t % nx); stride = nx; len = ny; }
+  else { base = t; stride = (long long)nx * ny; len = nz; }
+  int acc = 0;
+  for (int q = 0; q < len; ++q) {
+    acc += sat[base + q * stride];
+    sat[base + q * stride] = acc;
+  }
+}
+// allocated locations in the box [x0, x1] x [y0, y1] x [z0, z1], clipped to the grid (outside it
+// nothing is allocated)
+__device__ __forceinline__ int sat_count(const int *__restrict__ sat, int dx, int dy, int dz, int x0, int x1, int y0,
+                                         int y1, int z0, int z1) {
+  x0 = max(x0, 0); y0 = max(y0, 0); z0 = max(z0, 0);
+  x1 = min(x1, dx - 1); y1 = min(y1, dy - 1); z1 = min(z1, dz - 1);
+  if (x0 > x1 || y0 > y1 || z0 > z1) return 0;
+  const long long sx = 1, sy = dx + 1, sz = (long long)(dx + 1) * (dy + 1);
+  auto at = [&](int i, int j, int k) { return __ldg(&sat[k * sz + j * sy + i * sx]); };
+  ++x1; ++y1; ++z1;
+  return at(x1, y1, z1) - at(x0, y1, z1) - at(x1, y0, z1) - at(x1, y1, z0) + at(x0, y0, z1) + at(x0, y1, z0) +
+         at(x1, y0, z0) - at(x0, y0, z0);
+}
+// Grow each empty location's box from its distance cube: one layer at a time per face, round
+// robin, while the new layer holds no allocated location (counted exactly with the table), up to
+// kBoxMax blocks per face.  The box stays all-empty, so a ray inside it meets no allocated block
+// before its exit (exact skipping).
+__global__ void k_empty_box(int *grid, const int *__restrict__ sat, int dx, int dy, int dz) {
+  const long long cells = (long long)dx * dy * dz;
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const int gv = grid[c];
+  if (gv >= 0) return;
+  const int x = (int)(c % dx), y = (int)((c / dx) % dy), z = (int)(c / ((long long)dx * dy));
+  const int packed = -gv - 1;
+  int e[6];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) e[f] = (packed >> (kBoxBits * f)) & kBoxMax;
+  unsigned grow = 0x3f;
+  while (grow) {
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      if (!((grow >> f) & 1)) continue;
+      if (e[f] >= kBoxMax) { grow &= ~(1u << f); continue; }
+      int b[6] = {x - e[0], x + e[1], y - e[2], y + e[3], z - e[4], z + e[5]};
+      // the new layer beyond face f
+      const int ax = f >> 1;
+      if (f & 1) { b[2 * ax] = b[2 * ax + 1] + 1; b[2 * ax + 1] = b[2 * ax]; }
+      else { b[2 * ax + 1] = b[2 * ax] - 1; b[2 * ax] = b[2 * ax + 1]; }
+      if (sat_count(sat, dx, dy, dz, b[0], b[1], b[2], b[3], b[4], b[5]) == 0) ++e[f];
+      else grow &= ~(1u << f);
+    }
+  }
+  int np = 0;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) np |= e[f] << (kBoxBits * f);
+  grid[c] = -(1 + np);
 }
 
 
@@ -389,6 +468,18 @@ cudaError_t launch_empty_distance(int *grid, unsigned char *tmp0, unsigned char 
   return cudaGetLastError();
 }
 
+
+cudaError_t launch_empty_box(int *grid, int *sat, int dim_x, int dim_y, int dim_z, cudaStream_t s) {
+  const long long cells = (long long)dim_x * dim_y * dim_z;
+  if (cells == 0) return cudaSuccess;
+  const long long n = (long long)(dim_x + 1) * (dim_y + 1) * (dim_z + 1);
+  k_sat_fill<<<grid_for(n, 256), 256, 0, s>>>(grid, sat, dim_x, dim_y, dim_z);
+  k_sat_scan<<<grid_for((long long)(dim_y + 1) * (dim_z + 1), 128), 128, 0, s>>>(sat, 0, dim_x, dim_y, dim_z);
+  k_sat_scan<<<grid_for((long long)(dim_x + 1) * (dim_z + 1), 128), 128, 0, s>>>(sat, 1, dim_x, dim_y, dim_z);
+  k_sat_scan<<<grid_for((long long)(dim_x + 1) * (dim_y + 1), 128), 128, 0, s>>>(sat, 2, dim_x, dim_y, dim_z);
+  k_empty_box<<<grid_for(cells, 128), 128, 0, s>>>(grid, sat, dim_x, dim_y, dim_z);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_bricks(const int4 *keys, long long n, const HashEntry *table, unsigned int mask, const float *sdf,
                           const float *weight, const unsigned char *rgb, float4 *brick_a, float2 *brick_b,
