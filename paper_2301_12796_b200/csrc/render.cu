@@ -964,14 +964,19 @@ struct RayT {
     mode = p.n_bisect > 0 ? kBisect : kIllinois;
   }
 
-  // Advance (march only), evaluate one sample, update the state.  Returns true when the ray is
-  // finished (hit shaded, or no crossing in range).
-  __device__ __forceinline__ bool step(const RenderLaunch &p) {
+  int live_;  // live-direction byte of the point to evaluate, if the advance loop read it (-1: not)
+#ifdef DTSDF_STATS
+  long long c0_;
+#endif
+  // One step = advance() then evaluate().  Advance (march only) to the next point to evaluate;
+  // false when the ray is finished (no crossing in range: a miss).
+  __device__ __forceinline__ bool advance(const RenderLaunch &p) {
     const VolumeView &V = p.vol;
 #ifdef DTSDF_STATS
-    const long long c0 = clock64();
+    c0_ = clock64();
 #endif
-    int live = -1;  // live-direction byte of the point to evaluate, if the advance loop read it
+    int &live = live_;
+    live = -1;
     if (mode == kMarch) {
       // a4: advance to the next lattice point that needs an evaluation.  Every step skipped here
       // is exact (DESIGN.md §2 O2): lattice points in unallocated locations are invalid; in a
@@ -979,7 +984,7 @@ struct RayT {
       // another, no crossing can end or start.
       for (;;) {
         live = -1;
-        if (k > k1) return true;  // no crossing: a miss
+        if (k > k1) return false;  // no crossing: a miss
         t = (float)k * V.delta;
         locate(V, p.comb, t);
 #ifdef DTSDF_STATS
@@ -1107,6 +1112,17 @@ struct RayT {
     } else {
       locate(V, p.comb, t);
     }
+    return true;
+  }
+
+  // Evaluate the sample advance() located and update the state; true when the ray is finished
+  // (a hit, shaded after the loop).
+  __device__ __forceinline__ bool evaluate(const RenderLaunch &p) {
+    const VolumeView &V = p.vol;
+    const int live = live_;
+#ifdef DTSDF_STATS
+    const long long c0 = c0_;
+#endif
     SampleResult s;
 #ifdef DTSDF_STATS
     if (mode == kMarch) { ++st_march; --st_skip; } else ++st_refine;
@@ -1174,6 +1190,8 @@ struct RayT {
     }
     return false;
   }
+
+  __device__ __forceinline__ bool step(const RenderLaunch &p) { return !advance(p) || evaluate(p); }
 
   // a7 at the hit t = b (refinement frame): the evaluation of the last step again, with the
   // shading sums
@@ -1347,40 +1365,47 @@ __global__ void __launch_bounds__(DTSDF_CTA, DTSDF_RAYCAST_MINB) k_raycast(const
   }
   const int u = u0 + tx, vrel = v0 + ty;
   const int rows = p.row1 - p.row0;
-  if (u < p.width && vrel < rows) {
-    RayT<kComb> ray;
+  const bool inside = u < p.width && vrel < rows;
+  RayT<kComb> ray;
 #ifdef DTSDF_STATS
-    unsigned long long g_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+  unsigned long long g_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 #endif
-    ray.init(p, blockIdx.z, u, vrel);
+  if (inside) ray.init(p, blockIdx.z, u, vrel);
 #ifdef DTSDF_STATS
-    const long long c0 = clock64();
+  const long long c0 = clock64();
+  // per-step trace of one ray: clock at step start, cycles of the step, of its advance, mode
+  // before | after << 8, k before, k after, new blocks located, lookahead scans
+  // (all 32 lanes of the warp tile whose origin is dbg_trace_pix, 128 steps each)
+  const int tu = p.dbg_trace_pix & 0xffff, tv = p.dbg_trace_pix >> 16;
+  const bool tr = inside && p.dbg_trace && blockIdx.z == 0 && u - tu >= 0 && u - tu < 8 && vrel - tv >= 0 && vrel - tv < 4;
+  long long *tb = p.dbg_trace + (tr ? 8 * 128 * ((u - tu) + 8 * (vrel - tv)) : 0);
+  int n_tr = 0;
 #endif
+  if (inside) {
 #ifdef DTSDF_STATS
-    // per-step trace of one ray: clock at step start, cycles of the step, of its advance, mode
-    // before | after << 8, k before, k after, new blocks located, lookahead scans
-    // (all 32 lanes of the warp tile whose origin is dbg_trace_pix, 128 steps each)
-    const int tu = p.dbg_trace_pix & 0xffff, tv = p.dbg_trace_pix >> 16;
-    const bool tr = p.dbg_trace && blockIdx.z == 0 && u - tu >= 0 && u - tu < 8 && vrel - tv >= 0 && vrel - tv < 4;
-    long long *tb = p.dbg_trace + (tr ? 8 * 128 * ((u - tu) + 8 * (vrel - tv)) : 0);
-    int n_tr = 0;
     for (;;) {
       const long long s0 = clock64(), a0 = ray.cy_adv;
-      const int m0 = ray.mode, k0 = ray.k, nb0 = ray.st_newblk, ns0 = ray.st_scan, nl0 = ray.st_loc;
+      const int m0 = ray.mode, k0 = ray.k, nb0 = ray.st_newblk, ns0 = ray.st_scan, nl0 = ray.st_loc,
+                nj0 = ray.st_jump, ne0 = ray.st_empty;
       const bool done = ray.step(p);
       if (tr && n_tr < 127) {
         long long *e = tb + 8 * n_tr++;
         e[0] = s0; e[1] = clock64() - s0; e[2] = ray.cy_adv - a0; e[3] = m0 | (ray.mode << 8) | (ray.hit << 16);
-        e[4] = k0; e[5] = ray.k; e[6] = (ray.st_newblk - nb0) | ((long long)(ray.st_loc - nl0) << 16); e[7] = ray.st_scan - ns0;
+        e[4] = k0; e[5] = ray.k; e[6] = (ray.st_newblk - nb0) | ((long long)(ray.st_loc - nl0) << 16);
+        e[7] = (ray.st_scan - ns0) | ((long long)(ray.st_jump - nj0) << 16) | ((long long)(ray.st_empty - ne0) << 32);
       }
       if (done) break;
     }
-    if (tr) tb[8 * n_tr] = -1;
 #else
     while (!ray.step(p)) {
     }
 #endif
+  }
+#ifdef DTSDF_STATS
+  if (tr) tb[8 * n_tr] = -1;
+#endif
+  if (inside) {
     if (ray.hit) ray.shade(p);
 #ifdef DTSDF_STATS
     ray.cy_adv = clock64() - c0 - ray.cy_march - ray.cy_refine;  // everything outside the evaluations

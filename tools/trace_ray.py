@@ -56,16 +56,20 @@ for spec in sys.argv[2:]:
         steps = int(n.max())
         cyc = np.array([max(t[l, i, 1] for l in range(32) if i < n[l]) for i in range(steps)])
         locs = [[t[l, i, 6] >> 16 for l in range(32) if i < n[l]] for i in range(steps)]
+        tot = lambda sh: int(sum(((t[l, :n[l], 7] >> sh) & 0xffff).sum() for l in range(32)))
+        print(f"  {label}: lane totals: scans {tot(0)}, jumps {tot(16)}, empty-block steps {tot(32)}")
         print(f"  {label}: {steps} warp steps, {cyc.sum()} cycles ({cyc.sum() / steps:.0f}/step); "
               f"locates per step (max lane) {sum(max(x) for x in locs)}, (all lanes) {sum(sum(x) for x in locs)}")
         if label == "whole view":
-            print("    step  cycles  adv(slowest lane)  lanes M/B/I  locates max/mean  newblk max  scans max")
+            print("    step  cycles  adv(slowest lane)  lanes M/B/I  locates max/mean  newblk max  scans max  jumps max  empty max")
             for i in range(steps):
                 act = [l for l in range(32) if i < n[l]]
                 md = [t[l, i, 3] & 255 for l in act]
                 lc = np.array([t[l, i, 6] >> 16 for l in act])
                 nb = np.array([t[l, i, 6] & 0xffff for l in act])
-                sc = np.array([t[l, i, 7] for l in act])
+                sc = np.array([t[l, i, 7] & 0xffff for l in act])
+                jm = np.array([(t[l, i, 7] >> 16) & 0xffff for l in act])
+                em = np.array([(t[l, i, 7] >> 32) & 0xffff for l in act])
                 adv = max(t[l, i, 2] for l in act)
                 print(f"    {i:4d} {cyc[i]:7d} {adv:7d}   {md.count(0):2d}/{md.count(1):2d}/{md.count(2):2d}   "
-                      f"{lc.max():3d}/{lc.mean():5.2f}   {nb.max():3d}  {sc.max():3d}")
+                      f"{lc.max():3d}/{lc.mean():5.2f}   {nb.max():3d}  {sc.max():3d}  {jm.max():3d}  {em.max():3d}")
