@@ -154,6 +154,30 @@ def test_accelerations_are_result_invisible(R, c1, c2):
         R.set_option(OPT_TILE_ORDER, 1)
 
 
+def test_grown_empty_boxes_skip_exactly(R):
+    """Empty-space skipping through the grown boxes (k_empty_box) is exact: a room
+    with 64 boxes seen from 16 seeded scan poses -- inside the room, far outside it, grazing the
+    floor -- renders bit-identically with block skipping on (boxes) and off (every lattice
+    point located)."""
+    from paper_2301_12796_b200.dtsdf import OPT_BLOCK_SKIP
+    w = scenes.c1_room(n_boxes=64)
+    R.upload_volume(w.volume)
+    K = scenes.Intrinsics(fx=131.25, fy=131.25, cx=79.5, cy=59.5, width=160, height=120)
+    rng = np.random.default_rng([2301, 12796])
+    poses = np.concatenate([np.asarray(scenes.room_scan_poses(rng, n=8), np.float32),
+                            np.asarray(scenes.room_scan_poses(rng, n=4, radius=(5.0, 9.0), height=(0.1, 4.0)), np.float32),
+                            np.asarray(scenes.room_scan_poses(rng, n=4, radius=(1.0, 2.0), height=(0.05, 0.2)), np.float32)])
+    ref = R.render(poses, K)
+    assert (ref["depth"] > 0).float().mean() > 0.2
+    R.set_option(OPT_BLOCK_SKIP, 0)
+    try:
+        g = R.render(poses, K)
+    finally:
+        R.set_option(OPT_BLOCK_SKIP, 1)
+    for k in ref:
+        assert torch.equal(ref[k], g[k]), k
+
+
 def test_location_grid_and_hash_paths_agree(R, c1):
     """The dense location grid and the bitmap + hash-probe path resolve the same slots."""
     from paper_2301_12796_b200.dtsdf import OPT_LOCATION_GRID
