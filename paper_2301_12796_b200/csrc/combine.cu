@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
       const unsigned int sr = __ldg(&kFin.src[e]);
       dst[k] = __ldg(&kFin.dst[e]);
       const int ns = s_nb[sr >> 16];
-      DTSDF_CHECK(ns < (int)gridDim.x);
+      DTSDF_CHECK(ns < (int)gridDim.x && (sr >> 16) < 27 && (sr & 0xffffu) < kApronVox && dst[k] < kApronVox);
       if (ns >= 0) v[k] = __ldg(apin + (size_t)ns * kApronStride + (sr & 0xffffu));
     }
   }
@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_comb_finish(const __grid_con
     const unsigned int sr = __ldg(&kFin.rgb_src[tid]);
     rdst = __ldg(&kFin.rgb_dst[tid]);
     const int ns = s_nb[sr >> 16];
+    DTSDF_CHECK(ns < (int)gridDim.x && (sr >> 16) < 27 && (sr & 0xffffu) < kRgbApronVox && rdst < kRgbApronVox);
     if (ns >= 0) cv = __ldg(p.rgb + (size_t)ns * kRgbApronStride + (sr & 0xffffu));
   }
 #pragma unroll

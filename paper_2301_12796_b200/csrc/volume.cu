@@ -367,7 +367,10 @@ __device__ __forceinline__ int sat_count(const int *__restrict__ sat, int dx, in
   x1 = min(x1, dx - 1); y1 = min(y1, dy - 1); z1 = min(z1, dz - 1);
   if (x0 > x1 || y0 > y1 || z0 > z1) return 0;
   const long long sx = 1, sy = dx + 1, sz = (long long)(dx + 1) * (dy + 1);
-  auto at = [&](int i, int j, int k) { return __ldg(&sat[k * sz + j * sy + i * sx]); };
+  auto at = [&](int i, int j, int k) {
+    DTSDF_CHECK(i >= 0 && i <= dx && j >= 0 && j <= dy && k >= 0 && k <= dz);
+    return __ldg(&sat[k * sz + j * sy + i * sx]);
+  };
   ++x1; ++y1; ++z1;
   return at(x1, y1, z1) - at(x0, y1, z1) - at(x1, y0, z1) - at(x1, y1, z0) + at(x0, y0, z1) + at(x0, y1, z0) +
          at(x1, y0, z0) - at(x0, y0, z0);
@@ -404,7 +407,10 @@ __global__ void k_empty_box(int *grid, const int *__restrict__ sat, int dx, int 
   }
   int np = 0;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) np |= e[f] << (kBoxBits * f);
+  for (int f = 0; f < 6; ++f) {
+    DTSDF_CHECK(e[f] >= 0 && e[f] <= kBoxMax);
+    np |= e[f] << (kBoxBits * f);
+  }
   grid[c] = -(1 + np);
 }
 
