@@ -275,7 +275,7 @@ struct IcpState {
   double step, residual;
   long long inliers;
   int iterations, done, status;    // status 1: singular system
-  int pad;
+  unsigned int ticket;             // k_icp_reduce CTAs done this iteration (fused solve; 0 between launches)
 };
 
 struct IcpLaunch {
@@ -289,6 +289,7 @@ struct IcpLaunch {
   IcpState *state;
   double2 *pback;                  // [H][W] ((u - cx) / fx * z, (v - cy) / fy * z) of the frame (k_icp_backproject)
   double *col_fac, *row_fac;       // [W] (u - cx) / fx, [H] (v - cy) / fy: the rendered pixels' back-projection
+  int fused_solve;                 // 1: the last k_icp_reduce CTA of an iteration also solves (no k_icp_solve)
 };
 
 // host launchers (icp.cu)

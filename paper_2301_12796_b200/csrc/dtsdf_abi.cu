@@ -1430,6 +1430,7 @@ int dtsdf_icp(dtsdf_ctx *c, const float *depth, const float *ref_depth, const fl
   if (rc) return rc;
   L.min_step = prm.min_step;
   L.max_iters = prm.max_iters;
+  L.fused_solve = 1;
   IcpState init;
   std::memset(&init, 0, sizeof(init));
   for (int i = 0; i < 16; ++i) init.delta[i] = init_delta ? (double)init_delta[i] : ((i % 5) == 0 ? 1.0 : 0.0);
@@ -1445,11 +1446,8 @@ int dtsdf_icp(dtsdf_ctx *c, const float *depth, const float *ref_depth, const fl
   int launched = 0;
   for (int chunk = kIcpChunk; launched < prm.max_iters; chunk *= 2) {
     const int n = std::min(chunk, prm.max_iters - launched);
-    begin_timed(c, 2, s, &tl, 2 * n);
-    for (int it = 0; it < n; ++it) {
-      CK(c, launch_icp_reduce(L, s), "ICP reduce");
-      CK(c, launch_icp_solve(L, s), "ICP solve");
-    }
+    begin_timed(c, 2, s, &tl, n);
+    for (int it = 0; it < n; ++it) CK(c, launch_icp_reduce(L, s), "ICP reduce + solve");
     end_timed(c, s, &tl);
     launched += n;
     if (launched >= prm.max_iters) break;
@@ -1483,6 +1481,7 @@ int dtsdf_icp_normal_equations(dtsdf_ctx *c, const float *depth, const float *re
   if (rc) return rc;
   L.min_step = 0.0;
   L.max_iters = 1;
+  L.fused_solve = 0;
   IcpState init;
   std::memset(&init, 0, sizeof(init));
   for (int i = 0; i < 16; ++i) init.delta[i] = delta[i];

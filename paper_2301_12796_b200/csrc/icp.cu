@@ -91,6 +91,8 @@ __global__ void k_icp_backproject(const __grid_constant__ IcpLaunch p) {
                               __dmul_rn(__ddiv_rn(__dsub_rn((double)v, p.cy), p.fy), zd));
 }
 
+__device__ void icp_solve_body(const IcpLaunch &p, int n_partials);
+
 __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(const __grid_constant__ IcpLaunch p) {
   if (*((volatile int *)&p.state->done)) return;
   __shared__ double s_d[16];
@@ -122,6 +124,17 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_reduce(const __grid_constan
     for (int w = 1; w < kIcpThreads / 32; ++w) v += s_w[w][tid];
     p.partials[(size_t)blockIdx.x * kIcpSums + tid] = v;
   }
+  if (!p.fused_solve) return;
+  // the last CTA to finish this iteration solves it (one launch per iteration instead of two)
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&p.state->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  icp_solve_body(p, gridDim.x);
+  if (tid == 0) p.state->ticket = 0;
 }
 
 __device__ void se3_exp(const double xi[6], double T[16]) {
@@ -150,9 +163,10 @@ __device__ void se3_exp(const double xi[6], double T[16]) {
   T[15] = 1.0;
 }
 
-__global__ void __launch_bounds__(kIcpThreads) k_icp_solve(const __grid_constant__ IcpLaunch p, int n_partials) {
+// The partials' sum (thread t adds partials t, t + 256, ... in order, then the fixed warp / CTA tree:
+// the same bits whichever CTA runs it), the 6x6 solve and the DeltaT update.  All kIcpThreads threads.
+__device__ void icp_solve_body(const IcpLaunch &p, int n_partials) {
   IcpState *st = p.state;
-  if (*((volatile int *)&st->done)) return;
   __shared__ double s_sum[kIcpThreads / 32][kIcpSums];
   const int tid = threadIdx.x;
   // thread t sums partials t, t + 256, ... in order; then the fixed warp / CTA tree
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_solve(const __grid_constant
   for (int k = 0; k < kIcpSums; ++k) acc[k] = 0.0;
   for (int i = tid; i < n_partials; i += kIcpThreads)
 #pragma unroll
-    for (int k = 0; k < kIcpSums; ++k) acc[k] += p.partials[(size_t)i * kIcpSums + k];
+    for (int k = 0; k < kIcpSums; ++k) acc[k] += __ldcg(&p.partials[(size_t)i * kIcpSums + k]);
 #pragma unroll
   for (int k = 0; k < kIcpSums; ++k) {
     double v = acc[k];
@@ -229,6 +243,11 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_solve(const __grid_constant
   st->step = sqrt(nrm);
   st->iterations += 1;
   if (st->step < p.min_step || st->iterations >= p.max_iters) st->done = 1;
+}
+
+__global__ void __launch_bounds__(kIcpThreads) k_icp_solve(const __grid_constant__ IcpLaunch p, int n_partials) {
+  if (*((volatile int *)&p.state->done)) return;
+  icp_solve_body(p, n_partials);
 }
 
 int icp_partials(int width, int height) {
